@@ -1,0 +1,196 @@
+/*
+ * dconv_b200 — C ABI of the B200 (sm_100a) direct-convolution engine.
+ *
+ * Drop-in boundary for the reference artifact's conv execute calls
+ * (arxiv 1808.05567 artifact, /root/reference/proj). Every entry point
+ * below replaces one reference interface, cited as file:line (paths relative
+ * to proj/core). Plain C types only: device pointers, sizes, an opaque plan
+ * handle and a CUDA stream. All execute calls are ASYNCHRONOUS on `stream`;
+ * the synchronous reference contract (execute returns finished results) is
+ * restored by the C++ shim / Python mirror, which synchronise the stream.
+ *
+ * Layouts are the reference's, element for element:
+ *   activations  [n][c_b][h + 2*halo_h][w + 2*halo_w][vlen]  (blocked.hpp:47-51)
+ *   weights      [k_b][c_b][r][s][c][k]                      (blocked.hpp:112-115)
+ * stored as fp32 (the reference type) or bf16.
+ *
+ * Errors: every function returns a dconv_status_t whose non-zero values map
+ * 1:1 onto the reference exception classes (errors.hpp:8-57); the message is
+ * available from dconv_last_error() (thread-local).
+ */
+#ifndef DCONV_B200_H
+#define DCONV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dconv_stream_t; /* == cudaStream_t */
+
+typedef enum dconv_status {
+  DCONV_OK = 0,
+  DCONV_ERR_NON_INTEGRAL_SHAPE = 1,   /* errors.hpp:14 NonIntegralShape */
+  DCONV_ERR_INVALID_LAYER_SPEC = 2,   /* errors.hpp:18 InvalidLayerSpec */
+  DCONV_ERR_SHAPE_MISMATCH = 3,       /* errors.hpp:22 ShapeMismatch */
+  DCONV_ERR_INVALID_DESCRIPTOR = 4,   /* errors.hpp:26 InvalidDescriptor */
+  DCONV_ERR_OVERFLOW_RISK = 5,        /* errors.hpp:30 OverflowRisk */
+  DCONV_ERR_PLAN_INFEASIBLE = 6,      /* errors.hpp:34 PlanInfeasible */
+  DCONV_ERR_EMPTY_TRACE = 7,          /* errors.hpp:38 EmptyTrace */
+  DCONV_ERR_PLAN_TENSOR_MISMATCH = 8, /* errors.hpp:42 PlanTensorMismatch */
+  DCONV_ERR_INFEASIBLE_STRATEGY = 9,  /* errors.hpp:46 InfeasibleStrategy */
+  DCONV_ERR_CHAIN_SHAPE_MISMATCH = 10,/* errors.hpp:50 ChainShapeMismatch */
+  DCONV_ERR_PARSE = 11,               /* errors.hpp:54 ParseError */
+  DCONV_ERR_CUDA = 100,               /* CUDA runtime / driver failure */
+  DCONV_ERR_UNSUPPORTED = 101,        /* valid for the reference, not implemented on sm_100a */
+  DCONV_ERR_INVALID_ARGUMENT = 102    /* null pointer, bad enum */
+} dconv_status_t;
+
+/* ConvLayerSpec (layer_spec.hpp:12-38), field for field */
+typedef struct dconv_spec {
+  int N, C, K, H, W, R, S, stride, pad_h, pad_w, vlen;
+} dconv_spec_t;
+
+typedef enum dconv_dtype { DCONV_F32 = 0, DCONV_BF16 = 1 } dconv_dtype_t;
+
+/* arithmetic of the tensor-core passes */
+typedef enum dconv_math {
+  DCONV_MATH_F32 = 0, /* fp32-accurate: exact 3-way bf16 split, 6 products, fp32 accumulate */
+  DCONV_MATH_BF16 = 1 /* bf16 operands, fp32 accumulate */
+} dconv_math_t;
+
+/* BlockedActivationT (blocked.hpp:16-80) over device memory */
+typedef struct dconv_act {
+  void* data;
+  int n, c, h, w, vlen, halo_h, halo_w;
+  int dtype; /* dconv_dtype_t */
+} dconv_act_t;
+
+/* BlockedWeightT (blocked.hpp:84-125) over device memory */
+typedef struct dconv_wt {
+  void* data;
+  int k, c, r, s, vlen;
+  int dtype;
+} dconv_wt_t;
+
+/* FusedOp (kernel_streams.hpp:29-34); bias is a HOST array of K floats */
+typedef enum dconv_fused_kind {
+  DCONV_FUSE_NONE = -1,
+  DCONV_FUSE_RELU = 0,
+  DCONV_FUSE_BIAS_ADD = 1,
+  DCONV_FUSE_BIAS_RELU = 2
+} dconv_fused_kind_t;
+typedef struct dconv_fusion {
+  int kind;
+  const float* bias; /* host, K entries (BIAS_*), copied at plan creation */
+  int bias_len;
+} dconv_fusion_t;
+
+/* EngineConfig (config.hpp:10-20) plus sm_100a tile-selector overrides
+ * (0 = automatic). The CPU tunables are accepted for API compatibility. */
+typedef struct dconv_engine_config {
+  int min_accumulators, max_accumulators;
+  int64_t cache_budget_bytes;
+  int prefetch_lookahead, prefetch_enabled, streaming_stores;
+  int acc_chain_limit, i16_bound_in, i16_bound_wt;
+  int tile_mb;    /* FWD/BWD: 128-row m-blocks per CTA */
+  int tile_nb;    /* 16-channel output blocks per CTA */
+  int stages;     /* smem pipeline depth */
+  int upd_splits; /* UPD split-K factor */
+} dconv_engine_config_t;
+
+/* ---------------------------------------------------------------- basics */
+const char* dconv_last_error(void);
+const char* dconv_status_string(int status);
+int dconv_version(void);
+void dconv_engine_config_default(dconv_engine_config_t* cfg); /* config.hpp:10-20 */
+
+/* make_layer_spec (layer_spec.cpp:20-43); pad_h/pad_w < 0 = "same" default (R-1)/2 */
+int dconv_make_spec(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h, int pad_w, int vlen,
+                    dconv_spec_t* out);
+int dconv_spec_validate(const dconv_spec_t* spec);                 /* layer_spec.cpp:7-18 */
+int dconv_output_shape(const dconv_spec_t* spec, int* P, int* Q);  /* layer_spec.cpp:45-51 */
+int64_t dconv_pass_flops(const dconv_spec_t* spec);                /* harness.cpp:269-272 */
+int64_t dconv_act_elems(const dconv_act_t* a);                     /* blocked.hpp:29-34 */
+int64_t dconv_wt_elems(const dconv_wt_t* w);                       /* blocked.hpp:92-97 */
+
+/* ---------------------------------------------------------------- layouts (device, async) */
+/* to_blocked_activation (blocked.hpp:133-155): NCHW -> blocked, halo and tail lanes zero */
+int dconv_pack_act(const void* nchw, int src_dtype, const dconv_act_t* dst, dconv_stream_t stream);
+/* from_blocked_activation (blocked.hpp:157-178) */
+int dconv_unpack_act(const dconv_act_t* src, void* nchw, int dst_dtype, dconv_stream_t stream);
+/* to_blocked_weight / from_blocked_weight (blocked.hpp:180-213) */
+int dconv_pack_wt(const void* kcrs, int src_dtype, const dconv_wt_t* dst, dconv_stream_t stream);
+int dconv_unpack_wt(const dconv_wt_t* src, void* kcrs, int dst_dtype, dconv_stream_t stream);
+/* transform_weight_stride1 (propagation.hpp:20-33): dst has k = src.c, c = src.k */
+int dconv_transform_weight_dual(const dconv_wt_t* src, const dconv_wt_t* dst, dconv_stream_t stream);
+/* copy_with_halo (propagation.hpp:35-49) */
+int dconv_copy_with_halo(const dconv_act_t* src, const dconv_act_t* dst, dconv_stream_t stream);
+/* BlockedActivationT::zero_halo (blocked.hpp:67-79) */
+int dconv_zero_halo(const dconv_act_t* act, dconv_stream_t stream);
+/* apply_fused_op (propagation.cpp:193-215): post-hoc op on the interior */
+int dconv_apply_fused_op(const dconv_act_t* act, const dconv_fusion_t* op, dconv_stream_t stream);
+/* host-side seeded generators shared by bench and tests (util.hpp:40-71 splitmix64) */
+void dconv_fill_uniform_host(uint64_t seed, float lo, float hi, float* out, int64_t n);
+void dconv_fill_he_normal_host(uint64_t seed, float stddev, float* out, int64_t n);
+
+/* ---------------------------------------------------------------- forward */
+typedef struct dconv_fwd_plan* dconv_fwd_plan_t;
+/* make_forward_plan (propagation.cpp:42-54): tile selection replaces
+ * choose_loop_order / select_register_blocking / partition_threads / dryrun */
+int dconv_fwd_plan_create(const dconv_spec_t* spec, const dconv_fusion_t* fusion, const dconv_engine_config_t* cfg,
+                          int math, int out_halo_h, int out_halo_w, dconv_fwd_plan_t* plan);
+void dconv_fwd_plan_destroy(dconv_fwd_plan_t plan);
+/* JSON description of the chosen tiles (LayerReport.blocking analog, harness.hpp:48) */
+int dconv_fwd_plan_describe(dconv_fwd_plan_t plan, char* buf, size_t len);
+size_t dconv_fwd_workspace_bytes(dconv_fwd_plan_t plan);
+/* forward_into (propagation.cpp:56-61): writes the interior and zeroes the
+ * output halo; any input halo is accepted (padding is an OOB zero fill). */
+int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
+                  void* workspace, dconv_stream_t stream);
+/* number of this library's kernels one dconv_forward launches */
+int dconv_fwd_launches(dconv_fwd_plan_t plan);
+
+/* ---------------------------------------------------------------- backward-data */
+typedef struct dconv_bwd_plan* dconv_bwd_plan_t;
+typedef enum dconv_bwd_route {
+  DCONV_BWD_DUALITY_STRIDE1 = 0, /* propagation.hpp:11 */
+  DCONV_BWD_DUALITY_1x1 = 1,
+  DCONV_BWD_GENERIC = 2          /* stride-phase decomposition (GENERIC_GEMM analog) */
+} dconv_bwd_route_t;
+/* prepare_backward (propagation.cpp:217-276); weights are passed per execute call */
+int dconv_bwd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t* cfg, int math,
+                          dconv_bwd_plan_t* plan);
+void dconv_bwd_plan_destroy(dconv_bwd_plan_t plan);
+int dconv_bwd_route(dconv_bwd_plan_t plan); /* choose_backward_route (propagation.cpp:35-40) */
+int dconv_bwd_plan_describe(dconv_bwd_plan_t plan, char* buf, size_t len);
+size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan);
+/* backward_with (propagation.cpp:278-348): dI interior written, dI halo zeroed,
+ * off-lattice entries of strided routes exactly 0 */
+int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
+                        const dconv_act_t* grad_in, void* workspace, dconv_stream_t stream);
+int dconv_bwd_launches(dconv_bwd_plan_t plan);
+
+/* ---------------------------------------------------------------- weight update */
+typedef struct dconv_upd_plan* dconv_upd_plan_t;
+/* choose_update_strategy + choose_spatial_blocking (planner.cpp:107-173):
+ * split-K factor and pixel band per stage */
+int dconv_upd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t* cfg, int math,
+                          dconv_upd_plan_t* plan);
+void dconv_upd_plan_destroy(dconv_upd_plan_t plan);
+int dconv_upd_splits(dconv_upd_plan_t plan); /* WeightUpdateStrategy.copies analog */
+int dconv_upd_plan_describe(dconv_upd_plan_t plan, char* buf, size_t len);
+/* workspace depends on the operand dtypes / halos (fp32 operands are split once into bf16 pieces) */
+size_t dconv_upd_workspace_bytes(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out);
+/* weight_update (propagation.cpp:377-458) + reduce_weight_copies (:357-375):
+ * fixed-order split reduction -> bitwise reproducible. accumulate != 0 adds into dw. */
+int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out,
+                        const dconv_wt_t* grad_w, int accumulate, void* workspace, dconv_stream_t stream);
+int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCONV_B200_H */

@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/dconv_b200.h (libdconv_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``). There is no fallback: if the
+library is missing or fails to load, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libdconv_b200.so")
+
+
+class Spec(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("N", "C", "K", "H", "W", "R", "S", "stride", "pad_h", "pad_w", "vlen")]
+
+
+class Act(C.Structure):
+    _fields_ = [("data", C.c_void_p)] + [(n, C.c_int) for n in ("n", "c", "h", "w", "vlen", "halo_h", "halo_w",
+                                                                  "dtype")]
+
+
+class Wt(C.Structure):
+    _fields_ = [("data", C.c_void_p)] + [(n, C.c_int) for n in ("k", "c", "r", "s", "vlen", "dtype")]
+
+
+class Fusion(C.Structure):
+    _fields_ = [("kind", C.c_int), ("bias", C.POINTER(C.c_float)), ("bias_len", C.c_int)]
+
+
+class EngineCfg(C.Structure):
+    _fields_ = [("min_accumulators", C.c_int), ("max_accumulators", C.c_int), ("cache_budget_bytes", C.c_int64),
+                ("prefetch_lookahead", C.c_int), ("prefetch_enabled", C.c_int), ("streaming_stores", C.c_int),
+                ("acc_chain_limit", C.c_int), ("i16_bound_in", C.c_int), ("i16_bound_wt", C.c_int),
+                ("tile_mb", C.c_int), ("tile_nb", C.c_int), ("stages", C.c_int), ("upd_splits", C.c_int)]
+
+
+# status codes (include/dconv_b200.h) -> reference exception class names (errors.hpp:8-57)
+STATUS_NAMES = {
+    1: "NonIntegralShape", 2: "InvalidLayerSpec", 3: "ShapeMismatch", 4: "InvalidDescriptor", 5: "OverflowRisk",
+    6: "PlanInfeasible", 7: "EmptyTrace", 8: "PlanTensorMismatch", 9: "InfeasibleStrategy",
+    10: "ChainShapeMismatch", 11: "ParseError", 100: "CudaError", 101: "Unsupported", 102: "InvalidArgument",
+}
+
+# every symbol the header declares (tests check the export table against this list)
+EXPORTS = [
+    "dconv_last_error", "dconv_status_string", "dconv_version", "dconv_engine_config_default", "dconv_make_spec",
+    "dconv_spec_validate", "dconv_output_shape", "dconv_pass_flops", "dconv_act_elems", "dconv_wt_elems",
+    "dconv_pack_act", "dconv_unpack_act", "dconv_pack_wt", "dconv_unpack_wt", "dconv_transform_weight_dual",
+    "dconv_copy_with_halo", "dconv_zero_halo", "dconv_apply_fused_op", "dconv_fill_uniform_host",
+    "dconv_fill_he_normal_host", "dconv_fwd_plan_create", "dconv_fwd_plan_destroy", "dconv_fwd_plan_describe",
+    "dconv_fwd_workspace_bytes", "dconv_forward", "dconv_fwd_launches", "dconv_bwd_plan_create",
+    "dconv_bwd_plan_destroy", "dconv_bwd_route", "dconv_bwd_plan_describe", "dconv_bwd_workspace_bytes",
+    "dconv_backward_data", "dconv_bwd_launches", "dconv_upd_plan_create", "dconv_upd_plan_destroy",
+    "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
+    "dconv_upd_launches",
+]
+
+
+def _bind(lib):
+    P = C.POINTER
+    vp, i, sz, i64 = C.c_void_p, C.c_int, C.c_size_t, C.c_int64
+    sig = {
+        "dconv_last_error": (C.c_char_p, []),
+        "dconv_status_string": (C.c_char_p, [i]),
+        "dconv_version": (i, []),
+        "dconv_engine_config_default": (None, [P(EngineCfg)]),
+        "dconv_make_spec": (i, [i] * 11 + [P(Spec)]),
+        "dconv_spec_validate": (i, [P(Spec)]),
+        "dconv_output_shape": (i, [P(Spec), P(i), P(i)]),
+        "dconv_pass_flops": (i64, [P(Spec)]),
+        "dconv_act_elems": (i64, [P(Act)]),
+        "dconv_wt_elems": (i64, [P(Wt)]),
+        "dconv_pack_act": (i, [vp, i, P(Act), vp]),
+        "dconv_unpack_act": (i, [P(Act), vp, i, vp]),
+        "dconv_pack_wt": (i, [vp, i, P(Wt), vp]),
+        "dconv_unpack_wt": (i, [P(Wt), vp, i, vp]),
+        "dconv_transform_weight_dual": (i, [P(Wt), P(Wt), vp]),
+        "dconv_copy_with_halo": (i, [P(Act), P(Act), vp]),
+        "dconv_zero_halo": (i, [P(Act), vp]),
+        "dconv_apply_fused_op": (i, [P(Act), P(Fusion), vp]),
+        "dconv_fill_uniform_host": (None, [C.c_uint64, C.c_float, C.c_float, vp, i64]),
+        "dconv_fill_he_normal_host": (None, [C.c_uint64, C.c_float, vp, i64]),
+        "dconv_fwd_plan_create": (i, [P(Spec), P(Fusion), P(EngineCfg), i, i, i, P(vp)]),
+        "dconv_fwd_plan_destroy": (None, [vp]),
+        "dconv_fwd_plan_describe": (i, [vp, C.c_char_p, sz]),
+        "dconv_fwd_workspace_bytes": (sz, [vp]),
+        "dconv_forward": (i, [vp, P(Act), P(Wt), P(Act), vp, vp]),
+        "dconv_fwd_launches": (i, [vp]),
+        "dconv_bwd_plan_create": (i, [P(Spec), P(EngineCfg), i, P(vp)]),
+        "dconv_bwd_plan_destroy": (None, [vp]),
+        "dconv_bwd_route": (i, [vp]),
+        "dconv_bwd_plan_describe": (i, [vp, C.c_char_p, sz]),
+        "dconv_bwd_workspace_bytes": (sz, [vp]),
+        "dconv_backward_data": (i, [vp, P(Wt), P(Act), P(Act), vp, vp]),
+        "dconv_bwd_launches": (i, [vp]),
+        "dconv_upd_plan_create": (i, [P(Spec), P(EngineCfg), i, P(vp)]),
+        "dconv_upd_plan_destroy": (None, [vp]),
+        "dconv_upd_splits": (i, [vp]),
+        "dconv_upd_plan_describe": (i, [vp, C.c_char_p, sz]),
+        "dconv_upd_workspace_bytes": (sz, [vp, P(Act), P(Act)]),
+        "dconv_weight_update": (i, [vp, P(Act), P(Act), P(Wt), i, vp, vp]),
+        "dconv_upd_launches": (i, [vp, P(Act), P(Act)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = None
+
+
+def lib():
+    """Load libdconv_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc sm_100a) first")
+        _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib

@@ -1,0 +1,1377 @@
+// dconv_b200 C ABI implementation: plans (tile selection in place of the
+// reference's JIT / dryrun), TMA descriptor encoding, and launches of the
+// sm_100a kernels in kernels/*.cuh. See include/dconv_b200.h.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dconv_b200.h"
+#include "kernels/conv_fwd.cuh"
+#include "kernels/conv_upd.cuh"
+#include "kernels/layout.cuh"
+
+using namespace dconv_sm100;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(DCONV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return DCONV_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DCONV_ERR_CUDA;
+  }
+}
+
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ spec
+// layer_spec.cpp:7-18
+void validate_spec(const dconv_spec_t& s) {
+  if (s.N < 1 || s.C < 1 || s.K < 1 || s.H < 1 || s.W < 1 || s.R < 1 || s.S < 1)
+    fail(DCONV_ERR_INVALID_LAYER_SPEC, "all tensor extents must be >= 1");
+  if (s.stride < 1) fail(DCONV_ERR_INVALID_LAYER_SPEC, "stride must be >= 1");
+  if (s.pad_h < 0 || s.pad_w < 0) fail(DCONV_ERR_INVALID_LAYER_SPEC, "padding must be >= 0");
+  if (s.vlen < 1) fail(DCONV_ERR_INVALID_LAYER_SPEC, "vlen must be >= 1");
+  if (s.R > s.H + 2 * s.pad_h || s.S > s.W + 2 * s.pad_w)
+    fail(DCONV_ERR_NON_INTEGRAL_SHAPE, "filter exceeds padded input: R=" + std::to_string(s.R) +
+                                           " S=" + std::to_string(s.S) + " vs padded " +
+                                           std::to_string(s.H + 2 * s.pad_h) + "x" + std::to_string(s.W + 2 * s.pad_w));
+}
+int out_P(const dconv_spec_t& s) { return (s.H + 2 * s.pad_h - s.R) / s.stride + 1; }
+int out_Q(const dconv_spec_t& s) { return (s.W + 2 * s.pad_w - s.S) / s.stride + 1; }
+
+int64_t act_elems(const dconv_act_t& a) {
+  return static_cast<int64_t>(a.n) * cdiv(a.c, a.vlen) * (a.h + 2 * a.halo_h) * (a.w + 2 * a.halo_w) * a.vlen;
+}
+int64_t wt_elems(const dconv_wt_t& w) {
+  return static_cast<int64_t>(cdiv(w.k, w.vlen)) * cdiv(w.c, w.vlen) * w.r * w.s * w.vlen * w.vlen;
+}
+int esize(int dtype) { return dtype == DCONV_BF16 ? 2 : 4; }
+
+void check_dtype(int dt) {
+  if (dt != DCONV_F32 && dt != DCONV_BF16) fail(DCONV_ERR_INVALID_ARGUMENT, "dtype must be DCONV_F32 or DCONV_BF16");
+}
+void check_act(const dconv_act_t* a, const char* what) {
+  if (!a || !a->data) fail(DCONV_ERR_INVALID_ARGUMENT, std::string(what) + ": null activation");
+  check_dtype(a->dtype);
+  if (a->n < 1 || a->c < 1 || a->h < 1 || a->w < 1 || a->vlen < 1 || a->halo_h < 0 || a->halo_w < 0)
+    fail(DCONV_ERR_SHAPE_MISMATCH, std::string(what) + ": bad activation extents");
+  if (reinterpret_cast<uintptr_t>(a->data) % 16 != 0)
+    fail(DCONV_ERR_INVALID_ARGUMENT, std::string(what) + ": data must be 16-byte aligned");
+}
+void check_wt(const dconv_wt_t* w, const char* what) {
+  if (!w || !w->data) fail(DCONV_ERR_INVALID_ARGUMENT, std::string(what) + ": null weight");
+  check_dtype(w->dtype);
+  if (w->k < 1 || w->c < 1 || w->r < 1 || w->s < 1 || w->vlen < 1)
+    fail(DCONV_ERR_SHAPE_MISMATCH, std::string(what) + ": bad weight extents");
+}
+
+// ------------------------------------------------------------------ TMA encoding
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q), "cuTensorMapEncodeTiled");
+    if (q != cudaDriverEntryPointSuccess || !p) fail(DCONV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+CUtensorMap encode(int bf16, int rank, const void* base, const uint64_t* dims, const uint64_t* strides_bytes,
+                   const uint32_t* box, const uint32_t* estr, const char* what) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = estr ? estr[i] : 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  const CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 rank, const_cast<void*>(base), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(DCONV_ERR_CUDA, std::string("tensor map encode failed (") + what + ") code " +
+                                                  std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  }
+  return n;
+}
+
+constexpr int kSmemBudget = 227 * 1024 - 2048;  // dynamic smem per CTA (static barriers excluded)
+
+int grid1d(int64_t total, int block = 256) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv64(total, block), 148LL * 16)));
+}
+
+// ------------------------------------------------------------------ generic implicit-GEMM conv
+// The forward kernel's problem: a stride-`stride` correlation of an input
+// tensor with a phase-sorted tap list, written to an output surface.
+struct ConvProblem {
+  dconv_act_t in;  // input tensor (any halo)
+  int cb_red;      // reduction blocks (= in channel blocks)
+  int kb_out;      // output blocks
+  int P, Q;        // output extents
+  int R, S, stride;
+  int row_off, col_off;  // logical input coordinate of output (0,0), tap (0,0) (= -pad)
+};
+
+struct Taps {
+  int n_phases = 0;
+  int phase_row[kMaxPhases] = {}, phase_col[kMaxPhases] = {};
+  int phase_ntaps[kMaxPhases] = {}, phase_tap0[kMaxPhases] = {};
+  std::vector<int> r, s;  // phase-sorted original taps
+  std::vector<int> r2, s2;
+  int r2max = 0, s2max = 0, taps_box = 0;
+};
+
+// phase (a, b) holds taps r = a + stride*r2, s = b + stride*s2
+Taps phase_taps(int R, int S, int st) {
+  Taps t;
+  for (int a = 0; a < st; ++a)
+    for (int b = 0; b < st; ++b) {
+      std::vector<std::pair<int, int>> list;
+      for (int r = a; r < R; r += st)
+        for (int s = b; s < S; s += st) list.emplace_back(r, s);
+      if (list.empty()) continue;
+      if (t.n_phases >= kMaxPhases) fail(DCONV_ERR_UNSUPPORTED, "more than 4 stride phases (stride > 2)");
+      const int ph = t.n_phases++;
+      t.phase_row[ph] = a;
+      t.phase_col[ph] = b;
+      t.phase_tap0[ph] = static_cast<int>(t.r.size());
+      t.phase_ntaps[ph] = static_cast<int>(list.size());
+      t.taps_box = std::max(t.taps_box, static_cast<int>(list.size()));
+      for (auto& rs : list) {
+        t.r.push_back(rs.first);
+        t.s.push_back(rs.second);
+        t.r2.push_back(rs.first / st);
+        t.s2.push_back(rs.second / st);
+        t.r2max = std::max(t.r2max, rs.first / st);
+        t.s2max = std::max(t.s2max, rs.second / st);
+      }
+    }
+  if (static_cast<int>(t.r.size()) > kMaxTaps) fail(DCONV_ERR_UNSUPPORTED, "more than 64 filter taps");
+  return t;
+}
+
+struct FwdTile {
+  int mb = 1, nb = 1, stages = 2;
+};
+
+struct FwdLaunch {
+  FwdParams p;
+  CUtensorMap map_a, map_w;
+  dim3 grid;
+  int stages;
+  size_t smem;
+  bool raw_f32;
+  int pieces;
+};
+
+// Decide staging mode, tile and pipeline depth; encode TMA maps.
+FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* wprep, int pieces, int kb_prep,
+                          const dconv_engine_config_t* cfg) {
+  FwdLaunch L;
+  std::memset(&L.p, 0, sizeof(L.p));
+  FwdParams& p = L.p;
+  const dconv_act_t& in = pb.in;
+  const bool raw_f32 = in.dtype == DCONV_F32;
+  if (!raw_f32 && pieces == 3)
+    fail(DCONV_ERR_UNSUPPORTED, "fp32-accurate math needs fp32 activations (got bf16)");
+  L.raw_f32 = raw_f32;
+  L.pieces = pieces;
+  const int st = pb.stride;
+  const int hp = in.h + 2 * in.halo_h, wp = in.w + 2 * in.halo_w;
+  p.n_img = in.n;
+  p.in_cb = cdiv(in.c, 16);
+  p.cb_in = pb.cb_red;
+  p.kb_out = pb.kb_out;
+  p.P = pb.P;
+  p.Q = pb.Q;
+  p.stride = st;
+  p.n_phases = taps.n_phases;
+  for (int i = 0; i < taps.n_phases; ++i) {
+    p.phase_row[i] = taps.phase_row[i];
+    p.phase_col[i] = taps.phase_col[i];
+    p.phase_ntaps[i] = taps.phase_ntaps[i];
+    p.phase_tap0[i] = taps.phase_tap0[i];
+  }
+  p.taps_box = taps.taps_box;
+  // linear mode: the halo'd physical plane is the virtual grid
+  const bool linear = st == 1 && -pb.row_off == in.halo_h && -pb.col_off == in.halo_w;
+  p.linear = linear ? 1 : 0;
+  p.wsub = linear ? wp : pb.Q + taps.s2max;
+  p.in_row0 = pb.row_off;
+  p.in_col0 = pb.col_off;
+  for (size_t t = 0; t < taps.r.size(); ++t) p.tap_shift[t] = taps.r2[t] * p.wsub + taps.s2[t];
+  const int maxshift = taps.r2max * p.wsub + taps.s2max;
+
+  FwdTile tile;
+  const int kb_total = pb.kb_out;
+  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : 0;
+  const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16) : 0;
+  FwdStage layout;
+  int a_px = 0, lin_boxes = 0;
+  bool found = false;
+  // widest N tile first (fewer A re-reads), then the largest M tile whose
+  // stage fits >= 3 deep (>= 2 as a last resort)
+  for (int min_stages : {3, 2}) {
+    for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
+      const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
+      for (int mb : {2, 1}) {
+        if (want_mb && mb != want_mb) continue;
+        if (mb * 16 * nb > 512) continue;
+        const int Lpx = 128 * mb;
+        int apx, lb = 0;
+        if (linear) {
+          lb = cdiv(Lpx + maxshift, 128);
+          apx = lb * 128;
+        } else {
+          const int rows_box = (p.wsub + Lpx - 2 + maxshift) / p.wsub + 1;
+          if (p.wsub * st > 256 || rows_box * st > 256) continue;
+          apx = rows_box * p.wsub;
+        }
+        const FwdStage lay = fwd_stage_layout(apx, taps.taps_box, nb, pieces, raw_f32);
+        const int stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
+        if (stages < min_stages) continue;
+        tile.mb = mb;
+        tile.nb = nb;
+        tile.stages = (cfg && cfg->stages > 0) ? std::min(cfg->stages, stages) : stages;
+        layout = lay;
+        a_px = apx;
+        lin_boxes = lb;
+        found = true;
+        break;
+      }
+      if (want_nb || nb == 1) break;
+    }
+    if (found) break;
+  }
+  if (!found) fail(DCONV_ERR_PLAN_INFEASIBLE, "no forward tile fits shared memory / TMA box limits");
+  p.mb = tile.mb;
+  p.nb = tile.nb;
+  p.a_px = a_px;
+  p.lin_boxes = lin_boxes;
+  p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
+  L.stages = tile.stages;
+  L.smem = static_cast<size_t>(tile.stages) * layout.bytes;
+  L.grid = dim3(static_cast<unsigned>(in.n * p.tiles_per_img), static_cast<unsigned>(cdiv(kb_total, tile.nb)), 1);
+
+  // activation map
+  const int e = raw_f32 ? 4 : 8;             // elements per 16B
+  const int nch = raw_f32 ? 4 : 2;           // 16B chunks per pixel (vlen 16)
+  const uint64_t pix = raw_f32 ? 64 : 32;    // bytes per pixel
+  const uint64_t planes = static_cast<uint64_t>(in.n) * p.in_cb;
+  if (linear) {
+    const uint64_t dims[4] = {static_cast<uint64_t>(e), static_cast<uint64_t>(hp) * wp, static_cast<uint64_t>(nch),
+                              planes};
+    const uint64_t strides[3] = {pix, 16, pix * hp * wp};
+    const uint32_t box[4] = {static_cast<uint32_t>(e), 128, 1, 1};
+    L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation linear");
+  } else {
+    const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * pix;
+    const uint64_t dims[5] = {static_cast<uint64_t>(e), static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h),
+                              static_cast<uint64_t>(nch), planes};
+    const uint64_t strides[4] = {pix, pix * wp, 16, pix * wp * hp};
+    const uint32_t box[5] = {static_cast<uint32_t>(e), static_cast<uint32_t>(p.wsub * st),
+                             static_cast<uint32_t>((a_px / p.wsub) * st), static_cast<uint32_t>(nch), 1};
+    const uint32_t estr[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};
+    L.map_a = encode(!raw_f32, 5, base, dims, strides, box, estr, "activation rows");
+  }
+  // prepared weights [(pc*cb_red + cb)][t][2*kb_prep][16][8] bf16
+  {
+    const int T = static_cast<int>(taps.r.size());
+    const uint64_t dims[5] = {8, 16, static_cast<uint64_t>(2 * kb_prep), static_cast<uint64_t>(T),
+                              static_cast<uint64_t>(pieces) * pb.cb_red};
+    const uint64_t strides[4] = {16, 256, static_cast<uint64_t>(2 * kb_prep) * 256,
+                                 static_cast<uint64_t>(T) * 2 * kb_prep * 256};
+    const uint32_t box[5] = {8, 16, static_cast<uint32_t>(2 * tile.nb), static_cast<uint32_t>(taps.taps_box), 1};
+    L.map_w = encode(1, 5, wprep, dims, strides, box, nullptr, "prepared weights");
+  }
+  return L;
+}
+
+void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
+  auto go = [&](auto kern) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
+               "smem attribute");
+    kern<<<L.grid, kFwdThreads, L.smem, stream>>>(L.map_a, L.map_w, L.p, L.stages);
+  };
+  if (L.raw_f32) {
+    if (L.pieces == 3)
+      go(conv_fwd_kernel<true, 3>);
+    else
+      go(conv_fwd_kernel<true, 1>);
+  } else {
+    go(conv_fwd_kernel<false, 1>);
+  }
+  cuda_check(cudaGetLastError(), "conv_fwd_kernel launch");
+}
+
+// weight prep: src blocked weights -> bf16 pieces in the phase-sorted tap order
+// (tapmap_dev is uploaded once at plan creation so execute calls are graph-capturable)
+void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int kb_out,
+                        int dual, int pieces, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(cb_in) * n_taps * 2 * kb_out * 128;
+  const int kbs = cdiv(w.k, 16), cbs = cdiv(w.c, 16);
+  if (w.dtype == DCONV_F32)
+    weight_prep_kernel<float><<<grid1d(total), 256, 0, stream>>>(
+        reinterpret_cast<const float*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
+        tapmap_dev, n_taps, cb_in, kb_out, dual, pieces);
+  else
+    weight_prep_kernel<__nv_bfloat16><<<grid1d(total), 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
+        tapmap_dev, n_taps, cb_in, kb_out, dual, pieces);
+  cuda_check(cudaGetLastError(), "weight_prep launch");
+}
+
+size_t prep_bytes(int pieces, int cb_in, int taps, int kb_out) {
+  return static_cast<size_t>(pieces) * cb_in * taps * 2 * kb_out * 256;
+}
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+std::string json_tile(const FwdLaunch& L) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf),
+                "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u],"
+                "\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d}",
+                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.smem, L.grid.x, L.grid.y,
+                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px);
+  return buf;
+}
+
+int math_pieces(int math) {
+  if (math == DCONV_MATH_F32) return 3;
+  if (math == DCONV_MATH_BF16) return 1;
+  fail(DCONV_ERR_INVALID_ARGUMENT, "math must be DCONV_MATH_F32 or DCONV_MATH_BF16");
+}
+
+void copy_out(const std::string& s, char* buf, size_t len) {
+  if (!buf || len == 0) return;
+  const size_t n = std::min(len - 1, s.size());
+  std::memcpy(buf, s.data(), n);
+  buf[n] = 0;
+}
+
+}  // namespace
+
+// ====================================================================== plans
+struct dconv_fwd_plan {
+  dconv_spec_t spec;
+  int math, pieces;
+  int fuse_kind;
+  float* bias_dev = nullptr;  // kb*16 lanes, tail zero (plan.bias_lanes analog)
+  int out_halo_h, out_halo_w;
+  dconv_engine_config_t cfg;
+  bool has_cfg;
+  Taps taps;
+  int* tapmap_dev = nullptr;
+  std::string last_desc;
+};
+
+struct BwdPhase {
+  int a, b;            // output phase of dI
+  bool zero;           // no taps: lattice is zero
+  ConvProblem pb;      // stride-1 sub-problem (input dO)
+  Taps taps;           // single phase
+  std::vector<int> tapmap;  // prepared tap -> source r*S+s
+  size_t ws_off;
+};
+
+struct dconv_bwd_plan {
+  dconv_spec_t spec;
+  int math, pieces;
+  int route;
+  dconv_engine_config_t cfg;
+  bool has_cfg;
+  std::vector<BwdPhase> phases;
+  int* tapmap_dev = nullptr;  // concatenated tap maps
+  size_t ws_bytes = 0;
+  std::string last_desc;
+};
+
+struct dconv_upd_plan {
+  dconv_spec_t spec;
+  int math, pieces;
+  dconv_engine_config_t cfg;
+  bool has_cfg;
+  Taps taps;
+  std::string last_desc;
+};
+
+extern "C" {
+
+const char* dconv_last_error(void) { return g_err.c_str(); }
+
+const char* dconv_status_string(int s) {
+  switch (s) {
+    case DCONV_OK: return "ok";
+    case DCONV_ERR_NON_INTEGRAL_SHAPE: return "NonIntegralShape";
+    case DCONV_ERR_INVALID_LAYER_SPEC: return "InvalidLayerSpec";
+    case DCONV_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case DCONV_ERR_INVALID_DESCRIPTOR: return "InvalidDescriptor";
+    case DCONV_ERR_OVERFLOW_RISK: return "OverflowRisk";
+    case DCONV_ERR_PLAN_INFEASIBLE: return "PlanInfeasible";
+    case DCONV_ERR_EMPTY_TRACE: return "EmptyTrace";
+    case DCONV_ERR_PLAN_TENSOR_MISMATCH: return "PlanTensorMismatch";
+    case DCONV_ERR_INFEASIBLE_STRATEGY: return "InfeasibleStrategy";
+    case DCONV_ERR_CHAIN_SHAPE_MISMATCH: return "ChainShapeMismatch";
+    case DCONV_ERR_PARSE: return "ParseError";
+    case DCONV_ERR_CUDA: return "CudaError";
+    case DCONV_ERR_UNSUPPORTED: return "Unsupported";
+    case DCONV_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    default: return "unknown";
+  }
+}
+
+int dconv_version(void) { return 100; }
+
+void dconv_engine_config_default(dconv_engine_config_t* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->min_accumulators = 8;
+  c->max_accumulators = 28;
+  c->cache_budget_bytes = 512 * 1024;
+  c->prefetch_lookahead = 1;
+  c->prefetch_enabled = 1;
+  c->streaming_stores = 0;
+  c->acc_chain_limit = 512;
+  c->i16_bound_in = 256;
+  c->i16_bound_wt = 256;
+}
+
+int dconv_make_spec(int N, int C, int K, int H, int W, int R, int S, int stride, int pad_h, int pad_w, int vlen,
+                    dconv_spec_t* out) {
+  return guarded([&] {
+    if (!out) fail(DCONV_ERR_INVALID_ARGUMENT, "null spec");
+    if (pad_h < 0) pad_h = (R % 2 == 1) ? (R - 1) / 2 : 0;
+    if (pad_w < 0) pad_w = (S % 2 == 1) ? (S - 1) / 2 : 0;
+    dconv_spec_t s = {N, C, K, H, W, R, S, stride, pad_h, pad_w, vlen};
+    *out = s;
+    validate_spec(s);
+  });
+}
+
+int dconv_spec_validate(const dconv_spec_t* spec) {
+  return guarded([&] {
+    if (!spec) fail(DCONV_ERR_INVALID_ARGUMENT, "null spec");
+    validate_spec(*spec);
+  });
+}
+
+int dconv_output_shape(const dconv_spec_t* spec, int* P, int* Q) {
+  return guarded([&] {
+    if (!spec || !P || !Q) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
+    validate_spec(*spec);
+    *P = out_P(*spec);
+    *Q = out_Q(*spec);
+  });
+}
+
+int64_t dconv_pass_flops(const dconv_spec_t* s) {
+  if (!s || dconv_spec_validate(s) != DCONV_OK) return -1;
+  return 2LL * s->N * s->K * s->C * out_P(*s) * out_Q(*s) * s->R * s->S;
+}
+
+int64_t dconv_act_elems(const dconv_act_t* a) { return a ? act_elems(*a) : -1; }
+int64_t dconv_wt_elems(const dconv_wt_t* w) { return w ? wt_elems(*w) : -1; }
+
+// ------------------------------------------------------------------ layouts
+int dconv_pack_act(const void* nchw, int src_dtype, const dconv_act_t* dst, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(dst, "pack_act dst");
+    check_dtype(src_dtype);
+    if (!nchw) fail(DCONV_ERR_INVALID_ARGUMENT, "pack_act: null source");
+    const dconv_act_t& d = *dst;
+    const int g = grid1d(act_elems(d));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (src_dtype == DCONV_F32 && d.dtype == DCONV_F32)
+      pack_act_kernel<float, float><<<g, 256, 0, s>>>((const float*)nchw, (float*)d.data, d.n, d.c, d.h, d.w, d.vlen,
+                                                      d.halo_h, d.halo_w);
+    else if (src_dtype == DCONV_F32)
+      pack_act_kernel<float, __nv_bfloat16><<<g, 256, 0, s>>>((const float*)nchw, (__nv_bfloat16*)d.data, d.n, d.c,
+                                                              d.h, d.w, d.vlen, d.halo_h, d.halo_w);
+    else if (d.dtype == DCONV_F32)
+      pack_act_kernel<__nv_bfloat16, float><<<g, 256, 0, s>>>((const __nv_bfloat16*)nchw, (float*)d.data, d.n, d.c,
+                                                              d.h, d.w, d.vlen, d.halo_h, d.halo_w);
+    else
+      pack_act_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>(
+          (const __nv_bfloat16*)nchw, (__nv_bfloat16*)d.data, d.n, d.c, d.h, d.w, d.vlen, d.halo_h, d.halo_w);
+    cuda_check(cudaGetLastError(), "pack_act");
+  });
+}
+
+int dconv_unpack_act(const dconv_act_t* src, void* nchw, int dst_dtype, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(src, "unpack_act src");
+    check_dtype(dst_dtype);
+    if (!nchw) fail(DCONV_ERR_INVALID_ARGUMENT, "unpack_act: null destination");
+    const dconv_act_t& a = *src;
+    const int g = grid1d(static_cast<int64_t>(a.n) * a.c * a.h * a.w);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (a.dtype == DCONV_F32 && dst_dtype == DCONV_F32)
+      unpack_act_kernel<float, float><<<g, 256, 0, s>>>((const float*)a.data, (float*)nchw, a.n, a.c, a.h, a.w, a.vlen,
+                                                        a.halo_h, a.halo_w);
+    else if (a.dtype == DCONV_F32)
+      unpack_act_kernel<float, __nv_bfloat16><<<g, 256, 0, s>>>((const float*)a.data, (__nv_bfloat16*)nchw, a.n, a.c,
+                                                                a.h, a.w, a.vlen, a.halo_h, a.halo_w);
+    else if (dst_dtype == DCONV_F32)
+      unpack_act_kernel<__nv_bfloat16, float><<<g, 256, 0, s>>>((const __nv_bfloat16*)a.data, (float*)nchw, a.n, a.c,
+                                                                a.h, a.w, a.vlen, a.halo_h, a.halo_w);
+    else
+      unpack_act_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>(
+          (const __nv_bfloat16*)a.data, (__nv_bfloat16*)nchw, a.n, a.c, a.h, a.w, a.vlen, a.halo_h, a.halo_w);
+    cuda_check(cudaGetLastError(), "unpack_act");
+  });
+}
+
+int dconv_pack_wt(const void* kcrs, int src_dtype, const dconv_wt_t* dst, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(dst, "pack_wt dst");
+    check_dtype(src_dtype);
+    if (!kcrs) fail(DCONV_ERR_INVALID_ARGUMENT, "pack_wt: null source");
+    const dconv_wt_t& d = *dst;
+    const int g = grid1d(wt_elems(d));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (src_dtype == DCONV_F32 && d.dtype == DCONV_F32)
+      pack_wt_kernel<float, float><<<g, 256, 0, s>>>((const float*)kcrs, (float*)d.data, d.k, d.c, d.r, d.s, d.vlen);
+    else if (src_dtype == DCONV_F32)
+      pack_wt_kernel<float, __nv_bfloat16><<<g, 256, 0, s>>>((const float*)kcrs, (__nv_bfloat16*)d.data, d.k, d.c,
+                                                             d.r, d.s, d.vlen);
+    else if (d.dtype == DCONV_F32)
+      pack_wt_kernel<__nv_bfloat16, float><<<g, 256, 0, s>>>((const __nv_bfloat16*)kcrs, (float*)d.data, d.k, d.c,
+                                                             d.r, d.s, d.vlen);
+    else
+      pack_wt_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>((const __nv_bfloat16*)kcrs,
+                                                                     (__nv_bfloat16*)d.data, d.k, d.c, d.r, d.s,
+                                                                     d.vlen);
+    cuda_check(cudaGetLastError(), "pack_wt");
+  });
+}
+
+int dconv_unpack_wt(const dconv_wt_t* src, void* kcrs, int dst_dtype, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(src, "unpack_wt src");
+    check_dtype(dst_dtype);
+    if (!kcrs) fail(DCONV_ERR_INVALID_ARGUMENT, "unpack_wt: null destination");
+    const dconv_wt_t& w = *src;
+    const int g = grid1d(static_cast<int64_t>(w.k) * w.c * w.r * w.s);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (w.dtype == DCONV_F32 && dst_dtype == DCONV_F32)
+      unpack_wt_kernel<float, float><<<g, 256, 0, s>>>((const float*)w.data, (float*)kcrs, w.k, w.c, w.r, w.s, w.vlen);
+    else if (w.dtype == DCONV_F32)
+      unpack_wt_kernel<float, __nv_bfloat16><<<g, 256, 0, s>>>((const float*)w.data, (__nv_bfloat16*)kcrs, w.k, w.c,
+                                                               w.r, w.s, w.vlen);
+    else if (dst_dtype == DCONV_F32)
+      unpack_wt_kernel<__nv_bfloat16, float><<<g, 256, 0, s>>>((const __nv_bfloat16*)w.data, (float*)kcrs, w.k, w.c,
+                                                               w.r, w.s, w.vlen);
+    else
+      unpack_wt_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>(
+          (const __nv_bfloat16*)w.data, (__nv_bfloat16*)kcrs, w.k, w.c, w.r, w.s, w.vlen);
+    cuda_check(cudaGetLastError(), "unpack_wt");
+  });
+}
+
+int dconv_transform_weight_dual(const dconv_wt_t* src, const dconv_wt_t* dst, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(src, "transform src");
+    check_wt(dst, "transform dst");
+    const dconv_wt_t& a = *src;
+    const dconv_wt_t& b = *dst;
+    if (b.k != a.c || b.c != a.k || b.r != a.r || b.s != a.s || b.vlen != a.vlen || b.dtype != a.dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "transform_weight_dual: dst must be (k=src.c, c=src.k, same r, s, vlen, dtype)");
+    const int g = grid1d(wt_elems(b));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (a.dtype == DCONV_F32)
+      dual_wt_kernel<float><<<g, 256, 0, s>>>((const float*)a.data, (float*)b.data, a.k, a.c, a.r, a.s, a.vlen);
+    else
+      dual_wt_kernel<__nv_bfloat16><<<g, 256, 0, s>>>((const __nv_bfloat16*)a.data, (__nv_bfloat16*)b.data, a.k, a.c,
+                                                      a.r, a.s, a.vlen);
+    cuda_check(cudaGetLastError(), "dual_wt");
+  });
+}
+
+int dconv_copy_with_halo(const dconv_act_t* src, const dconv_act_t* dst, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(src, "copy_with_halo src");
+    check_act(dst, "copy_with_halo dst");
+    const dconv_act_t& a = *src;
+    const dconv_act_t& b = *dst;
+    if (a.n != b.n || a.c != b.c || a.h != b.h || a.w != b.w || a.vlen != b.vlen || a.dtype != b.dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "copy_with_halo: tensors differ beyond the halo");
+    const int g = grid1d(act_elems(b));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int cb = cdiv(a.c, a.vlen);
+    if (a.dtype == DCONV_F32)
+      rehalo_kernel<float><<<g, 256, 0, s>>>((const float*)a.data, (float*)b.data, a.n, cb, a.h, a.w, a.vlen,
+                                             a.halo_h, a.halo_w, b.halo_h, b.halo_w);
+    else
+      rehalo_kernel<__nv_bfloat16><<<g, 256, 0, s>>>((const __nv_bfloat16*)a.data, (__nv_bfloat16*)b.data, a.n, cb,
+                                                     a.h, a.w, a.vlen, a.halo_h, a.halo_w, b.halo_h, b.halo_w);
+    cuda_check(cudaGetLastError(), "rehalo");
+  });
+}
+
+int dconv_zero_halo(const dconv_act_t* act, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(act, "zero_halo");
+    const dconv_act_t& a = *act;
+    if (a.halo_h == 0 && a.halo_w == 0) return;
+    const int planes = a.n * cdiv(a.c, a.vlen);
+    const int64_t frame = (static_cast<int64_t>(a.h + 2 * a.halo_h) * (a.w + 2 * a.halo_w) -
+                           static_cast<int64_t>(a.h) * a.w);
+    const int g = grid1d(planes * frame * a.vlen);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (a.dtype == DCONV_F32)
+      zero_halo_kernel<float><<<g, 256, 0, s>>>((float*)a.data, planes, a.h, a.w, a.halo_h, a.halo_w, a.vlen);
+    else
+      zero_halo_kernel<__nv_bfloat16><<<g, 256, 0, s>>>((__nv_bfloat16*)a.data, planes, a.h, a.w, a.halo_h, a.halo_w,
+                                                        a.vlen);
+    cuda_check(cudaGetLastError(), "zero_halo");
+  });
+}
+
+}  // extern "C"
+
+namespace {
+template <typename T>
+__global__ void apply_op_kernel(T* __restrict__ d, int planes_n, int cb, int h, int w, int hh, int hw, int v,
+                                int kind, const float* __restrict__ bias) {
+  const int hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long total = static_cast<long long>(planes_n) * cb * h * w * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % v);
+    long long q = e / v;
+    const int x = static_cast<int>(q % w);
+    q /= w;
+    const int y = static_cast<int>(q % h);
+    q /= h;
+    const int b = static_cast<int>(q % cb);
+    const long long plane = q;  // n*cb + b
+    T* px = d + ((plane * hp + y + hh) * wp + x + hw) * v + lane;
+    float val = to_f<T>(*px);
+    if (kind != DCONV_FUSE_RELU) val += bias[b * v + lane];
+    if (kind != DCONV_FUSE_BIAS_ADD) val = val > 0.0f ? val : 0.0f;
+    *px = from_f<T>(val);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int dconv_apply_fused_op(const dconv_act_t* act, const dconv_fusion_t* op, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(act, "apply_fused_op");
+    if (!op || op->kind < DCONV_FUSE_RELU || op->kind > DCONV_FUSE_BIAS_RELU)
+      fail(DCONV_ERR_INVALID_ARGUMENT, "apply_fused_op: bad op");
+    const dconv_act_t& a = *act;
+    const int cb = cdiv(a.c, a.vlen);
+    float* bias_dev = nullptr;
+    if (op->kind != DCONV_FUSE_RELU) {
+      if (!op->bias || op->bias_len != a.c) fail(DCONV_ERR_SHAPE_MISMATCH, "apply_fused_op: bias length must equal channels");
+      std::vector<float> lanes(static_cast<size_t>(cb) * a.vlen, 0.0f);
+      std::copy(op->bias, op->bias + a.c, lanes.begin());
+      cuda_check(cudaMalloc(&bias_dev, lanes.size() * sizeof(float)), "bias alloc");
+      cuda_check(cudaMemcpy(bias_dev, lanes.data(), lanes.size() * sizeof(float), cudaMemcpyHostToDevice), "bias copy");
+    }
+    const int g = grid1d(static_cast<int64_t>(a.n) * cb * a.h * a.w * a.vlen);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (a.dtype == DCONV_F32)
+      apply_op_kernel<float><<<g, 256, 0, s>>>((float*)a.data, a.n, cb, a.h, a.w, a.halo_h, a.halo_w, a.vlen, op->kind,
+                                               bias_dev);
+    else
+      apply_op_kernel<__nv_bfloat16><<<g, 256, 0, s>>>((__nv_bfloat16*)a.data, a.n, cb, a.h, a.w, a.halo_h, a.halo_w,
+                                                       a.vlen, op->kind, bias_dev);
+    cuda_check(cudaGetLastError(), "apply_fused_op");
+    if (bias_dev) {
+      cuda_check(cudaStreamSynchronize(s), "apply_fused_op sync");
+      cudaFree(bias_dev);
+    }
+  });
+}
+
+// splitmix64 (util.hpp:46-52) uniform / He-normal generators, host side
+static uint64_t splitmix(uint64_t& st) {
+  st += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = st;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+void dconv_fill_uniform_host(uint64_t seed, float lo, float hi, float* out, int64_t n) {
+  uint64_t st = seed;
+  for (int64_t i = 0; i < n; ++i) {
+    const float u = static_cast<float>(splitmix(st) >> 40) * (1.0f / 16777216.0f);
+    out[i] = lo + (hi - lo) * u;
+  }
+}
+void dconv_fill_he_normal_host(uint64_t seed, float stddev, float* out, int64_t n) {
+  uint64_t st = seed;
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int64_t i = 0; i < n; ++i) {
+    const double u1 = static_cast<double>((splitmix(st) >> 11) + 1) * (1.0 / 9007199254740992.0);
+    const double u2 = static_cast<double>(splitmix(st) >> 11) * (1.0 / 9007199254740992.0);
+    out[i] = static_cast<float>(std::sqrt(-2.0 * std::log(u1)) * std::cos(two_pi * u2) * static_cast<double>(stddev));
+  }
+}
+
+// ------------------------------------------------------------------ forward
+int dconv_fwd_plan_create(const dconv_spec_t* spec, const dconv_fusion_t* fusion, const dconv_engine_config_t* cfg,
+                          int math, int out_halo_h, int out_halo_w, dconv_fwd_plan_t* plan) {
+  dconv_fwd_plan* pl = nullptr;
+  const int st = guarded([&] {
+    if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
+    validate_spec(*spec);
+    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
+    if (out_halo_h < 0 || out_halo_w < 0) fail(DCONV_ERR_INVALID_LAYER_SPEC, "output halo must be >= 0");
+    pl = new dconv_fwd_plan();
+    pl->spec = *spec;
+    pl->math = math;
+    pl->pieces = math_pieces(math);
+    pl->fuse_kind = fusion ? fusion->kind : DCONV_FUSE_NONE;
+    pl->out_halo_h = out_halo_h;
+    pl->out_halo_w = out_halo_w;
+    pl->has_cfg = cfg != nullptr;
+    if (cfg) pl->cfg = *cfg;
+    pl->taps = phase_taps(spec->R, spec->S, spec->stride);
+    if (pl->fuse_kind != DCONV_FUSE_NONE) {
+      if (pl->fuse_kind < DCONV_FUSE_RELU || pl->fuse_kind > DCONV_FUSE_BIAS_RELU)
+        fail(DCONV_ERR_INVALID_ARGUMENT, "bad fusion kind");
+      const int kb = cdiv(spec->K, 16);
+      std::vector<float> lanes(static_cast<size_t>(kb) * 16, 0.0f);
+      if (pl->fuse_kind != DCONV_FUSE_RELU) {
+        if (!fusion->bias || fusion->bias_len != spec->K)
+          fail(DCONV_ERR_SHAPE_MISMATCH, "apply_fused_op: bias length must equal channels");
+        std::copy(fusion->bias, fusion->bias + spec->K, lanes.begin());
+      }
+      cuda_check(cudaMalloc(&pl->bias_dev, lanes.size() * sizeof(float)), "bias alloc");
+      cuda_check(cudaMemcpy(pl->bias_dev, lanes.data(), lanes.size() * sizeof(float), cudaMemcpyHostToDevice),
+                 "bias upload");
+    }
+    cuda_check(cudaMalloc(&pl->tapmap_dev, kMaxTaps * sizeof(int)), "tapmap alloc");
+    std::vector<int> tapmap;
+    for (size_t t = 0; t < pl->taps.r.size(); ++t) tapmap.push_back(pl->taps.r[t] * spec->S + pl->taps.s[t]);
+    cuda_check(cudaMemcpy(pl->tapmap_dev, tapmap.data(), tapmap.size() * sizeof(int), cudaMemcpyHostToDevice),
+               "tapmap upload");
+    *plan = pl;
+  });
+  if (st != DCONV_OK && pl) {
+    if (pl->bias_dev) cudaFree(pl->bias_dev);
+    if (pl->tapmap_dev) cudaFree(pl->tapmap_dev);
+    delete pl;
+  }
+  return st;
+}
+
+void dconv_fwd_plan_destroy(dconv_fwd_plan_t plan) {
+  if (!plan) return;
+  if (plan->bias_dev) cudaFree(plan->bias_dev);
+  if (plan->tapmap_dev) cudaFree(plan->tapmap_dev);
+  delete plan;
+}
+
+size_t dconv_fwd_workspace_bytes(dconv_fwd_plan_t plan) {
+  if (!plan) return 0;
+  const dconv_spec_t& s = plan->spec;
+  return align256(prep_bytes(plan->pieces, cdiv(s.C, 16), s.R * s.S, cdiv(s.K, 16)));
+}
+
+int dconv_fwd_plan_describe(dconv_fwd_plan_t plan, char* buf, size_t len) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
+             len);
+  });
+}
+
+int dconv_fwd_launches(dconv_fwd_plan_t plan) { return plan ? 2 : 0; }
+
+int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
+                  void* workspace, dconv_stream_t stream) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    check_act(in, "forward input");
+    check_wt(wt, "forward weight");
+    check_act(out, "forward output");
+    if (!workspace) fail(DCONV_ERR_INVALID_ARGUMENT, "forward: null workspace");
+    const dconv_spec_t& s = plan->spec;
+    const int P = out_P(s), Q = out_Q(s);
+    // propagation.cpp:12-19 check_forward_tensors
+    if (in->n != s.N || in->c != s.C || in->h != s.H || in->w != s.W || in->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "forward: input does not match the layer spec");
+    if (wt->k != s.K || wt->c != s.C || wt->r != s.R || wt->s != s.S || wt->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "forward: weight does not match the layer spec");
+    if (out->n != s.N || out->c != s.K || out->h != P || out->w != Q || out->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "forward: output does not match the layer spec");
+    if (out->halo_h != plan->out_halo_h || out->halo_w != plan->out_halo_w)
+      fail(DCONV_ERR_PLAN_TENSOR_MISMATCH, "forward: output halo differs from the plan's output surface");
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
+    // weights -> bf16 pieces, phase-sorted taps
+    launch_weight_prep(*wt, static_cast<int>(plan->taps.r.size()), plan->tapmap_dev, workspace, cb, kb, 0,
+                       plan->pieces, cs);
+    ConvProblem pb;
+    pb.in = *in;
+    pb.cb_red = cb;
+    pb.kb_out = kb;
+    pb.P = P;
+    pb.Q = Q;
+    pb.R = s.R;
+    pb.S = s.S;
+    pb.stride = s.stride;
+    pb.row_off = -s.pad_h;
+    pb.col_off = -s.pad_w;
+    FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, kb, plan->has_cfg ? &plan->cfg : nullptr);
+    FwdParams& p = L.p;
+    p.out = out->data;
+    p.out_bf16 = out->dtype == DCONV_BF16;
+    p.out_cb = kb;
+    p.out_hp = P + 2 * out->halo_h;
+    p.out_wp = Q + 2 * out->halo_w;
+    p.out_y0 = out->halo_h;
+    p.out_x0 = out->halo_w;
+    p.out_scale = 1;
+    p.out_halo_h = out->halo_h;
+    p.out_halo_w = out->halo_w;
+    p.bias = (plan->fuse_kind == DCONV_FUSE_BIAS_ADD || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? plan->bias_dev
+                                                                                                  : nullptr;
+    p.relu = (plan->fuse_kind == DCONV_FUSE_RELU || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? 1 : 0;
+    launch_fwd(L, cs);
+    plan->last_desc = json_tile(L);
+  });
+}
+
+// ------------------------------------------------------------------ backward-data
+// propagation.cpp:35-40
+static int choose_route(const dconv_spec_t& s) {
+  if (s.stride == 1 && s.pad_h <= s.R - 1 && s.pad_w <= s.S - 1) return DCONV_BWD_DUALITY_STRIDE1;
+  if (s.R == 1 && s.S == 1) return DCONV_BWD_DUALITY_1x1;
+  return DCONV_BWD_GENERIC;
+}
+
+int dconv_bwd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t* cfg, int math,
+                          dconv_bwd_plan_t* plan) {
+  dconv_bwd_plan* pl = nullptr;
+  const int st = guarded([&] {
+    if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
+    validate_spec(*spec);
+    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
+    pl = new dconv_bwd_plan();
+    pl->spec = *spec;
+    pl->math = math;
+    pl->pieces = math_pieces(math);
+    pl->route = choose_route(*spec);
+    pl->has_cfg = cfg != nullptr;
+    if (cfg) pl->cfg = *cfg;
+    const dconv_spec_t& s = *spec;
+    const int P = out_P(s), Q = out_Q(s);
+    const int kb = cdiv(s.K, 16), cb = cdiv(s.C, 16);
+    const int stv = s.stride;
+    // Stride-phase decomposition of dI: phase (a, b) of dI is a stride-1
+    // correlation of dO with the flipped sub-filter W[a' + st*r2][b' + st*s2].
+    // Stride 1 degenerates to the single dual phase (DUALITY_STRIDE1).
+    size_t off = 0;
+    for (int a = 0; a < stv; ++a)
+      for (int b = 0; b < stv; ++b) {
+        BwdPhase ph;
+        ph.a = a;
+        ph.b = b;
+        const int ap = (a + s.pad_h) % stv, bp = (b + s.pad_w) % stv;
+        const int offa = (a + s.pad_h - ap) / stv, offb = (b + s.pad_w - bp) / stv;
+        const int R2 = ap < s.R ? cdiv(s.R - ap, stv) : 0;
+        const int S2 = bp < s.S ? cdiv(s.S - bp, stv) : 0;
+        const int ly = a < s.H ? cdiv(s.H - a, stv) : 0, lx = b < s.W ? cdiv(s.W - b, stv) : 0;
+        ph.zero = R2 == 0 || S2 == 0;
+        if (ly == 0 || lx == 0) continue;
+        ph.pb.cb_red = kb;
+        ph.pb.kb_out = cb;
+        ph.pb.P = ly;
+        ph.pb.Q = lx;
+        ph.pb.R = R2;
+        ph.pb.S = S2;
+        ph.pb.stride = 1;
+        ph.pb.row_off = offa - (R2 - 1);
+        ph.pb.col_off = offb - (S2 - 1);
+        ph.ws_off = off;
+        if (!ph.zero) {
+          ph.taps = phase_taps(R2, S2, 1);
+          for (size_t t = 0; t < ph.taps.r.size(); ++t) {
+            const int u = ph.taps.r[t], w = ph.taps.s[t];  // prepared tap (u, w) <- source tap, flipped
+            const int r = ap + stv * (R2 - 1 - u), sc = bp + stv * (S2 - 1 - w);
+            ph.tapmap.push_back(r * s.S + sc);
+          }
+          off += align256(prep_bytes(pl->pieces, kb, static_cast<int>(ph.tapmap.size()), cb));
+        }
+        pl->phases.push_back(ph);
+      }
+    pl->ws_bytes = off;
+    (void)P;
+    (void)Q;
+    std::vector<int> all;
+    for (auto& ph : pl->phases) all.insert(all.end(), ph.tapmap.begin(), ph.tapmap.end());
+    cuda_check(cudaMalloc(&pl->tapmap_dev, std::max<size_t>(1, all.size()) * sizeof(int)), "tapmap alloc");
+    if (!all.empty())
+      cuda_check(cudaMemcpy(pl->tapmap_dev, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice),
+                 "tapmap upload");
+    *plan = pl;
+  });
+  if (st != DCONV_OK && pl) {
+    if (pl->tapmap_dev) cudaFree(pl->tapmap_dev);
+    delete pl;
+  }
+  return st;
+}
+
+void dconv_bwd_plan_destroy(dconv_bwd_plan_t plan) {
+  if (!plan) return;
+  if (plan->tapmap_dev) cudaFree(plan->tapmap_dev);
+  delete plan;
+}
+
+int dconv_bwd_route(dconv_bwd_plan_t plan) { return plan ? plan->route : -1; }
+size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan) { return plan ? std::max<size_t>(plan->ws_bytes, 256) : 0; }
+int dconv_bwd_plan_describe(dconv_bwd_plan_t plan, char* buf, size_t len) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
+             len);
+  });
+}
+int dconv_bwd_launches(dconv_bwd_plan_t plan) {
+  if (!plan) return 0;
+  int n = 0;
+  for (auto& ph : plan->phases) n += ph.zero ? 1 : 2;
+  return n;
+}
+
+int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
+                        const dconv_act_t* grad_in, void* workspace, dconv_stream_t stream) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    check_wt(wt, "backward weight");
+    check_act(grad_out, "backward grad_out");
+    check_act(grad_in, "backward grad_in");
+    if (!workspace) fail(DCONV_ERR_INVALID_ARGUMENT, "backward: null workspace");
+    const dconv_spec_t& s = plan->spec;
+    const int P = out_P(s), Q = out_Q(s);
+    if (wt->k != s.K || wt->c != s.C || wt->r != s.R || wt->s != s.S || wt->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "backward: weight does not match the layer spec");
+    if (grad_out->n != s.N || grad_out->c != s.K || grad_out->h != P || grad_out->w != Q || grad_out->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "backward: grad_out does not match the layer spec");
+    if (grad_in->n != s.N || grad_in->c != s.C || grad_in->h != s.H || grad_in->w != s.W || grad_in->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "backward: grad_in does not match the layer spec");
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    const int kb = cdiv(s.K, 16), cb = cdiv(s.C, 16);
+    const int hp = s.H + 2 * grad_in->halo_h, wp = s.W + 2 * grad_in->halo_w;
+    std::string desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
+    int tap_off = 0;
+    bool first = true;
+    for (auto& ph : plan->phases) {
+      if (!first) desc += ",";
+      first = false;
+      if (ph.zero) {
+        const int planes = s.N * cb;
+        const int ly = cdiv(s.H - ph.a, s.stride), lx = cdiv(s.W - ph.b, s.stride);
+        const int g = grid1d(static_cast<int64_t>(planes) * ly * lx * 16);
+        if (grad_in->dtype == DCONV_F32)
+          zero_lattice_kernel<float><<<g, 256, 0, cs>>>((float*)grad_in->data, planes, s.H, s.W, hp, wp,
+                                                        grad_in->halo_h, grad_in->halo_w, s.stride, ph.a, ph.b);
+        else
+          zero_lattice_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((__nv_bfloat16*)grad_in->data, planes, s.H, s.W, hp,
+                                                                wp, grad_in->halo_h, grad_in->halo_w, s.stride, ph.a,
+                                                                ph.b);
+        cuda_check(cudaGetLastError(), "zero_lattice");
+        desc += "\"zero\"";
+        continue;
+      }
+      void* wprep = reinterpret_cast<char*>(workspace) + ph.ws_off;
+      launch_weight_prep(*wt, static_cast<int>(ph.tapmap.size()), plan->tapmap_dev + tap_off, wprep, kb, cb, 1,
+                         plan->pieces, cs);
+      tap_off += static_cast<int>(ph.tapmap.size());
+      ConvProblem pb = ph.pb;
+      pb.in = *grad_out;
+      FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, cb, plan->has_cfg ? &plan->cfg : nullptr);
+      FwdParams& p = L.p;
+      p.out = grad_in->data;
+      p.out_bf16 = grad_in->dtype == DCONV_BF16;
+      p.out_cb = cb;
+      p.out_hp = hp;
+      p.out_wp = wp;
+      p.out_y0 = grad_in->halo_h + ph.a;
+      p.out_x0 = grad_in->halo_w + ph.b;
+      p.out_scale = s.stride;
+      const bool single = s.stride == 1;
+      p.out_halo_h = single ? grad_in->halo_h : 0;
+      p.out_halo_w = single ? grad_in->halo_w : 0;
+      p.bias = nullptr;
+      p.relu = 0;
+      launch_fwd(L, cs);
+      desc += json_tile(L);
+    }
+    desc += "]}";
+    if (s.stride != 1) {
+      const int r = dconv_zero_halo(grad_in, stream);
+      if (r != DCONV_OK) fail(r, g_err);
+    }
+    plan->last_desc = desc;
+  });
+}
+
+}  // extern "C"
+
+// ====================================================================== weight update
+namespace {
+
+struct UpdLaunch {
+  UpdParams p;
+  CUtensorMap map_in, map_do;
+  dim3 grid;
+  int stages;
+  size_t smem;
+  size_t ws_in, ws_do, ws_partial;  // workspace byte sizes (piece tensors, partials)
+  bool split_in, split_do;
+};
+
+// Tile selection for the split-K UPD (replaces choose_update_strategy /
+// choose_spatial_blocking, planner.cpp:107-173): virtual-pixel band per stage,
+// k-tile width, tap groups bounded by TMEM, split factor for >= 2 waves.
+UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_act_t& dout, bool encode_maps,
+                   const void* in_pieces, const void* do_pieces, float* partial) {
+  UpdLaunch L;
+  std::memset(&L.p, 0, sizeof(L.p));
+  UpdParams& p = L.p;
+  const dconv_spec_t& s = pl.spec;
+  const int pieces = pl.pieces;
+  const int P = out_P(s), Q = out_Q(s);
+  const int st = s.stride;
+  const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
+  const Taps& taps = pl.taps;
+  L.split_in = !(in.dtype == DCONV_BF16 && pieces == 1);
+  L.split_do = !(dout.dtype == DCONV_BF16 && pieces == 1);
+  if (pieces == 3 && (in.dtype != DCONV_F32 || dout.dtype != DCONV_F32))
+    fail(DCONV_ERR_UNSUPPORTED, "fp32-accurate math needs fp32 operands");
+  p.n_img = s.N;
+  p.in_cb = cb;
+  p.do_cb = kb;
+  p.cb_in = cb;
+  p.kb_out = kb;
+  p.P = P;
+  p.Q = Q;
+  p.stride = st;
+  p.n_taps = s.R * s.S;
+  p.in_row0 = -s.pad_h;
+  p.in_col0 = -s.pad_w;
+  const bool linear = st == 1 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 && in.halo_h == 0 &&
+                      in.halo_w == 0 && dout.halo_h == 0 && dout.halo_w == 0;
+  p.linear = linear ? 1 : 0;
+  // k tile
+  int n_kt = cdiv(kb, 16);
+  p.nb = cdiv(kb, n_kt);
+  if (pl.has_cfg && pl.cfg.tile_nb > 0) p.nb = std::min(pl.cfg.tile_nb, 16);
+  const int NT = 16 * p.nb;
+  const int n_ktiles = cdiv(kb, p.nb);
+  const int n_ctiles = cdiv(cb, 8);
+  // geometry and pipeline depth
+  const int maxshift_rows = taps.r2max, s2max = taps.s2max;
+  int stages = 0;
+  UpdStage layout;
+  if (linear) {
+    p.wsub = Q;
+    for (int vs : {256, 128, 64, 32, 16}) {
+      layout = upd_stage_layout(vs, vs, p.nb, pieces);
+      stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(layout.bytes));
+      p.vs = vs;
+      p.a_px = vs;
+      if (stages >= 3) break;
+    }
+    p.stages_per_img = cdiv(P * Q, p.vs);
+  } else {
+    const int wmin = Q + s2max;
+    // prefer a 16-aligned virtual pitch with 1-row bands when it wastes <= 25%
+    const int w16 = (wmin + 15) / 16 * 16;
+    std::vector<std::pair<int, int>> cands;  // (wsub, rows_ps)
+    if (w16 * 4 <= wmin * 5) {
+      for (int rows : {4, 2, 1}) cands.emplace_back(w16, rows);
+    }
+    {
+      int g = 16;
+      while (g > 1 && wmin % g != 0) g >>= 1;
+      const int base_rows = 16 / g;
+      for (int m : {4, 2, 1}) cands.emplace_back(wmin, base_rows * m);
+      if (w16 * 4 > wmin * 5)
+        for (int rows : {2, 1}) cands.emplace_back(w16, rows);
+    }
+    bool ok = false;
+    for (auto& c : cands) {
+      const int wsub = c.first, rows_ps = c.second;
+      if (rows_ps > std::max(1, P) && rows_ps > 1 && c.second != cands.back().second) continue;
+      const int in_rows = rows_ps + maxshift_rows + (s2max > 0 ? 1 : 0);
+      if (wsub * st > 256 || in_rows * st > 256 || rows_ps > 256) continue;
+      layout = upd_stage_layout(in_rows * wsub, rows_ps * wsub, p.nb, pieces);
+      stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(layout.bytes));
+      if (stages < 2) continue;
+      p.wsub = wsub;
+      p.rows_ps = rows_ps;
+      p.in_rows = in_rows;
+      p.vs = rows_ps * wsub;
+      p.a_px = in_rows * wsub;
+      ok = true;
+      if (stages >= 3) break;
+    }
+    if (!ok) fail(DCONV_ERR_PLAN_INFEASIBLE, "no weight-update tile fits shared memory / TMA box limits");
+    p.stages_per_img = cdiv(P, p.rows_ps);
+  }
+  if (stages < 2) fail(DCONV_ERR_PLAN_INFEASIBLE, "weight-update stage does not fit shared memory");
+  if (pl.has_cfg && pl.cfg.stages > 0) stages = std::min(stages, pl.cfg.stages);
+  p.stages_total = s.N * p.stages_per_img;
+  for (size_t t = 0; t < taps.r.size(); ++t) {
+    p.tap_shift[t] = taps.r2[t] * p.wsub + taps.s2[t];
+    p.tap_src[t] = taps.r[t] * s.S + taps.s[t];
+  }
+  for (int i = 0; i < taps.n_phases; ++i) {
+    p.phase_row[i] = taps.phase_row[i];
+    p.phase_col[i] = taps.phase_col[i];
+  }
+  // tap groups: per phase, <= 512 TMEM columns of accumulators
+  p.tg = std::max(1, std::min(512 / NT, taps.taps_box));
+  p.n_tgroups = 0;
+  for (int ph = 0; ph < taps.n_phases; ++ph)
+    for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += p.tg) {
+      if (p.n_tgroups >= kMaxTapGroups) fail(DCONV_ERR_UNSUPPORTED, "too many tap groups");
+      p.tg_phase[p.n_tgroups] = ph;
+      p.tg_tap0[p.n_tgroups] = taps.phase_tap0[ph] + t0;
+      p.tg_ntaps[p.n_tgroups] = std::min(p.tg, taps.phase_ntaps[ph] - t0);
+      ++p.n_tgroups;
+    }
+  // split-K: >= 2 waves of CTAs, >= 2 stages per split
+  const int tiles = n_ctiles * p.n_tgroups * n_ktiles;
+  int splits = cdiv(2 * sm_count(), tiles);
+  splits = std::max(1, std::min(splits, std::max(1, p.stages_total / 2)));
+  if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
+  p.splits = splits;
+  p.c_pad = n_ctiles * 128;
+  p.k_pad = n_ktiles * NT;
+  p.partial = partial;
+  L.grid = dim3(static_cast<unsigned>(n_ctiles * p.n_tgroups), static_cast<unsigned>(n_ktiles),
+                static_cast<unsigned>(splits));
+  L.stages = stages;
+  L.smem = static_cast<size_t>(stages) * layout.bytes;
+  L.ws_in = L.split_in ? align256(static_cast<size_t>(pieces) * act_elems(in) * 2) : 0;
+  L.ws_do = L.split_do ? align256(static_cast<size_t>(pieces) * act_elems(dout) * 2) : 0;
+  L.ws_partial = align256(static_cast<size_t>(splits) * p.n_taps * p.c_pad * p.k_pad * sizeof(float));
+  if (!encode_maps) return L;
+  // operand maps over bf16 piece tensors (piece-major planes)
+  auto act_map = [&](const dconv_act_t& a, const void* data, int chans_blocks, bool is_in) {
+    const int hp = a.h + 2 * a.halo_h, wp = a.w + 2 * a.halo_w;
+    const uint64_t planes = static_cast<uint64_t>(is_in ? pieces : pieces) * a.n * chans_blocks;
+    if (linear) {
+      const uint64_t dims[4] = {8, static_cast<uint64_t>(a.h) * a.w, 2, planes};
+      const uint64_t strides[3] = {32, 16, static_cast<uint64_t>(a.h) * a.w * 32};
+      const uint32_t box[4] = {8, static_cast<uint32_t>(p.vs), 2, static_cast<uint32_t>(is_in ? 8 : p.nb)};
+      return encode(1, 4, data, dims, strides, box, nullptr, is_in ? "upd input linear" : "upd dO linear");
+    }
+    const char* base = reinterpret_cast<const char*>(data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 32;
+    const uint64_t dims[5] = {8, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), 2, planes};
+    const uint64_t strides[4] = {32, static_cast<uint64_t>(wp) * 32, 16, static_cast<uint64_t>(wp) * hp * 32};
+    const uint32_t box_in[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st), 2, 8};
+    const uint32_t box_do[5] = {8, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps), 2,
+                                static_cast<uint32_t>(p.nb)};
+    const uint32_t estr_in[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};
+    return is_in ? encode(1, 5, base, dims, strides, box_in, estr_in, "upd input rows")
+                 : encode(1, 5, base, dims, strides, box_do, nullptr, "upd dO rows");
+  };
+  L.map_in = act_map(in, in_pieces, cb, true);
+  L.map_do = act_map(dout, do_pieces, kb, false);
+  return L;
+}
+
+void launch_split(const dconv_act_t& a, void* dst, int pieces, cudaStream_t cs) {
+  const int64_t n = act_elems(a);
+  if (a.dtype == DCONV_F32) {
+    split_pieces_kernel<<<grid1d(n), 256, 0, cs>>>(reinterpret_cast<const float*>(a.data),
+                                                   reinterpret_cast<__nv_bfloat16*>(dst), n, pieces);
+  } else {
+    fail(DCONV_ERR_UNSUPPORTED, "bf16 operands with fp32-accurate math");
+  }
+  cuda_check(cudaGetLastError(), "split_pieces");
+}
+
+}  // namespace
+
+extern "C" {
+
+int dconv_upd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t* cfg, int math,
+                          dconv_upd_plan_t* plan) {
+  dconv_upd_plan* pl = nullptr;
+  const int st = guarded([&] {
+    if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
+    validate_spec(*spec);
+    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
+    pl = new dconv_upd_plan();
+    pl->spec = *spec;
+    pl->math = math;
+    pl->pieces = math_pieces(math);
+    pl->has_cfg = cfg != nullptr;
+    if (cfg) pl->cfg = *cfg;
+    pl->taps = phase_taps(spec->R, spec->S, spec->stride);
+    *plan = pl;
+  });
+  if (st != DCONV_OK && pl) delete pl;
+  return st;
+}
+
+void dconv_upd_plan_destroy(dconv_upd_plan_t plan) { delete plan; }
+
+static dconv_act_t default_act(const dconv_spec_t& s, bool grad, int dtype) {
+  dconv_act_t a;
+  std::memset(&a, 0, sizeof(a));
+  a.data = reinterpret_cast<void*>(256);
+  a.n = s.N;
+  a.c = grad ? s.K : s.C;
+  a.h = grad ? out_P(s) : s.H;
+  a.w = grad ? out_Q(s) : s.W;
+  a.vlen = 16;
+  a.halo_h = grad ? 0 : s.pad_h;
+  a.halo_w = grad ? 0 : s.pad_w;
+  a.dtype = dtype;
+  return a;
+}
+
+int dconv_upd_splits(dconv_upd_plan_t plan) {
+  if (!plan) return -1;
+  int v = -1;
+  guarded([&] {
+    const int dt = plan->pieces == 3 ? DCONV_F32 : DCONV_BF16;
+    v = plan_upd(*plan, default_act(plan->spec, false, dt), default_act(plan->spec, true, dt), false, nullptr,
+                 nullptr, nullptr)
+            .p.splits;
+  });
+  return v;
+}
+
+int dconv_upd_plan_describe(dconv_upd_plan_t plan, char* buf, size_t len) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
+             len);
+  });
+}
+
+size_t dconv_upd_workspace_bytes(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out) {
+  if (!plan || !in || !grad_out) return 0;
+  size_t v = 0;
+  guarded([&] {
+    const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    v = L.ws_in + L.ws_do + L.ws_partial;
+  });
+  return v;
+}
+
+int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out) {
+  if (!plan || !in || !grad_out) return 0;
+  int v = 0;
+  guarded([&] {
+    const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    v = 2 + (L.split_in ? 1 : 0) + (L.split_do ? 1 : 0);
+  });
+  return v;
+}
+
+int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out,
+                        const dconv_wt_t* grad_w, int accumulate, void* workspace, dconv_stream_t stream) {
+  return guarded([&] {
+    if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    check_act(in, "weight_update input");
+    check_act(grad_out, "weight_update grad_out");
+    check_wt(grad_w, "weight_update grad_w");
+    if (!workspace) fail(DCONV_ERR_INVALID_ARGUMENT, "weight_update: null workspace");
+    const dconv_spec_t& s = plan->spec;
+    const int P = out_P(s), Q = out_Q(s);
+    // propagation.cpp:383-393
+    if (in->n != s.N || in->c != s.C || in->h != s.H || in->w != s.W || in->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "weight_update: input does not match the layer spec");
+    if (grad_out->n != s.N || grad_out->c != s.K || grad_out->h != P || grad_out->w != Q ||
+        grad_out->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "weight_update: grad_out does not match the layer spec");
+    if (grad_w->k != s.K || grad_w->c != s.C || grad_w->r != s.R || grad_w->s != s.S || grad_w->vlen != s.vlen)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "weight_update: grad_w does not match the layer spec");
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    UpdLaunch L0 = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    char* ws = reinterpret_cast<char*>(workspace);
+    void* in_pc = L0.split_in ? ws : in->data;
+    void* do_pc = L0.split_do ? ws + L0.ws_in : grad_out->data;
+    float* partial = reinterpret_cast<float*>(ws + L0.ws_in + L0.ws_do);
+    if (L0.split_in) launch_split(*in, in_pc, plan->pieces, cs);
+    if (L0.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
+    UpdLaunch L = plan_upd(*plan, *in, *grad_out, true, in_pc, do_pc, partial);
+    auto go = [&](auto kern) {
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
+                 "smem attribute");
+      kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages);
+    };
+    if (plan->pieces == 3)
+      go(conv_upd_kernel<3>);
+    else
+      go(conv_upd_kernel<1>);
+    cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
+    const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
+    const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
+    upd_reduce_kernel<<<grid1d(total), 256, 0, cs>>>(partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K,
+                                                      cb, kb, grad_w->data, grad_w->dtype == DCONV_BF16,
+                                                      accumulate ? 1 : 0);
+    cuda_check(cudaGetLastError(), "upd_reduce launch");
+    char buf[512];
+    std::snprintf(buf, sizeof(buf),
+                  "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
+                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d}",
+                  L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
+                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces);
+    plan->last_desc = buf;
+  });
+}
+
+}  // extern "C"

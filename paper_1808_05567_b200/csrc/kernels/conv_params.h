@@ -1,0 +1,84 @@
+// Kernel parameter blocks shared between the host launch plan and the
+// sm_100a conv kernels. Plain structs so they can be passed by value.
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace dconv_sm100 {
+
+constexpr int kMaxTaps = 64;
+constexpr int kMaxPhases = 4;
+constexpr int kMaxTapGroups = 64;
+
+// Implicit-GEMM forward over the "virtual row" grid: output pixel (p, q) of
+// image n is virtual position v = p * wsub + q; tap t of phase ph reads the
+// phase sub-image at v + tap_shift[t]. A tile is L = 128 * mb consecutive
+// virtual positions of one image; the CTA computes them for 16 * nb output
+// channels.
+struct FwdParams {
+  int n_img;
+  int in_cb;           // channel blocks of the input tensor (plane index = n*in_cb + cb)
+  int cb_in;           // reduction channel blocks
+  int kb_out;          // output channel blocks (reduction result)
+  int P, Q;            // output extents (lattice units)
+  int wsub;            // virtual row pitch
+  int tiles_per_img;
+  int mb;              // 128-row m-blocks per tile
+  int nb;              // 16-channel output blocks per CTA
+  // A staging: smem chunk planes hold a_px pixels starting at virtual pixel a_px0
+  int linear;          // 1: virtual index == physical pixel index of the halo'd plane
+  int a_px;            // pixels per chunk plane per stage
+  int lin_boxes;       // linear mode: 128-pixel boxes per chunk plane
+  int in_row0, in_col0;// logical input coordinate of sub-image (0, 0)
+  int stride;
+  int n_phases;
+  int phase_row[kMaxPhases], phase_col[kMaxPhases];
+  int phase_ntaps[kMaxPhases], phase_tap0[kMaxPhases];
+  int tap_shift[kMaxTaps];  // phase-sorted
+  int taps_box;        // weight box taps (max taps per phase)
+  // output surface (blocked, may be a strided lattice)
+  void* out;
+  int out_bf16;
+  int out_cb;          // channel blocks of the output tensor
+  int out_hp, out_wp;  // physical extents
+  int out_y0, out_x0;  // physical position of lattice point (0, 0)
+  int out_scale;       // physical pixels per lattice step
+  int out_halo_h, out_halo_w;  // halo frame to zero (0 = none)
+  const float* bias;   // kb_out*16 lanes or null
+  int relu;
+};
+
+// Weight update: per (c-tile x tap group, k-tile, split) CTA, fp32 partial
+// dW[tap][c][k] over a contiguous range of stages. Operands are bf16 piece
+// tensors read by TMA: plane index = piece * (n_img * cb) + n * cb + block.
+struct UpdParams {
+  int n_img;
+  int in_cb, do_cb;    // channel blocks of the input / dO tensors
+  int cb_in, kb_out;
+  int P, Q;
+  int wsub;            // virtual row pitch (dO box width)
+  int linear;          // 1: both operands are dense planes (1x1, stride 1, pad 0, no halos)
+  int rows_ps;         // rows mode: output rows per stage
+  int vs;              // virtual pixels per stage (multiple of 16)
+  int a_px;            // input pixels per chunk plane per stage
+  int in_rows;         // rows mode: input sub-image rows per stage
+  int in_row0, in_col0;
+  int stride;
+  int stages_per_img;
+  int stages_total;
+  int splits;
+  int nb;              // K blocks per CTA (N = 16 * nb)
+  int tg;              // max taps per CTA
+  int n_tgroups;
+  int tg_phase[kMaxTapGroups];
+  int tg_tap0[kMaxTapGroups];
+  int tg_ntaps[kMaxTapGroups];
+  int phase_row[kMaxPhases], phase_col[kMaxPhases];
+  int tap_shift[kMaxTaps];
+  int tap_src[kMaxTaps];   // phase-sorted tap -> r*S + s
+  int n_taps;
+  float* partial;      // [split][tap(RS)][c_pad][k_pad]
+  int c_pad, k_pad;
+};
+
+}  // namespace dconv_sm100

@@ -1,0 +1,275 @@
+// Blocked-layout data movement on the device (HBM-bound; bitwise moves):
+//  * pack / unpack NCHW <-> NCHW{v}c with physical zero halo   (blocked.hpp:133-178)
+//  * pack / unpack KCRS <-> KCRS{v}c{v}k                        (blocked.hpp:180-213)
+//  * dual weight transform W'[c_b][k_b][R-1-r][S-1-s][k][c]     (propagation.hpp:20-33)
+//  * re-halo copy                                               (propagation.hpp:35-49)
+//  * weight prep: blocked weights -> bf16 piece layout read by the tcgen05
+//    kernels' weight TMA ([piece*Cb_in + cb][tap][2*Kb_out][16][8])
+// Grid-stride loops over the DESTINATION so every element (halo and tail
+// lanes included) is written exactly once: no separate memset.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace dconv_sm100 {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+#define DCONV_GRID_STRIDE(i, total) \
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < (total); \
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+
+// NCHW (S) -> blocked (D); dst element e = ((((n*cb + b)*hp + y)*wp + x)*v + lane)
+template <typename S, typename D>
+__global__ void pack_act_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int c, int h, int w, int v,
+                                int hh, int hw) {
+  const int cb = (c + v - 1) / v, hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long total = static_cast<long long>(n) * cb * hp * wp * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % v);
+    long long r = e / v;
+    const int x = static_cast<int>(r % wp) - hw;
+    r /= wp;
+    const int y = static_cast<int>(r % hp) - hh;
+    r /= hp;
+    const int b = static_cast<int>(r % cb);
+    const int img = static_cast<int>(r / cb);
+    const int ch = b * v + lane;
+    float val = 0.0f;
+    if (ch < c && y >= 0 && y < h && x >= 0 && x < w)
+      val = to_f<S>(src[((static_cast<long long>(img) * c + ch) * h + y) * w + x]);
+    dst[e] = from_f<D>(val);
+  }
+}
+
+// blocked (S) -> NCHW (D), interior only
+template <typename S, typename D>
+__global__ void unpack_act_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int c, int h, int w, int v,
+                                  int hh, int hw) {
+  const int cb = (c + v - 1) / v, hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long total = static_cast<long long>(n) * c * h * w;
+  DCONV_GRID_STRIDE(e, total) {
+    const int x = static_cast<int>(e % w);
+    long long r = e / w;
+    const int y = static_cast<int>(r % h);
+    r /= h;
+    const int ch = static_cast<int>(r % c);
+    const int img = static_cast<int>(r / c);
+    const long long so = ((((static_cast<long long>(img) * cb + ch / v) * hp + y + hh) * wp) + x + hw) * v + ch % v;
+    dst[e] = from_f<D>(to_f<S>(src[so]));
+  }
+}
+
+// KCRS -> blocked [kb][cb][r][s][c][k]
+template <typename S, typename D>
+__global__ void pack_wt_kernel(const S* __restrict__ src, D* __restrict__ dst, int k, int c, int r, int s, int v) {
+  const int kb = (k + v - 1) / v, cb = (c + v - 1) / v;
+  const long long total = static_cast<long long>(kb) * cb * r * s * v * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int kl = static_cast<int>(e % v);
+    const int cl = static_cast<int>((e / v) % v);
+    long long q = e / (static_cast<long long>(v) * v);
+    const int fs = static_cast<int>(q % s);
+    q /= s;
+    const int fr = static_cast<int>(q % r);
+    q /= r;
+    const int cbi = static_cast<int>(q % cb);
+    const int kbi = static_cast<int>(q / cb);
+    const int ko = kbi * v + kl, ci = cbi * v + cl;
+    float val = 0.0f;
+    if (ko < k && ci < c) val = to_f<S>(src[((static_cast<long long>(ko) * c + ci) * r + fr) * s + fs]);
+    dst[e] = from_f<D>(val);
+  }
+}
+
+template <typename S, typename D>
+__global__ void unpack_wt_kernel(const S* __restrict__ src, D* __restrict__ dst, int k, int c, int r, int s, int v) {
+  const int cb = (c + v - 1) / v;
+  const long long total = static_cast<long long>(k) * c * r * s;
+  DCONV_GRID_STRIDE(e, total) {
+    const int fs = static_cast<int>(e % s);
+    long long q = e / s;
+    const int fr = static_cast<int>(q % r);
+    q /= r;
+    const int ci = static_cast<int>(q % c);
+    const int ko = static_cast<int>(q / c);
+    const long long so =
+        ((((static_cast<long long>(ko / v) * cb + ci / v) * r + fr) * s + fs) * v + ci % v) * v + ko % v;
+    dst[e] = from_f<D>(to_f<S>(src[so]));
+  }
+}
+
+// dual weights: out (k<->c roles swapped) [cb'=k_b... ] as transform_weight_stride1
+template <typename T>
+__global__ void dual_wt_kernel(const T* __restrict__ src, T* __restrict__ dst, int k, int c, int r, int s, int v) {
+  // dst is a blocked weight with (k' = c, c' = k)
+  const int kb2 = (c + v - 1) / v, cb2 = (k + v - 1) / v;  // dst blocks
+  const int cb = (c + v - 1) / v;                          // src c blocks
+  const long long total = static_cast<long long>(kb2) * cb2 * r * s * v * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int kl = static_cast<int>(e % v);         // dst k lane = src c lane
+    const int cl = static_cast<int>((e / v) % v);   // dst c lane = src k lane
+    long long q = e / (static_cast<long long>(v) * v);
+    const int fs = static_cast<int>(q % s);
+    q /= s;
+    const int fr = static_cast<int>(q % r);
+    q /= r;
+    const int b_c2 = static_cast<int>(q % cb2);     // dst c block = src k block
+    const int b_k2 = static_cast<int>(q / cb2);     // dst k block = src c block
+    const int ko = b_c2 * v + cl, ci = b_k2 * v + kl;  // src (k, c)
+    T val = from_f<T>(0.0f);
+    if (ko < k && ci < c) {
+      const long long so =
+          ((((static_cast<long long>(b_c2) * cb + b_k2) * r + (r - 1 - fr)) * s + (s - 1 - fs)) * v + kl) * v + cl;
+      val = src[so];
+    }
+    dst[e] = val;
+  }
+}
+
+// copy interior into a tensor with a different halo; the new halo is zeroed
+template <typename T>
+__global__ void rehalo_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int cb, int h, int w, int v,
+                              int sh, int sw, int dh, int dw) {
+  const int hp = h + 2 * dh, wp = w + 2 * dw;
+  const int shp = h + 2 * sh, swp = w + 2 * sw;
+  const long long total = static_cast<long long>(n) * cb * hp * wp * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % v);
+    long long q = e / v;
+    const int x = static_cast<int>(q % wp) - dw;
+    q /= wp;
+    const int y = static_cast<int>(q % hp) - dh;
+    const long long plane = q / hp;
+    T val = from_f<T>(0.0f);
+    if (y >= 0 && y < h && x >= 0 && x < w) val = src[((plane * shp + y + sh) * swp + x + sw) * v + lane];
+    dst[e] = val;
+  }
+}
+
+// Weight prep for the tcgen05 kernels (vlen 16). dst layout (bf16):
+//   [(pc * cb_in + cbi)][t][ng][ci(16)][kk(8)],  ng = 2*kb_out groups of 8 output lanes
+// out channel o = (ng/2)*16 + (ng%2)*8 + kk, in channel i = cbi*16 + ci.
+// tapmap[t] = source tap r*S+s (or -1 for an all-zero tap).
+// dual = 0: out = k, in = c (forward). dual = 1: out = c, in = k (backward-data).
+// pieces = 3 stores the exact hi/mid/lo bf16 split of each fp32 weight.
+template <typename S>
+__global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
+                                   int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps, int cb_in,
+                                   int kb_out, int dual, int pieces) {
+  const long long per_piece = static_cast<long long>(cb_in) * n_taps * (2 * kb_out) * 128;
+  DCONV_GRID_STRIDE(e, per_piece) {
+    const int kk = static_cast<int>(e % 8);
+    const int ci = static_cast<int>((e / 8) % 16);
+    long long q = e / 128;
+    const int ng = static_cast<int>(q % (2 * kb_out));
+    q /= (2 * kb_out);
+    const int t = static_cast<int>(q % n_taps);
+    const int cbi = static_cast<int>(q / n_taps);
+    const int ob = ng / 2, ol = (ng % 2) * 8 + kk;  // out block / lane
+    const int ib = cbi, il = ci;                    // in block / lane
+    const int rs = tapmap[t];
+    float val = 0.0f;
+    if (rs >= 0) {
+      // blocked src [kb][cb][rs][c lane][k lane]
+      const int kb = dual ? ib : ob, cb = dual ? ob : ib;
+      const int cl = dual ? ol : il, kl = dual ? il : ol;
+      if (kb < kb_src && cb < cb_src)
+        val = to_f<S>(src[(((static_cast<long long>(kb) * cb_src + cb) * rs_src + rs) * 16 + cl) * 16 + kl]);
+    }
+    const __nv_bfloat16 h = __float2bfloat16_rn(val);
+    dst[e] = h;
+    if (pieces == 3) {
+      const float r1 = val - __bfloat162float(h);
+      const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+      dst[e + per_piece] = m;
+      dst[e + 2 * per_piece] = __float2bfloat16_rn(r1 - __bfloat162float(m));
+    }
+  }
+}
+
+// zero one phase lattice (a, b) of a blocked tensor's interior: rows a + st*y, cols b + st*x
+template <typename T>
+__global__ void zero_lattice_kernel(T* __restrict__ dst, int planes, int h, int w, int hp, int wp, int hh, int hw,
+                                    int st, int a, int b) {
+  const int ly = a < h ? (h - a + st - 1) / st : 0, lx = b < w ? (w - b + st - 1) / st : 0;
+  const long long total = static_cast<long long>(planes) * ly * lx * 16;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % 16);
+    long long q = e / 16;
+    const int x = static_cast<int>(q % lx);
+    q /= lx;
+    const int y = static_cast<int>(q % ly);
+    const long long plane = q / ly;
+    dst[((plane * hp + hh + a + st * y) * wp + hw + b + st * x) * 16 + lane] = from_f<T>(0.0f);
+  }
+}
+
+// zero only the halo frame of a blocked tensor (blocked.hpp:67-79 zero_halo)
+template <typename T>
+__global__ void zero_halo_kernel(T* __restrict__ dst, int planes, int h, int w, int hh, int hw, int v) {
+  const int hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long frame = static_cast<long long>(hp) * wp - static_cast<long long>(h) * w;
+  const long long total = static_cast<long long>(planes) * frame * v;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % v);
+    long long q = e / v;
+    const long long fi = q % frame;
+    const long long plane = q / frame;
+    int y, x;
+    const long long top = static_cast<long long>(hh) * wp;
+    if (fi < top) {
+      y = static_cast<int>(fi / wp);
+      x = static_cast<int>(fi % wp);
+    } else if (fi < 2 * top) {
+      y = hh + h + static_cast<int>((fi - top) / wp);
+      x = static_cast<int>((fi - top) % wp);
+    } else {
+      const long long side = fi - 2 * top;  // h rows x (2*hw) columns
+      y = hh + static_cast<int>(side / (2 * hw));
+      const int cx = static_cast<int>(side % (2 * hw));
+      x = cx < hw ? cx : w + cx;
+    }
+    dst[((plane * hp + y) * wp + x) * v + lane] = from_f<T>(0.0f);
+  }
+}
+
+// ReLU backward mask fused helper: g *= (y > 0) on blocked tensors of equal shape
+template <typename T>
+__global__ void relu_mask_kernel(T* __restrict__ g, const T* __restrict__ y, long long n) {
+  DCONV_GRID_STRIDE(e, n) {
+    if (!(to_f<T>(y[e]) > 0.0f)) g[e] = from_f<T>(0.0f);
+  }
+}
+
+// Split a blocked fp32 tensor into `pieces` bf16 tensors laid out one after
+// the other (piece-major): x == hi + mid + lo exactly (pieces = 3), or a
+// round-to-nearest cast (pieces = 1). Halo / tail elements map 0 -> 0.
+__global__ void split_pieces_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, long long n,
+                                    int pieces) {
+  DCONV_GRID_STRIDE(e, n) {
+    const float x = src[e];
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    dst[e] = h;
+    if (pieces == 3) {
+      const float r1 = x - __bfloat162float(h);
+      const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+      dst[e + n] = m;
+      dst[e + 2 * n] = __float2bfloat16_rn(r1 - __bfloat162float(m));
+    }
+  }
+}
+
+}  // namespace dconv_sm100
