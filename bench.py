@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""bench.py — the driver's benchmark contract for dconv-b200.
+
+Default workload (BASELINE.json configs[1], the config the per-layer metric
+is quoted on): ResNet-50 Table I layer 5, the 1x1 bottleneck conv
+N=32, C=256 -> K=64, 56x56, stride 1, pad 0; one step = forward +
+backward-data + weight-update, fp32-accurate (exact bf16x3 split, fp32
+accumulate), seeded synthetic inputs (uniform(-1,1) seed 0 activations,
+He-normal seed 1 weights, uniform(-1,1) seed 2 output gradients).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value  : whole-job GFLOP/s (pass_flops x 3 passes x ranks / max-over-ranks
+         device time), inputs resident in HBM, L2 flushed between steps.
+e2e    : same metric through the reference-facing call with HOST buffers:
+         pinned blocked tensors copied H2D, the three passes, outputs D2H.
+Multi-GPU (torchrun): weak scaling, each rank runs its own N=32 shard and the
+fp32 weight gradient is summed across ranks with NCCL all-reduce (the
+COPY_REDUCE exchange promoted to GPUs); max-over-ranks device time.
+--impl reference: the reference's own CPU direct engine (oracle/_ref, built
+from /root/reference sources) on all host cores, same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv GFLOP/s per layer (fwd/bwd/upd) and conv-stack images/s at 1/2/4/8 B200"
+WORKLOAD = dict(N=32, C=256, K=64, H=56, W=56, R=1, S=1, stride=1, pad_h=0, pad_w=0)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def alg_bytes(w, e_in=4, e_out=4):
+    """SURVEY.md 8(d) compulsory bytes per pass (halos not counted)."""
+    N, C, K, H, W, R, S = (w[k] for k in ("N", "C", "K", "H", "W", "R", "S"))
+    st = w["stride"]
+    P = (H + 2 * w["pad_h"] - R) // st + 1
+    Q = (W + 2 * w["pad_w"] - S) // st + 1
+    Cp = -(-C // 16) * 16
+    Kp = -(-K // 16) * 16
+    touched = N * Cp * P * Q if (R == 1 and S == 1 and st > 1) else N * Cp * H * W
+    fwd = e_in * (touched + Kp * Cp * R * S) + e_out * N * Kp * P * Q
+    bwd = e_in * (N * Kp * P * Q + Kp * Cp * R * S) + e_out * N * Cp * H * W
+    upd = e_in * (touched + N * Kp * P * Q) + 4 * Kp * Cp * R * S
+    return {"fwd": fwd, "bwd": bwd, "upd": upd}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the GPU is busy."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x80: "hw_power_brake",
+               0x100: "display_clocks_setting"}
+
+    def __init__(self, index=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001  (no NVML: report nothing rather than guess)
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if mask & bit and name != "gpu_idle":
+                            self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def report(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------- reference arm
+
+
+def cpu_inputs(w):
+    from oracle import oracle as orc
+
+    N, C, K, H, W, R, S = (w[k] for k in ("N", "C", "K", "H", "W", "R", "S"))
+    s = orc.spec(N, C, K, H, W, R, S, w["stride"], w["pad_h"], w["pad_w"], 16)
+    P, Q = orc.output_shape(s)
+    x = orc.uniform(0, (N, C, H, W))
+    wt = orc.he_normal(1, (K, C, R, S), C * R * S)
+    g = orc.uniform(2, (N, K, P, Q))
+    return orc, s, x, wt, g
+
+
+def cpu_step_reference(orc, s, x, wt, g, threads):
+    """One F+B+U step of the reference direct engine; returns seconds (sum of the
+    three timed execute calls, setup excluded as in bench_layer)."""
+    t = 0.0
+    for p, (a, b) in enumerate(((x, wt), (g, wt), (x, g))):
+        _, best, _ = orc.ref_direct_pass(s, p, threads, 1, a, b)
+        t += best / 1e3
+    return t
+
+
+def cpu_step_port(orc, s, x, wt, g, threads):
+    t0 = time.perf_counter()
+    orc.conv_forward(s, x, wt, threads)
+    orc.conv_backward(s, g, wt, threads)
+    orc.conv_update(s, x, g, threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    orc, s, x, wt, g = cpu_inputs(WORKLOAD)
+    threads = os.cpu_count() or 1
+    flops = 3 * orc.pass_flops(s)
+    kind = "reference" if orc.ref_available() else "port"
+    if kind == "port":
+        # the f64 naive port is ~100x slower: bounded sample of 2 images
+        s2 = orc.spec(2, s.C, s.K, s.H, s.W, s.R, s.S, s.stride, s.pad_h, s.pad_w, 16)
+        x, g = x[:2].copy(), g[:2].copy()
+        s, flops = s2, 3 * orc.pass_flops(s2)
+        step = lambda: cpu_step_port(orc, s, x, wt, g, threads)  # noqa: E731
+        sample = "naive f64 oracle port, 2 of 32 images, F+B+U"
+    else:
+        step = lambda: cpu_step_reference(orc, s, x, wt, g, threads)  # noqa: E731
+        sample = "reference direct engine (oracle/_ref), full N=32 F+B+U, plan setup excluded"
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = flops / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64)",
+        "config": {"workload": "resnet50_id5_1x1_bottleneck_fwd_bwd_upd", **WORKLOAD,
+                   "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- our arm
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1808_05567_b200 as d
+    from paper_1808_05567_b200 import _lib
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    w = WORKLOAD
+    math = d.Math.BF16 if args.math == "bf16" else d.Math.F32
+    spec = d.make_layer_spec(w["N"], w["C"], w["K"], w["H"], w["W"], w["R"], w["S"], w["stride"], w["pad_h"],
+                             w["pad_w"], 16)
+    P, Q = d.derive_output_shape(spec)
+    # seeded synthetic inputs (host generator in the product library; rank-dependent shards)
+    lib = _lib.lib()
+
+    def host(shape, seed, kind, fan_in=1):
+        a = np.empty(int(np.prod(shape)), np.float32)
+        if kind == "u":
+            lib.dconv_fill_uniform_host(seed + 1000 * rank, -1.0, 1.0, a.ctypes.data, a.size)
+        else:
+            lib.dconv_fill_he_normal_host(seed, float(np.sqrt(2.0 / fan_in)), a.ctypes.data, a.size)
+        return torch.from_numpy(a.reshape(shape))
+
+    x_h = host((spec.N, spec.C, spec.H, spec.W), 0, "u")
+    w_h = host((spec.K, spec.C, spec.R, spec.S), 1, "n", spec.C * spec.R * spec.S)
+    g_h = host((spec.N, spec.K, P, Q), 2, "u")
+    ib = d.to_blocked_activation(x_h.to(dev), spec)
+    wb = d.to_blocked_weight(w_h.to(dev), spec)
+    gb = d.to_blocked_activation(g_h.to(dev), 16, 0, 0)
+    fplan = d.make_forward_plan(spec, 1, None, None, math)
+    bctx = d.prepare_backward(spec, wb, 1, None, math)
+    uplan = d.UpdatePlan(spec, None, math)
+    out = d.BlockedActivation(spec.N, spec.K, P, Q, 16, 0, 0, torch.float32, dev)
+    gi = d.BlockedActivation(spec.N, spec.C, spec.H, spec.W, 16, 0, 0, torch.float32, dev)
+    dw = d.BlockedWeight(spec.K, spec.C, spec.R, spec.S, 16, torch.float32, dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        fplan.execute(ib, wb, out)
+        bctx.execute(wb, gb, gi)
+        uplan.execute(ib, gb, dw)
+        if pg is not None:
+            pg.all_reduce(dw.data)
+
+    launches = fplan.launches() + bctx.launches() + uplan.launches(ib, gb)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-resident timing (value)
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    lib.dconv_profile(1)
+    kern_ms = {"fwd": [], "bwd": [], "upd": []}
+    with sampler:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # evict L2 between steps (untimed)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            for k, idx in (("fwd", 0), ("bwd", 1), ("upd", 2)):
+                kern_ms[k].append(lib.dconv_profile_last_ms(idx))
+        barrier()
+    lib.dconv_profile(0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        pg.all_reduce(t_local, op=pg.ReduceOp.MAX)
+    total_ms = float(t_local.item())
+    ms_per_step = total_ms / args.steps
+    flops_step = 3 * d.pass_flops(spec)
+    value = world * flops_step / (ms_per_step * 1e-3) / 1e9
+
+    # ---------------- end to end through the host-buffer API (e2e)
+    e_in = 4
+    xb_host = torch.empty(ib.data.numel(), dtype=torch.float32).pin_memory()
+    gb_host = torch.empty(gb.data.numel(), dtype=torch.float32).pin_memory()
+    wb_host = torch.empty(wb.data.numel(), dtype=torch.float32).pin_memory()
+    xb_host.copy_(ib.data.cpu())
+    gb_host.copy_(gb.data.cpu())
+    wb_host.copy_(wb.data.cpu())
+    out_host = torch.empty(out.data.numel(), dtype=torch.float32).pin_memory()
+    gi_host = torch.empty(gi.data.numel(), dtype=torch.float32).pin_memory()
+    dw_host = torch.empty(dw.data.numel(), dtype=torch.float32).pin_memory()
+    h2d = (xb_host.numel() + gb_host.numel() + wb_host.numel()) * e_in
+    d2h = (out_host.numel() + gi_host.numel() + dw_host.numel()) * 4
+
+    def e2e_step():
+        ib.data.copy_(xb_host, non_blocking=True)
+        gb.data.copy_(gb_host, non_blocking=True)
+        wb.data.copy_(wb_host, non_blocking=True)
+        step()
+        out_host.copy_(out.data, non_blocking=True)
+        gi_host.copy_(gi.data, non_blocking=True)
+        dw_host.copy_(dw.data, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if pg is not None:
+        pg.all_reduce(e2e_ms, op=pg.ReduceOp.MAX)
+    e2e_value = world * flops_step / (float(e2e_ms.item()) * 1e-3) / 1e9
+
+    # ---------------- roofline of the dominant kernel
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    byts = alg_bytes(w)
+    avg = {k: sum(v) / len(v) for k, v in kern_ms.items() if v and min(v) > 0}
+    dom = max(avg, key=avg.get) if avg else "fwd"
+    achieved = byts[dom] / (avg.get(dom, float("nan")) * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": {"fwd": "conv_fwd_kernel", "bwd": "conv_fwd_kernel (dual)",
+                                           "upd": "conv_upd_kernel"}[dom],
+                "pass": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                "alg_bytes_per_launch": byts[dom], "kernel_ms": {k: round(v, 4) for k, v in avg.items()},
+                "share_of_step": round(avg.get(dom, 0) / ms_per_step, 3)}
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            orc, s_c, x_c, w_c, g_c = cpu_inputs(w)
+            threads = os.cpu_count() or 1
+            if orc.ref_available():
+                sec = cpu_step_reference(orc, s_c, x_c, w_c, g_c, threads)
+                cpu = {"value": round(3 * orc.pass_flops(s_c) / sec / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
+                       "kind": "reference",
+                       "sample": "reference direct engine (oracle/_ref), full N=32 F+B+U, one step"}
+            else:
+                s2 = orc.spec(2, s_c.C, s_c.K, s_c.H, s_c.W, s_c.R, s_c.S, 1, 0, 0, 16)
+                sec = cpu_step_port(orc, s2, x_c[:2].copy(), w_c, g_c[:2].copy(), threads)
+                cpu = {"value": round(3 * orc.pass_flops(s2) / sec / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
+                       "kind": "port", "sample": "naive f64 oracle port, 2 of 32 images, F+B+U"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if math == d.Math.F32 else "bf16",
+            "data": "synthetic (seeded splitmix64: uniform(-1,1) x/dO, He-normal W)",
+            "config": {"workload": "resnet50_id5_1x1_bottleneck_fwd_bwd_upd (BASELINE configs[1])", **w,
+                       "global_batch": w["N"] * world, "parallelism": f"dp{world}",
+                       "math": "fp32-accurate bf16x3 split (6 products, fp32 accumulate)" if math == d.Math.F32
+                       else "bf16 operands, fp32 accumulate",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "tiles": {"fwd": fplan.blocking, "bwd": bctx.blocking, "upd": uplan.blocking}},
+            "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches * args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": sampler.report(),
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--math", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

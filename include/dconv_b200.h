@@ -190,6 +190,14 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
                         const dconv_wt_t* grad_w, int accumulate, void* workspace, dconv_stream_t stream);
 int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out);
 
+/* ---------------------------------------------------------------- profiling */
+/* enable != 0: bracket each pass's main conv kernel(s) with CUDA events on the
+ * launch stream (0 forward, 1 backward-data, 2 weight-update) */
+int dconv_profile(int enable);
+/* device time of the last bracketed launch of pass `which` in ms (synchronises
+ * on its stop event); -1 if none */
+float dconv_profile_last_ms(int which);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,7 +55,7 @@ EXPORTS = [
     "dconv_bwd_plan_destroy", "dconv_bwd_route", "dconv_bwd_plan_describe", "dconv_bwd_workspace_bytes",
     "dconv_backward_data", "dconv_bwd_launches", "dconv_upd_plan_create", "dconv_upd_plan_destroy",
     "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
-    "dconv_upd_launches",
+    "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms",
 ]
 
 
@@ -103,6 +103,8 @@ def _bind(lib):
         "dconv_upd_workspace_bytes": (sz, [vp, P(Act), P(Act)]),
         "dconv_weight_update": (i, [vp, P(Act), P(Act), P(Wt), i, vp, vp]),
         "dconv_upd_launches": (i, [vp, P(Act), P(Act)]),
+        "dconv_profile": (i, [i]),
+        "dconv_profile_last_ms": (C.c_float, [i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

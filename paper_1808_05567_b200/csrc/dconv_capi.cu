@@ -132,6 +132,31 @@ CUtensorMap encode(int bf16, int rank, const void* base, const uint64_t* dims, c
   return m;
 }
 
+// ------------------------------------------------------------------ profiling hook
+// When enabled, CUDA events bracket the main conv kernel(s) of each pass on
+// the launch stream; dconv_profile_last_ms() reads the last interval.
+struct ProfSlot {
+  cudaEvent_t start = nullptr, stop = nullptr;
+  bool armed = false;
+};
+bool g_prof = false;
+ProfSlot g_slot[3];  // 0 forward, 1 backward-data, 2 weight-update
+
+void prof_begin(int which, cudaStream_t s) {
+  if (!g_prof) return;
+  ProfSlot& p = g_slot[which];
+  if (!p.start) {
+    cuda_check(cudaEventCreate(&p.start), "event");
+    cuda_check(cudaEventCreate(&p.stop), "event");
+  }
+  cuda_check(cudaEventRecord(p.start, s), "event record");
+}
+void prof_end(int which, cudaStream_t s) {
+  if (!g_prof) return;
+  cuda_check(cudaEventRecord(g_slot[which].stop, s), "event record");
+  g_slot[which].armed = true;
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -880,7 +905,9 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
     p.bias = (plan->fuse_kind == DCONV_FUSE_BIAS_ADD || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? plan->bias_dev
                                                                                                   : nullptr;
     p.relu = (plan->fuse_kind == DCONV_FUSE_RELU || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? 1 : 0;
+    prof_begin(0, cs);
     launch_fwd(L, cs);
+    prof_end(0, cs);
     plan->last_desc = json_tile(L);
   });
 }
@@ -1010,6 +1037,7 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
     std::string desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
     int tap_off = 0;
     bool first = true;
+    prof_begin(1, cs);
     for (auto& ph : plan->phases) {
       if (!first) desc += ",";
       first = false;
@@ -1053,6 +1081,7 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
       desc += json_tile(L);
     }
     desc += "]}";
+    prof_end(1, cs);
     if (s.stride != 1) {
       const int r = dconv_zero_halo(grad_in, stream);
       if (r != DCONV_OK) fail(r, g_err);
@@ -1068,6 +1097,7 @@ namespace {
 
 struct UpdLaunch {
   UpdParams p;
+  int passes;  // 1, or 3 (one A piece per pass)
   CUtensorMap map_in, map_do;
   dim3 grid;
   int stages;
@@ -1117,54 +1147,64 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   const int n_ctiles = cdiv(cb, 8);
   // geometry and pipeline depth
   const int maxshift_rows = taps.r2max, s2max = taps.s2max;
-  int stages = 0;
-  UpdStage layout;
-  if (linear) {
-    p.wsub = Q;
-    for (int vs : {256, 128, 64, 32, 16}) {
-      layout = upd_stage_layout(vs, vs, p.nb, pieces);
-      stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(layout.bytes));
-      p.vs = vs;
-      p.a_px = vs;
-      if (stages >= 3) break;
+  // Candidate (virtual pitch, band) geometries in preference order. A single
+  // pass stages all operand pieces; fp32-accurate shapes too wide for that
+  // fall back to three passes with one A piece each.
+  struct Cand {
+    int wsub, rows_ps, in_rows, vs, a_px, stages, passes;
+    UpdStage lay;
+  };
+  std::vector<Cand> cands;
+  auto add = [&](int wsub, int rows_ps, int in_rows, int vs, int a_px) {
+    if (!linear && (wsub * st > 256 || in_rows * st > 256 || rows_ps > 256)) return;
+    if (linear && vs > 256) return;
+    for (int passes : {1, 3}) {
+      if (passes == 3 && pieces == 1) continue;
+      const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, p.nb, pieces, pieces)
+                                       : upd_stage_layout(a_px, vs, p.nb, 1, 3);
+      const int stg = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
+      if (stg >= 2) cands.push_back({wsub, rows_ps, in_rows, vs, a_px, stg, passes, lay});
     }
-    p.stages_per_img = cdiv(P * Q, p.vs);
+  };
+  if (linear) {
+    for (int vs : {256, 128, 64, 32, 16}) add(Q, 0, 0, vs, vs);
   } else {
     const int wmin = Q + s2max;
-    // prefer a 16-aligned virtual pitch with 1-row bands when it wastes <= 25%
     const int w16 = (wmin + 15) / 16 * 16;
-    std::vector<std::pair<int, int>> cands;  // (wsub, rows_ps)
-    if (w16 * 4 <= wmin * 5) {
-      for (int rows : {4, 2, 1}) cands.emplace_back(w16, rows);
-    }
-    {
-      int g = 16;
-      while (g > 1 && wmin % g != 0) g >>= 1;
-      const int base_rows = 16 / g;
-      for (int m : {4, 2, 1}) cands.emplace_back(wmin, base_rows * m);
-      if (w16 * 4 > wmin * 5)
-        for (int rows : {2, 1}) cands.emplace_back(w16, rows);
-    }
-    bool ok = false;
-    for (auto& c : cands) {
-      const int wsub = c.first, rows_ps = c.second;
-      if (rows_ps > std::max(1, P) && rows_ps > 1 && c.second != cands.back().second) continue;
+    int g = 16;
+    while (g > 1 && wmin % g != 0) g >>= 1;
+    const int base_rows = 16 / g;  // rows so that rows * wmin % 16 == 0
+    std::vector<std::pair<int, int>> geo;
+    if (w16 * 4 <= wmin * 5)  // 16-aligned pitch wastes <= 25%: 1-row bands allowed
+      for (int rows : {4, 2, 1}) geo.emplace_back(w16, rows);
+    for (int m : {4, 2, 1}) geo.emplace_back(wmin, base_rows * m);
+    for (int rows : {2, 1}) geo.emplace_back(w16, rows);
+    for (auto& gr : geo) {
+      const int wsub = gr.first, rows_ps = gr.second;
+      if (rows_ps > P && !(wsub == wmin && rows_ps == base_rows)) continue;  // bands taller than the image
       const int in_rows = rows_ps + maxshift_rows + (s2max > 0 ? 1 : 0);
-      if (wsub * st > 256 || in_rows * st > 256 || rows_ps > 256) continue;
-      layout = upd_stage_layout(in_rows * wsub, rows_ps * wsub, p.nb, pieces);
-      stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(layout.bytes));
-      if (stages < 2) continue;
-      p.wsub = wsub;
-      p.rows_ps = rows_ps;
-      p.in_rows = in_rows;
-      p.vs = rows_ps * wsub;
-      p.a_px = in_rows * wsub;
-      ok = true;
-      if (stages >= 3) break;
+      add(wsub, rows_ps, in_rows, rows_ps * wsub, in_rows * wsub);
     }
-    if (!ok) fail(DCONV_ERR_PLAN_INFEASIBLE, "no weight-update tile fits shared memory / TMA box limits");
-    p.stages_per_img = cdiv(P, p.rows_ps);
   }
+  const Cand* best = nullptr;
+  for (int tier = 0; tier < 4 && !best; ++tier) {
+    const int want_passes = tier < 2 ? 1 : 3, want_stages = (tier % 2 == 0) ? 3 : 2;
+    for (auto& cd : cands)
+      if (cd.passes == want_passes && cd.stages >= want_stages) {
+        best = &cd;
+        break;
+      }
+  }
+  if (!best) fail(DCONV_ERR_PLAN_INFEASIBLE, "no weight-update tile fits shared memory / TMA box limits");
+  p.wsub = best->wsub;
+  p.rows_ps = best->rows_ps;
+  p.in_rows = best->in_rows;
+  p.vs = best->vs;
+  p.a_px = best->a_px;
+  int stages = best->stages;
+  const UpdStage layout = best->lay;
+  L.passes = best->passes;
+  p.stages_per_img = linear ? cdiv(P * Q, p.vs) : cdiv(P, p.rows_ps);
   if (stages < 2) fail(DCONV_ERR_PLAN_INFEASIBLE, "weight-update stage does not fit shared memory");
   if (pl.has_cfg && pl.cfg.stages > 0) stages = std::min(stages, pl.cfg.stages);
   p.stages_total = s.N * p.stages_per_img;
@@ -1316,7 +1356,7 @@ int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv
   int v = 0;
   guarded([&] {
     const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
-    v = 2 + (L.split_in ? 1 : 0) + (L.split_do ? 1 : 0);
+    v = 1 + L.passes + (L.split_in ? 1 : 0) + (L.split_do ? 1 : 0);
   });
   return v;
 }
@@ -1348,16 +1388,23 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     if (L0.split_in) launch_split(*in, in_pc, plan->pieces, cs);
     if (L0.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
     UpdLaunch L = plan_upd(*plan, *in, *grad_out, true, in_pc, do_pc, partial);
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern, int a_base, int acc) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                  "smem attribute");
-      kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages);
+      kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages, a_base, acc);
+      cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
     };
-    if (plan->pieces == 3)
-      go(conv_upd_kernel<3>);
-    else
-      go(conv_upd_kernel<1>);
-    cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
+    prof_begin(2, cs);
+    if (plan->pieces == 1) {
+      go(conv_upd_kernel<1, 1>, 0, 0);
+    } else if (L.passes == 1) {
+      go(conv_upd_kernel<3, 3>, 0, 0);
+    } else {
+      go(conv_upd_kernel<1, 3>, 0, 0);
+      go(conv_upd_kernel<1, 2>, 1, 1);
+      go(conv_upd_kernel<1, 1>, 2, 1);
+    }
+    prof_end(2, cs);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
     upd_reduce_kernel<<<grid1d(total), 256, 0, cs>>>(partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K,
@@ -1367,11 +1414,28 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     char buf[512];
     std::snprintf(buf, sizeof(buf),
                   "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
-                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d}",
+                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d}",
                   L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
-                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces);
+                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces, L.passes);
     plan->last_desc = buf;
   });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int dconv_profile(int enable) {
+  g_prof = enable != 0;
+  return DCONV_OK;
+}
+
+float dconv_profile_last_ms(int which) {
+  if (which < 0 || which > 2 || !g_slot[which].armed) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(g_slot[which].stop) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, g_slot[which].start, g_slot[which].stop) != cudaSuccess) return -1.0f;
+  return ms;
 }
 
 }  // extern "C"

@@ -32,21 +32,26 @@ struct UpdStage {
   uint32_t b_off, bytes;
 };
 
-__host__ __device__ inline UpdStage upd_stage_layout(int a_px, int vs, int nb, int pieces) {
+__host__ __device__ inline UpdStage upd_stage_layout(int a_px, int vs, int nb, int pa, int pb) {
   UpdStage L;
   L.a_plane = static_cast<uint32_t>(a_px) * 16u;
   L.b_plane = static_cast<uint32_t>(vs) * 16u;
   L.a_piece = 16u * L.a_plane;
   L.b_piece = 2u * nb * L.b_plane;
-  L.b_off = static_cast<uint32_t>(pieces) * L.a_piece;
-  L.bytes = (L.b_off + static_cast<uint32_t>(pieces) * L.b_piece + 1023u) & ~1023u;
+  L.b_off = static_cast<uint32_t>(pa) * L.a_piece;
+  L.bytes = (L.b_off + static_cast<uint32_t>(pb) * L.b_piece + 1023u) & ~1023u;
   return L;
 }
 
-template <int PIECES>
+// PA / PB: operand pieces staged per stage. The products (ia, ib) with
+// a_base + ia + ib <= 2 are accumulated, so one launch with PA = PB = 3 (or
+// PA = PB = 1 for bf16) covers everything, and when three A pieces do not
+// fit in smem the host runs three passes (a_base = 0, 1, 2 with PA = 1,
+// PB = 3 - a_base) that accumulate into the same partials.
+template <int PA, int PB>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     conv_upd_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
-                    const __grid_constant__ UpdParams p, int n_stages) {
+                    const __grid_constant__ UpdParams p, int n_stages, int a_base, int accumulate) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int NT = 16 * p.nb;
-  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PIECES);
+  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB);
   const uint32_t smem0 = smem_u32(smem);
 
   // CTA coordinates: x = c-tile * n_tgroups + tap group, y = k-tile, z = split
@@ -102,22 +107,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int n = stage / p.stages_per_img;
         const int band = stage % p.stages_per_img;
         uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
-        mbar_arrive_expect_tx(&full_bar[s], PIECES * (L.a_piece + L.b_piece));
-        for (int pc = 0; pc < PIECES; ++pc) {
-          const int pa = pc * in_planes + n * p.in_cb + ctile * 8;
-          const int pb = pc * do_planes + n * p.do_cb + ktile * p.nb;
+        mbar_arrive_expect_tx(&full_bar[s], PA * L.a_piece + PB * L.b_piece);
+        for (int pc = 0; pc < PA; ++pc) {
+          const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
           uint8_t* a_dst = st + pc * L.a_piece;
-          uint8_t* b_dst = st + L.b_off + pc * L.b_piece;
-          if (p.linear) {
-            const int v0 = band * p.vs;
-            tma_load_4d(a_dst, &map_in, &full_bar[s], 0, v0, 0, pa);
-            tma_load_4d(b_dst, &map_do, &full_bar[s], 0, v0, 0, pb);
-          } else {
-            const int row0 = band * p.rows_ps;
+          if (p.linear)
+            tma_load_4d(a_dst, &map_in, &full_bar[s], 0, band * p.vs, 0, pa);
+          else
             tma_load_5d(a_dst, &map_in, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
-                        p.in_row0 + p.stride * row0 + p.phase_row[ph], 0, pa);
-            tma_load_5d(b_dst, &map_do, &full_bar[s], 0, 0, row0, 0, pb);
-          }
+                        p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], 0, pa);
+        }
+        for (int pc = 0; pc < PB; ++pc) {
+          const int pb = pc * do_planes + n * p.do_cb + ktile * p.nb;
+          uint8_t* b_dst = st + L.b_off + pc * L.b_piece;
+          if (p.linear)
+            tma_load_4d(b_dst, &map_do, &full_bar[s], 0, band * p.vs, 0, pb);
+          else
+            tma_load_5d(b_dst, &map_do, &full_bar[s], 0, 0, band * p.rows_ps, 0, pb);
         }
       }
     }
@@ -136,17 +142,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * NT);
           for (int ks = 0; ks < ksteps; ++ks) {
 #pragma unroll
-            for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
-              const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
-              const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
-              // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels
-              const uint64_t ad = make_smem_desc(
-                  st + static_cast<uint32_t>(ia) * L.a_piece + static_cast<uint32_t>(ks * 16 + shift) * 16u, 128,
-                  L.a_plane);
-              const uint64_t bd = make_smem_desc(
-                  st + L.b_off + static_cast<uint32_t>(ib) * L.b_piece + static_cast<uint32_t>(ks) * 256u, 128,
-                  L.b_plane);
-              mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || ks > 0 || pr > 0) ? 1u : 0u);
+            for (int ia = 0; ia < PA; ++ia) {
+#pragma unroll
+              for (int ib = 0; ib < PB; ++ib) {
+                if (a_base + ia + ib > 2) continue;
+                // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels
+                const uint64_t ad = make_smem_desc(
+                    st + static_cast<uint32_t>(ia) * L.a_piece + static_cast<uint32_t>(ks * 16 + shift) * 16u, 128,
+                    L.a_plane);
+                const uint64_t bd = make_smem_desc(
+                    st + L.b_off + static_cast<uint32_t>(ib) * L.b_piece + static_cast<uint32_t>(ks) * 256u, 128,
+                    L.b_plane);
+                mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || ks > 0 || ia > 0 || ib > 0) ? 1u : 0u);
+              }
             }
           }
         }
@@ -174,10 +182,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
         const bool live = iters > 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          d[e] = live ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
-                                    __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = 0; e < 4; ++e) {
+          float4 v = live ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                        __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (accumulate) {
+            const float4 o = d[e];
+            v.x += o.x;
+            v.y += o.y;
+            v.z += o.z;
+            v.w += o.w;
+          }
+          d[e] = v;
+        }
       }
     }
   }
