@@ -229,16 +229,17 @@ struct FwdTile {
 
 struct FwdLaunch {
   FwdParams p;
-  CUtensorMap map_a, map_w;
+  CUtensorMap map_a;
   dim3 grid;
-  int stages;
+  int stages;      // piece-ring depth
+  int raw_stages;  // raw-ring depth (fp32 activations)
   size_t smem;
   bool raw_f32;
   int pieces;
 };
 
 // Decide staging mode, tile and pipeline depth; encode TMA maps.
-FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* wprep, int pieces, int kb_prep,
+FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* wprep, int pieces,
                           const dconv_engine_config_t* cfg) {
   FwdLaunch L;
   std::memset(&L.p, 0, sizeof(L.p));
@@ -279,17 +280,17 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   const int kb_total = pb.kb_out;
   const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : 0;
   const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16) : 0;
-  FwdStage layout;
-  int a_px = 0, lin_boxes = 0;
+  int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0;
+  FwdSmem layout;
   bool found = false;
-  // widest N tile first (fewer A re-reads), then the largest M tile whose
-  // stage fits >= 3 deep (>= 2 as a last resort)
-  for (int min_stages : {3, 2}) {
+  // widest N tile first (fewer activation re-reads), then the largest M tile;
+  // two TMEM accumulators of mb*16*nb columns must fit in 512
+  for (int want_pc : {3, 2}) {
     for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
       const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
       for (int mb : {2, 1}) {
         if (want_mb && mb != want_mb) continue;
-        if (mb * 16 * nb > 512) continue;
+        if (mb * 16 * nb > 256) continue;
         const int Lpx = 128 * mb;
         int apx, lb = 0;
         if (linear) {
@@ -300,13 +301,28 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           if (p.wsub * st > 256 || rows_box * st > 256) continue;
           apx = rows_box * p.wsub;
         }
-        const FwdStage lay = fwd_stage_layout(apx, taps.taps_box, nb, pieces, raw_f32);
-        const int stages = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
-        if (stages < min_stages) continue;
+        const FwdSmem lay = fwd_smem_layout(apx, taps.taps_box, nb, pieces, raw_f32, 1);
+        int pcs, rws = 0;
+        if (raw_f32) {
+          pcs = want_pc;
+          const int left = kSmemBudget - pcs * static_cast<int>(lay.pc_slot);
+          rws = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.raw_slot)) : 0;
+          if (rws < 2) continue;
+        } else {
+          pcs = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.pc_slot));
+          if (pcs < want_pc) continue;
+        }
         tile.mb = mb;
         tile.nb = nb;
-        tile.stages = (cfg && cfg->stages > 0) ? std::min(cfg->stages, stages) : stages;
-        layout = lay;
+        pc_st = pcs;
+        raw_st = rws;
+        if (cfg && cfg->stages > 0) {
+          if (raw_f32)
+            raw_st = std::max(2, std::min(cfg->stages, raw_st));
+          else
+            pc_st = std::max(2, std::min(cfg->stages, pc_st));
+        }
+        layout = fwd_smem_layout(apx, taps.taps_box, nb, pieces, raw_f32, pc_st);
         a_px = apx;
         lin_boxes = lb;
         found = true;
@@ -322,40 +338,45 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.a_px = a_px;
   p.lin_boxes = lin_boxes;
   p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
-  L.stages = tile.stages;
-  L.smem = static_cast<size_t>(tile.stages) * layout.bytes;
-  L.grid = dim3(static_cast<unsigned>(in.n * p.tiles_per_img), static_cast<unsigned>(cdiv(kb_total, tile.nb)), 1);
+  L.stages = pc_st;
+  L.raw_stages = raw_st;
+  L.smem = static_cast<size_t>(layout.raw_off) + static_cast<size_t>(raw_st) * layout.raw_slot;
+  const int n_tiles = in.n * p.tiles_per_img * cdiv(kb_total, tile.nb);
+  L.grid = dim3(static_cast<unsigned>(std::min(n_tiles, sm_count())), 1, 1);
 
+  p.n_taps = static_cast<int>(taps.r.size());
+  p.n_ntiles = cdiv(kb_total, tile.nb);
+  p.wprep = wprep;
   // activation map
-  const int e = raw_f32 ? 4 : 8;             // elements per 16B
-  const int nch = raw_f32 ? 4 : 2;           // 16B chunks per pixel (vlen 16)
-  const uint64_t pix = raw_f32 ? 64 : 32;    // bytes per pixel
   const uint64_t planes = static_cast<uint64_t>(in.n) * p.in_cb;
-  if (linear) {
-    const uint64_t dims[4] = {static_cast<uint64_t>(e), static_cast<uint64_t>(hp) * wp, static_cast<uint64_t>(nch),
-                              planes};
-    const uint64_t strides[3] = {pix, 16, pix * hp * wp};
-    const uint32_t box[4] = {static_cast<uint32_t>(e), 128, 1, 1};
-    L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation linear");
+  if (raw_f32) {
+    // fp32 pixels as 64B rows (16 lanes), converted to bf16 pieces in smem
+    if (linear) {
+      const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
+      const uint64_t strides[2] = {64, 64ull * hp * wp};
+      const uint32_t box[3] = {16, 128, 1};
+      L.map_a = encode(0, 3, in.data, dims, strides, box, nullptr, "activation linear f32");
+    } else {
+      const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * 64;
+      const uint64_t dims[4] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), planes};
+      const uint64_t strides[3] = {64, 64ull * wp, 64ull * wp * hp};
+      const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 1};
+      const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
+      L.map_a = encode(0, 4, base, dims, strides, box, estr, "activation rows f32");
+    }
+  } else if (linear) {
+    // bf16 straight into the canonical [chunk][pixel][16B] layout
+    const uint64_t dims[4] = {8, static_cast<uint64_t>(hp) * wp, 2, planes};
+    const uint64_t strides[3] = {32, 16, 32ull * hp * wp};
+    const uint32_t box[4] = {8, 128, 1, 1};
+    L.map_a = encode(1, 4, in.data, dims, strides, box, nullptr, "activation linear bf16");
   } else {
-    const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * pix;
-    const uint64_t dims[5] = {static_cast<uint64_t>(e), static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h),
-                              static_cast<uint64_t>(nch), planes};
-    const uint64_t strides[4] = {pix, pix * wp, 16, pix * wp * hp};
-    const uint32_t box[5] = {static_cast<uint32_t>(e), static_cast<uint32_t>(p.wsub * st),
-                             static_cast<uint32_t>((a_px / p.wsub) * st), static_cast<uint32_t>(nch), 1};
+    const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * 32;
+    const uint64_t dims[5] = {8, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), 2, planes};
+    const uint64_t strides[4] = {32, 32ull * wp, 16, 32ull * wp * hp};
+    const uint32_t box[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 2, 1};
     const uint32_t estr[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};
-    L.map_a = encode(!raw_f32, 5, base, dims, strides, box, estr, "activation rows");
-  }
-  // prepared weights [(pc*cb_red + cb)][t][2*kb_prep][16][8] bf16
-  {
-    const int T = static_cast<int>(taps.r.size());
-    const uint64_t dims[5] = {8, 16, static_cast<uint64_t>(2 * kb_prep), static_cast<uint64_t>(T),
-                              static_cast<uint64_t>(pieces) * pb.cb_red};
-    const uint64_t strides[4] = {16, 256, static_cast<uint64_t>(2 * kb_prep) * 256,
-                                 static_cast<uint64_t>(T) * 2 * kb_prep * 256};
-    const uint32_t box[5] = {8, 16, static_cast<uint32_t>(2 * tile.nb), static_cast<uint32_t>(taps.taps_box), 1};
-    L.map_w = encode(1, 5, wprep, dims, strides, box, nullptr, "prepared weights");
+    L.map_a = encode(1, 5, base, dims, strides, box, estr, "activation rows bf16");
   }
   return L;
 }
@@ -364,7 +385,7 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
   auto go = [&](auto kern) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                "smem attribute");
-    kern<<<L.grid, kFwdThreads, L.smem, stream>>>(L.map_a, L.map_w, L.p, L.stages);
+    kern<<<L.grid, kFwdThreadsP, L.smem, stream>>>(L.map_a, L.p, L.raw_stages, L.stages);
   };
   if (L.raw_f32) {
     if (L.pieces == 3)
@@ -379,33 +400,34 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
 
 // weight prep: src blocked weights -> bf16 pieces in the phase-sorted tap order
 // (tapmap_dev is uploaded once at plan creation so execute calls are graph-capturable)
-void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int kb_out,
-                        int dual, int pieces, cudaStream_t stream) {
-  const int64_t total = static_cast<int64_t>(cb_in) * n_taps * 2 * kb_out * 128;
+void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int nb,
+                        int n_ntiles, int dual, int pieces, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(cb_in) * n_ntiles * n_taps * 2 * nb * 128;
   const int kbs = cdiv(w.k, 16), cbs = cdiv(w.c, 16);
   if (w.dtype == DCONV_F32)
     weight_prep_kernel<float><<<grid1d(total), 256, 0, stream>>>(
         reinterpret_cast<const float*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
-        tapmap_dev, n_taps, cb_in, kb_out, dual, pieces);
+        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces);
   else
     weight_prep_kernel<__nv_bfloat16><<<grid1d(total), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
-        tapmap_dev, n_taps, cb_in, kb_out, dual, pieces);
+        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces);
   cuda_check(cudaGetLastError(), "weight_prep launch");
 }
 
+// upper bound over tilings: n_ntiles * nb <= kb_out + 15
 size_t prep_bytes(int pieces, int cb_in, int taps, int kb_out) {
-  return static_cast<size_t>(pieces) * cb_in * taps * 2 * kb_out * 256;
+  return static_cast<size_t>(pieces) * cb_in * taps * 2 * (kb_out + 15) * 256;
 }
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 std::string json_tile(const FwdLaunch& L) {
   char buf[512];
   std::snprintf(buf, sizeof(buf),
-                "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u],"
-                "\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d}",
-                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.smem, L.grid.x, L.grid.y,
-                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px);
+                "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,"
+                "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d}",
+                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.smem, L.grid.x,
+                L.p.n_img * L.p.tiles_per_img * L.p.n_ntiles, L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px);
   return buf;
 }
 
@@ -877,8 +899,6 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     // weights -> bf16 pieces, phase-sorted taps
-    launch_weight_prep(*wt, static_cast<int>(plan->taps.r.size()), plan->tapmap_dev, workspace, cb, kb, 0,
-                       plan->pieces, cs);
     ConvProblem pb;
     pb.in = *in;
     pb.cb_red = cb;
@@ -890,7 +910,8 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
     pb.stride = s.stride;
     pb.row_off = -s.pad_h;
     pb.col_off = -s.pad_w;
-    FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, kb, plan->has_cfg ? &plan->cfg : nullptr);
+    FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
+    launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces, cs);
     FwdParams& p = L.p;
     p.out = out->data;
     p.out_bf16 = out->dtype == DCONV_BF16;
@@ -1057,12 +1078,12 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
         continue;
       }
       void* wprep = reinterpret_cast<char*>(workspace) + ph.ws_off;
-      launch_weight_prep(*wt, static_cast<int>(ph.tapmap.size()), plan->tapmap_dev + tap_off, wprep, kb, cb, 1,
-                         plan->pieces, cs);
-      tap_off += static_cast<int>(ph.tapmap.size());
       ConvProblem pb = ph.pb;
       pb.in = *grad_out;
-      FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, cb, plan->has_cfg ? &plan->cfg : nullptr);
+      FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
+      launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, L.p.nb, L.p.n_ntiles, 1,
+                         plan->pieces, cs);
+      tap_off += static_cast<int>(ph.tapmap.size());
       FwdParams& p = L.p;
       p.out = grad_in->data;
       p.out_bf16 = grad_in->dtype == DCONV_BF16;

@@ -20,8 +20,9 @@
 // Weights are pre-laid-out bf16 pieces (layout.cuh weight_prep_kernel), one
 // TMA box per piece per stage.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (+TMEM owner),
-// w2..w7 converters (fp32 activations only), w4..w7 epilogue.
+// Warp roles (448 threads): w0 activation TMA producer, w1 MMA issuer (+TMEM
+// owner), w2 weight producer (fp32 path), w4..w7 epilogue, w8..w13 converters
+// (fp32 activations only). Persistent over tiles with double-buffered TMEM.
 //
 // Numerics: pieces = 1 is bf16 x bf16 -> fp32 (TMEM). pieces = 3 splits every
 // fp32 operand into hi + mid + lo bf16 (exact) and accumulates the six
@@ -43,20 +44,25 @@ __device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return static_cast<uint32_t>(__bfloat16_as_ushort(a)) | (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
 }
 
+// two fp32 -> packed bf16x2, round to nearest even (one F2FP.BF16.F32.PACK_AB)
+__device__ __forceinline__ uint32_t cvt2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ float lo_f(uint32_t p) { return __uint_as_float(p << 16); }
+__device__ __forceinline__ float hi_f(uint32_t p) { return __uint_as_float(p & 0xFFFF0000u); }
+
 // Exact 3-way split of 8 fp32 values into 16B bf16 rows (hi, mid, lo).
 // x == hi + mid + lo for every finite normal x (8 significant bits each).
 __device__ __forceinline__ void split8(const float (&x)[8], uint4& h, uint4& m, uint4& l) {
   uint32_t hh[4], mm[4], ll[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    __nv_bfloat16 a0 = __float2bfloat16_rn(x[2 * e]), b0 = __float2bfloat16_rn(x[2 * e + 1]);
-    const float ra = x[2 * e] - __bfloat162float(a0), rb = x[2 * e + 1] - __bfloat162float(b0);
-    __nv_bfloat16 a1 = __float2bfloat16_rn(ra), b1 = __float2bfloat16_rn(rb);
-    __nv_bfloat16 a2 = __float2bfloat16_rn(ra - __bfloat162float(a1));
-    __nv_bfloat16 b2 = __float2bfloat16_rn(rb - __bfloat162float(b1));
-    hh[e] = pack2(a0, b0);
-    mm[e] = pack2(a1, b1);
-    ll[e] = pack2(a2, b2);
+    hh[e] = cvt2(x[2 * e], x[2 * e + 1]);
+    const float ra = x[2 * e] - lo_f(hh[e]), rb = x[2 * e + 1] - hi_f(hh[e]);
+    mm[e] = cvt2(ra, rb);
+    ll[e] = cvt2(ra - lo_f(mm[e]), rb - hi_f(mm[e]));
   }
   h = make_uint4(hh[0], hh[1], hh[2], hh[3]);
   m = make_uint4(mm[0], mm[1], mm[2], mm[3]);
@@ -64,10 +70,7 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& h, uint4& m, 
 }
 
 __device__ __forceinline__ uint4 cast8(const float (&x)[8]) {
-  return make_uint4(pack2(__float2bfloat16_rn(x[0]), __float2bfloat16_rn(x[1])),
-                    pack2(__float2bfloat16_rn(x[2]), __float2bfloat16_rn(x[3])),
-                    pack2(__float2bfloat16_rn(x[4]), __float2bfloat16_rn(x[5])),
-                    pack2(__float2bfloat16_rn(x[6]), __float2bfloat16_rn(x[7])));
+  return make_uint4(cvt2(x[0], x[1]), cvt2(x[2], x[3]), cvt2(x[4], x[5]), cvt2(x[6], x[7]));
 }
 
 // 16 fp32 accumulator columns -> 16 lanes at `dst`
@@ -98,61 +101,74 @@ __device__ __forceinline__ void store16_zero(void* dst, int out_bf16) {
   }
 }
 
-// byte offsets of one pipeline stage: [raw fp32 A (4 planes)] [A pieces] [W pieces]
-struct FwdStage {
-  uint32_t a_plane;  // bytes per 16B-chunk plane (a_px * 16)
-  uint32_t pc_off;   // A pieces start
-  uint32_t w_off;    // weights start
+// Shared-memory plan: a RAW ring (fp32 activations as landed by TMA,
+// [pixel][64B]; fp32 path only) and a PIECE ring ({A bf16 pieces, W bf16
+// pieces}) that the tensor core reads. The raw ring runs ahead of the piece
+// ring so enough HBM bytes stay in flight while converters and MMAs work.
+struct FwdSmem {
+  uint32_t a_plane;  // bytes per 16B-chunk plane of the A pieces (a_px * 16)
+  uint32_t raw_slot; // bytes per raw slot (a_px * 64), 0 for bf16 inputs
   uint32_t w_piece;  // bytes per weight piece
-  uint32_t bytes;    // stage stride
+  uint32_t pc_slot;  // bytes per piece slot
+  uint32_t raw_off;  // raw ring starts after the piece ring
 };
 
-__host__ __device__ inline FwdStage fwd_stage_layout(int a_px, int taps_box, int nb, int pieces, bool raw_f32) {
-  FwdStage L;
+__host__ __device__ inline FwdSmem fwd_smem_layout(int a_px, int taps_box, int nb, int pieces, bool raw_f32,
+                                                   int piece_stages) {
+  FwdSmem L;
   L.a_plane = static_cast<uint32_t>(a_px) * 16u;
-  L.pc_off = raw_f32 ? 4u * L.a_plane : 0u;
-  L.w_off = (L.pc_off + static_cast<uint32_t>(pieces) * 2u * L.a_plane + 127u) & ~127u;
+  L.raw_slot = raw_f32 ? ((static_cast<uint32_t>(a_px) * 64u + 1023u) & ~1023u) : 0u;
   L.w_piece = static_cast<uint32_t>(taps_box) * (2u * nb) * 256u;
-  L.bytes = (L.w_off + static_cast<uint32_t>(pieces) * L.w_piece + 1023u) & ~1023u;
+  L.pc_slot = (static_cast<uint32_t>(pieces) * (2u * L.a_plane + L.w_piece) + 1023u) & ~1023u;
+  L.raw_off = static_cast<uint32_t>(piece_stages) * L.pc_slot;
   return L;
 }
 
+constexpr int kFwdWarps = 14;  // w0 A/raw producer, w1 MMA, w2 W producer, w3 idle, w4-7 epilogue, w8-13 converters
+constexpr int kFwdThreadsP = kFwdWarps * 32;
+constexpr int kCvtWarp0 = 8, kCvtWarps = 6;
+
+// Persistent implicit-GEMM forward: grid = #SMs, CTA c handles tiles c, c+G, ...
+// (tile = (image, virtual-row block) x output-channel tile). Two TMEM
+// accumulator buffers let the epilogue of tile i overlap the mainloop of i+1.
 template <bool RAW_F32, int PIECES>
-__global__ void __launch_bounds__(kFwdThreads, 1)
-    conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w,
-                    const __grid_constant__ FwdParams p, int n_stages) {
+__global__ void __launch_bounds__(kFwdThreadsP, 1)
+    conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ FwdParams p, int raw_stages,
+                    int pc_stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full_bar[kMaxStages];   // TMA bytes landed
-  __shared__ __align__(8) uint64_t conv_bar[kMaxStages];   // converter pieces written
-  __shared__ __align__(8) uint64_t empty_bar[kMaxStages];  // MMA done with the stage
-  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_conv[kMaxStages], pc_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const FwdStage L = fwd_stage_layout(p.a_px, p.taps_box, p.nb, PIECES, RAW_F32);
+  const FwdSmem L = fwd_smem_layout(p.a_px, p.taps_box, p.nb, PIECES, RAW_F32, pc_stages);
   const uint32_t smem0 = smem_u32(smem);
-
-  const int n = blockIdx.x / p.tiles_per_img;
-  const int v0 = (blockIdx.x % p.tiles_per_img) * 128 * p.mb;
-  const int ntile = blockIdx.y;
   const int NT = 16 * p.nb;
   const int k_iters = p.cb_in * p.n_phases;
-  const int row0 = v0 / p.wsub;
-  const int a_px0 = p.linear ? v0 : row0 * p.wsub;  // virtual index of smem pixel 0
+  const int n_mtiles = p.n_img * p.tiles_per_img;
+  const int n_tiles = n_mtiles * p.n_ntiles;
+  const uint32_t acc_cols = static_cast<uint32_t>(p.mb * NT);
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(p.mb * NT)) tmem_cols <<= 1;
+  while (tmem_cols < 2u * acc_cols) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_w);
-    for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&conv_bar[s], kConvThreads / 32);
-      mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < raw_stages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], kCvtWarps);
     }
-    mbar_init(&accum_bar, 1);
+    for (int s = 0; s < pc_stages; ++s) {
+      mbar_init(&pc_full[s], 1);
+      mbar_init(&pc_conv[s], kCvtWarps);
+      mbar_init(&pc_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
@@ -161,112 +177,190 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
 
+  // tile t -> (n, v0, ntile); output-channel tiles innermost so consecutive
+  // CTAs share the activation tile through L2
+  auto tile_coords = [&](int t, int& n, int& v0, int& ntile) {
+    ntile = t % p.n_ntiles;
+    const int mt = t / p.n_ntiles;
+    n = mt / p.tiles_per_img;
+    v0 = (mt % p.tiles_per_img) * 128 * p.mb;
+  };
+  const uint32_t w_tap = (2u * p.nb) * 256u;
+
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ activation producer
     if (lane == 0) {
-      constexpr int kChunks = RAW_F32 ? 4 : 2;  // 16B chunk planes of the staged activation
-      const uint32_t a_bytes = kChunks * L.a_plane;
-      for (int it = 0; it < k_iters; ++it) {
-        const int s = it % n_stages;
-        const uint32_t use = static_cast<uint32_t>(it / n_stages);
-        mbar_wait(&empty_bar[s], (use & 1u) ^ 1u);
-        const int cb = it / p.n_phases;
-        const int ph = it % p.n_phases;
-        uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
-        mbar_arrive_expect_tx(&full_bar[s], a_bytes + PIECES * L.w_piece);
-        const int plane = n * p.in_cb + cb;
-        if (p.linear) {
-          // box {e, 128 px, 1 chunk, 1 plane}
-          for (int c = 0; c < kChunks; ++c)
-            for (int i = 0; i < p.lin_boxes; ++i)
-              tma_load_4d(st + c * L.a_plane + i * 128 * 16, &map_a, &full_bar[s], 0, a_px0 + i * 128, c, plane);
-        } else {
-          // box {e, wsub*stride cols, rows*stride rows, all chunks, 1 plane}
-          tma_load_5d(st, &map_a, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
-                      p.in_row0 + p.stride * row0 + p.phase_row[ph], 0, plane);
+      const uint32_t a_bytes = RAW_F32 ? static_cast<uint32_t>(p.a_px) * 64u : 2u * L.a_plane;
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int n, v0, ntile;
+        tile_coords(t, n, v0, ntile);
+        const int row0 = v0 / p.wsub;
+        const int a_px0 = p.linear ? v0 : row0 * p.wsub;
+        for (int it = 0; it < k_iters; ++it, ++g) {
+          const int cb = it / p.n_phases, ph = it % p.n_phases;
+          const int plane = n * p.in_cb + cb;
+          if (RAW_F32) {
+            const int s = g % raw_stages;
+            mbar_wait(&raw_empty[s], ((g / raw_stages) & 1u) ^ 1u);
+            uint8_t* dst = smem + L.raw_off + s * L.raw_slot;
+            mbar_arrive_expect_tx(&raw_full[s], a_bytes);
+            if (p.linear) {
+              for (int i = 0; i < p.lin_boxes; ++i)
+                tma_load_3d(dst + i * 128 * 64, &map_a, &raw_full[s], 0, a_px0 + i * 128, plane);
+            } else {
+              tma_load_4d(dst, &map_a, &raw_full[s], 0, p.in_col0 + p.phase_col[ph],
+                          p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
+            }
+          } else {
+            const int s = g % pc_stages;
+            mbar_wait(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u);
+            uint8_t* dst = smem + s * L.pc_slot;
+            const uint32_t w_bytes = static_cast<uint32_t>(p.phase_ntaps[ph]) * w_tap;
+            mbar_arrive_expect_tx(&pc_full[s], a_bytes + PIECES * w_bytes);
+            if (p.linear) {
+              for (int c = 0; c < 2; ++c)
+                for (int i = 0; i < p.lin_boxes; ++i)
+                  tma_load_4d(dst + c * L.a_plane + i * 128 * 16, &map_a, &pc_full[s], 0, a_px0 + i * 128, c, plane);
+            } else {
+              tma_load_5d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
+                          p.in_row0 + p.stride * row0 + p.phase_row[ph], 0, plane);
+            }
+            const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
+            const long long w_blk = static_cast<long long>(p.n_taps) * w_tap;
+            for (int pc = 0; pc < PIECES; ++pc)
+              bulk_load(dst + PIECES * 2 * L.a_plane + pc * L.w_piece,
+                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
+                            static_cast<long long>(p.phase_tap0[ph]) * w_tap,
+                        w_bytes, &pc_full[s]);
+          }
         }
-        for (int pc = 0; pc < PIECES; ++pc)
-          tma_load_5d(st + L.w_off + pc * L.w_piece, &map_w, &full_bar[s], 0, 0, 2 * p.nb * ntile,
-                      p.phase_tap0[ph], pc * p.cb_in + cb);
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ weight producer (fp32 path)
+    if (RAW_F32 && lane == 0) {
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
+      const long long w_blk = static_cast<long long>(p.n_taps) * w_tap;
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int n, v0, ntile;
+        tile_coords(t, n, v0, ntile);
+        for (int it = 0; it < k_iters; ++it, ++g) {
+          const int cb = it / p.n_phases, ph = it % p.n_phases;
+          const int s = g % pc_stages;
+          mbar_wait(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u);
+          const uint32_t w_bytes = static_cast<uint32_t>(p.phase_ntaps[ph]) * w_tap;
+          mbar_arrive_expect_tx(&pc_full[s], PIECES * w_bytes);
+          uint8_t* dst = smem + s * L.pc_slot + PIECES * 2 * L.a_plane;
+          for (int pc = 0; pc < PIECES; ++pc)
+            bulk_load(dst + pc * L.w_piece,
+                      wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
+                          static_cast<long long>(p.phase_tap0[ph]) * w_tap,
+                      w_bytes, &pc_full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
-    const uint32_t w_tap = (2u * p.nb) * 256u;
-    const int v_off = v0 - a_px0;
-    for (int it = 0; it < k_iters; ++it) {
-      const int s = it % n_stages;
-      const uint32_t par = static_cast<uint32_t>(it / n_stages) & 1u;
-      mbar_wait(&full_bar[s], par);
-      if (RAW_F32) mbar_wait(&conv_bar[s], par);
+    uint32_t g = 0, tl = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      int n, v0, ntile;
+      tile_coords(t, n, v0, ntile);
+      const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
+      const int v_off = v0 - a_px0;
+      const uint32_t acc = tl & 1u;
+      mbar_wait(&acc_empty[acc], ((tl >> 1) & 1u) ^ 1u);
       tc_fence_after();
-      const int ph = it % p.n_phases;
-      const uint32_t st = smem0 + static_cast<uint32_t>(s) * L.bytes;
-      if (elect_one()) {
-        const int ntaps = p.phase_ntaps[ph];
-        for (int t = 0; t < ntaps; ++t) {
-          const int shift = p.tap_shift[p.phase_tap0[ph] + t];
-          for (int mb = 0; mb < p.mb; ++mb) {
-            const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
-            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(mb * NT);
+      const uint32_t d_base = tmem_base + acc * acc_cols;
+      for (int it = 0; it < k_iters; ++it, ++g) {
+        const int s = g % pc_stages;
+        const uint32_t par = (g / pc_stages) & 1u;
+        mbar_wait(&pc_full[s], par);
+        if (RAW_F32) mbar_wait(&pc_conv[s], par);
+        tc_fence_after();
+        const int ph = it % p.n_phases;
+        const uint32_t st = smem0 + s * L.pc_slot;
+        const uint32_t wst = st + PIECES * 2 * L.a_plane;
+        if (elect_one()) {
+          const int ntaps = p.phase_ntaps[ph];
+          for (int tp = 0; tp < ntaps; ++tp) {
+            const int shift = p.tap_shift[p.phase_tap0[ph] + tp];
+            for (int mb = 0; mb < p.mb; ++mb) {
+              const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
+              const uint32_t d_tmem = d_base + static_cast<uint32_t>(mb * NT);
 #pragma unroll
-            for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
-              // products (ia, ib) with ia + ib <= 2
-              const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
-              const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
-              const uint64_t ad =
-                  make_smem_desc(st + L.pc_off + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128);
-              const uint64_t bd = make_smem_desc(st + L.w_off + ib * L.w_piece + t * w_tap, 128, 256);
-              mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || t > 0 || pr > 0) ? 1u : 0u);
+              for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
+                // products (ia, ib) with ia + ib <= 2
+                const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
+                const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
+                const uint64_t ad =
+                    make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128);
+                const uint64_t bd = make_smem_desc(wst + ib * L.w_piece + tp * w_tap, 128, 256);
+                mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || tp > 0 || pr > 0) ? 1u : 0u);
+              }
             }
           }
+          mma_commit(&pc_empty[s]);
+          if (it == k_iters - 1) mma_commit(&acc_full[acc]);
         }
-        mma_commit(&empty_bar[s]);
-        if (it == k_iters - 1) mma_commit(&accum_bar);
+        __syncwarp();
       }
-      __syncwarp();
     }
-  } else {
+  } else if (warp >= kCvtWarp0) {
+    // ------------------------------------------------------------ converters (smem fp32 -> bf16 pieces)
     if (RAW_F32) {
-      // ---------------------------------------------------------- converters (smem fp32 -> bf16 pieces)
-      const int ct = threadIdx.x - kConvWarp0 * 32;
-      const int items = 2 * p.a_px;  // (16B bf16 chunk, pixel)
-      for (int it = 0; it < k_iters; ++it) {
-        const int s = it % n_stages;
-        mbar_wait(&full_bar[s], static_cast<uint32_t>(it / n_stages) & 1u);
-        uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
-        for (int i = ct; i < items; i += kConvThreads) {
-          const int c = i / p.a_px;
-          const int j = i - c * p.a_px;
-          const float4 a = *reinterpret_cast<const float4*>(st + (2 * c) * L.a_plane + j * 16);
-          const float4 b = *reinterpret_cast<const float4*>(st + (2 * c + 1) * L.a_plane + j * 16);
-          const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-          uint8_t* dst = st + L.pc_off + c * L.a_plane + j * 16;
-          if (PIECES == 3) {
-            uint4 h, m, l;
-            split8(v, h, m, l);
-            *reinterpret_cast<uint4*>(dst) = h;
-            *reinterpret_cast<uint4*>(dst + 2 * L.a_plane) = m;
-            *reinterpret_cast<uint4*>(dst + 4 * L.a_plane) = l;
-          } else {
-            *reinterpret_cast<uint4*>(dst) = cast8(v);
+      const int ct = threadIdx.x - kCvtWarp0 * 32;
+      const int items = 2 * p.a_px;  // (pixel, 16B bf16 chunk)
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int it = 0; it < k_iters; ++it, ++g) {
+          const int rs = g % raw_stages, ps = g % pc_stages;
+          mbar_wait(&raw_full[rs], (g / raw_stages) & 1u);
+          mbar_wait(&pc_empty[ps], ((g / pc_stages) & 1u) ^ 1u);
+          const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
+          uint8_t* pcs = smem + ps * L.pc_slot;
+          for (int i = ct; i < items; i += kCvtWarps * 32) {
+            const int j = i >> 1, c = i & 1;
+            const float4 a = *reinterpret_cast<const float4*>(raw + j * 64 + c * 32);
+            const float4 b = *reinterpret_cast<const float4*>(raw + j * 64 + c * 32 + 16);
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint8_t* dst = pcs + c * L.a_plane + j * 16;
+            if (PIECES == 3) {
+              uint4 h, m, l;
+              split8(v, h, m, l);
+              *reinterpret_cast<uint4*>(dst) = h;
+              *reinterpret_cast<uint4*>(dst + 2 * L.a_plane) = m;
+              *reinterpret_cast<uint4*>(dst + 4 * L.a_plane) = l;
+            } else {
+              *reinterpret_cast<uint4*>(dst) = cast8(v);
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&raw_empty[rs]);
+            mbar_arrive(&pc_conv[ps]);
           }
         }
-        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv_bar[s]);
       }
     }
-    if (warp >= 4) {
-      // ---------------------------------------------------------- epilogue
-      mbar_wait(&accum_bar, 0);
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (warps 4..7: TMEM lane quarters)
+    const int qrow = (warp % 4) * 32;
+    const int row = qrow + lane;
+    const int v_end = p.P * p.wsub;
+    const int esz = p.out_bf16 ? 2 : 4;
+    uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      int n, v0, ntile;
+      tile_coords(t, n, v0, ntile);
+      const uint32_t acc = tl & 1u;
+      mbar_wait(&acc_full[acc], (tl >> 1) & 1u);
       tc_fence_after();
-      const int qrow = (warp % 4) * 32;
-      const int row = qrow + lane;
-      const int v_end = p.P * p.wsub;
-      const int esz = p.out_bf16 ? 2 : 4;
-      uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
+      const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
       for (int mb = 0; mb < p.mb; ++mb) {
         const int v = v0 + mb * 128 + row;
         const int pp = v / p.wsub;
@@ -274,11 +368,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const bool valid = v < v_end && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
-        for (int g = 0; g < p.nb; ++g) {
+        for (int gq = 0; gq < p.nb; ++gq) {
           uint32_t r[16];
-          tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(mb * NT + g * 16), r);
+          tmem_ld16(d_base + static_cast<uint32_t>(mb * NT + gq * 16), r);
           tmem_ld_wait();
-          const int kb = ntile * p.nb + g;
+          const int kb = ntile * p.nb + gq;
           if (!valid || kb >= p.kb_out) continue;
           float vals[16];
 #pragma unroll
@@ -305,6 +399,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
   }
   tc_fence_before();

@@ -36,6 +36,9 @@ struct FwdParams {
   int phase_ntaps[kMaxPhases], phase_tap0[kMaxPhases];
   int tap_shift[kMaxTaps];  // phase-sorted
   int taps_box;        // weight box taps (max taps per phase)
+  int n_taps;          // total taps (phase-sorted) in the prepared weights
+  int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
+  const void* wprep;   // prepared bf16 weights [pc][cb][ntile][tap][2nb][16][8]
   // output surface (blocked, may be a strided lattice)
   void* out;
   int out_bf16;

@@ -160,25 +160,28 @@ __global__ void rehalo_kernel(const T* __restrict__ src, T* __restrict__ dst, in
 }
 
 // Weight prep for the tcgen05 kernels (vlen 16). dst layout (bf16):
-//   [(pc * cb_in + cbi)][t][ng][ci(16)][kk(8)],  ng = 2*kb_out groups of 8 output lanes
-// out channel o = (ng/2)*16 + (ng%2)*8 + kk, in channel i = cbi*16 + ci.
+//   [pc][cbi][ntile][t][ng][ci(16)][kk(8)],  ng = 2*nb groups of 8 output lanes per tile
+// out channel o = (ntile*nb + ng/2)*16 + (ng%2)*8 + kk, in channel i = cbi*16 + ci; every
+// (pc, cbi, ntile, phase) slice is contiguous so the kernel stages it with one bulk copy.
 // tapmap[t] = source tap r*S+s (or -1 for an all-zero tap).
 // dual = 0: out = k, in = c (forward). dual = 1: out = c, in = k (backward-data).
 // pieces = 3 stores the exact hi/mid/lo bf16 split of each fp32 weight.
 template <typename S>
 __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
                                    int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps, int cb_in,
-                                   int kb_out, int dual, int pieces) {
-  const long long per_piece = static_cast<long long>(cb_in) * n_taps * (2 * kb_out) * 128;
+                                   int nb, int n_ntiles, int dual, int pieces) {
+  const long long per_piece = static_cast<long long>(cb_in) * n_ntiles * n_taps * (2 * nb) * 128;
   DCONV_GRID_STRIDE(e, per_piece) {
     const int kk = static_cast<int>(e % 8);
     const int ci = static_cast<int>((e / 8) % 16);
     long long q = e / 128;
-    const int ng = static_cast<int>(q % (2 * kb_out));
-    q /= (2 * kb_out);
+    const int ng = static_cast<int>(q % (2 * nb));
+    q /= (2 * nb);
     const int t = static_cast<int>(q % n_taps);
-    const int cbi = static_cast<int>(q / n_taps);
-    const int ob = ng / 2, ol = (ng % 2) * 8 + kk;  // out block / lane
+    q /= n_taps;
+    const int nt = static_cast<int>(q % n_ntiles);
+    const int cbi = static_cast<int>(q / n_ntiles);
+    const int ob = nt * nb + ng / 2, ol = (ng % 2) * 8 + kk;  // out block / lane
     const int ib = cbi, il = ci;                    // in block / lane
     const int rs = tapmap[t];
     float val = 0.0f;
