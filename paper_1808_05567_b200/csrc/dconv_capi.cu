@@ -112,7 +112,8 @@ EncodeTiledFn encode_fn() {
 }
 
 CUtensorMap encode(int bf16, int rank, const void* base, const uint64_t* dims, const uint64_t* strides_bytes,
-                   const uint32_t* box, const uint32_t* estr, const char* what) {
+                   const uint32_t* box, const uint32_t* estr, const char* what,
+                   CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   cuuint64_t d[5], st[4];
@@ -125,7 +126,7 @@ CUtensorMap encode(int bf16, int rank, const void* base, const uint64_t* dims, c
   }
   const CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                  rank, const_cast<void*>(base), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(DCONV_ERR_CUDA, std::string("tensor map encode failed (") + what + ") code " +
                                                   std::to_string(static_cast<int>(r)));
@@ -168,6 +169,7 @@ int sm_count() {
 }
 
 constexpr int kSmemBudget = 227 * 1024 - 2048;  // dynamic smem per CTA (static barriers excluded)
+constexpr int kFwdBudget = kSmemBudget - static_cast<int>(kEpiStageBytes) - 1024;  // minus epilogue staging
 
 int grid1d(int64_t total, int block = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv64(total, block), 148LL * 16)));
@@ -233,6 +235,7 @@ struct FwdLaunch {
   dim3 grid;
   int stages;      // piece-ring depth
   int raw_stages;  // raw-ring depth (fp32 activations)
+  int w_stages;    // weight-ring depth
   size_t smem;
   bool raw_f32;
   int pieces;
@@ -280,17 +283,23 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   const int kb_total = pb.kb_out;
   const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : 0;
   const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16) : 0;
-  int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0;
+  int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0, w_st = 0, acc_bufs = 2;
   FwdSmem layout;
   bool found = false;
   // widest N tile first (fewer activation re-reads), then the largest M tile;
-  // two TMEM accumulators of mb*16*nb columns must fit in 512
-  for (int want_pc : {3, 2}) {
+  // two TMEM accumulators of mb*16*nb columns must fit in 512. Weight stages
+  // hold up to w_taps taps (big filters stream taps through several stages).
+  int w_taps = taps.taps_box;
+  for (int want_pc : {3, 2, 1}) {
     for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
       const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
       for (int mb : {2, 1}) {
         if (want_mb && mb != want_mb) continue;
-        if (mb * 16 * nb > 256) continue;
+        // accumulators: (pieces == 3 ? 2 : 1) x mb x 16nb columns, double-buffered when they fit
+        const int acc_cols = (pieces == 3 ? 2 : 1) * mb * 16 * nb;
+        if (acc_cols > 512) continue;
+        const int bufs = 2 * acc_cols <= 512 ? 2 : 1;
+        if (bufs == 1 && mb == 2) continue;
         const int Lpx = 128 * mb;
         int apx, lb = 0;
         if (linear) {
@@ -301,28 +310,48 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           if (p.wsub * st > 256 || rows_box * st > 256) continue;
           apx = rows_box * p.wsub;
         }
-        const FwdSmem lay = fwd_smem_layout(apx, taps.taps_box, nb, pieces, raw_f32, 1);
-        int pcs, rws = 0;
+        // weight stage <= 32 KB
+        int wt = taps.taps_box;
+        while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > 32 * 1024)
+          wt = (wt + 1) / 2;
+        const FwdSmem lay = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1);
+        int pcs, rws = 0, wss;
+        // weight ring: enough slots to cover L2 latency, bounded to ~1/4 of smem
+        wss = std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lay.w_slot)));
         if (raw_f32) {
           pcs = want_pc;
-          const int left = kSmemBudget - pcs * static_cast<int>(lay.pc_slot);
+          int left = kFwdBudget - pcs * static_cast<int>(lay.pc_slot) - wss * static_cast<int>(lay.w_slot);
           rws = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.raw_slot)) : 0;
-          if (rws < 2) continue;
+          if (rws < 3 && wss > 2) {  // give raw slots priority over weight depth
+            wss = 2;
+            left = kFwdBudget - pcs * static_cast<int>(lay.pc_slot) - wss * static_cast<int>(lay.w_slot);
+            rws = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.raw_slot)) : 0;
+          }
+          if (rws < (want_pc == 1 ? 1 : 2)) continue;
         } else {
-          pcs = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.pc_slot));
+          int left = kFwdBudget - wss * static_cast<int>(lay.w_slot);
+          pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.pc_slot)) : 0;
+          if (pcs < want_pc && wss > 2) {
+            wss = 2;
+            left = kFwdBudget - wss * static_cast<int>(lay.w_slot);
+            pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.pc_slot)) : 0;
+          }
           if (pcs < want_pc) continue;
         }
         tile.mb = mb;
         tile.nb = nb;
+        acc_bufs = bufs;
         pc_st = pcs;
         raw_st = rws;
+        w_st = wss;
+        w_taps = wt;
         if (cfg && cfg->stages > 0) {
           if (raw_f32)
-            raw_st = std::max(2, std::min(cfg->stages, raw_st));
+            raw_st = std::max(1, std::min(cfg->stages, raw_st));
           else
-            pc_st = std::max(2, std::min(cfg->stages, pc_st));
+            pc_st = std::max(1, std::min(cfg->stages, pc_st));
         }
-        layout = fwd_smem_layout(apx, taps.taps_box, nb, pieces, raw_f32, pc_st);
+        layout = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, pc_st, w_st);
         a_px = apx;
         lin_boxes = lb;
         found = true;
@@ -335,16 +364,19 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   if (!found) fail(DCONV_ERR_PLAN_INFEASIBLE, "no forward tile fits shared memory / TMA box limits");
   p.mb = tile.mb;
   p.nb = tile.nb;
+  p.acc_bufs = acc_bufs;
   p.a_px = a_px;
   p.lin_boxes = lin_boxes;
   p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
   L.stages = pc_st;
   L.raw_stages = raw_st;
-  L.smem = static_cast<size_t>(layout.raw_off) + static_cast<size_t>(raw_st) * layout.raw_slot;
+  L.w_stages = w_st;
+  L.smem = static_cast<size_t>(layout.raw_off) + static_cast<size_t>(raw_st) * layout.raw_slot + kEpiStageBytes;
   const int n_tiles = in.n * p.tiles_per_img * cdiv(kb_total, tile.nb);
   L.grid = dim3(static_cast<unsigned>(std::min(n_tiles, sm_count())), 1, 1);
 
   p.n_taps = static_cast<int>(taps.r.size());
+  p.w_taps = w_taps;
   p.n_ntiles = cdiv(kb_total, tile.nb);
   p.wprep = wprep;
   // activation map
@@ -355,14 +387,14 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
       const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
       const uint64_t strides[2] = {64, 64ull * hp * wp};
       const uint32_t box[3] = {16, 128, 1};
-      L.map_a = encode(0, 3, in.data, dims, strides, box, nullptr, "activation linear f32");
+      L.map_a = encode(0, 3, in.data, dims, strides, box, nullptr, "activation linear f32", CU_TENSOR_MAP_SWIZZLE_64B);
     } else {
       const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * 64;
       const uint64_t dims[4] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), planes};
       const uint64_t strides[3] = {64, 64ull * wp, 64ull * wp * hp};
       const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 1};
       const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
-      L.map_a = encode(0, 4, base, dims, strides, box, estr, "activation rows f32");
+      L.map_a = encode(0, 4, base, dims, strides, box, estr, "activation rows f32", CU_TENSOR_MAP_SWIZZLE_64B);
     }
   } else if (linear) {
     // bf16 straight into the canonical [chunk][pixel][16B] layout
@@ -381,11 +413,16 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   return L;
 }
 
+long long* g_fwd_dbg = nullptr;  // dconv_debug_counters(): per-CTA role cycle counters
+int g_fwd_dbg_mode = 0;
+
 void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
+  L.p.dbg = g_fwd_dbg;
+  L.p.dbg_mode = g_fwd_dbg_mode;
   auto go = [&](auto kern) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                "smem attribute");
-    kern<<<L.grid, kFwdThreadsP, L.smem, stream>>>(L.map_a, L.p, L.raw_stages, L.stages);
+    kern<<<L.grid, kFwdThreadsP, L.smem, stream>>>(L.map_a, L.p, L.raw_stages, L.stages, L.w_stages);
   };
   if (L.raw_f32) {
     if (L.pieces == 3)
@@ -424,9 +461,10 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 std::string json_tile(const FwdLaunch& L) {
   char buf[512];
   std::snprintf(buf, sizeof(buf),
-                "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,"
+                "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
                 "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d}",
-                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.smem, L.grid.x,
+                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
+                L.grid.x,
                 L.p.n_img * L.p.tiles_per_img * L.p.n_ntiles, L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px);
   return buf;
 }
@@ -1159,6 +1197,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   const bool linear = st == 1 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 && in.halo_h == 0 &&
                       in.halo_w == 0 && dout.halo_h == 0 && dout.halo_w == 0;
   p.linear = linear ? 1 : 0;
+  // tap stacking for narrow inputs (< 8 channel blocks, e.g. the 3-channel stem)
+  const bool stacked = !linear && cb < 8 && s.R * s.S > 1;
+  p.stack = stacked ? 8 / cb : 1;
+  p.cb_eff = stacked ? cb : 8;
   // k tile
   int n_kt = cdiv(kb, 16);
   p.nb = cdiv(kb, n_kt);
@@ -1203,7 +1245,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     for (auto& gr : geo) {
       const int wsub = gr.first, rows_ps = gr.second;
       if (rows_ps > P && !(wsub == wmin && rows_ps == base_rows)) continue;  // bands taller than the image
-      const int in_rows = rows_ps + maxshift_rows + (s2max > 0 ? 1 : 0);
+      const int in_rows = stacked ? rows_ps : rows_ps + maxshift_rows + (s2max > 0 ? 1 : 0);
       add(wsub, rows_ps, in_rows, rows_ps * wsub, in_rows * wsub);
     }
   }
@@ -1237,17 +1279,35 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     p.phase_row[i] = taps.phase_row[i];
     p.phase_col[i] = taps.phase_col[i];
   }
-  // tap groups: per phase, <= 512 TMEM columns of accumulators
-  p.tg = std::max(1, std::min(512 / NT, taps.taps_box));
-  p.n_tgroups = 0;
   for (int ph = 0; ph < taps.n_phases; ++ph)
-    for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += p.tg) {
+    for (int t = 0; t < taps.phase_ntaps[ph]; ++t) p.tap_ph[taps.phase_tap0[ph] + t] = ph;
+  for (size_t t = 0; t < taps.r.size(); ++t) {
+    p.tap_r2[t] = taps.r2[t];
+    p.tap_s2[t] = taps.s2[t];
+  }
+  p.n_tgroups = 0;
+  if (stacked) {
+    // one accumulator per CTA holding `stack` consecutive (phase-sorted) taps
+    p.tg = 1;
+    for (int t0 = 0; t0 < static_cast<int>(taps.r.size()); t0 += p.stack) {
       if (p.n_tgroups >= kMaxTapGroups) fail(DCONV_ERR_UNSUPPORTED, "too many tap groups");
-      p.tg_phase[p.n_tgroups] = ph;
-      p.tg_tap0[p.n_tgroups] = taps.phase_tap0[ph] + t0;
-      p.tg_ntaps[p.n_tgroups] = std::min(p.tg, taps.phase_ntaps[ph] - t0);
+      p.tg_phase[p.n_tgroups] = p.tap_ph[t0];
+      p.tg_tap0[p.n_tgroups] = t0;
+      p.tg_ntaps[p.n_tgroups] = std::min(p.stack, static_cast<int>(taps.r.size()) - t0);
       ++p.n_tgroups;
     }
+  } else {
+    // tap groups: per phase, <= 512 TMEM columns of accumulators
+    p.tg = std::max(1, std::min(512 / NT, taps.taps_box));
+    for (int ph = 0; ph < taps.n_phases; ++ph)
+      for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += p.tg) {
+        if (p.n_tgroups >= kMaxTapGroups) fail(DCONV_ERR_UNSUPPORTED, "too many tap groups");
+        p.tg_phase[p.n_tgroups] = ph;
+        p.tg_tap0[p.n_tgroups] = taps.phase_tap0[ph] + t0;
+        p.tg_ntaps[p.n_tgroups] = std::min(p.tg, taps.phase_ntaps[ph] - t0);
+        ++p.n_tgroups;
+      }
+  }
   // split-K: >= 2 waves of CTAs, >= 2 stages per split
   const int tiles = n_ctiles * p.n_tgroups * n_ktiles;
   int splits = cdiv(2 * sm_count(), tiles);
@@ -1278,7 +1338,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     const char* base = reinterpret_cast<const char*>(data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 32;
     const uint64_t dims[5] = {8, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), 2, planes};
     const uint64_t strides[4] = {32, static_cast<uint64_t>(wp) * 32, 16, static_cast<uint64_t>(wp) * hp * 32};
-    const uint32_t box_in[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st), 2, 8};
+    const uint32_t box_in[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st), 2,
+                                static_cast<uint32_t>(p.cb_eff)};
     const uint32_t box_do[5] = {8, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps), 2,
                                 static_cast<uint32_t>(p.nb)};
     const uint32_t estr_in[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};
@@ -1460,3 +1521,17 @@ float dconv_profile_last_ms(int which) {
 }
 
 }  // extern "C"
+
+extern "C" {
+/* debug: point the forward kernel's per-CTA role counters at a device buffer
+ * (>= 16 * #SMs int64), or null to disable */
+int dconv_debug_counters(void* dev_buf) {
+  g_fwd_dbg = reinterpret_cast<long long*>(dev_buf);
+  return DCONV_OK;
+}
+/* debug: forward-kernel ablation bits (1 skip global stores, 2 skip TMEM loads); 0 in production */
+int dconv_debug_mode(int mode) {
+  g_fwd_dbg_mode = mode;
+  return DCONV_OK;
+}
+}

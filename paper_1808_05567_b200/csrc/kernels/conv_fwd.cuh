@@ -109,23 +109,53 @@ struct FwdSmem {
   uint32_t a_plane;  // bytes per 16B-chunk plane of the A pieces (a_px * 16)
   uint32_t raw_slot; // bytes per raw slot (a_px * 64), 0 for bf16 inputs
   uint32_t w_piece;  // bytes per weight piece
-  uint32_t pc_slot;  // bytes per piece slot
-  uint32_t raw_off;  // raw ring starts after the piece ring
+  uint32_t pc_slot;  // bytes per A-piece slot
+  uint32_t w_slot;   // bytes per weight slot (all pieces)
+  uint32_t w_off;    // weight ring start (after the piece ring)
+  uint32_t raw_off;  // raw ring start (after the weight ring)
+  uint32_t epi_off;  // epilogue staging (4 warps x 32 pixels x 64B) after the raw ring
 };
 
+// three independent rings: A pieces (MMA operand), weights (MMA operand, own
+// prefetch depth so their L2 latency hides behind other stages), raw fp32
 __host__ __device__ inline FwdSmem fwd_smem_layout(int a_px, int taps_box, int nb, int pieces, bool raw_f32,
-                                                   int piece_stages) {
+                                                   int piece_stages, int w_stages) {
   FwdSmem L;
   L.a_plane = static_cast<uint32_t>(a_px) * 16u;
   L.raw_slot = raw_f32 ? ((static_cast<uint32_t>(a_px) * 64u + 1023u) & ~1023u) : 0u;
-  L.w_piece = static_cast<uint32_t>(taps_box) * (2u * nb) * 256u;
-  L.pc_slot = (static_cast<uint32_t>(pieces) * (2u * L.a_plane + L.w_piece) + 1023u) & ~1023u;
-  L.raw_off = static_cast<uint32_t>(piece_stages) * L.pc_slot;
+  L.w_piece = static_cast<uint32_t>(taps_box) * (2u * nb) * 256u;  // taps_box = taps per weight stage
+  L.pc_slot = (static_cast<uint32_t>(pieces) * 2u * L.a_plane + 1023u) & ~1023u;
+  L.w_slot = (static_cast<uint32_t>(pieces) * L.w_piece + 1023u) & ~1023u;
+  L.w_off = static_cast<uint32_t>(piece_stages) * L.pc_slot;
+  L.raw_off = L.w_off + static_cast<uint32_t>(w_stages) * L.w_slot;
+  L.epi_off = 0;  // set by the caller: raw_off + raw_stages * raw_slot
   return L;
 }
+constexpr uint32_t kEpiStageBytes = 0;
 
-constexpr int kFwdWarps = 14;  // w0 A/raw producer, w1 MMA, w2 W producer, w3 idle, w4-7 epilogue, w8-13 converters
+// 16B chunk k of pixel j in a 64B-row buffer written by TMA with SWIZZLE_64B
+// (Swizzle<2,4,3>: chunk bits [4,6) ^= row-pair bits [7,9))
+__device__ __forceinline__ uint32_t sw64(uint32_t j, uint32_t k) { return j * 64u + ((k ^ ((j >> 1) & 3u)) << 4); }
+
+// optional per-CTA role counters (debug builds of the plan only): slot layout
+// [0] producer wait, [1] converter wait raw, [2] converter wait slot, [3] converter busy,
+// [4] MMA wait operands, [5] MMA wait accumulator, [6] epilogue wait, [7] epilogue busy, [8] total
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long* acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
+// w0 activation producer, w1 MMA, w2 weight producer, w3 idle, w4-7 epilogue
+// (one warp per TMEM lane quarter), w8-13 converters in two groups of three that
+// take alternate pipeline stages
+constexpr int kFwdWarps = 14;
 constexpr int kFwdThreadsP = kFwdWarps * 32;
+constexpr int kEpiWarp0 = 4, kEpiWarps = 4;
 constexpr int kCvtWarp0 = 8, kCvtWarps = 6;
 
 // Persistent implicit-GEMM forward: grid = #SMs, CTA c handles tiles c, c+G, ...
@@ -134,40 +164,54 @@ constexpr int kCvtWarp0 = 8, kCvtWarps = 6;
 template <bool RAW_F32, int PIECES>
 __global__ void __launch_bounds__(kFwdThreadsP, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ FwdParams p, int raw_stages,
-                    int pc_stages) {
+                    int pc_stages, int w_stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
   __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_conv[kMaxStages], pc_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t w_full[kMaxStages], w_empty[kMaxStages];
   __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const FwdSmem L = fwd_smem_layout(p.a_px, p.taps_box, p.nb, PIECES, RAW_F32, pc_stages);
+  FwdSmem L = fwd_smem_layout(p.a_px, p.w_taps, p.nb, PIECES, RAW_F32, pc_stages, w_stages);
+  L.epi_off = L.raw_off + static_cast<uint32_t>(raw_stages) * L.raw_slot;
   const uint32_t smem0 = smem_u32(smem);
   const int NT = 16 * p.nb;
   const int k_iters = p.cb_in * p.n_phases;
   const int n_mtiles = p.n_img * p.tiles_per_img;
   const int n_tiles = n_mtiles * p.n_ntiles;
-  const uint32_t acc_cols = static_cast<uint32_t>(p.mb * NT);
+  // fp32-accurate mode keeps the a0*b0 products and the five correction
+  // products in separate accumulators: the large sum then takes 6x fewer
+  // (truncating) fp32 accumulation steps; the epilogue adds the two
+  constexpr uint32_t kAccs = PIECES == 3 ? 2u : 1u;
+  const uint32_t acc_cols = kAccs * static_cast<uint32_t>(p.mb * NT);
+  // two converter groups alternate stages; a 1-deep ring would let the second
+  // group wait on a phase two ahead (parity aliasing), so it falls back to one group
+  const int cvt_groups = (raw_stages >= 2 && pc_stages >= 2) ? 2 : 1;
+  const int cvt_group_warps = kCvtWarps / cvt_groups;
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < 2u * acc_cols) tmem_cols <<= 1;
+  while (tmem_cols < static_cast<uint32_t>(p.acc_bufs) * acc_cols) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     for (int s = 0; s < raw_stages; ++s) {
       mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], kCvtWarps);
+      mbar_init(&raw_empty[s], cvt_group_warps);
     }
     for (int s = 0; s < pc_stages; ++s) {
       mbar_init(&pc_full[s], 1);
-      mbar_init(&pc_conv[s], kCvtWarps);
+      mbar_init(&pc_conv[s], cvt_group_warps);
       mbar_init(&pc_empty[s], 1);
+    }
+    for (int s = 0; s < w_stages; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);
+      mbar_init(&acc_empty[a], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -176,6 +220,9 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
+  long long* dbg = p.dbg ? p.dbg + static_cast<long long>(blockIdx.x) * 16 : nullptr;
+  long long t_start = clock64();
+  long long c_a = 0, c_b = 0, c_c = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
 
   // tile t -> (n, v0, ntile); output-channel tiles innermost so consecutive
   // CTAs share the activation tile through L2
@@ -202,7 +249,7 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
           const int plane = n * p.in_cb + cb;
           if (RAW_F32) {
             const int s = g % raw_stages;
-            mbar_wait(&raw_empty[s], ((g / raw_stages) & 1u) ^ 1u);
+            mbar_wait_t(&raw_empty[s], ((g / raw_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + L.raw_off + s * L.raw_slot;
             mbar_arrive_expect_tx(&raw_full[s], a_bytes);
             if (p.linear) {
@@ -214,10 +261,9 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
             }
           } else {
             const int s = g % pc_stages;
-            mbar_wait(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u);
+            mbar_wait_t(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
-            const uint32_t w_bytes = static_cast<uint32_t>(p.phase_ntaps[ph]) * w_tap;
-            mbar_arrive_expect_tx(&pc_full[s], a_bytes + PIECES * w_bytes);
+            mbar_arrive_expect_tx(&pc_full[s], a_bytes);
             if (p.linear) {
               for (int c = 0; c < 2; ++c)
                 for (int i = 0; i < p.lin_boxes; ++i)
@@ -226,105 +272,129 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
               tma_load_5d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
                           p.in_row0 + p.stride * row0 + p.phase_row[ph], 0, plane);
             }
-            const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
-            const long long w_blk = static_cast<long long>(p.n_taps) * w_tap;
-            for (int pc = 0; pc < PIECES; ++pc)
-              bulk_load(dst + PIECES * 2 * L.a_plane + pc * L.w_piece,
-                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
-                            static_cast<long long>(p.phase_tap0[ph]) * w_tap,
-                        w_bytes, &pc_full[s]);
           }
         }
       }
+      if (dbg) dbg[0] = c_a;
     }
   } else if (warp == 2) {
-    // ------------------------------------------------------------ weight producer (fp32 path)
-    if (RAW_F32 && lane == 0) {
+    // ------------------------------------------------------------ weight producer (own ring)
+    // one weight stage = up to w_taps taps of one (c_b, phase): large filters
+    // (7x7 stem) stream their taps through several small stages
+    if (lane == 0) {
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
       const long long w_blk = static_cast<long long>(p.n_taps) * w_tap;
       uint32_t g = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         int n, v0, ntile;
         tile_coords(t, n, v0, ntile);
-        for (int it = 0; it < k_iters; ++it, ++g) {
+        for (int it = 0; it < k_iters; ++it) {
           const int cb = it / p.n_phases, ph = it % p.n_phases;
-          const int s = g % pc_stages;
-          mbar_wait(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u);
-          const uint32_t w_bytes = static_cast<uint32_t>(p.phase_ntaps[ph]) * w_tap;
-          mbar_arrive_expect_tx(&pc_full[s], PIECES * w_bytes);
-          uint8_t* dst = smem + s * L.pc_slot + PIECES * 2 * L.a_plane;
-          for (int pc = 0; pc < PIECES; ++pc)
-            bulk_load(dst + pc * L.w_piece,
-                      wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
-                          static_cast<long long>(p.phase_tap0[ph]) * w_tap,
-                      w_bytes, &pc_full[s]);
+          for (int t0 = 0; t0 < p.phase_ntaps[ph]; t0 += p.w_taps, ++g) {
+            const int nt = min(p.w_taps, p.phase_ntaps[ph] - t0);
+            const int s = g % w_stages;
+            mbar_wait(&w_empty[s], ((g / w_stages) & 1u) ^ 1u);
+            const uint32_t w_bytes = static_cast<uint32_t>(nt) * w_tap;
+            mbar_arrive_expect_tx(&w_full[s], PIECES * w_bytes);
+            uint8_t* dst = smem + L.w_off + s * L.w_slot;
+            for (int pc = 0; pc < PIECES; ++pc)
+              bulk_load(dst + pc * L.w_piece,
+                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
+                            static_cast<long long>(p.phase_tap0[ph] + t0) * w_tap,
+                        w_bytes, &w_full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
-    uint32_t g = 0, tl = 0;
+    uint32_t g = 0, gw = 0, tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
       tile_coords(t, n, v0, ntile);
       const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
       const int v_off = v0 - a_px0;
-      const uint32_t acc = tl & 1u;
-      mbar_wait(&acc_empty[acc], ((tl >> 1) & 1u) ^ 1u);
+      const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+      const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+      mbar_wait_t(&acc_empty[acc], apar ^ 1u, dbg ? &c_b : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols;
       for (int it = 0; it < k_iters; ++it, ++g) {
         const int s = g % pc_stages;
         const uint32_t par = (g / pc_stages) & 1u;
-        mbar_wait(&pc_full[s], par);
-        if (RAW_F32) mbar_wait(&pc_conv[s], par);
-        tc_fence_after();
+        if (RAW_F32)
+          mbar_wait_t(&pc_conv[s], par, dbg ? &c_a : nullptr);
+        else
+          mbar_wait_t(&pc_full[s], par, dbg ? &c_a : nullptr);
         const int ph = it % p.n_phases;
         const uint32_t st = smem0 + s * L.pc_slot;
-        const uint32_t wst = st + PIECES * 2 * L.a_plane;
-        if (elect_one()) {
-          const int ntaps = p.phase_ntaps[ph];
-          for (int tp = 0; tp < ntaps; ++tp) {
-            const int shift = p.tap_shift[p.phase_tap0[ph] + tp];
-            for (int mb = 0; mb < p.mb; ++mb) {
-              const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
-              const uint32_t d_tmem = d_base + static_cast<uint32_t>(mb * NT);
+        const int ntaps = p.phase_ntaps[ph];
+        for (int t0 = 0; t0 < ntaps; t0 += p.w_taps, ++gw) {
+          const int ws = gw % w_stages;
+          mbar_wait_t(&w_full[ws], (gw / w_stages) & 1u, dbg ? &c_a : nullptr);
+          tc_fence_after();
+          const uint32_t wst = smem0 + L.w_off + ws * L.w_slot;
+          const int nt = min(p.w_taps, ntaps - t0);
+          if (elect_one()) {
+            for (int tp = 0; tp < nt; ++tp) {
+              const int shift = p.tap_shift[p.phase_tap0[ph] + t0 + tp];
+              for (int mb = 0; mb < p.mb; ++mb) {
+                const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
+                const uint32_t d_hi = d_base + static_cast<uint32_t>(mb * NT);
+                const uint32_t d_lo = d_hi + static_cast<uint32_t>(p.mb * NT);
+                const bool first = it == 0 && t0 == 0 && tp == 0;
 #pragma unroll
-              for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
-                // products (ia, ib) with ia + ib <= 2
-                const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
-                const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
-                const uint64_t ad =
-                    make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128);
-                const uint64_t bd = make_smem_desc(wst + ib * L.w_piece + tp * w_tap, 128, 256);
-                mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || tp > 0 || pr > 0) ? 1u : 0u);
+                for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
+                  // products (ia, ib) with ia + ib <= 2
+                  const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
+                  const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
+                  const uint64_t ad =
+                      make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128);
+                  const uint64_t bd = make_smem_desc(wst + ib * L.w_piece + tp * w_tap, 128, 256);
+                  if (pr == 0)
+                    mma_bf16(d_hi, ad, bd, idesc, first ? 0u : 1u);
+                  else
+                    mma_bf16(d_lo, ad, bd, idesc, (first && pr == 1) ? 0u : 1u);
+                }
               }
             }
+            mma_commit(&w_empty[ws]);
+            if (t0 + p.w_taps >= ntaps) {
+              mma_commit(&pc_empty[s]);
+              if (it == k_iters - 1) mma_commit(&acc_full[acc]);
+            }
           }
-          mma_commit(&pc_empty[s]);
-          if (it == k_iters - 1) mma_commit(&acc_full[acc]);
+          __syncwarp();
         }
-        __syncwarp();
       }
+    }
+    if (dbg && lane == 0) {
+      dbg[4] = c_a;
+      dbg[5] = c_b;
     }
   } else if (warp >= kCvtWarp0) {
     // ------------------------------------------------------------ converters (smem fp32 -> bf16 pieces)
     if (RAW_F32) {
-      const int ct = threadIdx.x - kCvtWarp0 * 32;
-      const int items = 2 * p.a_px;  // (pixel, 16B bf16 chunk)
+      const int grp = (warp - kCvtWarp0) / cvt_group_warps;  // this group converts stages g % cvt_groups == grp
+      const int ct = threadIdx.x - (kCvtWarp0 + grp * cvt_group_warps) * 32;
+      const int items = 2 * ((p.a_px + 31) / 32) * 32;  // (pixel, 16B bf16 chunk)
       uint32_t g = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         for (int it = 0; it < k_iters; ++it, ++g) {
+          if (static_cast<int>(g % cvt_groups) != grp) continue;
           const int rs = g % raw_stages, ps = g % pc_stages;
-          mbar_wait(&raw_full[rs], (g / raw_stages) & 1u);
-          mbar_wait(&pc_empty[ps], ((g / pc_stages) & 1u) ^ 1u);
+          mbar_wait_t(&raw_full[rs], (g / raw_stages) & 1u, dbg ? &c_a : nullptr);
+          mbar_wait_t(&pc_empty[ps], ((g / pc_stages) & 1u) ^ 1u, dbg ? &c_b : nullptr);
           const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
           uint8_t* pcs = smem + ps * L.pc_slot;
-          for (int i = ct; i < items; i += kCvtWarps * 32) {
-            const int j = i >> 1, c = i & 1;
-            const float4 a = *reinterpret_cast<const float4*>(raw + j * 64 + c * 32);
-            const float4 b = *reinterpret_cast<const float4*>(raw + j * 64 + c * 32 + 16);
+          for (int i = ct; i < items; i += cvt_group_warps * 32) {
+            // a warp converts one bf16 chunk c of 32 consecutive pixels: swizzled
+            // reads and contiguous piece writes are both bank-conflict free
+            const int c = (i >> 5) & 1, j = ((i >> 6) << 5) | (i & 31);
+            if (j >= p.a_px) continue;
+            const float4 a = *reinterpret_cast<const float4*>(raw + sw64(j, 2 * c));
+            const float4 b = *reinterpret_cast<const float4*>(raw + sw64(j, 2 * c + 1));
             const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
             uint8_t* dst = pcs + c * L.a_plane + j * 16;
             if (PIECES == 3) {
@@ -345,11 +415,17 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
           }
         }
       }
+      if (dbg && threadIdx.x == kCvtWarp0 * 32) {
+        dbg[1] = c_a;
+        dbg[2] = c_b;
+        dbg[3] = clock64() - t_start - c_a - c_b;
+      }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue (warps 4..7: TMEM lane quarters)
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue (warps 4..7)
+    // warp -> TMEM lane quarter (warp % 4)
     const int qrow = (warp % 4) * 32;
-    const int row = qrow + lane;
+    const int g_lo = 0, g_hi = p.nb;
     const int v_end = p.P * p.wsub;
     const int esz = p.out_bf16 ? 2 : 4;
     uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
@@ -357,45 +433,57 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
       tile_coords(t, n, v0, ntile);
-      const uint32_t acc = tl & 1u;
-      mbar_wait(&acc_full[acc], (tl >> 1) & 1u);
+      const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+      const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+      mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
       for (int mb = 0; mb < p.mb; ++mb) {
-        const int v = v0 + mb * 128 + row;
+        const int v = v0 + mb * 128 + qrow + lane;
         const int pp = v / p.wsub;
         const int qq = v - pp * p.wsub;
         const bool valid = v < v_end && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
-        for (int gq = 0; gq < p.nb; ++gq) {
-          uint32_t r[16];
-          tmem_ld16(d_base + static_cast<uint32_t>(mb * NT + gq * 16), r);
+        for (int g0 = g_lo; g0 < g_hi; g0 += 2) {
+          // two 16-column TMEM loads in flight, one wait
+          const int ng = min(2, g_hi - g0);
+          uint32_t r[2][16], rl[2][16];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (k < ng && !(p.dbg_mode & 2)) {
+              tmem_ld16(d_base + static_cast<uint32_t>(mb * NT + (g0 + k) * 16), r[k]);
+              if (PIECES == 3) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
+            }
           tmem_ld_wait();
-          const int kb = ntile * p.nb + gq;
-          if (!valid || kb >= p.kb_out) continue;
-          float vals[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) vals[e] = __uint_as_float(r[e]);
-          // APPLY after the final reduction step (kernel_streams.cpp:96-120)
-          if (p.bias != nullptr) {
+          for (int k = 0; k < 2; ++k) {
+            const int kb = ntile * p.nb + g0 + k;
+            if (k >= ng || !valid || kb >= p.kb_out) continue;
+            float vals[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
-          }
-          if (p.relu) {
+            for (int e = 0; e < 16; ++e)
+              vals[e] = PIECES == 3 ? __uint_as_float(r[k][e]) + __uint_as_float(rl[k][e]) : __uint_as_float(r[k][e]);
+            // APPLY after the final reduction step (kernel_streams.cpp:96-120)
+            if (p.bias != nullptr) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) vals[e] = vals[e] > 0.0f ? vals[e] : 0.0f;
-          }
-          const long long plane = static_cast<long long>(n) * p.out_cb + kb;
-          store16(obase + ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz, vals, p.out_bf16);
-          if (p.out_halo_h | p.out_halo_w) {
-            // zero the halo pixels whose clamp onto the interior is this pixel
-            const int dy0 = pp == 0 ? -p.out_halo_h : 0, dy1 = pp == p.P - 1 ? p.out_halo_h : 0;
-            const int dx0 = qq == 0 ? -p.out_halo_w : 0, dx1 = qq == p.Q - 1 ? p.out_halo_w : 0;
-            for (int dy = dy0; dy <= dy1; ++dy)
-              for (int dx = dx0; dx <= dx1; ++dx)
-                if (dy != 0 || dx != 0)
-                  store16_zero(obase + ((plane * p.out_hp + y + dy) * p.out_wp + x + dx) * 16LL * esz, p.out_bf16);
+              for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = vals[e] > 0.0f ? vals[e] : 0.0f;
+            }
+            const long long plane = static_cast<long long>(n) * p.out_cb + kb;
+            if (!(p.dbg_mode & 1)) store16(obase + ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz, vals, p.out_bf16);
+            if (p.out_halo_h | p.out_halo_w) {
+              // zero the halo pixels whose clamp onto the interior is this pixel
+              const int dy0 = pp == 0 ? -p.out_halo_h : 0, dy1 = pp == p.P - 1 ? p.out_halo_h : 0;
+              const int dx0 = qq == 0 ? -p.out_halo_w : 0, dx1 = qq == p.Q - 1 ? p.out_halo_w : 0;
+              for (int dy = dy0; dy <= dy1; ++dy)
+                for (int dx = dx0; dx <= dx1; ++dx)
+                  if (dy != 0 || dx != 0)
+                    store16_zero(obase + ((plane * p.out_hp + y + dy) * p.out_wp + x + dx) * 16LL * esz, p.out_bf16);
+            }
           }
         }
       }
@@ -403,7 +491,12 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
+    if (dbg && threadIdx.x == kEpiWarp0 * 32) {
+      dbg[6] = c_a;
+      dbg[7] = clock64() - t_start - c_a;
+    }
   }
+  if (dbg && threadIdx.x == 0) dbg[8] = clock64() - t_start;
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);

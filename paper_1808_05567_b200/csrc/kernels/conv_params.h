@@ -25,6 +25,7 @@ struct FwdParams {
   int tiles_per_img;
   int mb;              // 128-row m-blocks per tile
   int nb;              // 16-channel output blocks per CTA
+  int acc_bufs;        // TMEM accumulator buffers (2 = epilogue overlaps the next tile)
   // A staging: smem chunk planes hold a_px pixels starting at virtual pixel a_px0
   int linear;          // 1: virtual index == physical pixel index of the halo'd plane
   int a_px;            // pixels per chunk plane per stage
@@ -35,7 +36,8 @@ struct FwdParams {
   int phase_row[kMaxPhases], phase_col[kMaxPhases];
   int phase_ntaps[kMaxPhases], phase_tap0[kMaxPhases];
   int tap_shift[kMaxTaps];  // phase-sorted
-  int taps_box;        // weight box taps (max taps per phase)
+  int taps_box;        // max taps per phase
+  int w_taps;          // taps per weight pipeline stage (<= taps_box)
   int n_taps;          // total taps (phase-sorted) in the prepared weights
   int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
   const void* wprep;   // prepared bf16 weights [pc][cb][ntile][tap][2nb][16][8]
@@ -49,6 +51,8 @@ struct FwdParams {
   int out_halo_h, out_halo_w;  // halo frame to zero (0 = none)
   const float* bias;   // kb_out*16 lanes or null
   int relu;
+  long long* dbg;      // optional per-CTA role cycle counters (16 per CTA), null in production
+  int dbg_mode;        // ablation bits (debug only): 1 skip global stores, 2 skip TMEM loads
 };
 
 // Weight update: per (c-tile x tap group, k-tile, split) CTA, fp32 partial
@@ -79,6 +83,11 @@ struct UpdParams {
   int phase_row[kMaxPhases], phase_col[kMaxPhases];
   int tap_shift[kMaxTaps];
   int tap_src[kMaxTaps];   // phase-sorted tap -> r*S + s
+  // tap stacking (layers with < 8 input channel blocks): the 128 MMA rows hold
+  // `stack` taps x cb_eff channel blocks, each slot staged by its own shifted box
+  int stack;               // 1 = shared-tile mode (taps via descriptor shifts)
+  int cb_eff;
+  int tap_ph[kMaxTaps], tap_r2[kMaxTaps], tap_s2[kMaxTaps];
   int n_taps;
   float* partial;      // [split][tap(RS)][c_pad][k_pad]
   int c_pad, k_pad;

@@ -107,15 +107,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int n = stage / p.stages_per_img;
         const int band = stage % p.stages_per_img;
         uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
-        mbar_arrive_expect_tx(&full_bar[s], PA * L.a_piece + PB * L.b_piece);
+        const uint32_t a_bytes =
+            p.stack > 1 ? static_cast<uint32_t>(ntaps * 2 * p.cb_eff) * L.a_plane : L.a_piece;
+        mbar_arrive_expect_tx(&full_bar[s], PA * a_bytes + PB * L.b_piece);
         for (int pc = 0; pc < PA; ++pc) {
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
           uint8_t* a_dst = st + pc * L.a_piece;
-          if (p.linear)
+          if (p.stack > 1) {
+            // one shifted box per stacked tap: slot j = tap tap0 + j, cb_eff blocks
+            for (int j = 0; j < ntaps; ++j) {
+              const int tp = tap0 + j, tph = p.tap_ph[tp];
+              tma_load_5d(a_dst + j * 2 * p.cb_eff * L.a_plane, &map_in, &full_bar[s], 0,
+                          p.in_col0 + p.phase_col[tph] + p.stride * p.tap_s2[tp],
+                          p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]), 0, pa);
+            }
+          } else if (p.linear) {
             tma_load_4d(a_dst, &map_in, &full_bar[s], 0, band * p.vs, 0, pa);
-          else
+          } else {
             tma_load_5d(a_dst, &map_in, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
                         p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], 0, pa);
+          }
         }
         for (int pc = 0; pc < PB; ++pc) {
           const int pb = pc * do_planes + n * p.do_cb + ktile * p.nb;
@@ -137,8 +148,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_after();
       const uint32_t st = smem0 + static_cast<uint32_t>(s) * L.bytes;
       if (elect_one()) {
-        for (int t = 0; t < ntaps; ++t) {
-          const int shift = p.tap_shift[tap0 + t];
+        const int n_acc = p.stack > 1 ? 1 : ntaps;  // stacked: one accumulator holds all the group's taps
+        for (int t = 0; t < n_acc; ++t) {
+          const int shift = p.stack > 1 ? 0 : p.tap_shift[tap0 + t];
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * NT);
           for (int ks = 0; ks < ksteps; ++ks) {
 #pragma unroll
@@ -171,14 +183,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(&accum_bar, 0);
       tc_fence_after();
     }
-    for (int t = 0; t < ntaps; ++t) {
-      const int rs = p.tap_src[tap0 + t];
+    const int n_acc = p.stack > 1 ? 1 : ntaps;
+    for (int t = 0; t < n_acc; ++t) {
+      // stacked: TMEM row = (slot j, channel c) of tap tap0 + j
+      const int slot = p.stack > 1 ? (qrow + lane) / (16 * p.cb_eff) : 0;
+      const int c_row = p.stack > 1 ? (qrow + lane) % (16 * p.cb_eff) : c_glob;
+      const bool row_ok = p.stack > 1 ? slot < ntaps : true;
+      const int rs = p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : t)];
       float* dst_row =
-          p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_glob) * p.k_pad + ktile * NT;
+          p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
       for (int g = 0; g < p.nb; ++g) {
         uint32_t r[16];
         tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(t * NT + g * 16), r);
         tmem_ld_wait();
+        if (!row_ok) continue;
         float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
         const bool live = iters > 0;
 #pragma unroll

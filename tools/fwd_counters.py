@@ -1,0 +1,43 @@
+"""Dev tool: per-role cycle counters of the forward kernel (cfg2 FWD / BWD)."""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import paper_1808_05567_b200 as d  # noqa: E402
+from paper_1808_05567_b200 import _lib  # noqa: E402
+
+lib = _lib.lib()
+lib.dconv_debug_counters.argtypes = [C.c_void_p]
+lib.dconv_debug_mode(int(os.environ.get("DBG_MODE", "0")))
+math = d.Math.BF16 if (len(sys.argv) > 1 and sys.argv[1] == "bf16") else d.Math.F32
+spec = d.make_layer_spec(32, 256, 64, 56, 56, 1, 1, 1, 0, 0, 16)
+x = torch.rand(32, 256, 56, 56, device="cuda") * 2 - 1
+w = torch.randn(64, 256, 1, 1, device="cuda") * 0.088
+g = torch.rand(32, 64, 56, 56, device="cuda") * 2 - 1
+ib, wb, gb = d.to_blocked_activation(x, spec), d.to_blocked_weight(w, spec), d.to_blocked_activation(g, 16, 0, 0)
+fp = d.make_forward_plan(spec, 1, None, None, math)
+bc = d.prepare_backward(spec, wb, 1, None, math)
+out = d.BlockedActivation(32, 64, 56, 56, 16, 0, 0)
+gi = d.BlockedActivation(32, 256, 56, 56, 16, 0, 0)
+buf = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+names = ["prod_wait", "cvt_wait_raw", "cvt_wait_slot", "cvt_busy", "mma_wait_ops", "mma_wait_acc", "epi_wait",
+         "epi_busy", "total"]
+for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.execute(wb, gb, gi))):
+    run()
+    torch.cuda.synchronize()
+    lib.dconv_debug_counters(buf.data_ptr())
+    buf.zero_()
+    run()
+    torch.cuda.synchronize()
+    lib.dconv_debug_counters(None)
+    v = buf.view(148, 16)[:, :9].double().mean(0).tolist()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(5):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    print(label, math.name, "us/launch", round(s.elapsed_time(e) * 200, 1), {n: round(x / 1e3, 1) for n, x in zip(names, v)}, "(kcycles, mean over CTAs)")
