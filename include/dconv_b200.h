@@ -153,6 +153,19 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
 /* number of this library's kernels one dconv_forward launches */
 int dconv_fwd_launches(dconv_fwd_plan_t plan);
 
+/* Graph-executor epilogue (run_chain analog, harness.cpp:311-358, extended to
+ * training): v = acc (+bias) (+add[px]); relu; v *= (mask[px] > 0).
+ * add / mask are device tensors with the OUTPUT's geometry and dtype (null = off):
+ * add carries a residual (forward) or the other branch's gradient (backward),
+ * mask the forward activation whose ReLU the gradient passes back through. */
+typedef struct dconv_epilogue {
+  const void* add;
+  const void* mask;
+  int relu;
+} dconv_epilogue_t;
+int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
+                     const dconv_epilogue_t* ep, void* workspace, dconv_stream_t stream);
+
 /* ---------------------------------------------------------------- backward-data */
 typedef struct dconv_bwd_plan* dconv_bwd_plan_t;
 typedef enum dconv_bwd_route {
@@ -172,6 +185,21 @@ size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan);
 int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
                         const dconv_act_t* grad_in, void* workspace, dconv_stream_t stream);
 int dconv_bwd_launches(dconv_bwd_plan_t plan);
+/* backward_data with the graph epilogue; for strided layers `add` must be null
+ * or grad_in->data itself (in-place gradient accumulation) */
+int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
+                           const dconv_act_t* grad_in, const dconv_epilogue_t* ep, void* workspace,
+                           dconv_stream_t stream);
+
+/* ---------------------------------------------------------------- graph-executor ops */
+/* 3x3 / stride 2 / pad 1 max pool (ResNet stem) on halo-0 blocked tensors;
+ * argmax: n*c_b*P*Q*16 bytes, consumed by the backward (gather, no atomics) */
+int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argmax, dconv_stream_t stream);
+/* mask (nullable, grad_in's geometry): ReLU backward of the pooled activation */
+int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in, const void* mask,
+                      dconv_stream_t stream);
+/* w -= lr * g on fp32 blocked weights */
+int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t stream);
 
 /* ---------------------------------------------------------------- weight update */
 typedef struct dconv_upd_plan* dconv_upd_plan_t;

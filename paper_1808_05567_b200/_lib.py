@@ -30,6 +30,10 @@ class Fusion(C.Structure):
     _fields_ = [("kind", C.c_int), ("bias", C.POINTER(C.c_float)), ("bias_len", C.c_int)]
 
 
+class Epilogue(C.Structure):
+    _fields_ = [("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int)]
+
+
 class EngineCfg(C.Structure):
     _fields_ = [("min_accumulators", C.c_int), ("max_accumulators", C.c_int), ("cache_budget_bytes", C.c_int64),
                 ("prefetch_lookahead", C.c_int), ("prefetch_enabled", C.c_int), ("streaming_stores", C.c_int),
@@ -55,7 +59,8 @@ EXPORTS = [
     "dconv_bwd_plan_destroy", "dconv_bwd_route", "dconv_bwd_plan_describe", "dconv_bwd_workspace_bytes",
     "dconv_backward_data", "dconv_bwd_launches", "dconv_upd_plan_create", "dconv_upd_plan_destroy",
     "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
-    "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms",
+    "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms", "dconv_forward_ex", "dconv_backward_data_ex",
+    "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_sgd",
 ]
 
 
@@ -104,6 +109,11 @@ def _bind(lib):
         "dconv_weight_update": (i, [vp, P(Act), P(Act), P(Wt), i, vp, vp]),
         "dconv_upd_launches": (i, [vp, P(Act), P(Act)]),
         "dconv_profile": (i, [i]),
+        "dconv_forward_ex": (i, [vp, P(Act), P(Wt), P(Act), P(Epilogue), vp, vp]),
+        "dconv_backward_data_ex": (i, [vp, P(Wt), P(Act), P(Act), P(Epilogue), vp, vp]),
+        "dconv_maxpool_fwd": (i, [P(Act), P(Act), vp, vp]),
+        "dconv_maxpool_bwd": (i, [P(Act), vp, P(Act), vp, vp]),
+        "dconv_sgd": (i, [P(Wt), P(Wt), C.c_float, vp]),
         "dconv_profile_last_ms": (C.c_float, [i]),
     }
     for name, (res, args) in sig.items():

@@ -290,7 +290,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   // two TMEM accumulators of mb*16*nb columns must fit in 512. Weight stages
   // hold up to w_taps taps (big filters stream taps through several stages).
   int w_taps = taps.taps_box;
-  for (int want_pc : {3, 2, 1}) {
+  for (int tier = 0; tier < 6 && !found; ++tier) {
+    const int want_pc = tier < 2 ? 3 : tier < 4 ? 2 : 1;
+    const int want_bufs = (tier % 2 == 0) ? 2 : 1;
     for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
       const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
       for (int mb : {2, 1}) {
@@ -300,6 +302,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         if (acc_cols > 512) continue;
         const int bufs = 2 * acc_cols <= 512 ? 2 : 1;
         if (bufs == 1 && mb == 2) continue;
+        if (bufs < want_bufs) continue;
         const int Lpx = 128 * mb;
         int apx, lb = 0;
         if (linear) {
@@ -359,7 +362,6 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
       }
       if (want_nb || nb == 1) break;
     }
-    if (found) break;
   }
   if (!found) fail(DCONV_ERR_PLAN_INFEASIBLE, "no forward tile fits shared memory / TMA box limits");
   p.mb = tile.mb;
@@ -917,6 +919,11 @@ int dconv_fwd_launches(dconv_fwd_plan_t plan) { return plan ? 2 : 0; }
 
 int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
                   void* workspace, dconv_stream_t stream) {
+  return dconv_forward_ex(plan, in, wt, out, nullptr, workspace, stream);
+}
+
+int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
+                     const dconv_epilogue_t* ep, void* workspace, dconv_stream_t stream) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     check_act(in, "forward input");
@@ -964,6 +971,11 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
     p.bias = (plan->fuse_kind == DCONV_FUSE_BIAS_ADD || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? plan->bias_dev
                                                                                                   : nullptr;
     p.relu = (plan->fuse_kind == DCONV_FUSE_RELU || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? 1 : 0;
+    if (ep) {
+      p.add = ep->add;
+      p.mask = ep->mask;
+      p.relu |= ep->relu ? 1 : 0;
+    }
     prof_begin(0, cs);
     launch_fwd(L, cs);
     prof_end(0, cs);
@@ -1067,6 +1079,11 @@ int dconv_bwd_plan_describe(dconv_bwd_plan_t plan, char* buf, size_t len) {
              len);
   });
 }
+int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
+                        const dconv_act_t* grad_in, void* workspace, dconv_stream_t stream) {
+  return dconv_backward_data_ex(plan, wt, grad_out, grad_in, nullptr, workspace, stream);
+}
+
 int dconv_bwd_launches(dconv_bwd_plan_t plan) {
   if (!plan) return 0;
   int n = 0;
@@ -1074,8 +1091,9 @@ int dconv_bwd_launches(dconv_bwd_plan_t plan) {
   return n;
 }
 
-int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
-                        const dconv_act_t* grad_in, void* workspace, dconv_stream_t stream) {
+int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
+                           const dconv_act_t* grad_in, const dconv_epilogue_t* ep, void* workspace,
+                           dconv_stream_t stream) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     check_wt(wt, "backward weight");
@@ -1093,6 +1111,9 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     const int kb = cdiv(s.K, 16), cb = cdiv(s.C, 16);
     const int hp = s.H + 2 * grad_in->halo_h, wp = s.W + 2 * grad_in->halo_w;
+    const bool accumulate = ep && ep->add && ep->add == grad_in->data;
+    if (ep && ep->add && !accumulate && s.stride != 1)
+      fail(DCONV_ERR_UNSUPPORTED, "backward_data_ex: strided layers accept add == grad_in only");
     std::string desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
     int tap_off = 0;
     bool first = true;
@@ -1101,6 +1122,10 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
       if (!first) desc += ",";
       first = false;
       if (ph.zero) {
+        if (accumulate) {  // adding zeros: nothing to do
+          desc += "\"skip\"";
+          continue;
+        }
         const int planes = s.N * cb;
         const int ly = cdiv(s.H - ph.a, s.stride), lx = cdiv(s.W - ph.b, s.stride);
         const int g = grid1d(static_cast<int64_t>(planes) * ly * lx * 16);
@@ -1136,6 +1161,11 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
       p.out_halo_w = single ? grad_in->halo_w : 0;
       p.bias = nullptr;
       p.relu = 0;
+      if (ep) {
+        p.add = ep->add;
+        p.mask = ep->mask;
+        p.relu = ep->relu ? 1 : 0;
+      }
       launch_fwd(L, cs);
       desc += json_tile(L);
     }
@@ -1489,7 +1519,7 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     prof_end(2, cs);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
-    upd_reduce_kernel<<<grid1d(total), 256, 0, cs>>>(partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K,
+    upd_reduce_kernel<<<grid1d(total, 64), 64, 0, cs>>>(partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K,
                                                       cb, kb, grad_w->data, grad_w->dtype == DCONV_BF16,
                                                       accumulate ? 1 : 0);
     cuda_check(cudaGetLastError(), "upd_reduce launch");
@@ -1535,3 +1565,65 @@ int dconv_debug_mode(int mode) {
   return DCONV_OK;
 }
 }
+
+extern "C" {
+
+int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argmax, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(in, "maxpool input");
+    check_act(out, "maxpool output");
+    if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
+    const int P = (in->h + 2 - 3) / 2 + 1, Q = (in->w + 2 - 3) / 2 + 1;
+    if (in->vlen != 16 || out->vlen != 16 || in->halo_h || in->halo_w || out->halo_h || out->halo_w ||
+        out->n != in->n || out->c != in->c || out->h != P || out->w != Q || out->dtype != in->dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "maxpool: expects halo-0 vlen-16 tensors, out = (h+2-3)/2+1");
+    const int planes = in->n * cdiv(in->c, 16);
+    const int g = grid1d(static_cast<int64_t>(planes) * P * Q * 16);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (in->dtype == DCONV_F32)
+      maxpool_fwd_kernel<float><<<g, 256, 0, cs>>>((const float*)in->data, (float*)out->data, (uint8_t*)argmax,
+                                                   planes, in->h, in->w, P, Q);
+    else
+      maxpool_fwd_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)in->data,
+                                                           (__nv_bfloat16*)out->data, (uint8_t*)argmax, planes,
+                                                           in->h, in->w, P, Q);
+    cuda_check(cudaGetLastError(), "maxpool_fwd");
+  });
+}
+
+int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in,
+                      const void* mask, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(grad_out, "maxpool grad_out");
+    check_act(grad_in, "maxpool grad_in");
+    if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
+    const int planes = grad_in->n * cdiv(grad_in->c, 16);
+    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w * 16);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (grad_in->dtype == DCONV_F32)
+      maxpool_bwd_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
+                                                   (float*)grad_in->data, (const float*)mask, planes, grad_in->h,
+                                                   grad_in->w, grad_out->h, grad_out->w);
+    else
+      maxpool_bwd_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)grad_out->data,
+                                                           (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data,
+                                                           (const __nv_bfloat16*)mask, planes, grad_in->h,
+                                                           grad_in->w, grad_out->h, grad_out->w);
+    cuda_check(cudaGetLastError(), "maxpool_bwd");
+  });
+}
+
+int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(w, "sgd weight");
+    check_wt(g, "sgd grad");
+    if (w->dtype != DCONV_F32 || g->dtype != DCONV_F32 || wt_elems(*w) != wt_elems(*g))
+      fail(DCONV_ERR_SHAPE_MISMATCH, "sgd: fp32 tensors of equal size required");
+    const int64_t n = wt_elems(*w);
+    sgd_kernel<<<grid1d(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>((float*)w->data,
+                                                                              (const float*)g->data, lr, n);
+    cuda_check(cudaGetLastError(), "sgd");
+  });
+}
+
+}  // extern "C"

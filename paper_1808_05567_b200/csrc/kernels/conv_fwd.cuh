@@ -90,6 +90,30 @@ __device__ __forceinline__ void store16(void* dst, const float* v, int out_bf16)
   }
 }
 
+// 16 lanes at `src` (bf16 or fp32) -> fp32
+__device__ __forceinline__ void load16(const void* src, int bf16, float* v) {
+  if (bf16) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    const uint4 a = s[0], b = s[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  } else {
+    const float4* s = reinterpret_cast<const float4*>(src);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 t = s[e];
+      v[4 * e] = t.x;
+      v[4 * e + 1] = t.y;
+      v[4 * e + 2] = t.z;
+      v[4 * e + 3] = t.w;
+    }
+  }
+}
+
 __device__ __forceinline__ void store16_zero(void* dst, int out_bf16) {
   const uint4 z = make_uint4(0, 0, 0, 0);
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -469,12 +493,25 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
+            const long long plane = static_cast<long long>(n) * p.out_cb + kb;
+            const long long px_off = ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz;
+            if (p.add != nullptr) {  // residual add / gradient sum
+              float a[16];
+              load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += a[e];
+            }
             if (p.relu) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = vals[e] > 0.0f ? vals[e] : 0.0f;
             }
-            const long long plane = static_cast<long long>(n) * p.out_cb + kb;
-            if (!(p.dbg_mode & 1)) store16(obase + ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz, vals, p.out_bf16);
+            if (p.mask != nullptr) {  // ReLU backward: gradient through the forward activation
+              float m[16];
+              load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
+            }
+            if (!(p.dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
             if (p.out_halo_h | p.out_halo_w) {
               // zero the halo pixels whose clamp onto the interior is this pixel
               const int dy0 = pp == 0 ? -p.out_halo_h : 0, dy1 = pp == p.P - 1 ? p.out_halo_h : 0;

@@ -51,6 +51,10 @@ struct FwdParams {
   int out_halo_h, out_halo_w;  // halo frame to zero (0 = none)
   const float* bias;   // kb_out*16 lanes or null
   int relu;
+  // fused graph epilogue (executor): v += add[px]; v = relu(v); v *= (mask[px] > 0).
+  // add / mask share the output surface's geometry and dtype (null = off)
+  const void* add;
+  const void* mask;
   long long* dbg;      // optional per-CTA role cycle counters (16 per CTA), null in production
   int dbg_mode;        // ablation bits (debug only): 1 skip global stores, 2 skip TMEM loads
 };

@@ -240,8 +240,17 @@ __global__ void upd_reduce_kernel(const float* __restrict__ partial, int splits,
     float sum = 0.0f;
     if (c < C && k < K) {
       const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
-      sum = src[0];
-      for (int sp = 1; sp < splits; ++sp) sum += src[sp * split_stride];
+      sum = __ldg(src);
+      // fixed index order; loads batched 8 deep for memory-level parallelism
+      int sp = 1;
+      for (; sp + 8 <= splits; sp += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sp + u) * split_stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
+      }
+      for (; sp < splits; ++sp) sum += __ldg(src + sp * split_stride);
     }
     if (dw_bf16) {
       __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dw) + e;

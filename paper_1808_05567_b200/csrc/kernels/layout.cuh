@@ -249,6 +249,69 @@ __global__ void zero_halo_kernel(T* __restrict__ dst, int planes, int h, int w, 
   }
 }
 
+// 3x3 / stride-2 / pad-1 max pool on blocked tensors (ResNet stem), halo 0.
+// Stores the argmax tap (0..8, first max in row-major order) for the backward.
+template <typename T>
+__global__ void maxpool_fwd_kernel(const T* __restrict__ in, T* __restrict__ out, uint8_t* __restrict__ arg,
+                                   int planes, int h, int w, int p, int q) {
+  const long long total = static_cast<long long>(planes) * p * q * 16;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % 16);
+    long long r = e / 16;
+    const int x = static_cast<int>(r % q);
+    r /= q;
+    const int y = static_cast<int>(r % p);
+    const long long plane = r / p;
+    float best = -INFINITY;
+    int bi = 0;
+    for (int dy = 0; dy < 3; ++dy)
+      for (int dx = 0; dx < 3; ++dx) {
+        const int iy = 2 * y - 1 + dy, ix = 2 * x - 1 + dx;
+        if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
+        const float v = to_f<T>(in[((plane * h + iy) * w + ix) * 16 + lane]);
+        if (v > best) {
+          best = v;
+          bi = dy * 3 + dx;
+        }
+      }
+    out[e] = from_f<T>(best);
+    arg[e] = static_cast<uint8_t>(bi);
+  }
+}
+
+// gather form of the max-pool backward (deterministic, no atomics): each input
+// pixel sums the output gradients of the <= 4 windows whose argmax it is
+template <typename T>
+__global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __restrict__ arg,
+                                   T* __restrict__ gin, const T* __restrict__ mask, int planes, int h, int w, int p,
+                                   int q) {
+  const long long total = static_cast<long long>(planes) * h * w * 16;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % 16);
+    long long r = e / 16;
+    const int ix = static_cast<int>(r % w);
+    r /= w;
+    const int iy = static_cast<int>(r % h);
+    const long long plane = r / h;
+    float acc = 0.0f;
+    for (int y = (iy + 1) / 2 - 1; y <= (iy + 1) / 2; ++y)
+      for (int x = (ix + 1) / 2 - 1; x <= (ix + 1) / 2; ++x) {
+        if (y < 0 || y >= p || x < 0 || x >= q) continue;
+        const int dy = iy - (2 * y - 1), dx = ix - (2 * x - 1);
+        if (dy < 0 || dy > 2 || dx < 0 || dx > 2) continue;
+        const long long o = ((plane * p + y) * q + x) * 16 + lane;
+        if (arg[o] == dy * 3 + dx) acc += to_f<T>(gout[o]);
+      }
+    if (mask != nullptr && !(to_f<T>(mask[e]) > 0.0f)) acc = 0.0f;  // ReLU backward of the pooled activation
+    gin[e] = from_f<T>(acc);
+  }
+}
+
+// SGD on fp32 master weights: w -= lr * g (blocked layouts, identical shapes)
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, long long n) {
+  DCONV_GRID_STRIDE(e, n) { w[e] -= lr * g[e]; }
+}
+
 // ReLU backward mask fused helper: g *= (y > 0) on blocked tensors of equal shape
 template <typename T>
 __global__ void relu_mask_kernel(T* __restrict__ g, const T* __restrict__ y, long long n) {
