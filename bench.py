@@ -85,17 +85,15 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                if util > 0:
-                    self.samples.append(mhz)
-                    for bit, name in self.REASONS.items():
-                        if mask & bit and name != "gpu_idle":
-                            self.reasons.add(name)
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv is not None:
@@ -382,6 +380,230 @@ def run_ours(args):
     return 0
 
 
+# ---------------------------------------------------------------------- ResNet-50 conv stack (cfg4)
+
+
+def stack_cpu_reference(threads, n_img=2):
+    """Reference direct engine on every distinct conv of the stack (F + B + U,
+    one timed call each, plan setup excluded), N = n_img images, summed with
+    the stack multiplicities; the stem's backward-data is skipped."""
+    from oracle import oracle as orc
+    from paper_1808_05567_b200 import executor as ex
+
+    nodes = ex.resnet50_conv_stack()
+    shapes = ex.tensor_shapes(nodes)
+    mult = {}
+    for nd in nodes:
+        if isinstance(nd, ex.ConvNode):
+            c, h, w = shapes[nd.src]
+            key = (nd.C, nd.K, h, w, nd.R, nd.S, nd.stride, nd.pad, nd.src == "x")
+            mult[key] = mult.get(key, 0) + 1
+    total = 0.0
+    for (C, K, H, W, R, S, st, pad, stem), m in mult.items():
+        s = orc.spec(n_img, C, K, H, W, R, S, st, pad, pad, 16)
+        P, Q = orc.output_shape(s)
+        x = orc.uniform(0, (n_img, C, H, W))
+        wt = orc.he_normal(1, (K, C, R, S), C * R * S)
+        g = orc.uniform(2, (n_img, K, P, Q))
+        t = 0.0
+        for pss, (a, b) in enumerate(((x, wt), (g, wt), (x, g))):
+            if pss == 1 and stem:
+                continue
+            _, best, _ = orc.ref_direct_pass(s, pss, threads, 1, a, b)
+            t += best / 1e3
+        total += m * t
+    return n_img / total, f"reference direct engine (oracle/_ref), {n_img} images x {len(mult)} distinct convs, F+B+U"
+
+
+def run_stack(args):
+    import numpy as np
+    import torch
+
+    import paper_1808_05567_b200 as d
+    from paper_1808_05567_b200 import _lib
+    from paper_1808_05567_b200 import executor as ex
+
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as orc
+
+        threads = os.cpu_count() or 1
+        if not orc.ref_available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+            return 0
+        times = []
+        for _ in range(max(1, args.steps // 10)):
+            ips, sample = stack_cpu_reference(threads)
+            times.append(ips)
+        value = sum(times) / len(times)
+        line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
+                "steps": len(times), "warmup": 0, "ms_per_step": round(256 / value * 1e3, 1),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded splitmix64)",
+                "config": {"workload": "resnet50_conv_stack (BASELINE configs[3])", "global_batch": 256,
+                           "parallelism": "cpu threads"},
+                "cpu_baseline": {"value": round(value, 4), "unit": "images/s", "cores": threads, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": round(value, 4), "unit": "images/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    global_batch = args.global_batch
+    n = global_batch // world
+    nodes = ex.resnet50_conv_stack(224)
+    e = ex.ConvStackExecutor(nodes, n, 224, d.Math.BF16, "cuda", group=pg, lr=1e-5)
+    lib = _lib.lib()
+    # seeded synthetic images (rank shard) and top gradient
+    x_h = torch.empty(n, 3, 224, 224, dtype=torch.float32)
+    lib.dconv_fill_uniform_host(1000 * rank, -1.0, 1.0, x_h.data_ptr(), x_h.numel())
+    x_pin = x_h.pin_memory()
+    x_dev = torch.empty_like(x_h, device=dev)
+    c, h, w = e.shapes[nodes[-1].out]
+    g_h = torch.empty(n, c, h, w, dtype=torch.float32)
+    lib.dconv_fill_uniform_host(2 + 1000 * rank, -1.0, 1.0, g_h.data_ptr(), g_h.numel())
+    dtop = d.to_blocked_activation(g_h.to(dev), 16, 0, 0, dtype=torch.bfloat16)
+    loss_dev = torch.zeros(1, dtype=torch.float32, device=dev)
+    loss_pin = torch.zeros(1, dtype=torch.float32).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    import ctypes
+
+    from paper_1808_05567_b200 import api as dapi
+
+    def pack_input():
+        dapi._check(lib.dconv_pack_act(x_dev.data_ptr(), 0, ctypes.byref(e.act["x"].to_c()), stream.cuda_stream))
+
+    x_dev.copy_(x_pin)
+    pack_input()
+
+    def step():
+        e.step(dtop)
+
+    def loss_of_step():
+        top = e.act[nodes[-1].out].data
+        loss_dev.copy_((top.float() * dtop.data.float()).sum().reshape(1))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if world == 1 and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        run = graph.replay
+    else:
+        run = step
+    launches = e.launches_per_step()
+
+    def barrier():
+        if pg is not None:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run()
+        e1.record(stream)
+        barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if pg is not None:
+        import torch.distributed as dist
+
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item())
+    value = global_batch / (ms_per_step * 1e-3)
+    # end to end: H2D of this step's images (pinned), pack, step, loss D2H
+    h2d = x_pin.numel() * 4
+
+    def e2e_step():
+        x_dev.copy_(x_pin, non_blocking=True)
+        pack_input()
+        run()
+        loss_of_step()
+        loss_pin.copy_(loss_dev, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if pg is not None:
+        import torch.distributed as dist
+
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = global_batch / (float(e2e_ms.item()) * 1e-3)
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            sustained = float(json.load(f).get("bf16_tflops_sustained", bf16_peak))
+    except (OSError, ValueError):
+        sustained = bf16_peak
+    flops_img = ex.step_flops_per_image(nodes)
+    achieved = flops_img * n / (ms_per_step * 1e-3) / 1e12
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as orc
+
+            if orc.ref_available():
+                ips, sample = stack_cpu_reference(os.cpu_count() or 1)
+                cpu = {"value": round(ips, 4), "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",
+                       "sample": sample}
+        except Exception as ex_:  # noqa: BLE001
+            cpu = {"value": None, "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex_}"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded splitmix64 images 3x224x224 and top gradient; He-normal weights)",
+            "config": {"workload": "resnet50_conv_stack (BASELINE configs[3]): 53 convs F+B+U, ReLU/residual fused,"
+                                   " stem max-pool, SGD, NCCL dW all-reduce", "global_batch": global_batch,
+                       "per_gpu_batch": n, "image": 224, "parallelism": f"dp{world}",
+                       "cuda_graph": graph is not None, "l2": "working set >> L2 (activations ~GBs)"},
+            "e2e": {"value": round(e2e_value, 2), "unit": "images/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": launches * args.steps,
+            "roofline": {"bound": "tensor", "kernel": "whole step (53 convs x F/B/U)", "achieved": round(achieved, 1),
+                         "peak": sustained, "unit": "TFLOP/s", "frac": round(achieved / sustained, 4),
+                         "traffic": None, "peak_source": peak_src + " bf16_tflops_sustained",
+                         "flops_per_image": flops_img},
+            "cpu_baseline": cpu,
+            "clocks": sampler.report(),
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -390,9 +612,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--math", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--workload", default="layer", choices=["layer", "resnet50"])
+    ap.add_argument("--global-batch", type=int, default=256)
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload == "resnet50":
+        return run_stack(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
