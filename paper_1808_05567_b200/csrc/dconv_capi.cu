@@ -273,6 +273,10 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   // linear mode: the halo'd physical plane is the virtual grid
   const bool linear = st == 1 && -pb.row_off == in.halo_h && -pb.col_off == in.halo_w;
   p.linear = linear ? 1 : 0;
+  // multi-image tiles: 1x1 stride-1 on halo-free planes of <= 128 pixels
+  const int hw = in.h * in.w;
+  const bool mimg_ok = linear && pb.R == 1 && pb.S == 1 && in.halo_h == 0 && in.halo_w == 0 && hw <= 128 &&
+                       (cfg == nullptr || cfg->tile_mb == 0 || cfg->tile_mb == 2);
   p.wsub = linear ? wp : pb.Q + taps.s2max;
   p.in_row0 = pb.row_off;
   p.in_col0 = pb.col_off;
@@ -305,7 +309,10 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         if (bufs < want_bufs) continue;
         const int Lpx = 128 * mb;
         int apx, lb = 0;
-        if (linear) {
+        if (mimg_ok) {
+          if (mb != 2) continue;
+          apx = Lpx;
+        } else if (linear) {
           lb = cdiv(Lpx + maxshift, 128);
           apx = lb * 128;
         } else {
@@ -368,49 +375,48 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.nb = tile.nb;
   p.acc_bufs = acc_bufs;
   p.a_px = a_px;
+  p.a_load_px = a_px;
   p.lin_boxes = lin_boxes;
   p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
+  p.mimg = 0;
+  if (mimg_ok) {
+    p.mimg = (128 * tile.mb) / hw;
+    p.a_load_px = p.mimg * hw;
+  }
   L.stages = pc_st;
   L.raw_stages = raw_st;
   L.w_stages = w_st;
   L.smem = static_cast<size_t>(layout.raw_off) + static_cast<size_t>(raw_st) * layout.raw_slot + kEpiStageBytes;
-  const int n_tiles = in.n * p.tiles_per_img * cdiv(kb_total, tile.nb);
+  const int n_tiles = (p.mimg > 0 ? cdiv(in.n, p.mimg) : in.n * p.tiles_per_img) * cdiv(kb_total, tile.nb);
   L.grid = dim3(static_cast<unsigned>(std::min(n_tiles, sm_count())), 1, 1);
 
   p.n_taps = static_cast<int>(taps.r.size());
   p.w_taps = w_taps;
   p.n_ntiles = cdiv(kb_total, tile.nb);
   p.wprep = wprep;
-  // activation map
+  // activation map: fp32 as 64 B pixel rows (SWIZZLE_64B, converted to pieces in smem),
+  // bf16 as 32 B pixel rows (SWIZZLE_32B, read in place by the MMA)
   const uint64_t planes = static_cast<uint64_t>(in.n) * p.in_cb;
-  if (raw_f32) {
-    // fp32 pixels as 64B rows (16 lanes), converted to bf16 pieces in smem
-    if (linear) {
-      const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
-      const uint64_t strides[2] = {64, 64ull * hp * wp};
-      const uint32_t box[3] = {16, 128, 1};
-      L.map_a = encode(0, 3, in.data, dims, strides, box, nullptr, "activation linear f32", CU_TENSOR_MAP_SWIZZLE_64B);
-    } else {
-      const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * 64;
-      const uint64_t dims[4] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), planes};
-      const uint64_t strides[3] = {64, 64ull * wp, 64ull * wp * hp};
-      const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 1};
-      const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
-      L.map_a = encode(0, 4, base, dims, strides, box, estr, "activation rows f32", CU_TENSOR_MAP_SWIZZLE_64B);
-    }
+  const uint64_t pix = raw_f32 ? 64 : 32;
+  const CUtensorMapSwizzle swz = raw_f32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  if (p.mimg > 0) {
+    const uint64_t dims[4] = {16, static_cast<uint64_t>(hw), static_cast<uint64_t>(p.in_cb),
+                              static_cast<uint64_t>(in.n)};
+    const uint64_t strides[3] = {pix, pix * hw, pix * hw * p.in_cb};
+    const uint32_t box[4] = {16, static_cast<uint32_t>(hw), 1, static_cast<uint32_t>(p.mimg)};
+    L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation multi-image", swz);
   } else if (linear) {
-    // bf16 straight into the canonical [chunk][pixel][16B] layout
-    const uint64_t dims[4] = {8, static_cast<uint64_t>(hp) * wp, 2, planes};
-    const uint64_t strides[3] = {32, 16, 32ull * hp * wp};
-    const uint32_t box[4] = {8, 128, 1, 1};
-    L.map_a = encode(1, 4, in.data, dims, strides, box, nullptr, "activation linear bf16");
+    const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
+    const uint64_t strides[2] = {pix, pix * hp * wp};
+    const uint32_t box[3] = {16, 128, 1};
+    L.map_a = encode(!raw_f32, 3, in.data, dims, strides, box, nullptr, "activation linear", swz);
   } else {
-    const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * 32;
-    const uint64_t dims[5] = {8, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), 2, planes};
-    const uint64_t strides[4] = {32, 32ull * wp, 16, 32ull * wp * hp};
-    const uint32_t box[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 2, 1};
-    const uint32_t estr[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};
-    L.map_a = encode(1, 5, base, dims, strides, box, estr, "activation rows bf16");
+    const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * pix;
+    const uint64_t dims[4] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), planes};
+    const uint64_t strides[3] = {pix, pix * wp, pix * wp * hp};
+    const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 1};
+    const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
+    L.map_a = encode(!raw_f32, 4, base, dims, strides, box, estr, "activation rows", swz);
   }
   return L;
 }
@@ -464,10 +470,12 @@ std::string json_tile(const FwdLaunch& L) {
   char buf[512];
   std::snprintf(buf, sizeof(buf),
                 "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
-                "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d}",
+                "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d,"
+                "\"mimg\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
                 L.grid.x,
-                L.p.n_img * L.p.tiles_per_img * L.p.n_ntiles, L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px);
+                (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
+                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg);
   return buf;
 }
 

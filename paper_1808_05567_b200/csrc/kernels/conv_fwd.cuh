@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   const uint32_t smem0 = smem_u32(smem);
   const int NT = 16 * p.nb;
   const int k_iters = p.cb_in * p.n_phases;
-  const int n_mtiles = p.n_img * p.tiles_per_img;
+  const int n_mtiles = p.mimg > 0 ? (p.n_img + p.mimg - 1) / p.mimg : p.n_img * p.tiles_per_img;
   const int n_tiles = n_mtiles * p.n_ntiles;
   // fp32-accurate mode keeps the a0*b0 products and the five correction
   // products in separate accumulators: the large sum then takes 6x fewer
@@ -253,15 +253,20 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   auto tile_coords = [&](int t, int& n, int& v0, int& ntile) {
     ntile = t % p.n_ntiles;
     const int mt = t / p.n_ntiles;
-    n = mt / p.tiles_per_img;
-    v0 = (mt % p.tiles_per_img) * 128 * p.mb;
+    if (p.mimg > 0) {  // multi-image tile: images [n, n + mimg), rows = (image, pixel)
+      n = mt * p.mimg;
+      v0 = 0;
+    } else {
+      n = mt / p.tiles_per_img;
+      v0 = (mt % p.tiles_per_img) * 128 * p.mb;
+    }
   };
   const uint32_t w_tap = (2u * p.nb) * 256u;
 
   if (warp == 0) {
     // ------------------------------------------------------------ activation producer
     if (lane == 0) {
-      const uint32_t a_bytes = RAW_F32 ? static_cast<uint32_t>(p.a_px) * 64u : 2u * L.a_plane;
+      const uint32_t a_bytes = static_cast<uint32_t>(p.a_load_px) * (RAW_F32 ? 64u : 32u);
       uint32_t g = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         int n, v0, ntile;
@@ -276,7 +281,9 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
             mbar_wait_t(&raw_empty[s], ((g / raw_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + L.raw_off + s * L.raw_slot;
             mbar_arrive_expect_tx(&raw_full[s], a_bytes);
-            if (p.linear) {
+            if (p.mimg > 0) {
+              tma_load_4d(dst, &map_a, &raw_full[s], 0, 0, cb, n);  // box {16, hw, 1, mimg}
+            } else if (p.linear) {
               for (int i = 0; i < p.lin_boxes; ++i)
                 tma_load_3d(dst + i * 128 * 64, &map_a, &raw_full[s], 0, a_px0 + i * 128, plane);
             } else {
@@ -288,13 +295,15 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
             mbar_wait_t(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
             mbar_arrive_expect_tx(&pc_full[s], a_bytes);
-            if (p.linear) {
-              for (int c = 0; c < 2; ++c)
-                for (int i = 0; i < p.lin_boxes; ++i)
-                  tma_load_4d(dst + c * L.a_plane + i * 128 * 16, &map_a, &pc_full[s], 0, a_px0 + i * 128, c, plane);
+            // bf16 pixels as SWIZZLE_32B rows: the MMA reads them in place
+            if (p.mimg > 0) {
+              tma_load_4d(dst, &map_a, &pc_full[s], 0, 0, cb, n);  // box {16, hw, 1, mimg}
+            } else if (p.linear) {
+              for (int i = 0; i < p.lin_boxes; ++i)
+                tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, a_px0 + i * 128, plane);
             } else {
-              tma_load_5d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
-                          p.in_row0 + p.stride * row0 + p.phase_row[ph], 0, plane);
+              tma_load_4d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
+                          p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
             }
           }
         }
@@ -374,7 +383,8 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
                   const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
                   const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
                   const uint64_t ad =
-                      make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128);
+                      RAW_F32 ? make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128)
+                              : make_smem_desc_sw32(st + static_cast<uint32_t>(v_off + mb * 128 + shift) * 32u);
                   const uint64_t bd = make_smem_desc(wst + ib * L.w_piece + tp * w_tap, 128, 256);
                   if (pr == 0)
                     mma_bf16(d_hi, ad, bd, idesc, first ? 0u : 1u);
@@ -463,10 +473,20 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
       for (int mb = 0; mb < p.mb; ++mb) {
-        const int v = v0 + mb * 128 + qrow + lane;
+        int v = v0 + mb * 128 + qrow + lane;
+        int nn = n;
+        bool valid;
+        if (p.mimg > 0) {  // row -> (image, pixel) of the multi-image tile
+          const int img = v / v_end;
+          nn = n + img;
+          v -= img * v_end;
+          valid = img < p.mimg && nn < p.n_img;
+        } else {
+          valid = v < v_end;
+        }
         const int pp = v / p.wsub;
         const int qq = v - pp * p.wsub;
-        const bool valid = v < v_end && qq < p.Q;
+        valid = valid && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
         for (int g0 = g_lo; g0 < g_hi; g0 += 2) {
@@ -493,7 +513,7 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
-            const long long plane = static_cast<long long>(n) * p.out_cb + kb;
+            const long long plane = static_cast<long long>(nn) * p.out_cb + kb;
             const long long px_off = ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz;
             if (p.add != nullptr) {  // residual add / gradient sum
               float a[16];

@@ -28,7 +28,9 @@ struct FwdParams {
   int acc_bufs;        // TMEM accumulator buffers (2 = epilogue overlaps the next tile)
   // A staging: smem chunk planes hold a_px pixels starting at virtual pixel a_px0
   int linear;          // 1: virtual index == physical pixel index of the halo'd plane
+  int mimg;            // >0: multi-image tiles (1x1 stride 1, small planes): mimg whole images per tile
   int a_px;            // pixels per chunk plane per stage
+  int a_load_px;       // pixels the activation TMA writes per stage
   int lin_boxes;       // linear mode: 128-pixel boxes per chunk plane
   int in_row0, in_col0;// logical input coordinate of sub-image (0, 0)
   int stride;

@@ -145,6 +145,20 @@ __device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo,
   return d;
 }
 
+// K-major SWIZZLE_32B canonical layout: rows of 32 B (one pixel's 16 bf16
+// lanes), 8-row atoms (SBO = 256 B), TMA-written with CU_TENSOR_MAP_SWIZZLE_32B.
+// The hardware swizzles on absolute smem address bits, so any 32 B-aligned
+// start (a pixel-shifted tap) is valid with base_offset = 0 (tools/probe_sw32.cu).
+__device__ __forceinline__ uint64_t make_smem_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;         // LBO (unused for swizzled K-major) = 16 B
+  d |= static_cast<uint64_t>(256 >> 4) << 32;  // SBO = 8 rows x 32 B
+  d |= static_cast<uint64_t>(1) << 46;         // version 1
+  d |= static_cast<uint64_t>(6) << 61;         // SWIZZLE_32B
+  return d;
+}
+
 // a_fmt/b_fmt: 1 = BF16, 2 = TF32; majors: 0 = K-major, 1 = MN-major
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t fmt, uint32_t a_major, uint32_t b_major, uint32_t M,
                                                   uint32_t N) {
