@@ -82,21 +82,26 @@ class ClockSampler:
         except Exception:  # noqa: BLE001  (no NVML: report nothing rather than guess)
             self.nv = None
 
+    def _sample(self):
+        try:
+            mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+            mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append(mhz)
+            for bit, name in self.REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append(mhz)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
+            self._sample()
             time.sleep(0.002)
 
     def __enter__(self):
+        # may be entered once per timed region; samples accumulate
         if self.nv is not None:
+            self._stop.clear()
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -105,6 +110,7 @@ class ClockSampler:
         self._stop.set()
         if self._t is not None:
             self._t.join()
+            self._t = None
 
     def report(self):
         if self.nv is None:
@@ -266,9 +272,14 @@ def run_ours(args):
         barrier()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # evict L2 between steps (untimed)
+            # untimed spin so the whole step is queued before its first kernel
+            # runs: the events then bracket device work, not host launch gaps
+            torch.cuda._sleep(1_000_000)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
+            if sampler.nv is not None:
+                sampler._sample()  # one reading per step while the GPU is busy
             torch.cuda.synchronize()
             for k, idx in (("fwd", 0), ("bwd", 1), ("upd", 2)):
                 kern_ms[k].append(lib.dconv_profile_last_ms(idx))
@@ -285,37 +296,40 @@ def run_ours(args):
     value = world * flops_step / (ms_per_step * 1e-3) / 1e9
 
     # ---------------- end to end through the host-buffer API (e2e)
-    e_in = 4
-    xb_host = torch.empty(ib.data.numel(), dtype=torch.float32).pin_memory()
-    gb_host = torch.empty(gb.data.numel(), dtype=torch.float32).pin_memory()
-    wb_host = torch.empty(wb.data.numel(), dtype=torch.float32).pin_memory()
-    xb_host.copy_(ib.data.cpu())
-    gb_host.copy_(gb.data.cpu())
-    wb_host.copy_(wb.data.cpu())
-    out_host = torch.empty(out.data.numel(), dtype=torch.float32).pin_memory()
-    gi_host = torch.empty(gi.data.numel(), dtype=torch.float32).pin_memory()
-    dw_host = torch.empty(dw.data.numel(), dtype=torch.float32).pin_memory()
-    h2d = (xb_host.numel() + gb_host.numel() + wb_host.numel()) * e_in
-    d2h = (out_host.numel() + gi_host.numel() + dw_host.numel()) * 4
+    # dconv_host_step_run: the reference's host-memory execute contract; the batch
+    # streams through the GPU in image chunks with H2D / kernels / D2H overlapped
+    B = d.BlockedActivation
+
+    def pinned(t):
+        return t.data.cpu().pin_memory()
+
+    x_hb = B(ib.n, ib.c, ib.h, ib.w, 16, ib.halo_h, ib.halo_w, device="cpu", data=pinned(ib))
+    g_hb = B(gb.n, gb.c, gb.h, gb.w, 16, 0, 0, device="cpu", data=pinned(gb))
+    w_hb = d.BlockedWeight(wb.k, wb.c, wb.r, wb.s, 16, device="cpu", data=pinned(wb))
+    y_hb = B(out.n, out.c, out.h, out.w, 16, 0, 0, device="cpu", data=pinned(out))
+    dx_hb = B(gi.n, gi.c, gi.h, gi.w, 16, 0, 0, device="cpu", data=pinned(gi))
+    dw_hb = d.BlockedWeight(dw.k, dw.c, dw.r, dw.s, 16, device="cpu", data=pinned(dw))
+    h2d = (x_hb.data.numel() + g_hb.data.numel() + w_hb.data.numel()) * 4
+    d2h = (y_hb.data.numel() + dx_hb.data.numel() + dw_hb.data.numel()) * 4
+    hstep = d.HostStep(spec, math, args.chunk)
 
     def e2e_step():
-        ib.data.copy_(xb_host, non_blocking=True)
-        gb.data.copy_(gb_host, non_blocking=True)
-        wb.data.copy_(wb_host, non_blocking=True)
-        step()
-        out_host.copy_(out.data, non_blocking=True)
-        gi_host.copy_(gi.data, non_blocking=True)
-        dw_host.copy_(dw.data, non_blocking=True)
+        hstep.run(x_hb, w_hb, g_hb, y_hb, dx_hb, dw_hb, sync=False)
+        if pg is not None:  # data-parallel dW sum (64 KiB) through the device
+            dw.data.copy_(dw_hb.data, non_blocking=True)
+            pg.all_reduce(dw.data)
+            dw_hb.data.copy_(dw.data, non_blocking=True)
 
     for _ in range(max(1, args.warmup // 2)):
         e2e_step()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
-    barrier()
+    with sampler:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
     if pg is not None:
         pg.all_reduce(e2e_ms, op=pg.ReduceOp.MAX)
@@ -367,7 +381,9 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "tiles": {"fwd": fplan.blocking, "bwd": bctx.blocking, "upd": uplan.blocking}},
             "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "api": "dconv_host_step_run (pinned host blocked tensors)",
+                    "chunk_images": hstep.chunk, "ms_per_step": round(float(e2e_ms.item()), 4),
+                    "gpu_launches_per_step": hstep.launches()},
             "gpu_launches": launches * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -615,6 +631,7 @@ def main():
     ap.add_argument("--workload", default="layer", choices=["layer", "resnet50"])
     ap.add_argument("--global-batch", type=int, default=256)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--chunk", type=int, default=8, help="images per host-step chunk (e2e); 0 = N/4")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -218,6 +218,23 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
                         const dconv_wt_t* grad_w, int accumulate, void* workspace, dconv_stream_t stream);
 int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out);
 
+/* ---------------------------------------------------------------- host-buffer step */
+/* One layer step on HOST tensors (pinned for overlap), the reference's
+ * execute contract (propagation.cpp:56-61 forward_into, :237-261 backward_with,
+ * :377-458 weight_update take host memory): the batch streams through the GPU
+ * in chunks of `chunk_images` (0 = N/4) with H2D of chunk i+1, the kernels of
+ * chunk i and D2H of chunk i-1 overlapped on internal streams. Descriptor
+ * `data` fields are HOST pointers. A null y / dx / dw skips that pass. The
+ * call is asynchronous on `stream`, which completes after every copy. */
+typedef struct dconv_host_step* dconv_host_step_t;
+int dconv_host_step_create(const dconv_spec_t* spec, int math, int chunk_images, dconv_host_step_t* step);
+void dconv_host_step_destroy(dconv_host_step_t step);
+int dconv_host_step_chunk(dconv_host_step_t step);
+int dconv_host_step_run(dconv_host_step_t step, const dconv_act_t* x, const dconv_wt_t* w, const dconv_act_t* dy,
+                        const dconv_act_t* y, const dconv_act_t* dx, const dconv_wt_t* dw, dconv_stream_t stream);
+/* kernels launched by the last run */
+int dconv_host_step_launches(dconv_host_step_t step);
+
 /* ---------------------------------------------------------------- profiling */
 /* enable != 0: bracket each pass's main conv kernel(s) with CUDA events on the
  * launch stream (0 forward, 1 backward-data, 2 weight-update) */

@@ -9,7 +9,7 @@ from ._lib import lib as _load_lib
 from .api import (  # noqa: F401
     BackwardContext, BackwardRoute, BlockedActivation, BlockedWeight, ChainShapeMismatch, ConvLayerSpec, CudaError,
     EmptyTrace, EngineConfig, Error, ExecutionPlan, FusedOp, FusedOpKind, InfeasibleStrategy, InvalidArgument,
-    InvalidDescriptor, InvalidLayerSpec, Math, NonIntegralShape, OverflowRisk, ParseError, PlanInfeasible,
+    HostStep, InvalidDescriptor, InvalidLayerSpec, Math, NonIntegralShape, OverflowRisk, ParseError, PlanInfeasible,
     PlanTensorMismatch, ShapeMismatch, Unsupported, UpdateMode, UpdatePlan, WeightUpdateStrategy, apply_fused_op,
     backward, backward_with, choose_backward_route, choose_spatial_blocking, choose_update_strategy, copy_with_halo,
     derive_output_shape, forward, forward_into, from_blocked_activation, from_blocked_weight, make_forward_plan,

@@ -60,7 +60,8 @@ EXPORTS = [
     "dconv_backward_data", "dconv_bwd_launches", "dconv_upd_plan_create", "dconv_upd_plan_destroy",
     "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
     "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms", "dconv_forward_ex", "dconv_backward_data_ex",
-    "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_sgd",
+    "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_sgd", "dconv_host_step_create", "dconv_host_step_destroy",
+    "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches",
 ]
 
 
@@ -114,6 +115,11 @@ def _bind(lib):
         "dconv_maxpool_fwd": (i, [P(Act), P(Act), vp, vp]),
         "dconv_maxpool_bwd": (i, [P(Act), vp, P(Act), vp, vp]),
         "dconv_sgd": (i, [P(Wt), P(Wt), C.c_float, vp]),
+        "dconv_host_step_create": (i, [P(Spec), i, i, P(vp)]),
+        "dconv_host_step_destroy": (None, [vp]),
+        "dconv_host_step_chunk": (i, [vp]),
+        "dconv_host_step_run": (i, [vp, P(Act), P(Wt), P(Act), P(Act), P(Act), P(Wt), vp]),
+        "dconv_host_step_launches": (i, [vp]),
         "dconv_profile_last_ms": (C.c_float, [i]),
     }
     for name, (res, args) in sig.items():

@@ -679,3 +679,46 @@ def weight_update(spec: ConvLayerSpec, inp: BlockedActivation, grad_out: Blocked
     plan.execute(inp, grad_out, dw)
     _sync(sync)
     return dw
+
+
+class HostStep:
+    """One layer step (forward, backward-data, weight update) on HOST tensors:
+    the reference's execute contract (forward_into propagation.cpp:56-61,
+    backward_with :237-261, weight_update :377-458 all take host memory and
+    return finished results). The batch streams through the GPU in image
+    chunks with copies and kernels overlapped (dconv_host_step_run). Host
+    tensors are CPU BlockedActivation / BlockedWeight storages; pin them
+    (``pin_memory()``) for full-duplex overlap."""
+
+    def __init__(self, spec: ConvLayerSpec, math: Math = Math.F32, chunk_images: int = 0):
+        self.spec, self.math = spec, Math(math)
+        self._h = C.c_void_p()
+        _check(_lib.lib().dconv_host_step_create(C.byref(spec.to_c()), int(math), int(chunk_images),
+                                                 C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().dconv_host_step_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+    @property
+    def chunk(self) -> int:
+        return _lib.lib().dconv_host_step_chunk(self._h)
+
+    def launches(self) -> int:
+        return _lib.lib().dconv_host_step_launches(self._h)
+
+    def run(self, x: Optional[BlockedActivation], w: Optional[BlockedWeight], dy: Optional[BlockedActivation],
+            y: Optional[BlockedActivation] = None, dx: Optional[BlockedActivation] = None,
+            dw: Optional[BlockedWeight] = None, sync: bool = True) -> None:
+        for t in (x, w, dy, y, dx, dw):
+            if t is not None and t.data.device.type != "cpu":
+                raise InvalidArgument("HostStep.run: tensors must live in host memory")
+        ref = lambda t: C.byref(t.to_c()) if t is not None else None  # noqa: E731
+        _check(_lib.lib().dconv_host_step_run(self._h, ref(x), ref(w), ref(dy), ref(y), ref(dx), ref(dw),
+                                              _stream_ptr()))
+        _sync(sync)

@@ -270,3 +270,51 @@ def test_weight_update_validation(dconv):
         dconv.weight_update(spec, ib, gb, None, 3, 1)
     with pytest.raises(dconv.ShapeMismatch):
         dconv.weight_update(spec, dconv.BlockedActivation(4, 8, 8, 8, 8, 0, 0), gb)
+
+
+# ------------------------------------------------------------------ host-buffer step (chunked, overlapped)
+
+
+@pytest.mark.parametrize("shape,chunk", [((6, 32, 48, 12, 12, 3, 3, 1, 1, 1), 4), ((5, 16, 32, 14, 14, 1, 1, 2, 0, 0), 2),
+                                         ((4, 64, 16, 8, 8, 1, 1, 1, 0, 0), 0)])
+@pytest.mark.parametrize("math", [0, 1])
+def test_host_step_matches_device_passes(dconv, orc, shape, chunk, math):
+    """dconv_host_step_run on host tensors == the device-resident passes: forward
+    and backward-data bitwise (same kernels per image), dW to rounding (the
+    chunked split-K sums in another fixed order) and to the oracle."""
+    N, C_, K, H, W, R, S, st, ph, pw = shape
+    spec = dconv.make_layer_spec(N, C_, K, H, W, R, S, st, ph, pw, 16)
+    P, Q = dconv.derive_output_shape(spec)
+    x = orc.random_f32(31, (N, C_, H, W))
+    w = orc.random_f32(32, (K, C_, R, S)) * 0.2
+    g = orc.random_f32(33, (N, K, P, Q))
+    ib = dconv.to_blocked_activation(dev(x), spec)
+    wb = dconv.to_blocked_weight(dev(w), spec)
+    gb = dconv.to_blocked_activation(dev(g), 16, 0, 0)
+    y_ref = dconv.forward(spec, ib, wb, dconv.make_forward_plan(spec, 1, None, None, math))
+    dx_ref = dconv.backward_with(dconv.prepare_backward(spec, wb, 1, None, math), gb)
+    dw_ref = dconv.weight_update(spec, ib, gb, None, dtype=math)
+
+    def host(t):
+        return t.data.cpu().pin_memory()
+
+    B = dconv.BlockedActivation
+    xh = B(ib.n, ib.c, ib.h, ib.w, 16, ib.halo_h, ib.halo_w, device="cpu", data=host(ib))
+    gh = B(gb.n, gb.c, gb.h, gb.w, 16, 0, 0, device="cpu", data=host(gb))
+    wh = dconv.BlockedWeight(K, C_, R, S, 16, device="cpu", data=host(wb))
+    yh = B(N, K, P, Q, 16, 0, 0, device="cpu", data=torch.full_like(host(y_ref), 7.0))
+    dxh = B(N, C_, H, W, 16, 0, 0, device="cpu", data=torch.full_like(host(dx_ref), 7.0))
+    dwh = dconv.BlockedWeight(K, C_, R, S, 16, device="cpu", data=torch.full_like(host(dw_ref), 7.0))
+    step = dconv.HostStep(spec, math, chunk)
+    for _ in range(2):  # second run reuses plans and staging
+        step.run(xh, wh, gh, yh, dxh, dwh)
+        assert torch.equal(yh.data, y_ref.data.cpu())
+        assert torch.equal(dxh.data, dx_ref.data.cpu())
+        gate(orc, dw_ref.data.cpu().numpy(), dwh.data.numpy(), math)
+    assert step.launches() > 0
+    # pass selection: forward only
+    yh.data.fill_(7.0)
+    step.run(xh, wh, None, yh)
+    assert torch.equal(yh.data, y_ref.data.cpu())
+    with pytest.raises(dconv.InvalidArgument):
+        step.run(ib, wb, gb, y_ref)
