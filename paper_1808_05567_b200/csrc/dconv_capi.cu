@@ -1201,6 +1201,9 @@ struct UpdLaunch {
   size_t smem;
   size_t ws_in, ws_do, ws_partial;  // workspace byte sizes (piece tensors, partials)
   bool split_in, split_do;
+  // fp32 operands converted in shared memory (conv_upd_raw_kernel)
+  bool raw = false, cat = false;
+  int raw_stages = 0, pc_stages = 0;
 };
 
 // Tile selection for the split-K UPD (replaces choose_update_strategy /
@@ -1296,7 +1299,38 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
         break;
       }
   }
+  // fp32 tensors: convert in shared memory when a raw ring (>= 2 deep) and a
+  // piece ring fit; otherwise split through HBM (conv_upd_kernel)
+  const bool want_raw = in.dtype == DCONV_F32 && dout.dtype == DCONV_F32 && !(pl.has_cfg && pl.cfg.stages < 0);
+  if (want_raw) {
+    const Cand* rb = nullptr;
+    int rbest_r = 0, rbest_s = 0;
+    const int tiers[3][2] = {{3, 2}, {2, 2}, {2, 1}};
+    for (int tier = 0; tier < 3 && !rb; ++tier)
+      for (auto& cd : cands) {
+        if (cd.passes != 1) continue;
+        const int a_planes = stacked ? cb : 8;
+        const UpdRawLayout rl = upd_raw_layout(cd.a_px, cd.vs, p.nb, pieces, stacked ? p.stack : 1, a_planes, 1);
+        const int sp = tiers[tier][1];
+        const int64_t left = static_cast<int64_t>(kSmemBudget) - static_cast<int64_t>(sp) * rl.pc_slot;
+        const int rr = left > 0 ? static_cast<int>(std::min<int64_t>(kMaxStages, left / rl.raw_slot)) : 0;
+        if (rr >= tiers[tier][0]) {
+          rb = &cd;
+          rbest_r = rr;
+          rbest_s = sp;
+          break;
+        }
+      }
+    if (rb) {
+      best = rb;
+      L.raw = true;
+      L.raw_stages = rbest_r;
+      L.pc_stages = rbest_s;
+      if (pl.has_cfg && pl.cfg.stages > 0) L.raw_stages = std::max(2, std::min(L.raw_stages, pl.cfg.stages));
+    }
+  }
   if (!best) fail(DCONV_ERR_PLAN_INFEASIBLE, "no weight-update tile fits shared memory / TMA box limits");
+  if (L.raw) L.split_in = L.split_do = false;
   p.wsub = best->wsub;
   p.rows_ps = best->rows_ps;
   p.in_rows = best->in_rows;
@@ -1335,8 +1369,11 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       ++p.n_tgroups;
     }
   } else {
-    // tap groups: per phase, <= 512 TMEM columns of accumulators
-    p.tg = std::max(1, std::min(512 / NT, taps.taps_box));
+    // tap groups: per phase, <= 512 TMEM columns of accumulators. The
+    // concatenated-piece MMA (3 column groups per tap) is used when every tap
+    // of a phase still fits and N = 3 NT is a legal MMA width.
+    L.cat = L.raw && pieces == 3 && 3 * NT <= 256 && 3 * NT * taps.taps_box <= 512;
+    p.tg = std::max(1, std::min(512 / (L.cat ? 3 * NT : NT), taps.taps_box));
     for (int ph = 0; ph < taps.n_phases; ++ph)
       for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += p.tg) {
         if (p.n_tgroups >= kMaxTapGroups) fail(DCONV_ERR_UNSUPPORTED, "too many tap groups");
@@ -1348,7 +1385,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   }
   // split-K: >= 2 waves of CTAs, >= 2 stages per split
   const int tiles = n_ctiles * p.n_tgroups * n_ktiles;
-  int splits = cdiv(2 * sm_count(), tiles);
+  // raw path: one CTA per SM (smem-bound), one wave; HBM-split path: >= 2 waves
+  int splits = L.raw ? std::max(1, sm_count() / tiles) : cdiv(2 * sm_count(), tiles);
   splits = std::max(1, std::min(splits, std::max(1, p.stages_total / 2)));
   if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
   p.splits = splits;
@@ -1359,6 +1397,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
                 static_cast<unsigned>(splits));
   L.stages = stages;
   L.smem = static_cast<size_t>(stages) * layout.bytes;
+  if (L.raw) {
+    const UpdRawLayout rl = upd_raw_layout(p.a_px, p.vs, p.nb, pieces, stacked ? p.stack : 1, p.cb_eff, L.raw_stages);
+    L.smem = static_cast<size_t>(rl.pc_off) + static_cast<size_t>(L.pc_stages) * rl.pc_slot;
+  }
   L.ws_in = L.split_in ? align256(static_cast<size_t>(pieces) * act_elems(in) * 2) : 0;
   L.ws_do = L.split_do ? align256(static_cast<size_t>(pieces) * act_elems(dout) * 2) : 0;
   L.ws_partial = align256(static_cast<size_t>(splits) * p.n_taps * p.c_pad * p.k_pad * sizeof(float));
@@ -1384,6 +1426,36 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     return is_in ? encode(1, 5, base, dims, strides, box_in, estr_in, "upd input rows")
                  : encode(1, 5, base, dims, strides, box_do, nullptr, "upd dO rows");
   };
+  // raw fp32 maps: 64 B pixel rows, SWIZZLE_64B (converters read them swizzled)
+  auto raw_map = [&](const dconv_act_t& a, bool is_in) {
+    const int hp = a.h + 2 * a.halo_h, wp = a.w + 2 * a.halo_w;
+    const uint64_t planes = static_cast<uint64_t>(a.n) * (is_in ? cb : kb);
+    const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_64B;
+    if (linear) {
+      const uint64_t dims[3] = {16, static_cast<uint64_t>(a.h) * a.w, planes};
+      const uint64_t strides[2] = {64, static_cast<uint64_t>(a.h) * a.w * 64};
+      const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs), static_cast<uint32_t>(is_in ? 8 : p.nb)};
+      return encode(0, 3, a.data, dims, strides, box, nullptr, is_in ? "upd input linear f32" : "upd dO linear f32",
+                    swz);
+    }
+    const char* base = reinterpret_cast<const char*>(a.data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 64;
+    const uint64_t dims[4] = {16, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), planes};
+    const uint64_t strides[3] = {64, static_cast<uint64_t>(wp) * 64, static_cast<uint64_t>(wp) * hp * 64};
+    if (is_in) {
+      const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st),
+                               static_cast<uint32_t>(p.cb_eff)};
+      const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
+      return encode(0, 4, base, dims, strides, box, estr, "upd input rows f32", swz);
+    }
+    const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps),
+                             static_cast<uint32_t>(p.nb)};
+    return encode(0, 4, base, dims, strides, box, nullptr, "upd dO rows f32", swz);
+  };
+  if (L.raw) {
+    L.map_in = raw_map(in, true);
+    L.map_do = raw_map(dout, false);
+    return L;
+  }
   L.map_in = act_map(in, in_pieces, cb, true);
   L.map_do = act_map(dout, do_pieces, kb, false);
   return L;
@@ -1514,8 +1586,21 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
       kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages, a_base, acc);
       cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
     };
+    auto go_raw = [&](auto kern) {
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
+                 "smem attribute");
+      kern<<<L.grid, kUpdRawWarps * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages, L.pc_stages);
+      cuda_check(cudaGetLastError(), "conv_upd_raw_kernel launch");
+    };
     prof_begin(2, cs);
-    if (plan->pieces == 1) {
+    if (L.raw) {
+      if (plan->pieces == 1)
+        go_raw(conv_upd_raw_kernel<1, false>);
+      else if (L.cat)
+        go_raw(conv_upd_raw_kernel<3, true>);
+      else
+        go_raw(conv_upd_raw_kernel<3, false>);
+    } else if (plan->pieces == 1) {
       go(conv_upd_kernel<1, 1>, 0, 0);
     } else if (L.passes == 1) {
       go(conv_upd_kernel<3, 3>, 0, 0);
@@ -1527,16 +1612,18 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     prof_end(2, cs);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
-    upd_reduce_kernel<<<grid1d(total, 64), 64, 0, cs>>>(partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K,
-                                                      cb, kb, grad_w->data, grad_w->dtype == DCONV_BF16,
-                                                      accumulate ? 1 : 0);
+    upd_reduce_kernel<<<static_cast<unsigned>(cdiv64(total, 32)), dim3(32, kRedGroups), 0, cs>>>(
+        partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K, cb, kb, grad_w->data,
+        grad_w->dtype == DCONV_BF16, accumulate ? 1 : 0);
     cuda_check(cudaGetLastError(), "upd_reduce launch");
     char buf[512];
     std::snprintf(buf, sizeof(buf),
                   "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
-                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d}",
+                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
+                  "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d}",
                   L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
-                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces, L.passes);
+                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces, L.passes,
+                  L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0);
     plan->last_desc = buf;
   });
 }

@@ -221,44 +221,365 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);
 }
 
+// ---------------------------------------------------------------------------
+// fp32 operands converted in shared memory (no HBM piece tensors).
+//
+// Stage = the same operand boxes as conv_upd_kernel, but TMA brings the fp32
+// pixels (64 B rows, SWIZZLE_64B) into a RAW ring; converter warps split them
+// into bf16 pieces (PIECES = 3: exact hi/mid/lo; 1: round to bf16) in the
+// canonical MN-major layout of a PIECE ring that the MMA reads. HBM traffic
+// is the fp32 tensors once; the split never round-trips through HBM.
+//
+// CAT (PIECES = 3 only): the three dO pieces sit consecutively along N, so
+// A0 x [B0|B1|B2], A1 x [B0|B1] and A2 x B0 are three MMAs of N = 3NT, 2NT
+// and NT instead of six of N = NT (half the A-operand smem reads). The
+// accumulator has three column groups X | Y | Z (X = a0 b0, Y and Z collect
+// the corrections); the epilogue adds them.
+//
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (+TMEM owner),
+// w4..w11 converters during the main loop; w4..w7 then run the epilogue.
+constexpr int kUpdRawWarps = 12;
+constexpr int kUpdCvtWarp0 = 4, kUpdCvtWarps = 8;
+
+struct UpdRawLayout {
+  uint32_t a_sub;     // raw bytes of one A box (1 KiB aligned; stacked: one per tap slot)
+  uint32_t a_raw;     // raw A bytes per stage
+  uint32_t raw_slot;  // raw ring slot (A boxes then the dO box)
+  uint32_t pc_slot;   // piece ring slot (UpdStage layout with PA = PB = pieces)
+  uint32_t pc_off;    // piece ring start
+};
+
+__host__ __device__ inline UpdRawLayout upd_raw_layout(int a_px, int vs, int nb, int pieces, int a_boxes,
+                                                       int a_planes_per_box, int raw_stages) {
+  UpdRawLayout L;
+  L.a_sub = (static_cast<uint32_t>(a_planes_per_box) * a_px * 64u + 1023u) & ~1023u;
+  L.a_raw = L.a_sub * a_boxes;
+  L.raw_slot = (L.a_raw + static_cast<uint32_t>(nb) * vs * 64u + 1023u) & ~1023u;
+  L.pc_slot = upd_stage_layout(a_px, vs, nb, pieces, pieces).bytes;
+  L.pc_off = L.raw_slot * raw_stages;
+  return L;
+}
+
+// 16 B chunk k of row j of a SWIZZLE_64B box whose start is 1 KiB aligned
+__device__ __forceinline__ uint32_t sw64_row(uint32_t j, uint32_t k) { return j * 64u + ((k ^ ((j >> 1) & 3u)) << 4); }
+
+template <int PIECES, bool CAT>
+__global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
+    conv_upd_raw_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
+                        const __grid_constant__ UpdParams p, int raw_stages, int pc_stages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int NT = 16 * p.nb;
+  const int ctile = blockIdx.x / p.n_tgroups;
+  const int tgrp = blockIdx.x % p.n_tgroups;
+  const int ktile = blockIdx.y;
+  const int split = blockIdx.z;
+  const int per = (p.stages_total + p.splits - 1) / p.splits;
+  const int s_begin = split * per;
+  const int s_end = min(p.stages_total, s_begin + per);
+  const int iters = s_end > s_begin ? s_end - s_begin : 0;
+  const int ph = p.tg_phase[tgrp];
+  const int tap0 = p.tg_tap0[tgrp];
+  const int ntaps = p.tg_ntaps[tgrp];
+  const bool stacked = p.stack > 1;
+  const int a_boxes = stacked ? ntaps : 1;
+  const int a_planes = stacked ? p.cb_eff : 8;  // channel blocks per A box
+  const UpdRawLayout R = upd_raw_layout(p.a_px, p.vs, p.nb, PIECES, stacked ? p.stack : 1, a_planes, raw_stages);
+  const UpdStage S = upd_stage_layout(p.a_px, p.vs, p.nb, PIECES, PIECES);
+  const uint32_t smem0 = smem_u32(smem);
+  constexpr int kGroups = CAT ? 3 : 1;  // accumulator column groups per tap
+  const int acc_w = kGroups * NT;
+
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(p.tg * acc_w)) tmem_cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_in);
+    tma_prefetch_desc(&map_do);
+    for (int s = 0; s < raw_stages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], kUpdCvtWarps);
+    }
+    for (int s = 0; s < pc_stages; ++s) {
+      mbar_init(&pc_full[s], kUpdCvtWarps);
+      mbar_init(&pc_empty[s], 1);
+    }
+    mbar_init(&accum_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (fp32 boxes)
+    if (lane == 0) {
+      const uint32_t a_box_bytes = static_cast<uint32_t>(a_planes) * p.a_px * 64u;
+      const uint32_t b_bytes = static_cast<uint32_t>(p.nb) * p.vs * 64u;
+      for (int it = 0; it < iters; ++it) {
+        const int s = it % raw_stages;
+        mbar_wait(&raw_empty[s], (static_cast<uint32_t>(it / raw_stages) & 1u) ^ 1u);
+        const int stage = s_begin + it;
+        const int n = stage / p.stages_per_img;
+        const int band = stage % p.stages_per_img;
+        uint8_t* st = smem + static_cast<uint32_t>(s) * R.raw_slot;
+        mbar_arrive_expect_tx(&raw_full[s], a_box_bytes * a_boxes + b_bytes);
+        const int pa = n * p.in_cb + ctile * 8;
+        if (stacked) {
+          for (int j = 0; j < ntaps; ++j) {
+            const int tp = tap0 + j, tph = p.tap_ph[tp];
+            tma_load_4d(st + j * R.a_sub, &map_in, &raw_full[s], 0,
+                        p.in_col0 + p.phase_col[tph] + p.stride * p.tap_s2[tp],
+                        p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]), pa);
+          }
+        } else if (p.linear) {
+          tma_load_3d(st, &map_in, &raw_full[s], 0, band * p.vs, pa);
+        } else {
+          tma_load_4d(st, &map_in, &raw_full[s], 0, p.in_col0 + p.phase_col[ph],
+                      p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], pa);
+        }
+        const int pb = n * p.do_cb + ktile * p.nb;
+        if (p.linear)
+          tma_load_3d(st + R.a_raw, &map_do, &raw_full[s], 0, band * p.vs, pb);
+        else
+          tma_load_4d(st + R.a_raw, &map_do, &raw_full[s], 0, 0, band * p.rows_ps, pb);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const int ksteps = p.vs / 16;
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % pc_stages;
+      mbar_wait(&pc_full[s], static_cast<uint32_t>(it / pc_stages) & 1u);
+      tc_fence_after();
+      const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * R.pc_slot;
+      if (elect_one()) {
+        const int n_acc = stacked ? 1 : ntaps;
+        for (int t = 0; t < n_acc; ++t) {
+          const int shift = stacked ? 0 : p.tap_shift[tap0 + t];
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * acc_w);
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const bool first = it == 0 && ks == 0;
+            // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels
+            auto adesc = [&](int ia) {
+              return make_smem_desc(st + static_cast<uint32_t>(ia) * S.a_piece +
+                                        static_cast<uint32_t>(ks * 16 + shift) * 16u,
+                                    128, S.a_plane);
+            };
+            auto bdesc = [&](int ib) {
+              return make_smem_desc(st + S.b_off + static_cast<uint32_t>(ib) * S.b_piece +
+                                        static_cast<uint32_t>(ks) * 256u,
+                                    128, S.b_plane);
+            };
+            if (CAT) {
+              // X|Y|Z += a0 [b0|b1|b2];  Y|Z += a1 [b0|b1];  Z += a2 b0
+              mma_bf16(d_tmem, adesc(0), bdesc(0), make_idesc(1, 1, 1, 128, 3u * NT), first ? 0u : 1u);
+              mma_bf16(d_tmem + NT, adesc(1), bdesc(0), make_idesc(1, 1, 1, 128, 2u * NT), 1u);
+              mma_bf16(d_tmem + 2 * NT, adesc(2), bdesc(0), make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT)),
+                       1u);
+            } else {
+              const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
+#pragma unroll
+              for (int ia = 0; ia < PIECES; ++ia)
+#pragma unroll
+                for (int ib = 0; ib < PIECES; ++ib) {
+                  if (ia + ib > 2) continue;
+                  mma_bf16(d_tmem, adesc(ia), bdesc(ib), idesc, (first && ia == 0 && ib == 0) ? 0u : 1u);
+                }
+            }
+          }
+        }
+        mma_commit(&pc_empty[s]);
+        if (it == iters - 1) mma_commit(&accum_bar);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= kUpdCvtWarp0) {
+    // ------------------------------------------------------------ converters (fp32 raw -> bf16 pieces)
+    // Work unit = one 16 B-chunk plane (8 channels) of one operand: A has
+    // a_boxes * a_planes * 2 <= 16 of them, dO 2 * nb <= 32. Warp cw owns chunk
+    // planes cw, cw + 8, ... of each operand for the whole kernel, so all
+    // index math is hoisted out of the stage loop; a warp's lanes walk the
+    // plane's pixels 32 at a time (conflict-free swizzled reads, contiguous writes).
+    const int cw = warp - kUpdCvtWarp0;
+    const int a_cps = a_boxes * a_planes * 2, b_cps = 2 * p.nb;
+    // slots 0-1: A chunk planes cw, cw + 8; slots 2-5: dO chunk planes cw + 8 j (npx = 0: unused)
+    uint32_t src_base[6], dst_base[6], piece_str[6], cp_rows0[6], cp_c0[6];
+    int cp_npx[6];
+#pragma unroll
+    for (int u = 0; u < 6; ++u) {
+      const bool is_a = u < 2;
+      const int cp = cw + kUpdCvtWarps * (is_a ? u : u - 2);
+      const bool ok = cp < (is_a ? a_cps : b_cps);
+      cp_npx[u] = ok ? (is_a ? p.a_px : p.vs) : 0;
+      cp_c0[u] = 2u * (cp & 1);
+      if (is_a) {
+        const int pl = (cp >> 1) % a_planes, box = (cp >> 1) / a_planes;
+        src_base[u] = box * R.a_sub;
+        cp_rows0[u] = pl * p.a_px;
+        dst_base[u] = static_cast<uint32_t>(cp) * S.a_plane;
+        piece_str[u] = S.a_piece;
+      } else {
+        src_base[u] = R.a_raw;
+        cp_rows0[u] = (cp >> 1) * p.vs;
+        dst_base[u] = S.b_off + static_cast<uint32_t>(cp) * S.b_plane;
+        piece_str[u] = S.b_piece;
+      }
+    }
+    int rs = 0, ps = 0;
+    uint32_t rph = 0, pph = 0;
+    for (int it = 0; it < iters; ++it) {
+      mbar_wait(&raw_full[rs], rph);
+      mbar_wait(&pc_empty[ps], pph ^ 1u);
+      const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
+      uint8_t* pcs = smem + R.pc_off + static_cast<uint32_t>(ps) * R.pc_slot;
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        const uint32_t piece_stride = piece_str[u];
+        const uint8_t* src0 = raw + src_base[u];
+        uint8_t* dst0 = pcs + dst_base[u];
+        const uint32_t row0 = cp_rows0[u];
+        const uint32_t c0 = cp_c0[u];
+        for (int px = lane; px < cp_npx[u]; px += 32) {
+          const uint32_t row = row0 + px;
+          const uint8_t* src = src0 + sw64_row(row, c0);
+          const float4 a = *reinterpret_cast<const float4*>(src);
+          // chunk c0 + 1 of the same row: bit 4 flips under the row's XOR pattern
+          const float4 b = *reinterpret_cast<const float4*>(src0 + (sw64_row(row, c0) ^ 16u));
+          const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          uint8_t* dst = dst0 + px * 16;
+          if (PIECES == 3) {
+            uint4 h, m, l;
+            split8(v, h, m, l);
+            *reinterpret_cast<uint4*>(dst) = h;
+            *reinterpret_cast<uint4*>(dst + piece_stride) = m;
+            *reinterpret_cast<uint4*>(dst + 2 * piece_stride) = l;
+          } else {
+            *reinterpret_cast<uint4*>(dst) = cast8(v);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rs]);
+        mbar_arrive(&pc_full[ps]);
+      }
+      if (++rs == raw_stages) {
+        rs = 0;
+        rph ^= 1u;
+      }
+      if (++ps == pc_stages) {
+        ps = 0;
+        pph ^= 1u;
+      }
+    }
+    if (warp < kUpdCvtWarp0 + 4) {
+      // -------------------------------------------------------- epilogue (w4..w7: TMEM lane quarters)
+      const int qrow = (warp % 4) * 32;
+      const int c_glob = ctile * 128 + qrow + lane;
+      if (iters > 0) {
+        mbar_wait(&accum_bar, 0);
+        tc_fence_after();
+      }
+      const int n_acc = stacked ? 1 : ntaps;
+      for (int t = 0; t < n_acc; ++t) {
+        const int slot = stacked ? (qrow + lane) / (16 * p.cb_eff) : 0;
+        const int c_row = stacked ? (qrow + lane) % (16 * p.cb_eff) : c_glob;
+        const bool row_ok = stacked ? slot < ntaps : true;
+        const int rs = p.tap_src[tap0 + (stacked ? (row_ok ? slot : 0) : t)];
+        float* dst_row =
+            p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(t * acc_w);
+        for (int g = 0; g < p.nb; ++g) {
+          uint32_t r[16], ry[16], rz[16];
+          tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
+          if (CAT) {
+            tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
+            tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
+          }
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
+          const bool live = iters > 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int q = 4 * e + u;
+              vv[u] = CAT ? __uint_as_float(r[q]) + (__uint_as_float(ry[q]) + __uint_as_float(rz[q]))
+                          : __uint_as_float(r[q]);
+              if (!live) vv[u] = 0.0f;
+            }
+            d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);
+}
+
 // Fixed-order reduction of the split partials into the blocked dW
 // [k_b][c_b][r][s][c][k] (tail lanes written as exact zeros).
-// reduce_weight_copies analog (propagation.cpp:357-375): sum = copy0; sum += copy_g.
-__global__ void upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C,
-                                  int K, int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
-  const long long total = static_cast<long long>(kb) * cb * n_taps * 256;
+// reduce_weight_copies analog (propagation.cpp:357-375). Block = 32 partial
+// elements (coalesced along k) x kRedGroups split groups: group y sums splits
+// y, y + G, y + 2G, ... in increasing order, then the G group sums are added in
+// group order — the same fixed order on every run, so dW is bitwise reproducible.
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(32 * kRedGroups)
+    upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C, int K,
+                      int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
+  __shared__ float red[kRedGroups][33];
+  const int kw = kb * 16, cw = cb * 16;
+  const long long total = static_cast<long long>(n_taps) * cw * kw;
+  const long long f = static_cast<long long>(blockIdx.x) * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  const bool in_range = f < total;
+  const int k = in_range ? static_cast<int>(f % kw) : 0;
+  const int c = in_range ? static_cast<int>((f / kw) % cw) : 0;
+  const int rs = in_range ? static_cast<int>(f / (static_cast<long long>(kw) * cw)) : 0;
+  const bool live = in_range && c < C && k < K;
   const long long split_stride = static_cast<long long>(n_taps) * c_pad * k_pad;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int kl = static_cast<int>(e % 16);
-    const int cl = static_cast<int>((e / 16) % 16);
-    const long long blk = e / 256;  // ((kbi * cb + cbi) * n_taps + rs)
-    const int rs = static_cast<int>(blk % n_taps);
-    const int cbi = static_cast<int>((blk / n_taps) % cb);
-    const int kbi = static_cast<int>(blk / (static_cast<long long>(n_taps) * cb));
-    const int c = cbi * 16 + cl, k = kbi * 16 + kl;
-    float sum = 0.0f;
-    if (c < C && k < K) {
-      const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
-      sum = __ldg(src);
-      // fixed index order; loads batched 8 deep for memory-level parallelism
-      int sp = 1;
-      for (; sp + 8 <= splits; sp += 8) {
-        float v[8];
+  float sum = 0.0f;
+  if (live) {
+    const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
+    int sp = y;
+    for (; sp + 3 * kRedGroups < splits; sp += 4 * kRedGroups) {
+      float v[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sp + u) * split_stride);
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (sp + u * kRedGroups) * split_stride);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sum += v[u];
-      }
-      for (; sp < splits; ++sp) sum += __ldg(src + sp * split_stride);
+      for (int u = 0; u < 4; ++u) sum += v[u];
     }
-    if (dw_bf16) {
-      __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dw) + e;
-      *d = __float2bfloat16_rn(accumulate ? sum + __bfloat162float(*d) : sum);
-    } else {
-      float* d = reinterpret_cast<float*>(dw) + e;
-      *d = accumulate ? *d + sum : sum;
-    }
+    for (; sp < splits; sp += kRedGroups) sum += __ldg(src + sp * split_stride);
+  }
+  red[y][threadIdx.x] = sum;
+  __syncthreads();
+  if (y != 0 || !in_range) return;
+  float tot = red[0][threadIdx.x];
+#pragma unroll
+  for (int g = 1; g < kRedGroups; ++g) tot += red[g][threadIdx.x];
+  if (!live) tot = 0.0f;
+  const int kbi = k / 16, kl = k % 16, cbi = c / 16, cl = c % 16;
+  const long long e = ((static_cast<long long>(kbi) * cb + cbi) * n_taps + rs) * 256 + cl * 16 + kl;
+  if (dw_bf16) {
+    __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dw) + e;
+    *d = __float2bfloat16_rn(accumulate ? tot + __bfloat162float(*d) : tot);
+  } else {
+    float* d = reinterpret_cast<float*>(dw) + e;
+    *d = accumulate ? *d + tot : tot;
   }
 }
 
