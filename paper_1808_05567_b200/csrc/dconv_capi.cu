@@ -239,6 +239,7 @@ struct FwdLaunch {
   size_t smem;
   bool raw_f32;
   int pieces;
+  bool ts = false;  // A pieces staged in tensor memory (single-tap fp32 problems)
 };
 
 // Decide staging mode, tile and pipeline depth; encode TMA maps.
@@ -294,6 +295,66 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   // two TMEM accumulators of mb*16*nb columns must fit in 512. Weight stages
   // hold up to w_taps taps (big filters stream taps through several stages).
   int w_taps = taps.taps_box;
+  // TS: single-tap problems on fp32 activations stage the A pieces in TMEM
+  // (mb = 1; accumulators + a ring of pieces*8 columns per stage <= 512)
+  L.ts = raw_f32 && taps.r.size() == 1 && !(cfg && (cfg->tile_mb == 2 || cfg->stages < 0));
+  int kc = 1;
+  p.w_resident = 0;
+  if (L.ts) {
+    const int ring = pieces * 8;
+    for (int want_bufs : {2, 1}) {
+      for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
+        const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
+        const int acc_cols = (pieces == 3 ? 2 : 1) * 16 * nb;
+        const int left = 512 - want_bufs * acc_cols;
+        // channel blocks per stage: amortise the per-stage barrier / issue cost
+        int kcx = std::min(4, pb.cb_red);
+        while (kcx > 1 && (left <= 0 || left / (ring * kcx) < 2)) kcx >>= 1;
+        const int ring_st = left > 0 ? std::min(kMaxStages, left / (ring * kcx)) : 0;
+        if (left > 0 && ring_st >= 2) {
+          const int apx = 128;
+          const int lb = (linear && !mimg_ok) ? 1 : 0;
+          if (!linear) {
+            const int rows_box = (p.wsub + 128 - 2) / p.wsub + 1;
+            if (p.wsub * st > 256 || rows_box * st > 256) break;
+          }
+          const int apx_rows = linear ? apx : ((p.wsub + 128 - 2) / p.wsub + 1) * p.wsub;
+          // resident weight slice: every CTA keeps one output-channel tile for the
+          // whole launch (grid % n_ntiles == 0) and the slice fits beside the raw ring
+          const int n_nt_tiles = cdiv(kb_total, nb);
+          const int m_tiles = mimg_ok ? cdiv(in.n, 128 / hw) : in.n * cdiv(pb.P * p.wsub, 128);
+          const int grid_est = std::min(m_tiles * n_nt_tiles, sm_count());
+          const int res_bytes = pb.cb_red * pieces * nb * 512;
+          const bool resident = grid_est % n_nt_tiles == 0 && res_bytes <= 120 * 1024;
+          const FwdSmem lay = fwd_smem_layout(apx_rows * kcx, resident ? pb.cb_red : kcx, nb, pieces, true, 0, 1);
+          int wss = resident ? 1
+                             : std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lay.w_slot)));
+          // keep room for the TMA-store staging of dense outputs
+          const int left_s = kFwdBudget - static_cast<int>(kEpiStagingBytes) - wss * static_cast<int>(lay.w_slot);
+          int rws = left_s > 0 ? std::min<int>(kMaxStages, left_s / static_cast<int>(lay.raw_slot)) : 0;
+          if (cfg && cfg->stages > 0) rws = std::max(1, std::min(cfg->stages, rws));
+          if (rws >= 2) {
+            tile.mb = 1;
+            tile.nb = nb;
+            acc_bufs = want_bufs;
+            pc_st = ring_st;
+            raw_st = rws;
+            w_st = wss;
+            w_taps = 1;
+            kc = kcx;
+            p.w_resident = resident ? 1 : 0;
+            layout = fwd_smem_layout(apx_rows * kc, resident ? pb.cb_red : kc, nb, pieces, true, 0, w_st);
+            a_px = apx_rows;
+            lin_boxes = lb;
+            found = true;
+          }
+        }
+        if (want_nb || nb == 1) break;
+      }
+      if (found) break;
+    }
+    if (!found) L.ts = false;
+  }
   for (int tier = 0; tier < 6 && !found; ++tier) {
     const int want_pc = tier < 2 ? 3 : tier < 4 ? 2 : 1;
     const int want_bufs = (tier % 2 == 0) ? 2 : 1;
@@ -373,13 +434,14 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   if (!found) fail(DCONV_ERR_PLAN_INFEASIBLE, "no forward tile fits shared memory / TMA box limits");
   p.mb = tile.mb;
   p.nb = tile.nb;
+  p.kc = kc;
   p.acc_bufs = acc_bufs;
   p.a_px = a_px;
   p.a_load_px = a_px;
   p.lin_boxes = lin_boxes;
   p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
   p.mimg = 0;
-  if (mimg_ok) {
+  if (mimg_ok && (tile.mb == 2 || L.ts)) {
     p.mimg = (128 * tile.mb) / hw;
     p.a_load_px = p.mimg * hw;
   }
@@ -403,18 +465,19 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     const uint64_t dims[4] = {16, static_cast<uint64_t>(hw), static_cast<uint64_t>(p.in_cb),
                               static_cast<uint64_t>(in.n)};
     const uint64_t strides[3] = {pix, pix * hw, pix * hw * p.in_cb};
-    const uint32_t box[4] = {16, static_cast<uint32_t>(hw), 1, static_cast<uint32_t>(p.mimg)};
+    const uint32_t box[4] = {16, static_cast<uint32_t>(hw), static_cast<uint32_t>(kc), static_cast<uint32_t>(p.mimg)};
     L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation multi-image", swz);
   } else if (linear) {
     const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
     const uint64_t strides[2] = {pix, pix * hp * wp};
-    const uint32_t box[3] = {16, 128, 1};
+    const uint32_t box[3] = {16, 128, static_cast<uint32_t>(kc)};
     L.map_a = encode(!raw_f32, 3, in.data, dims, strides, box, nullptr, "activation linear", swz);
   } else {
     const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * pix;
     const uint64_t dims[4] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h), planes};
     const uint64_t strides[3] = {pix, pix * wp, pix * wp * hp};
-    const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st), 1};
+    const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>((a_px / p.wsub) * st),
+                             static_cast<uint32_t>(kc)};
     const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
     L.map_a = encode(!raw_f32, 4, base, dims, strides, box, estr, "activation rows", swz);
   }
@@ -427,18 +490,48 @@ int g_fwd_dbg_mode = 0;
 void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
   L.p.dbg = g_fwd_dbg;
   L.p.dbg_mode = g_fwd_dbg_mode;
-  auto go = [&](auto kern) {
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
+  // dense outputs (no halo / lattice / padding columns / multi-image rows):
+  // the epilogue stages 32-pixel slabs in smem and TMA-stores them
+  FwdParams& p = L.p;
+  const int esz = p.out_bf16 ? 2 : 4;
+  const size_t staging = kEpiStagingBytes;
+  size_t smem = L.smem;
+  p.tma_store = 0;
+  CUtensorMap map_out, map_out2;
+  std::memset(&map_out, 0, sizeof(map_out));
+  std::memset(&map_out2, 0, sizeof(map_out2));
+  if (p.mimg == 0 && p.out_halo_h == 0 && p.out_halo_w == 0 && p.out_scale == 1 && p.out_y0 == 0 &&
+      p.out_x0 == 0 && p.out_hp == p.P && p.out_wp == p.Q && p.wsub == p.Q && !(p.dbg_mode & 1) &&
+      L.smem + staging <= static_cast<size_t>(kSmemBudget)) {
+    const uint64_t pq = static_cast<uint64_t>(p.P) * p.Q;
+    const uint64_t dims[4] = {16, pq, static_cast<uint64_t>(p.out_cb), static_cast<uint64_t>(p.n_img)};
+    const uint64_t strides[3] = {16ull * esz, pq * 16 * esz, pq * 16 * esz * p.out_cb};
+    const uint32_t box[4] = {16, 32, 1, 1};
+    map_out = encode(p.out_bf16, 4, p.out, dims, strides, box, nullptr, "output slab",
+                     p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+    const uint32_t box2[4] = {16, 32, 2, 1};
+    map_out2 = encode(p.out_bf16, 4, p.out, dims, strides, box2, nullptr, "output slab pair",
+                      p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+    p.tma_store = 1;
+    smem = L.smem + staging;
+  }
+  auto go = [&](auto kern, int threads) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
-    kern<<<L.grid, kFwdThreadsP, L.smem, stream>>>(L.map_a, L.p, L.raw_stages, L.stages, L.w_stages);
+    kern<<<L.grid, threads, smem, stream>>>(L.map_a, map_out, map_out2, L.p, L.raw_stages, L.stages, L.w_stages);
   };
-  if (L.raw_f32) {
+  if (L.ts) {
     if (L.pieces == 3)
-      go(conv_fwd_kernel<true, 3>);
+      go(conv_fwd_kernel<true, 3, true>, kFwdThreadsTS);
     else
-      go(conv_fwd_kernel<true, 1>);
+      go(conv_fwd_kernel<true, 1, true>, kFwdThreadsTS);
+  } else if (L.raw_f32) {
+    if (L.pieces == 3)
+      go(conv_fwd_kernel<true, 3>, kFwdThreadsP);
+    else
+      go(conv_fwd_kernel<true, 1>, kFwdThreadsP);
   } else {
-    go(conv_fwd_kernel<false, 1>);
+    go(conv_fwd_kernel<false, 1>, kFwdThreadsP);
   }
   cuda_check(cudaGetLastError(), "conv_fwd_kernel launch");
 }
@@ -471,11 +564,11 @@ std::string json_tile(const FwdLaunch& L) {
   std::snprintf(buf, sizeof(buf),
                 "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
                 "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d,"
-                "\"mimg\":%d}",
+                "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
                 L.grid.x,
                 (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
-                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg);
+                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store);
   return buf;
 }
 

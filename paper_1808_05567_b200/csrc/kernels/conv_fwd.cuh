@@ -160,6 +160,8 @@ constexpr uint32_t kEpiStageBytes = 0;
 // 16B chunk k of pixel j in a 64B-row buffer written by TMA with SWIZZLE_64B
 // (Swizzle<2,4,3>: chunk bits [4,6) ^= row-pair bits [7,9))
 __device__ __forceinline__ uint32_t sw64(uint32_t j, uint32_t k) { return j * 64u + ((k ^ ((j >> 1) & 3u)) << 4); }
+// 16B chunk k of row j in a 32B-row SWIZZLE_32B buffer (Swizzle<1,4,3>: bit 4 ^= bit 7)
+__device__ __forceinline__ uint32_t sw32(uint32_t j, uint32_t k) { return j * 32u + ((k ^ ((j >> 2) & 1u)) << 4); }
 
 // optional per-CTA role counters (debug builds of the plan only): slot layout
 // [0] producer wait, [1] converter wait raw, [2] converter wait slot, [3] converter busy,
@@ -173,6 +175,28 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long
     mbar_wait(bar, parity);
   }
 }
+__device__ __forceinline__ void mbar_wait_bt(uint64_t* bar, uint32_t parity, long long* acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait_backoff(bar, parity);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait_backoff(bar, parity);
+  }
+}
+
+// position in a ring of n slots: slot index and the mbarrier phase parity of
+// its current fill (no integer division on the per-stage path)
+struct RingPos {
+  int idx = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void adv(int n) {
+    if (++idx == n) {
+      idx = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 // w0 activation producer, w1 MMA, w2 weight producer, w3 idle, w4-7 epilogue
 // (one warp per TMEM lane quarter), w8-13 converters in two groups of three that
@@ -185,9 +209,37 @@ constexpr int kCvtWarp0 = 8, kCvtWarps = 6;
 // Persistent implicit-GEMM forward: grid = #SMs, CTA c handles tiles c, c+G, ...
 // (tile = (image, virtual-row block) x output-channel tile). Two TMEM
 // accumulator buffers let the epilogue of tile i overlap the mainloop of i+1.
-template <bool RAW_F32, int PIECES>
-__global__ void __launch_bounds__(kFwdThreadsP, 1)
-    conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ FwdParams p, int raw_stages,
+// TS (single-tap problems, fp32 activations): the converters write the A
+// pieces straight into TENSOR memory (tcgen05.st, a ring of PIECES x 8
+// columns per stage after the accumulators) and the MMA reads A from TMEM —
+// the A operand then costs no shared-memory bandwidth at all, which is what
+// bounds the smem-staged fp32 path at small N. 16 warps: two converter groups
+// of four (one warp per TMEM lane quarter) alternate stages.
+constexpr int kFwdWarpsTS = 16;
+constexpr uint32_t kEpiSlots = 4;  // TMA-store slabs per epilogue warp (2 KiB each)
+constexpr uint32_t kEpiStagingBytes = 4u * kEpiSlots * 2048u;
+constexpr int kFwdThreadsTS = kFwdWarpsTS * 32;
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem] (A: lane = row, 8 columns = 16 packed bf16, low half = even k)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <bool RAW_F32, int PIECES, bool TS = false>
+__global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
+    conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_out,
+                    const __grid_constant__ CUtensorMap map_out2, const __grid_constant__ FwdParams p, int raw_stages,
                     int pc_stages, int w_stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
@@ -198,11 +250,14 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  FwdSmem L = fwd_smem_layout(p.a_px, p.w_taps, p.nb, PIECES, RAW_F32, pc_stages, w_stages);
+  // a stage carries kc channel blocks: raw slot = kc planes, weight piece = kc x w_taps taps
+  FwdSmem L = fwd_smem_layout(p.a_px * p.kc, p.w_resident ? p.cb_in : p.w_taps * p.kc, p.nb, PIECES, RAW_F32,
+                              TS ? 0 : pc_stages, w_stages);
   L.epi_off = L.raw_off + static_cast<uint32_t>(raw_stages) * L.raw_slot;
   const uint32_t smem0 = smem_u32(smem);
   const int NT = 16 * p.nb;
-  const int k_iters = p.cb_in * p.n_phases;
+  const int kc_stages = (p.cb_in + p.kc - 1) / p.kc;
+  const int k_iters = kc_stages * p.n_phases;
   const int n_mtiles = p.mimg > 0 ? (p.n_img + p.mimg - 1) / p.mimg : p.n_img * p.tiles_per_img;
   const int n_tiles = n_mtiles * p.n_ntiles;
   // fp32-accurate mode keeps the a0*b0 products and the five correction
@@ -213,10 +268,14 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   // two converter groups alternate stages; a 1-deep ring would let the second
   // group wait on a phase two ahead (parity aliasing), so it falls back to one group
   const int cvt_groups = (raw_stages >= 2 && pc_stages >= 2) ? 2 : 1;
-  const int cvt_group_warps = kCvtWarps / cvt_groups;
+  const int cvt_group_warps = TS ? 4 : kCvtWarps / cvt_groups;
+  // TS: A-piece ring in TMEM after the accumulators
+  const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
+  constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
+  const uint32_t ring_slot = static_cast<uint32_t>(p.kc) * kRingCols;
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(p.acc_bufs) * acc_cols) tmem_cols <<= 1;
+  while (tmem_cols < ring_col0 + (TS ? static_cast<uint32_t>(pc_stages) * ring_slot : 0u)) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -246,7 +305,12 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   const uint32_t tmem_base = tmem_base_sh;
   long long* dbg = p.dbg ? p.dbg + static_cast<long long>(blockIdx.x) * 16 : nullptr;
   long long t_start = clock64();
-  long long c_a = 0, c_b = 0, c_c = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
+  if (dbg && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    dbg[9] = static_cast<long long>(gt);
+  }
+  long long c_a = 0, c_b = 0, c_c = 0, c_d = 0, c_e = 0, c_f = 0, c_g = 0, c_h = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
 
   // tile t -> (n, v0, ntile); output-channel tiles innermost so consecutive
   // CTAs share the activation tile through L2
@@ -266,23 +330,29 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ activation producer
     if (lane == 0) {
-      const uint32_t a_bytes = static_cast<uint32_t>(p.a_load_px) * (RAW_F32 ? 64u : 32u);
+      const uint32_t a_bytes = static_cast<uint32_t>(p.a_load_px) * (RAW_F32 ? 64u : 32u) * p.kc;
       uint32_t g = 0;
+      RingPos rp;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         int n, v0, ntile;
         tile_coords(t, n, v0, ntile);
         const int row0 = v0 / p.wsub;
         const int a_px0 = p.linear ? v0 : row0 * p.wsub;
-        for (int it = 0; it < k_iters; ++it, ++g) {
-          const int cb = it / p.n_phases, ph = it % p.n_phases;
-          const int plane = n * p.in_cb + cb;
+        int cb = 0, ph = 0;
+        for (int it = 0; it < k_iters; ++it, ++g, rp.adv(RAW_F32 ? raw_stages : pc_stages)) {
+          if (it > 0 && ++ph == p.n_phases) {
+            ph = 0;
+            ++cb;
+          }
+          const int plane = n * p.in_cb + cb * p.kc;
           if (RAW_F32) {
-            const int s = g % raw_stages;
-            mbar_wait_t(&raw_empty[s], ((g / raw_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
+            const int s = rp.idx;
+            mbar_wait_t(&raw_empty[s], rp.ph ^ 1u, dbg ? &c_a : nullptr);
+            if (dbg && blockIdx.x == 0 && g < 256) dbg[gridDim.x * 16 + g * 8 + 6] = clock64() - t_start;
             uint8_t* dst = smem + L.raw_off + s * L.raw_slot;
             mbar_arrive_expect_tx(&raw_full[s], a_bytes);
             if (p.mimg > 0) {
-              tma_load_4d(dst, &map_a, &raw_full[s], 0, 0, cb, n);  // box {16, hw, 1, mimg}
+              tma_load_4d(dst, &map_a, &raw_full[s], 0, 0, cb * p.kc, n);  // box {16, hw, kc, mimg}
             } else if (p.linear) {
               for (int i = 0; i < p.lin_boxes; ++i)
                 tma_load_3d(dst + i * 128 * 64, &map_a, &raw_full[s], 0, a_px0 + i * 128, plane);
@@ -291,8 +361,8 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
                           p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
             }
           } else {
-            const int s = g % pc_stages;
-            mbar_wait_t(&pc_empty[s], ((g / pc_stages) & 1u) ^ 1u, dbg ? &c_a : nullptr);
+            const int s = rp.idx;
+            mbar_wait_t(&pc_empty[s], rp.ph ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
             mbar_arrive_expect_tx(&pc_full[s], a_bytes);
             // bf16 pixels as SWIZZLE_32B rows: the MMA reads them in place
@@ -314,27 +384,50 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
     // ------------------------------------------------------------ weight producer (own ring)
     // one weight stage = up to w_taps taps of one (c_b, phase): large filters
     // (7x7 stem) stream their taps through several small stages
-    if (lane == 0) {
+    if (lane == 0 && p.w_resident) {
+      // single-tap plan whose CTA always sees the same output-channel tile:
+      // the whole slice [piece][c_b][2nb][256 B] is loaded once
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
+      const int ntile = blockIdx.x % p.n_ntiles;
+      if (blockIdx.x < n_tiles) {
+        mbar_arrive_expect_tx(&w_full[0], PIECES * p.cb_in * w_tap);
+        uint8_t* dst = smem + L.w_off;
+        for (int cb = 0; cb < p.cb_in; ++cb)
+          for (int pc = 0; pc < PIECES; ++pc)
+            bulk_load(dst + pc * L.w_piece + cb * w_tap,
+                      wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_tap, w_tap,
+                      &w_full[0]);
+      }
+    } else if (lane == 0) {
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
       const long long w_blk = static_cast<long long>(p.n_taps) * w_tap;
       uint32_t g = 0;
+      RingPos wp;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         int n, v0, ntile;
         tile_coords(t, n, v0, ntile);
+        int cb = 0, ph = 0;
         for (int it = 0; it < k_iters; ++it) {
-          const int cb = it / p.n_phases, ph = it % p.n_phases;
-          for (int t0 = 0; t0 < p.phase_ntaps[ph]; t0 += p.w_taps, ++g) {
+          if (it > 0 && ++ph == p.n_phases) {
+            ph = 0;
+            ++cb;
+          }
+          const int kc_eff = min(p.kc, p.cb_in - cb * p.kc);
+          for (int t0 = 0; t0 < p.phase_ntaps[ph]; t0 += p.w_taps, ++g, wp.adv(w_stages)) {
             const int nt = min(p.w_taps, p.phase_ntaps[ph] - t0);
-            const int s = g % w_stages;
-            mbar_wait(&w_empty[s], ((g / w_stages) & 1u) ^ 1u);
+            const int s = wp.idx;
+            mbar_wait(&w_empty[s], wp.ph ^ 1u);
+            if (p.dbg && blockIdx.x == 0 && g < 256) p.dbg[gridDim.x * 16 + g * 8 + 7] = clock64() - t_start;
             const uint32_t w_bytes = static_cast<uint32_t>(nt) * w_tap;
-            mbar_arrive_expect_tx(&w_full[s], PIECES * w_bytes);
+            mbar_arrive_expect_tx(&w_full[s], PIECES * kc_eff * w_bytes);
             uint8_t* dst = smem + L.w_off + s * L.w_slot;
-            for (int pc = 0; pc < PIECES; ++pc)
-              bulk_load(dst + pc * L.w_piece,
-                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_blk +
-                            static_cast<long long>(p.phase_tap0[ph] + t0) * w_tap,
-                        w_bytes, &w_full[s]);
+            // slot layout [piece][kk][tap]: piece stride w_piece = kc * w_taps taps
+            for (int kk = 0; kk < kc_eff; ++kk)
+              for (int pc = 0; pc < PIECES; ++pc)
+                bulk_load(dst + pc * L.w_piece + kk * w_bytes,
+                          wsrc + ((static_cast<long long>(pc) * p.cb_in + cb * p.kc + kk) * p.n_ntiles + ntile) * w_blk +
+                              static_cast<long long>(p.phase_tap0[ph] + t0) * w_tap,
+                          w_bytes, &w_full[s]);
           }
         }
       }
@@ -342,7 +435,12 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
-    uint32_t g = 0, gw = 0, tl = 0;
+    uint32_t g = 0, tl = 0;
+    RingPos pcp, wpp;
+    if (p.w_resident && blockIdx.x < n_tiles) {
+      mbar_wait(&w_full[0], 0);
+      tc_fence_after();
+    }
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
       tile_coords(t, n, v0, ntile);
@@ -353,59 +451,164 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
       mbar_wait_t(&acc_empty[acc], apar ^ 1u, dbg ? &c_b : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols;
-      for (int it = 0; it < k_iters; ++it, ++g) {
-        const int s = g % pc_stages;
-        const uint32_t par = (g / pc_stages) & 1u;
+      int ph = -1, cbi = -1;
+      for (int it = 0; it < k_iters; ++it, ++g, pcp.adv(pc_stages)) {
+        const int s = pcp.idx;
+        const uint32_t par = pcp.ph;
+        if (++ph == p.n_phases) ph = 0;
+        if (ph == 0) ++cbi;
+        long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
         if (RAW_F32)
           mbar_wait_t(&pc_conv[s], par, dbg ? &c_a : nullptr);
         else
           mbar_wait_t(&pc_full[s], par, dbg ? &c_a : nullptr);
-        const int ph = it % p.n_phases;
+        if (trace && lane == 0) trace[0] = clock64() - t_start;
         const uint32_t st = smem0 + s * L.pc_slot;
         const int ntaps = p.phase_ntaps[ph];
-        for (int t0 = 0; t0 < ntaps; t0 += p.w_taps, ++gw) {
-          const int ws = gw % w_stages;
-          mbar_wait_t(&w_full[ws], (gw / w_stages) & 1u, dbg ? &c_a : nullptr);
+        const int kc_eff = min(p.kc, p.cb_in - cbi * p.kc);
+        const int w_kk0 = p.w_resident ? cbi * p.kc : 0;  // resident slice: channel block index
+        for (int t0 = 0; t0 < ntaps; t0 += p.w_taps, wpp.adv(w_stages)) {
+          const int ws = wpp.idx;
+          if (!p.w_resident) mbar_wait_t(&w_full[ws], wpp.ph, dbg ? &c_a : nullptr);
+          if (trace && lane == 0) trace[1] = clock64() - t_start;
           tc_fence_after();
           const uint32_t wst = smem0 + L.w_off + ws * L.w_slot;
           const int nt = min(p.w_taps, ntaps - t0);
           if (elect_one()) {
+            for (int kk = 0; kk < kc_eff; ++kk)
             for (int tp = 0; tp < nt; ++tp) {
               const int shift = p.tap_shift[p.phase_tap0[ph] + t0 + tp];
               for (int mb = 0; mb < p.mb; ++mb) {
                 const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
                 const uint32_t d_hi = d_base + static_cast<uint32_t>(mb * NT);
                 const uint32_t d_lo = d_hi + static_cast<uint32_t>(p.mb * NT);
-                const bool first = it == 0 && t0 == 0 && tp == 0;
+                const bool first = it == 0 && t0 == 0 && tp == 0 && kk == 0;
 #pragma unroll
                 for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
                   // products (ia, ib) with ia + ib <= 2
                   const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
                   const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
-                  const uint64_t ad =
-                      RAW_F32 ? make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128)
-                              : make_smem_desc_sw32(st + static_cast<uint32_t>(v_off + mb * 128 + shift) * 32u);
-                  const uint64_t bd = make_smem_desc(wst + ib * L.w_piece + tp * w_tap, 128, 256);
-                  if (pr == 0)
-                    mma_bf16(d_hi, ad, bd, idesc, first ? 0u : 1u);
-                  else
-                    mma_bf16(d_lo, ad, bd, idesc, (first && pr == 1) ? 0u : 1u);
+                  const uint64_t bd =
+                      make_smem_desc(wst + ib * L.w_piece + ((w_kk0 + kk) * nt + tp) * w_tap, 128, 256);
+                  const uint32_t acc_in = pr == 0 ? (first ? 0u : 1u) : ((first && pr == 1) ? 0u : 1u);
+                  const uint32_t d_t = pr == 0 ? d_hi : d_lo;
+                  if (p.dbg_mode & 8) {
+                    // ablation: no MMAs
+                  } else if (TS) {
+                    mma_bf16_ts(d_t,
+                                tmem_base + ring_col0 + static_cast<uint32_t>(s) * ring_slot +
+                                    static_cast<uint32_t>(kk) * kRingCols + ia * 8u,
+                                bd, idesc, acc_in);
+                  } else {
+                    const uint64_t ad =
+                        RAW_F32
+                            ? make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128)
+                            : make_smem_desc_sw32(st + static_cast<uint32_t>(v_off + mb * 128 + shift) * 32u);
+                    mma_bf16(d_t, ad, bd, idesc, acc_in);
+                  }
                 }
               }
             }
-            mma_commit(&w_empty[ws]);
+            if (!p.w_resident) mma_commit(&w_empty[ws]);
             if (t0 + p.w_taps >= ntaps) {
               mma_commit(&pc_empty[s]);
               if (it == k_iters - 1) mma_commit(&acc_full[acc]);
             }
           }
           __syncwarp();
+          if (trace && lane == 0) trace[2] = clock64() - t_start;
         }
       }
     }
     if (dbg && lane == 0) {
       dbg[4] = c_a;
       dbg[5] = c_b;
+    }
+  } else if (TS && warp >= kCvtWarp0) {
+    // ------------------------------------------------------------ TS converters (smem fp32 -> TMEM pieces)
+    // group = (warp - 8) / 4 takes stages g % cvt_groups == group; a warp owns
+    // TMEM lanes (warp % 4) * 32 .. +31 = A rows = pixels v_off + row
+    const int grp = (warp - kCvtWarp0) / 4;
+    const uint32_t q = static_cast<uint32_t>(warp % 4);
+    const int row = static_cast<int>(q) * 32 + lane;
+    uint32_t g = 0;
+    RingPos rr, pr;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int n, v0, ntile;
+      tile_coords(t, n, v0, ntile);
+      const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
+      // raw row of this thread's pixel in channel block kk of the stage: base + kk * kstride
+      uint32_t base, kstride;
+      if (p.mimg > 0) {  // slot = [image][kk][pixel]
+        const int hw = p.a_load_px / p.mimg;
+        const int img = row / hw;
+        base = img < p.mimg ? static_cast<uint32_t>(img * p.kc * hw + (row - img * hw)) : 0u;
+        kstride = static_cast<uint32_t>(hw);
+      } else {           // slot = [kk][pixel]
+        base = static_cast<uint32_t>(v0 - a_px0 + row);
+        kstride = static_cast<uint32_t>(p.a_px);
+      }
+      int ph = -1, cbi = -1;
+      for (int it = 0; it < k_iters; ++it, ++g, rr.adv(raw_stages), pr.adv(pc_stages)) {
+        if (++ph == p.n_phases) ph = 0;
+        if (ph == 0) ++cbi;
+        if (static_cast<int>(g & static_cast<uint32_t>(cvt_groups - 1)) != grp) continue;
+        const int rs = rr.idx, ps = pr.idx;
+        mbar_wait_bt(&raw_full[rs], rr.ph, dbg ? &c_a : nullptr);
+        long long* ctr = (dbg && blockIdx.x == 0 && g < 256 && lane == 0 && q == 0) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
+        if (ctr) ctr[3] = clock64() - t_start;
+        mbar_wait_bt(&pc_empty[ps], pr.ph ^ 1u, dbg ? &c_b : nullptr);
+        if (ctr) ctr[4] = clock64() - t_start;
+        tc_fence_after();
+        const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
+        const int kc_eff = min(p.kc, p.cb_in - cbi * p.kc);
+        if (!(p.dbg_mode & 4))
+        for (int kk = 0; kk < kc_eff; ++kk) {
+        const uint32_t px = base + static_cast<uint32_t>(kk) * kstride;
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 f = *reinterpret_cast<const float4*>(raw + sw64(px, k));
+          v[4 * k] = f.x;
+          v[4 * k + 1] = f.y;
+          v[4 * k + 2] = f.z;
+          v[4 * k + 3] = f.w;
+        }
+        const uint32_t col = tmem_base + (q * 32u << 16) + ring_col0 + static_cast<uint32_t>(ps) * ring_slot +
+                             static_cast<uint32_t>(kk) * kRingCols;
+        if (PIECES == 3) {
+          uint32_t h[8], m[8], l[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            h[e] = cvt2(v[2 * e], v[2 * e + 1]);
+            const float ra = v[2 * e] - lo_f(h[e]), rb = v[2 * e + 1] - hi_f(h[e]);
+            m[e] = cvt2(ra, rb);
+            l[e] = cvt2(ra - lo_f(m[e]), rb - hi_f(m[e]));
+          }
+          tmem_st8(col, h);
+          tmem_st8(col + 8, m);
+          tmem_st8(col + 16, l);
+        } else {
+          uint32_t h[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) h[e] = cvt2(v[2 * e], v[2 * e + 1]);
+          tmem_st8(col, h);
+        }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (ctr) ctr[5] = clock64() - t_start;
+        if (lane == 0) {
+          mbar_arrive(&raw_empty[rs]);
+          mbar_arrive(&pc_conv[ps]);
+        }
+      }
+    }
+    if (dbg && threadIdx.x == kCvtWarp0 * 32) {
+      dbg[1] = c_a;
+      dbg[2] = c_b;
+      dbg[3] = clock64() - t_start - c_a - c_b;
     }
   } else if (warp >= kCvtWarp0) {
     // ------------------------------------------------------------ converters (smem fp32 -> bf16 pieces)
@@ -414,12 +617,13 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
       const int ct = threadIdx.x - (kCvtWarp0 + grp * cvt_group_warps) * 32;
       const int items = 2 * ((p.a_px + 31) / 32) * 32;  // (pixel, 16B bf16 chunk)
       uint32_t g = 0;
+      RingPos rr, pr;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        for (int it = 0; it < k_iters; ++it, ++g) {
-          if (static_cast<int>(g % cvt_groups) != grp) continue;
-          const int rs = g % raw_stages, ps = g % pc_stages;
-          mbar_wait_t(&raw_full[rs], (g / raw_stages) & 1u, dbg ? &c_a : nullptr);
-          mbar_wait_t(&pc_empty[ps], ((g / pc_stages) & 1u) ^ 1u, dbg ? &c_b : nullptr);
+        for (int it = 0; it < k_iters; ++it, ++g, rr.adv(raw_stages), pr.adv(pc_stages)) {
+          if (static_cast<int>(g & static_cast<uint32_t>(cvt_groups - 1)) != grp) continue;
+          const int rs = rr.idx, ps = pr.idx;
+          mbar_wait_t(&raw_full[rs], rr.ph, dbg ? &c_a : nullptr);
+          mbar_wait_t(&pc_empty[ps], pr.ph ^ 1u, dbg ? &c_b : nullptr);
           const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
           uint8_t* pcs = smem + ps * L.pc_slot;
           for (int i = ct; i < items; i += cvt_group_warps * 32) {
@@ -455,15 +659,15 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
         dbg[3] = clock64() - t_start - c_a - c_b;
       }
     }
-  } else if (warp >= kEpiWarp0) {
-    // ------------------------------------------------------------ epilogue (warps 4..7)
-    // warp -> TMEM lane quarter (warp % 4)
+  } else if (warp >= kEpiWarp0 && p.tma_store && p.add == nullptr && p.mask == nullptr) {
+    // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
+    // two output blocks per step: one 32-column TMEM load per accumulator, one
+    // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
     const int qrow = (warp % 4) * 32;
-    const int g_lo = 0, g_hi = p.nb;
-    const int v_end = p.P * p.wsub;
-    const int esz = p.out_bf16 ? 2 : 4;
-    uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
-    uint32_t tl = 0;
+    const uint32_t esz = p.out_bf16 ? 2u : 4u;
+    const uint32_t slot_bytes = 2u * 32u * 16u * esz;
+    uint8_t* stg0 = smem + L.epi_off + (warp % 4) * 2u * 4096u;
+    uint32_t n_st = 0, tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
       tile_coords(t, n, v0, ntile);
@@ -473,6 +677,93 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
       for (int mb = 0; mb < p.mb; ++mb) {
+        for (int g0 = 0; g0 < p.nb; g0 += 2) {
+          const int kb0 = ntile * p.nb + g0;
+          if (kb0 >= p.kb_out) break;
+          const bool pair = g0 + 1 < p.nb;
+          uint32_t r[32], rl[32];
+          tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
+          if (PIECES == 3) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
+          tmem_ld_wait();
+          uint8_t* stg = stg0 + (n_st & 1u) * 4096u;
+          if (n_st >= 2) {  // this slot's previous store must have left smem
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j == 1 && !pair) break;
+            const int kb = kb0 + j;
+            float vals[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              vals[e] = PIECES == 3 ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
+                                    : __uint_as_float(r[16 * j + e]);
+            if (p.bias != nullptr && kb < p.kb_out) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
+            }
+            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
+            if (p.out_bf16) {
+              const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
+              const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
+              *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
+              *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<float4*>(stg + sw64(row, c)) =
+                    make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            // rows past P*Q and blocks past K are clipped by the tensor bounds
+            tma_store_4d(pair ? &map_out2 : &map_out, stg, 0, v0 + mb * 128 + qrow, kb0, n);
+            bulk_commit_group();
+          }
+          ++n_st;
+          (void)slot_bytes;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+    if (lane == 0) bulk_wait_group0();
+    if (dbg && threadIdx.x == kEpiWarp0 * 32) {
+      dbg[6] = c_a;
+      dbg[7] = clock64() - t_start - c_a;
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue (warps 4..7)
+    // warp -> TMEM lane quarter (warp % 4)
+    const int qrow = (warp % 4) * 32;
+    const int g_lo = 0, g_hi = p.nb;
+    const int v_end = p.P * p.wsub;
+    const int esz = p.out_bf16 ? 2 : 4;
+    uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
+    // TMA-store staging: a ring of kEpiSlots [32 px][16 lanes] slabs per warp
+    // (SWIZZLE_64B fp32 / 32B bf16), one bulk store per (32 pixels, block)
+    const uint32_t slab = 32u * 16u * esz;
+    uint8_t* stg0 = smem + L.epi_off + (warp % 4) * kEpiSlots * 2048u;
+    uint32_t n_st = 0;
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      int n, v0, ntile;
+      tile_coords(t, n, v0, ntile);
+      const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+      const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+      mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
+      if (!(p.dbg_mode & 16)) tc_fence_after();
+      long long t_e0 = dbg ? clock64() : 0;
+      const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
+      for (int mb = 0; mb < ((p.dbg_mode & 32) ? 0 : p.mb); ++mb) {
         int v = v0 + mb * 128 + qrow + lane;
         int nn = n;
         bool valid;
@@ -489,10 +780,11 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
         valid = valid && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
-        for (int g0 = g_lo; g0 < g_hi; g0 += 2) {
+        for (int g0 = g_lo; g0 < ((p.dbg_mode & 64) ? g_lo : g_hi); g0 += 2) {
           // two 16-column TMEM loads in flight, one wait
           const int ng = min(2, g_hi - g0);
           uint32_t r[2][16], rl[2][16];
+          const long long t_l0 = dbg ? clock64() : 0;
 #pragma unroll
           for (int k = 0; k < 2; ++k)
             if (k < ng && !(p.dbg_mode & 2)) {
@@ -500,22 +792,26 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
               if (PIECES == 3) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
             }
           tmem_ld_wait();
+          if (dbg) c_c += clock64() - t_l0;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             const int kb = ntile * p.nb + g0 + k;
-            if (k >= ng || !valid || kb >= p.kb_out) continue;
+            if (k >= ng) continue;
+            if (!p.tma_store && (!valid || kb >= p.kb_out)) continue;
+            const long long tv0 = dbg ? clock64() : 0;
             float vals[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               vals[e] = PIECES == 3 ? __uint_as_float(r[k][e]) + __uint_as_float(rl[k][e]) : __uint_as_float(r[k][e]);
             // APPLY after the final reduction step (kernel_streams.cpp:96-120)
-            if (p.bias != nullptr) {
+            if (p.bias != nullptr && kb < p.kb_out) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
             const long long plane = static_cast<long long>(nn) * p.out_cb + kb;
             const long long px_off = ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz;
-            if (p.add != nullptr) {  // residual add / gradient sum
+            const bool live = valid && kb < p.kb_out;  // rows / blocks the TMA store clips anyway
+            if (p.add != nullptr && live) {  // residual add / gradient sum
               float a[16];
               load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
 #pragma unroll
@@ -525,11 +821,53 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = vals[e] > 0.0f ? vals[e] : 0.0f;
             }
-            if (p.mask != nullptr) {  // ReLU backward: gradient through the forward activation
+            if (p.mask != nullptr && live) {  // ReLU backward: gradient through the forward activation
               float m[16];
               load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
+            }
+            if (p.tma_store) {
+              if (kb >= p.kb_out) continue;  // blocks of the next n-tile belong to another CTA
+              uint8_t* stg = stg0 + (n_st % kEpiSlots) * 2048u;
+              const long long tq0 = dbg ? clock64() : 0;
+              if (n_st >= kEpiSlots) {  // that slab's previous store must have left smem
+                if (lane == 0) bulk_wait_group_read<kEpiSlots - 1>();
+                __syncwarp();
+              }
+              const long long tq1 = dbg ? clock64() : 0;
+              if (dbg) c_g += tq0 - tv0;
+              const uint32_t row = static_cast<uint32_t>(lane);
+              if (p.out_bf16) {
+                const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
+                const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
+                *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
+                *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
+              } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                  *reinterpret_cast<float4*>(stg + sw64(row, c)) =
+                      make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
+              }
+              // dense output: box {16 lanes, 32 pixels, 1 block, 1 image}; rows past
+              // P*Q are clipped by the tensor bounds
+              const long long tq2 = dbg ? clock64() : 0;
+              fence_proxy_async_smem();
+              __syncwarp();
+              const long long tq3 = dbg ? clock64() : 0;
+              if (lane == 0) {
+                tma_store_4d(&map_out, stg, 0, v0 + mb * 128 + qrow, kb, n);
+                bulk_commit_group();
+              }
+              if (dbg) {
+                c_d += tq1 - tq0;
+                c_e += tq3 - tq2;
+                c_f += clock64() - tq3;
+                c_h += tq2 - tq1;
+              }
+              ++n_st;
+              (void)slab;
+              continue;
             }
             if (!(p.dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
             if (p.out_halo_h | p.out_halo_w) {
@@ -544,16 +882,32 @@ __global__ void __launch_bounds__(kFwdThreadsP, 1)
           }
         }
       }
-      tc_fence_before();
+      if (dbg) c_b += clock64() - t_e0;
+      if (!(p.dbg_mode & 16)) tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
+    if (p.tma_store && lane == 0) bulk_wait_group0();
     if (dbg && threadIdx.x == kEpiWarp0 * 32) {
       dbg[6] = c_a;
       dbg[7] = clock64() - t_start - c_a;
+      dbg[11] = c_b;  // tile bodies (TMEM loads .. stores)
+      dbg[12] = c_c;  // of which TMEM loads + wait
+      dbg[13] = c_d;  // TMA-store slab waits
+      dbg[14] = c_e;  // proxy fence + syncwarp
+      dbg[15] = c_f;  // TMA issue
+      if (p.dbg) {
+        p.dbg[gridDim.x * 16 + 2048 + blockIdx.x * 2] = c_g;      // vals .. relu
+        p.dbg[gridDim.x * 16 + 2048 + blockIdx.x * 2 + 1] = c_h;  // staging writes
+      }
     }
   }
-  if (dbg && threadIdx.x == 0) dbg[8] = clock64() - t_start;
+  if (dbg && threadIdx.x == 0) {
+    dbg[8] = clock64() - t_start;
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    dbg[10] = static_cast<long long>(gt);
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);

@@ -40,6 +40,9 @@ struct FwdParams {
   int tap_shift[kMaxTaps];  // phase-sorted
   int taps_box;        // max taps per phase
   int w_taps;          // taps per weight pipeline stage (<= taps_box)
+  int kc;              // input channel blocks per pipeline stage (single-tap TS plans; else 1)
+  int w_resident;      // 1: the CTA's whole weight slice stays in smem (loaded once)
+  int tma_store;       // 1: epilogue stages 32-pixel slabs in smem and TMA-stores them (dense outputs)
   int n_taps;          // total taps (phase-sorted) in the prepared weights
   int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
   const void* wprep;   // prepared bf16 weights [pc][cb][ntile][tap][2nb][16][8]
