@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -325,7 +326,8 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           const int m_tiles = mimg_ok ? cdiv(in.n, 128 / hw) : in.n * cdiv(pb.P * p.wsub, 128);
           const int grid_est = std::min(m_tiles * n_nt_tiles, sm_count());
           const int res_bytes = pb.cb_red * pieces * nb * 512;
-          const bool resident = grid_est % n_nt_tiles == 0 && res_bytes <= 120 * 1024;
+          const bool resident = grid_est % n_nt_tiles == 0 && res_bytes <= 120 * 1024 &&
+                                cdiv(pb.cb_red, kcx) <= kMaxStages && !getenv("DCONV_NO_RESIDENT");
           const FwdSmem lay = fwd_smem_layout(apx_rows * kcx, resident ? pb.cb_red : kcx, nb, pieces, true, 0, 1);
           int wss = resident ? 1
                              : std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lay.w_slot)));

@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       mbar_init(&pc_conv[s], cvt_group_warps);
       mbar_init(&pc_empty[s], 1);
     }
-    for (int s = 0; s < w_stages; ++s) {
+    const int n_wbar = p.w_resident ? kc_stages : w_stages;  // resident: one per stage group
+    for (int s = 0; s < n_wbar; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
     }
@@ -390,13 +391,17 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
       const int ntile = blockIdx.x % p.n_ntiles;
       if (blockIdx.x < n_tiles) {
-        mbar_arrive_expect_tx(&w_full[0], PIECES * p.cb_in * w_tap);
+        // one barrier per stage's kc channel blocks, in stage order
         uint8_t* dst = smem + L.w_off;
-        for (int cb = 0; cb < p.cb_in; ++cb)
-          for (int pc = 0; pc < PIECES; ++pc)
-            bulk_load(dst + pc * L.w_piece + cb * w_tap,
-                      wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_tap, w_tap,
-                      &w_full[0]);
+        for (int ks = 0; ks < kc_stages; ++ks) {
+          const int cb0 = ks * p.kc, cb1 = min(p.cb_in, cb0 + p.kc);
+          mbar_arrive_expect_tx(&w_full[ks], PIECES * (cb1 - cb0) * w_tap);
+          for (int cb = cb0; cb < cb1; ++cb)
+            for (int pc = 0; pc < PIECES; ++pc)
+              bulk_load(dst + pc * L.w_piece + cb * w_tap,
+                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_tap, w_tap,
+                        &w_full[ks]);
+        }
       }
     } else if (lane == 0) {
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wprep);
@@ -437,10 +442,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
     uint32_t g = 0, tl = 0;
     RingPos pcp, wpp;
-    if (p.w_resident && blockIdx.x < n_tiles) {
-      mbar_wait(&w_full[0], 0);
-      tc_fence_after();
-    }
+    uint32_t w_res_seen = 0;  // resident slice: stage groups whose weights have landed
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
       tile_coords(t, n, v0, ntile);
@@ -469,7 +471,12 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
         const int w_kk0 = p.w_resident ? cbi * p.kc : 0;  // resident slice: channel block index
         for (int t0 = 0; t0 < ntaps; t0 += p.w_taps, wpp.adv(w_stages)) {
           const int ws = wpp.idx;
-          if (!p.w_resident) mbar_wait_t(&w_full[ws], wpp.ph, dbg ? &c_a : nullptr);
+          if (!p.w_resident) {
+            mbar_wait_t(&w_full[ws], wpp.ph, dbg ? &c_a : nullptr);
+          } else if (static_cast<uint32_t>(cbi) >= w_res_seen) {  // first tile only
+            mbar_wait(&w_full[cbi], 0);
+            w_res_seen = cbi + 1;
+          }
           if (trace && lane == 0) trace[1] = clock64() - t_start;
           tc_fence_after();
           const uint32_t wst = smem0 + L.w_off + ws * L.w_slot;
@@ -902,14 +909,14 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       }
     }
   }
+  tc_fence_before();
+  __syncthreads();
   if (dbg && threadIdx.x == 0) {
     dbg[8] = clock64() - t_start;
     uint64_t gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     dbg[10] = static_cast<long long>(gt);
   }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);
 }
 

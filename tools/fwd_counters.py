@@ -30,6 +30,9 @@ for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.
     torch.cuda.synchronize()
     lib.dconv_debug_counters(buf.data_ptr())
     buf.zero_()
+    if os.environ.get("FLUSH"):
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+        flush.fill_(1)
     run()
     torch.cuda.synchronize()
     lib.dconv_debug_counters(None)
@@ -45,7 +48,7 @@ for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.
     print(label, "vals..relu kcyc %.1f staging kcyc %.1f" % (ex[0].item(), ex[1].item()))
     print(label, getattr(fp if label == "fwd" else bc, "blocking", None))
     if os.environ.get("TRACE") and label == "fwd":
-        tr = buf[148 * 16:].view(256, 8).tolist()
+        tr = buf[148 * 16:148 * 16 + 2048].view(256, 8).tolist()
         print("stage: prod_issue wprod_issue | cvt: raw_seen slot_free done | mma: conv_seen w_seen issued")
         for i in range(0, 100):
             t = tr[i]

@@ -58,3 +58,7 @@ kern.sort(key=lambda e: e.time_range.start)
 per = len(kern) // STEPS
 spans = [kern[i * per + per - 1].time_range.end - kern[i * per].time_range.start for i in range(STEPS)]
 print("span first->last kernel per step (us):", [round(s, 1) for s in spans])
+print("last step, kernel by kernel (start offset us, duration us):")
+t0 = kern[(STEPS - 1) * per].time_range.start
+for e in kern[(STEPS - 1) * per:]:
+    print(f"  {e.time_range.start - t0:8.1f} {e.device_time:8.2f}  {e.name[:60]}")
