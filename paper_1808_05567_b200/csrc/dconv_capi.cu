@@ -489,7 +489,10 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
 long long* g_fwd_dbg = nullptr;  // dconv_debug_counters(): per-CTA role cycle counters
 int g_fwd_dbg_mode = 0;
 
-void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
+// prof_slot >= 0: bracket the kernel launch with the profiling events (after
+// all host-side encoding, so the interval is device time of the kernel)
+void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof_open = true,
+                bool prof_close = true) {
   L.p.dbg = g_fwd_dbg;
   L.p.dbg_mode = g_fwd_dbg_mode;
   // dense outputs (no halo / lattice / padding columns / multi-image rows):
@@ -520,7 +523,9 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream) {
   auto go = [&](auto kern, int threads) {
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
+    if (prof_slot >= 0 && prof_open) prof_begin(prof_slot, stream);
     kern<<<L.grid, threads, smem, stream>>>(L.map_a, map_out, map_out2, L.p, L.raw_stages, L.stages, L.w_stages);
+    if (prof_slot >= 0 && prof_close) prof_end(prof_slot, stream);
   };
   if (L.ts) {
     if (L.pieces == 3)
@@ -1079,9 +1084,7 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
       p.mask = ep->mask;
       p.relu |= ep->relu ? 1 : 0;
     }
-    prof_begin(0, cs);
-    launch_fwd(L, cs);
-    prof_end(0, cs);
+    launch_fwd(L, cs, 0);
     plan->last_desc = json_tile(L);
   });
 }
@@ -1220,7 +1223,8 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
     std::string desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
     int tap_off = 0;
     bool first = true;
-    prof_begin(1, cs);
+    int n_conv = 0, conv_i = 0;
+    for (auto& ph : plan->phases) n_conv += ph.zero ? 0 : 1;
     for (auto& ph : plan->phases) {
       if (!first) desc += ",";
       first = false;
@@ -1269,11 +1273,11 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
         p.mask = ep->mask;
         p.relu = ep->relu ? 1 : 0;
       }
-      launch_fwd(L, cs);
+      launch_fwd(L, cs, 1, conv_i == 0, conv_i == n_conv - 1);
+      ++conv_i;
       desc += json_tile(L);
     }
     desc += "]}";
-    prof_end(1, cs);
     if (s.stride != 1) {
       const int r = dconv_zero_halo(grad_in, stream);
       if (r != DCONV_OK) fail(r, g_err);
@@ -1675,19 +1679,21 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     if (L0.split_in) launch_split(*in, in_pc, plan->pieces, cs);
     if (L0.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
     UpdLaunch L = plan_upd(*plan, *in, *grad_out, true, in_pc, do_pc, partial);
+    bool opened = false;  // profiling bracket opens right before the first conv kernel
     auto go = [&](auto kern, int a_base, int acc) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                  "smem attribute");
+      if (!opened) prof_begin(2, cs), opened = true;
       kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages, a_base, acc);
       cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
     };
     auto go_raw = [&](auto kern) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                  "smem attribute");
+      if (!opened) prof_begin(2, cs), opened = true;
       kern<<<L.grid, kUpdRawWarps * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages, L.pc_stages);
       cuda_check(cudaGetLastError(), "conv_upd_raw_kernel launch");
     };
-    prof_begin(2, cs);
     if (L.raw) {
       if (plan->pieces == 1)
         go_raw(conv_upd_raw_kernel<1, false>);

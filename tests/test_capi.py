@@ -48,7 +48,8 @@ def test_library_is_sm100a(dconv):
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
-    for mnem in ("UTCHMMA", "UTMALDG", "LDTM"):  # tcgen05.mma, TMA tile loads, tcgen05.ld
+    # tcgen05.mma, TMA tile loads / stores, tcgen05.ld / tcgen05.st (A staged in TMEM), bulk copies
+    for mnem in ("UTCHMMA", "UTMALDG", "UTMASTG", "LDTM", "STTM", "UBLKCP"):
         assert mnem in sass, mnem
 
 
