@@ -524,7 +524,20 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
     if (prof_slot >= 0 && prof_open) prof_begin(prof_slot, stream);
-    kern<<<L.grid, threads, smem, stream>>>(L.map_a, map_out, map_out2, L.p, L.raw_stages, L.stages, L.w_stages);
+    // programmatic dependent launch: the kernel starts while the weight prep that
+    // precedes it finishes (its weight producer waits on griddepcontrol.wait)
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = (prof_slot >= 0 && prof_open) ? 0 : 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = L.grid;
+    lc.blockDim = dim3(threads, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    lc.attrs = &attr;
+    lc.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&lc, kern, L.map_a, map_out, map_out2, L.p, L.raw_stages, L.stages, L.w_stages),
+               "conv_fwd_kernel launch");
     if (prof_slot >= 0 && prof_close) prof_end(prof_slot, stream);
   };
   if (L.ts) {
@@ -1713,9 +1726,21 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     prof_end(2, cs);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
-    upd_reduce_kernel<<<static_cast<unsigned>(cdiv64(total, 32)), dim3(32, kRedGroups), 0, cs>>>(
-        partial, L.p.splits, s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K, cb, kb, grad_w->data,
-        grad_w->dtype == DCONV_BF16, accumulate ? 1 : 0);
+    {
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr.val.programmaticStreamSerializationAllowed = g_prof ? 0 : 1;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(static_cast<unsigned>(cdiv64(total, 32)), 1, 1);
+      lc.blockDim = dim3(32, kRedGroups, 1);
+      lc.stream = cs;
+      lc.attrs = &attr;
+      lc.numAttrs = 1;
+      cuda_check(cudaLaunchKernelEx(&lc, upd_reduce_kernel, static_cast<const float*>(partial), L.p.splits,
+                                    s.R * s.S, L.p.c_pad, L.p.k_pad, s.C, s.K, cb, kb, grad_w->data,
+                                    grad_w->dtype == DCONV_BF16 ? 1 : 0, accumulate ? 1 : 0),
+                 "upd_reduce launch");
+    }
     cuda_check(cudaGetLastError(), "upd_reduce launch");
     char buf[512];
     std::snprintf(buf, sizeof(buf),

@@ -385,6 +385,9 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     // ------------------------------------------------------------ weight producer (own ring)
     // one weight stage = up to w_taps taps of one (c_b, phase): large filters
     // (7x7 stem) stream their taps through several small stages
+    // the weight prep kernel that precedes this launch may still be running
+    // (programmatic dependent launch): its output is read only after this wait
+    if (lane == 0) pdl_wait_primary();
     if (lane == 0 && p.w_resident) {
       // single-tap plan whose CTA always sees the same output-channel tile:
       // the whole slice [piece][c_b][2nb][256 B] is loaded once

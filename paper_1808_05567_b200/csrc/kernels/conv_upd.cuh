@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
         mbar_wait(&accum_bar, 0);
         tc_fence_after();
       }
+      if (warp == kUpdCvtWarp0 && lane == 0) pdl_launch_dependents();  // the reduce may get scheduled
       const int n_acc = stacked ? 1 : ntaps;
       for (int t = 0; t < n_acc; ++t) {
         const int slot = stacked ? (qrow + lane) / (16 * p.cb_eff) : 0;
@@ -542,6 +543,7 @@ __global__ void __launch_bounds__(32 * kRedGroups)
     upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C, int K,
                       int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
   __shared__ float red[kRedGroups][33];
+  pdl_wait_primary();  // launched as a programmatic dependent of the UPD kernel
   const int kw = kb * 16, cw = cb * 16;
   const long long total = static_cast<long long>(n_taps) * cw * kw;
   const long long f = static_cast<long long>(blockIdx.x) * 32 + threadIdx.x;

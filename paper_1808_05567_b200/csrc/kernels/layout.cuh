@@ -170,6 +170,9 @@ template <typename S>
 __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
                                    int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps, int cb_in,
                                    int nb, int n_ntiles, int dual, int pieces) {
+  // the conv kernel launched after this one (programmatic dependent launch) may
+  // start its prologue and activation loads now; it waits before reading weights
+  pdl_launch_dependents();
   const long long per_piece = static_cast<long long>(cb_in) * n_ntiles * n_taps * (2 * nb) * 128;
   DCONV_GRID_STRIDE(e, per_piece) {
     const int kk = static_cast<int>(e % 8);
