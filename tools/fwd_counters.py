@@ -22,7 +22,7 @@ fp = d.make_forward_plan(spec, 1, None, None, math)
 bc = d.prepare_backward(spec, wb, 1, None, math)
 out = d.BlockedActivation(32, 64, 56, 56, 16, 0, 0)
 gi = d.BlockedActivation(32, 256, 56, 56, 16, 0, 0)
-buf = torch.zeros(148 * 16 + 8 * 256 + 2 * 148, dtype=torch.int64, device="cuda")
+buf = torch.zeros(148 * 16 + 8 * 256 + 2 * 148 + 5 * 148, dtype=torch.int64, device="cuda")
 names = ["prod_wait", "cvt_wait_raw", "cvt_wait_slot", "cvt_busy", "mma_wait_ops", "mma_wait_acc", "epi_wait",
          "epi_busy", "total"]
 for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.execute(wb, gb, gi))):
@@ -44,7 +44,9 @@ for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.
     print(label, "CTA start us: min %.2f max %.2f | end us: min %.2f max %.2f | total kcyc max %.1f" % (
         starts.min().item(), starts.max().item(), ends.min().item(), ends.max().item(), per[:, 8].max().item() / 1e3),
         "epi bodies kcyc %.1f (tmem ld %.1f slab-wait %.1f fence %.1f tma %.1f)" % tuple(per[:, i].double().mean().item() / 1e3 for i in (11, 12, 13, 14, 15)))
-    ex = buf[148 * 16 + 2048:].view(148, 2).double().mean(0) / 1e3
+    ex = buf[148 * 16 + 2048:148 * 16 + 2048 + 296].view(148, 2).double().mean(0) / 1e3
+    mm = buf[148 * 16 + 2048 + 296:].view(148, 5).double().mean(0) / 1e3
+    print(label, "MMA warp kcyc: wait %.1f misc %.1f fence %.1f issue %.1f commit %.1f" % tuple(mm.tolist()))
     print(label, "vals..relu kcyc %.1f staging kcyc %.1f" % (ex[0].item(), ex[1].item()))
     print(label, getattr(fp if label == "fwd" else bc, "blocking", None))
     if os.environ.get("TRACE") and label == "fwd":

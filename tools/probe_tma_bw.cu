@@ -1,0 +1,132 @@
+// Probe: HBM read throughput of TMA tile loads with the FWD kernel's box shapes
+// (fp32 NCHW16c planes, 64 B pixel rows, SWIZZLE_64B) as a function of ring depth.
+// One thread per CTA issues loads into an R-slot ring and re-arms a slot as soon
+// as it lands (no consumer work), 148 CTAs, L2 flushed before each run.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <vector>
+#include "../paper_1808_05567_b200/csrc/kernels/sm100_ptx.cuh"
+using namespace dconv_sm100;
+
+constexpr int kPlanes = 512, kHW = 3136, kCb = 16;  // 32 images x 16 channel blocks x 56x56
+
+// plain vectorised loads for comparison
+__global__ void ldg_reader(const float4* __restrict__ x, size_t n, float* out) {
+  float acc = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
+__global__ void reader(const __grid_constant__ CUtensorMap map, int ring, int box_px, int box_planes, int n_tiles,
+                       int dummy) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[16];
+  const uint32_t slot = box_px * box_planes * 64;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ring; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int tiles_per_img = (kHW + box_px - 1) / box_px;
+  const int stages_per_tile = kCb / box_planes;
+  int issued = 0, done = 0;
+  auto issue = [&](int g) {
+    const int t = blockIdx.x + (g / stages_per_tile) * gridDim.x;
+    const int it = g % stages_per_tile;
+    const int n = t / tiles_per_img, v0 = (t % tiles_per_img) * box_px;
+    const int s = g % ring;
+    mbar_arrive_expect_tx(&full[s], slot);
+    tma_load_3d(smem + s * slot, &map, &full[s], 0, v0, n * kCb + it * box_planes);
+  };
+  const int my_tiles = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int total = my_tiles * stages_per_tile;
+  for (; issued < ring && issued < total; ++issued) issue(issued);
+  for (; done < total; ++done) {
+    mbar_wait(&full[done % ring], (done / ring) & 1);
+    if (issued < total) issue(issued++);
+  }
+  (void)dummy;
+}
+
+typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  const size_t bytes = (size_t)kPlanes * kHW * 64;
+  void* x;
+  cudaMalloc(&x, bytes);
+  cudaMemset(x, 0, bytes);
+  void* flush;
+  cudaMalloc(&flush, 256 << 20);
+  Enc enc;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  cudaFuncSetAttribute(reader, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  {
+    float* o;
+    cudaMalloc(&o, 4);
+    for (int clean = 0; clean < 2; ++clean)
+    for (int blocks : {148 * 4, 148 * 8}) {
+      float best = 1e9;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(flush, rep, 256 << 20);
+        // clean = 1: read the flush buffer back so L2 holds clean lines (write-backs happen here, untimed)
+        if (clean) ldg_reader<<<148 * 8, 512>>>((const float4*)flush, (256 << 20) / 16, o);
+        cudaEventRecord(a);
+        ldg_reader<<<blocks, 512>>>((const float4*)x, bytes / 16, o);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      printf("ldg reader %d blocks, %s flush: %.1f us %.0f GB/s\n", blocks, clean ? "write+read" : "write", best * 1e3, bytes / (best * 1e-3) / 1e9);
+    }
+  }
+  const int shapes[][2] = {{128, 4}, {128, 2}};
+  float* o2;
+  cudaMalloc(&o2, 4);
+  for (int clean = 0; clean < 2; ++clean)
+  for (int ctas_per_sm : {1})
+  for (auto& sh : shapes)
+    for (int promo = 0; promo < 1; ++promo)
+      for (int ring : {3, 6}) {
+        const int box_px = sh[0], box_planes = sh[1];
+        if ((size_t)ring * box_px * box_planes * 64 * ctas_per_sm > 200 * 1024) continue;
+        CUtensorMap map;
+        cuuint64_t dims[3] = {16, (cuuint64_t)kHW, (cuuint64_t)kPlanes};
+        cuuint64_t st[2] = {64, (cuuint64_t)kHW * 64};
+        cuuint32_t box[3] = {16, (cuuint32_t)box_px, (cuuint32_t)box_planes}, es[3] = {1, 1, 1};
+        enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, x, dims, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, promo ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const int n_tiles = 32 * ((kHW + box_px - 1) / box_px);
+        float best = 1e9;
+        for (int rep = 0; rep < 3; ++rep) {
+          cudaMemset(flush, rep, 256 << 20);
+          if (clean) ldg_reader<<<148 * 8, 512>>>((const float4*)flush, (256 << 20) / 16, o2);
+          cudaEventRecord(a);
+          reader<<<148 * ctas_per_sm, 32, ring * box_px * box_planes * 64>>>(map, ring, box_px, box_planes, n_tiles, 0);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          if (ms < best) best = ms;
+        }
+        const cudaError_t e = cudaGetLastError();
+        printf("%s flush ctas/SM %d box {16,%d,%d} ring %d (%zu KB in flight): %.1f us  %.0f GB/s %s\n",
+               clean ? "write+read" : "write", ctas_per_sm, box_px, box_planes, ring,
+               (size_t)ring * box_px * box_planes * 64 / 1024, best * 1e3, bytes / (best * 1e-3) / 1e9,
+               e == cudaSuccess ? "" : cudaGetErrorString(e));
+      }
+  return 0;
+}
