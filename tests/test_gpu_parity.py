@@ -144,6 +144,37 @@ def test_table_i_update(dconv, orc, lid):
         assert torch.equal(a.data, b.data), "weight update must be bitwise reproducible"
 
 
+# ------------------------------------------------------------------ cfg5: the Inception-v3 layer mix (BASELINE configs[4])
+
+# (C, K, H, W, R, S, stride, pad_h, pad_w): 1x1 reductions, the factorised 1x7 / 7x1
+# and 1x3 / 3x1 convolutions (pad on the long axis), the valid 3x3/s2 grid reduction
+CFG5 = [
+    (192, 64, 35, 35, 1, 1, 1, 0, 0), (768, 192, 17, 17, 1, 1, 1, 0, 0), (1280, 320, 8, 8, 1, 1, 1, 0, 0),
+    (160, 160, 17, 17, 1, 7, 1, 0, 3), (160, 160, 17, 17, 7, 1, 1, 3, 0), (192, 192, 17, 17, 1, 7, 1, 0, 3),
+    (192, 192, 17, 17, 7, 1, 1, 3, 0), (288, 384, 35, 35, 3, 3, 2, 0, 0), (384, 384, 8, 8, 1, 3, 1, 0, 1),
+    (384, 384, 8, 8, 3, 1, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("row", CFG5, ids=[f"{r[0]}to{r[1]}_{r[4]}x{r[5]}s{r[6]}_{r[2]}" for r in CFG5])
+def test_cfg5_inception_layers(dconv, orc, row):
+    """FWD / BWD / UPD of every cfg5 layer shape against the oracle (N=2), both
+    math modes (cfg5 itself is bf16)."""
+    C_, K, H, W, R, S, st, ph, pw = row
+    N = 2
+    s = orc.spec(N, C_, K, H, W, R, S, st, ph, pw, 16)
+    spec = dconv.make_layer_spec(N, C_, K, H, W, R, S, st, ph, pw, 16)
+    P, Q = orc.output_shape(s)
+    x = orc.uniform(7, (N, C_, H, W))
+    w = orc.he_normal(8, (K, C_, R, S), C_ * R * S)
+    g = orc.uniform(9, (N, K, P, Q))
+    rf, rb, ru = orc.conv_forward(s, x, w), orc.conv_backward(s, g, w), orc.conv_update(s, x, g)
+    for M in (dconv.Math.BF16, dconv.Math.F32):
+        gate(orc, rf, dconv.from_blocked_activation(run_fwd(dconv, spec, x, w, M)).cpu().numpy(), M)
+        gate(orc, rb, dconv.from_blocked_activation(run_bwd(dconv, spec, g, w, M)).cpu().numpy(), M)
+        gate(orc, ru, dconv.from_blocked_weight(run_upd(dconv, spec, x, g, M)).cpu().numpy(), M)
+
+
 # ------------------------------------------------------------------ BASELINE configs at full size
 
 
