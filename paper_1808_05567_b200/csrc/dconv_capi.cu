@@ -402,14 +402,38 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           }
           if (rws < (want_pc == 1 ? 1 : 2)) continue;
         } else {
-          int left = kFwdBudget - wss * static_cast<int>(lay.w_slot);
-          pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.pc_slot)) : 0;
-          if (pcs < want_pc && wss > 2) {
-            wss = 2;
-            left = kFwdBudget - wss * static_cast<int>(lay.w_slot);
-            pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lay.pc_slot)) : 0;
+          // single-tap bf16 problems carry kc channel blocks per stage (amortises the
+          // per-stage barrier / commit cost over kc x mb MMAs)
+          int kcx = (taps.r.size() == 1) ? std::min(4, pb.cb_red) : 1;
+          pcs = 0;
+          for (; kcx >= 1; kcx = kcx > 1 ? kcx / 2 : 0) {
+            const FwdSmem lk = fwd_smem_layout(apx * kcx, wt * kcx, nb, pieces, raw_f32, 1, 1);
+            int wsk = std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lk.w_slot)));
+            int left = kFwdBudget - static_cast<int>(kEpiStagingBytes) - wsk * static_cast<int>(lk.w_slot);
+            pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
+            if (pcs < want_pc && wsk > 2) {
+              wsk = 2;
+              left = kFwdBudget - static_cast<int>(kEpiStagingBytes) - wsk * static_cast<int>(lk.w_slot);
+              pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
+            }
+            if (kcx == 1 && pcs < want_pc) {  // no room for the TMA-store staging: plain budget
+              wsk = std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lk.w_slot)));
+              left = kFwdBudget - wsk * static_cast<int>(lk.w_slot);
+              pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
+              if (pcs < want_pc && wsk > 2) {
+                wsk = 2;
+                left = kFwdBudget - wsk * static_cast<int>(lk.w_slot);
+                pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
+              }
+            }
+            if (pcs >= want_pc) {
+              wss = wsk;
+              kc = kcx;
+              break;
+            }
           }
           if (pcs < want_pc) continue;
+          if (kc > 1 && linear && !mimg_ok) lb = 1;  // one box of Lpx pixels x kc blocks
         }
         tile.mb = mb;
         tile.nb = nb;
@@ -424,7 +448,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           else
             pc_st = std::max(1, std::min(cfg->stages, pc_st));
         }
-        layout = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, pc_st, w_st);
+        layout = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, pc_st, w_st);
         a_px = apx;
         lin_boxes = lb;
         found = true;
@@ -467,12 +491,15 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     const uint64_t dims[4] = {16, static_cast<uint64_t>(hw), static_cast<uint64_t>(p.in_cb),
                               static_cast<uint64_t>(in.n)};
     const uint64_t strides[3] = {pix, pix * hw, pix * hw * p.in_cb};
-    const uint32_t box[4] = {16, static_cast<uint32_t>(hw), static_cast<uint32_t>(kc), static_cast<uint32_t>(p.mimg)};
+    // TS converters read any row order: one box of kc blocks; the smem-MMA path needs
+    // each block's rows contiguous, so it issues one box per block
+    const uint32_t box[4] = {16, static_cast<uint32_t>(hw), static_cast<uint32_t>(L.ts ? kc : 1),
+                             static_cast<uint32_t>(p.mimg)};
     L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation multi-image", swz);
   } else if (linear) {
     const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
     const uint64_t strides[2] = {pix, pix * hp * wp};
-    const uint32_t box[3] = {16, 128, static_cast<uint32_t>(kc)};
+    const uint32_t box[3] = {16, static_cast<uint32_t>(kc > 1 ? a_px : 128), static_cast<uint32_t>(kc)};
     L.map_a = encode(!raw_f32, 3, in.data, dims, strides, box, nullptr, "activation linear", swz);
   } else {
     const char* base = reinterpret_cast<const char*>(in.data) + (static_cast<uint64_t>(in.halo_h) * wp + in.halo_w) * pix;
@@ -1495,11 +1522,34 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
         ++p.n_tgroups;
       }
   }
-  // split-K: >= 2 waves of CTAs, >= 2 stages per split
+  // split-K factor (choose_update_strategy analog, planner.cpp:54-143: the same
+  // trade-off of partial-copy traffic against parallelism, for 148 SMs):
+  // minimise max(MMA time over the busy SMs, HBM time of operands + partials
+  // written and re-read by the reduce); one CTA per SM (smem-bound)
   const int tiles = n_ctiles * p.n_tgroups * n_ktiles;
-  // raw path: one CTA per SM (smem-bound), one wave; HBM-split path: >= 2 waves
-  int splits = L.raw ? std::max(1, sm_count() / tiles) : cdiv(2 * sm_count(), tiles);
-  splits = std::max(1, std::min(splits, std::max(1, p.stages_total / 2)));
+  const int sms = sm_count();
+  const double op_bytes = (in.dtype == DCONV_BF16 ? 2.0 : 4.0) * (static_cast<double>(act_elems(in)) +
+                                                                  static_cast<double>(act_elems(dout)) * n_ctiles);
+  const double dw_part = 4.0 * p.n_taps * (n_ctiles * 128.0) * (n_ktiles * NT);
+  const double mma_flops = 2.0 * (n_ctiles * 128.0) * (n_ktiles * NT) * p.n_taps * static_cast<double>(p.stages_total) *
+                           p.vs * (pieces == 3 ? 6.0 : 1.0);
+  const double sm_rate = 4.5e12;  // dense bf16 MMA FLOP/s per SM at these tile shapes (~50 % of 1332 TF / 148)
+  int splits = 1;
+  double best_t = 1e30;
+  const int max_splits = std::max(1, std::min(cdiv(2 * sms, tiles), std::max(1, p.stages_total / 2)));
+  for (int sp = 1; sp <= max_splits; ++sp) {
+    const int ctas = tiles * sp;
+    const int waves = cdiv(ctas, sms);
+    const double t_mma = mma_flops / ctas * waves / sm_rate;
+    // HBM time, also bounded by what the busy SMs can pull (~30 GB/s each through the TMA rings)
+    const double bytes = op_bytes + (sp > 1 ? 2.0 : 1.0) * sp * dw_part;
+    const double t_mem = std::max(bytes / 5.5e12, bytes / (std::min(ctas, sms) * 30.0e9));
+    const double t = std::max(t_mma, t_mem);
+    if (t < best_t * 0.98) {
+      best_t = t;
+      splits = sp;
+    }
+  }
   if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
   p.splits = splits;
   p.c_pad = n_ctiles * 128;
@@ -1731,8 +1781,12 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
       attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr.val.programmaticStreamSerializationAllowed = g_prof ? 0 : 1;
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(static_cast<unsigned>(cdiv64(total, 32)), 1, 1);
-      lc.blockDim = dim3(32, kRedGroups, 1);
+      // split groups per element: enough memory-level parallelism for many splits,
+      // all 256 threads on distinct elements when there are few
+      const int G = L.p.splits >= 32 ? kRedGroups : L.p.splits >= 8 ? 2 : 1;
+      const int TX = 256 / G;
+      lc.gridDim = dim3(static_cast<unsigned>(cdiv64(total, TX)), 1, 1);
+      lc.blockDim = dim3(TX, G, 1);
       lc.stream = cs;
       lc.attrs = &attr;
       lc.numAttrs = 1;

@@ -368,10 +368,14 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
             mbar_arrive_expect_tx(&pc_full[s], a_bytes);
             // bf16 pixels as SWIZZLE_32B rows: the MMA reads them in place
             if (p.mimg > 0) {
-              tma_load_4d(dst, &map_a, &pc_full[s], 0, 0, cb, n);  // box {16, hw, 1, mimg}
+              for (int kk = 0; kk < p.kc; ++kk)  // box {16, hw, 1, mimg} per block: rows contiguous per block
+                tma_load_4d(dst + kk * p.a_px * 32, &map_a, &pc_full[s], 0, 0, cb * p.kc + kk, n);
             } else if (p.linear) {
-              for (int i = 0; i < p.lin_boxes; ++i)
-                tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, a_px0 + i * 128, plane);
+              if (p.kc > 1)  // one box {16, a_px, kc}
+                tma_load_3d(dst, &map_a, &pc_full[s], 0, a_px0, plane);
+              else
+                for (int i = 0; i < p.lin_boxes; ++i)
+                  tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, a_px0 + i * 128, plane);
             } else {
               tma_load_4d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
                           p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
                     const uint64_t ad =
                         RAW_F32
                             ? make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128)
-                            : make_smem_desc_sw32(st + static_cast<uint32_t>(v_off + mb * 128 + shift) * 32u);
+                            : make_smem_desc_sw32(st + static_cast<uint32_t>(kk * p.a_px + v_off + mb * 128 + shift) * 32u);
                     mma_bf16(d_t, ad, bd, idesc, acc_in);
                   }
                 }

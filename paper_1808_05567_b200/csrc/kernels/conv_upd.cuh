@@ -538,15 +538,16 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
 // elements (coalesced along k) x kRedGroups split groups: group y sums splits
 // y, y + G, y + 2G, ... in increasing order, then the G group sums are added in
 // group order — the same fixed order on every run, so dW is bitwise reproducible.
-constexpr int kRedGroups = 8;
-__global__ void __launch_bounds__(32 * kRedGroups)
+constexpr int kRedGroups = 8;  // max split groups per element (blockDim.y)
+__global__ void __launch_bounds__(256)
     upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C, int K,
                       int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
-  __shared__ float red[kRedGroups][33];
+  __shared__ float red[8192 + 256];  // [G][TX + 1], G * TX = 256
   pdl_wait_primary();  // launched as a programmatic dependent of the UPD kernel
+  const int G = blockDim.y, TX = blockDim.x;  // G split groups x TX consecutive elements
   const int kw = kb * 16, cw = cb * 16;
   const long long total = static_cast<long long>(n_taps) * cw * kw;
-  const long long f = static_cast<long long>(blockIdx.x) * 32 + threadIdx.x;
+  const long long f = static_cast<long long>(blockIdx.x) * TX + threadIdx.x;
   const int y = threadIdx.y;
   const bool in_range = f < total;
   const int k = in_range ? static_cast<int>(f % kw) : 0;
@@ -558,22 +559,24 @@ __global__ void __launch_bounds__(32 * kRedGroups)
   if (live) {
     const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
     int sp = y;
-    for (; sp + 3 * kRedGroups < splits; sp += 4 * kRedGroups) {
+    for (; sp + 3 * G < splits; sp += 4 * G) {
       float v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (sp + u * kRedGroups) * split_stride);
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (sp + u * G) * split_stride);
 #pragma unroll
       for (int u = 0; u < 4; ++u) sum += v[u];
     }
-    for (; sp < splits; sp += kRedGroups) sum += __ldg(src + sp * split_stride);
+    for (; sp < splits; sp += G) sum += __ldg(src + sp * split_stride);
   }
-  red[y][threadIdx.x] = sum;
-  __syncthreads();
-  if (y != 0 || !in_range) return;
-  float tot = red[0][threadIdx.x];
-#pragma unroll
-  for (int g = 1; g < kRedGroups; ++g) tot += red[g][threadIdx.x];
-  if (!live) tot = 0.0f;
+  if (G > 1) {
+    red[y * (TX + 1) + threadIdx.x] = sum;
+    __syncthreads();
+    if (y != 0) return;
+    sum = red[threadIdx.x];
+    for (int g = 1; g < G; ++g) sum += red[g * (TX + 1) + threadIdx.x];
+  }
+  if (!in_range) return;
+  const float tot = live ? sum : 0.0f;
   const int kbi = k / 16, kl = k % 16, cbi = c / 16, cl = c % 16;
   const long long e = ((static_cast<long long>(kbi) * cb + cbi) * n_taps + rs) * 256 + cl * 16 + kl;
   if (dw_bf16) {
