@@ -673,13 +673,14 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
         dbg[3] = clock64() - t_start - c_a - c_b;
       }
     }
-  } else if (warp >= kEpiWarp0 && p.tma_store && p.add == nullptr && p.mask == nullptr) {
+  } else if (warp >= kEpiWarp0 && p.tma_store) {
     // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
     // two output blocks per step: one 32-column TMEM load per accumulator, one
     // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
     const int qrow = (warp % 4) * 32;
     const uint32_t esz = p.out_bf16 ? 2u : 4u;
     const uint32_t slot_bytes = 2u * 32u * 16u * esz;
+    const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
     uint8_t* stg0 = smem + L.epi_off + (warp % 4) * 2u * 4096u;
     uint32_t n_st = 0, tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
@@ -717,9 +718,25 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
+            // dense output: pixel v of plane (n, kb) at ((n*out_cb + kb)*P*Q + v)*16 lanes
+            const int v = v0 + mb * 128 + qrow + lane;
+            const bool live = v < v_end && kb < p.kb_out;
+            const long long px_off = ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz;
+            if (p.add != nullptr && live) {  // residual add / gradient sum
+              float a[16];
+              load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += a[e];
+            }
             if (p.relu) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
+            }
+            if (p.mask != nullptr && live) {  // ReLU backward through the forward activation
+              float m[16];
+              load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
             const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
             if (p.out_bf16) {
