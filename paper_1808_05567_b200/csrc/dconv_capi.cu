@@ -1853,7 +1853,7 @@ int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argma
         out->n != in->n || out->c != in->c || out->h != P || out->w != Q || out->dtype != in->dtype)
       fail(DCONV_ERR_SHAPE_MISMATCH, "maxpool: expects halo-0 vlen-16 tensors, out = (h+2-3)/2+1");
     const int planes = in->n * cdiv(in->c, 16);
-    const int g = grid1d(static_cast<int64_t>(planes) * P * Q * 16);
+    const int g = grid1d(static_cast<int64_t>(planes) * P * Q);
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (in->dtype == DCONV_F32)
       maxpool_fwd_kernel<float><<<g, 256, 0, cs>>>((const float*)in->data, (float*)out->data, (uint8_t*)argmax,
@@ -1873,7 +1873,7 @@ int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dco
     check_act(grad_in, "maxpool grad_in");
     if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
     const int planes = grad_in->n * cdiv(grad_in->c, 16);
-    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w * 16);
+    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w);
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (grad_in->dtype == DCONV_F32)
       maxpool_bwd_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,

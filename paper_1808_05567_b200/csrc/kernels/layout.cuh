@@ -254,59 +254,116 @@ __global__ void zero_halo_kernel(T* __restrict__ dst, int planes, int h, int w, 
 
 // 3x3 / stride-2 / pad-1 max pool on blocked tensors (ResNet stem), halo 0.
 // Stores the argmax tap (0..8, first max in row-major order) for the backward.
+// 16 lanes of one pixel-block <-> registers (bf16: two 16 B vectors, fp32: four)
+template <typename T>
+__device__ __forceinline__ void ld16f(const T* p, float (&v)[16]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint4 a = reinterpret_cast<const uint4*>(p)[0], b = reinterpret_cast<const uint4*>(p)[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 t = reinterpret_cast<const float4*>(p)[e];
+      v[4 * e] = t.x;
+      v[4 * e + 1] = t.y;
+      v[4 * e + 2] = t.z;
+      v[4 * e + 3] = t.w;
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st16f(T* p, const float (&v)[16]) {
+  if constexpr (sizeof(T) == 2) {
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      reinterpret_cast<float4*>(p)[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+  }
+}
+
+// 3x3 / stride 2 / pad 1 max-pool (the ResNet stem pool), one thread per output
+// pixel-block (16 lanes); argmax = window position dy*3+dx of the first maximum
 template <typename T>
 __global__ void maxpool_fwd_kernel(const T* __restrict__ in, T* __restrict__ out, uint8_t* __restrict__ arg,
                                    int planes, int h, int w, int p, int q) {
-  const long long total = static_cast<long long>(planes) * p * q * 16;
+  const long long total = static_cast<long long>(planes) * p * q;
   DCONV_GRID_STRIDE(e, total) {
-    const int lane = static_cast<int>(e % 16);
-    long long r = e / 16;
-    const int x = static_cast<int>(r % q);
-    r /= q;
+    const int x = static_cast<int>(e % q);
+    const long long r = e / q;
     const int y = static_cast<int>(r % p);
     const long long plane = r / p;
-    float best = -INFINITY;
-    int bi = 0;
+    float best[16], v[16];
+    uint32_t bi[4] = {0, 0, 0, 0};  // 16 argmax bytes
+#pragma unroll
+    for (int l = 0; l < 16; ++l) best[l] = -INFINITY;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx) {
         const int iy = 2 * y - 1 + dy, ix = 2 * x - 1 + dx;
         if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
-        const float v = to_f<T>(in[((plane * h + iy) * w + ix) * 16 + lane]);
-        if (v > best) {
-          best = v;
-          bi = dy * 3 + dx;
-        }
+        ld16f(in + ((plane * h + iy) * w + ix) * 16, v);
+        const uint32_t code = static_cast<uint32_t>(dy * 3 + dx);
+#pragma unroll
+        for (int l = 0; l < 16; ++l)
+          if (v[l] > best[l]) {
+            best[l] = v[l];
+            bi[l / 4] = (bi[l / 4] & ~(0xFFu << (8 * (l % 4)))) | (code << (8 * (l % 4)));
+          }
       }
-    out[e] = from_f<T>(best);
-    arg[e] = static_cast<uint8_t>(bi);
+    st16f(out + e * 16, best);
+    reinterpret_cast<uint4*>(arg)[e] = make_uint4(bi[0], bi[1], bi[2], bi[3]);
   }
 }
 
 // gather form of the max-pool backward (deterministic, no atomics): each input
-// pixel sums the output gradients of the <= 4 windows whose argmax it is
+// pixel-block sums the output gradients of the <= 4 windows whose argmax it is
 template <typename T>
 __global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __restrict__ arg,
                                    T* __restrict__ gin, const T* __restrict__ mask, int planes, int h, int w, int p,
                                    int q) {
-  const long long total = static_cast<long long>(planes) * h * w * 16;
+  const long long total = static_cast<long long>(planes) * h * w;
   DCONV_GRID_STRIDE(e, total) {
-    const int lane = static_cast<int>(e % 16);
-    long long r = e / 16;
-    const int ix = static_cast<int>(r % w);
-    r /= w;
+    const int ix = static_cast<int>(e % w);
+    const long long r = e / w;
     const int iy = static_cast<int>(r % h);
     const long long plane = r / h;
-    float acc = 0.0f;
+    float acc[16], g[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] = 0.0f;
     for (int y = (iy + 1) / 2 - 1; y <= (iy + 1) / 2; ++y)
       for (int x = (ix + 1) / 2 - 1; x <= (ix + 1) / 2; ++x) {
         if (y < 0 || y >= p || x < 0 || x >= q) continue;
         const int dy = iy - (2 * y - 1), dx = ix - (2 * x - 1);
         if (dy < 0 || dy > 2 || dx < 0 || dx > 2) continue;
-        const long long o = ((plane * p + y) * q + x) * 16 + lane;
-        if (arg[o] == dy * 3 + dx) acc += to_f<T>(gout[o]);
+        const long long o = (plane * p + y) * q + x;
+        const uint4 a4 = reinterpret_cast<const uint4*>(arg)[o];
+        const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w};
+        const uint32_t code = static_cast<uint32_t>(dy * 3 + dx);
+        ld16f(gout + o * 16, g);
+#pragma unroll
+        for (int l = 0; l < 16; ++l)
+          if (((aw[l / 4] >> (8 * (l % 4))) & 0xFFu) == code) acc[l] += g[l];
       }
-    if (mask != nullptr && !(to_f<T>(mask[e]) > 0.0f)) acc = 0.0f;  // ReLU backward of the pooled activation
-    gin[e] = from_f<T>(acc);
+    if (mask != nullptr) {  // ReLU backward of the pooled activation
+      float m[16];
+      ld16f(mask + e * 16, m);
+#pragma unroll
+      for (int l = 0; l < 16; ++l)
+        if (!(m[l] > 0.0f)) acc[l] = 0.0f;
+    }
+    st16f(gin + e * 16, acc);
   }
 }
 

@@ -349,3 +349,39 @@ def test_host_step_matches_device_passes(dconv, orc, shape, chunk, math):
     assert torch.equal(yh.data, y_ref.data.cpu())
     with pytest.raises(dconv.InvalidArgument):
         step.run(ib, wb, gb, y_ref)
+
+
+# ------------------------------------------------------------------ stem max-pool (executor building block)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_maxpool_3x3s2_matches_torch(dconv, orc, dtype):
+    """dconv_maxpool_fwd / _bwd (3x3, stride 2, pad 1) on blocked tensors against
+    torch's max_pool2d and its autograd (random data: no ties); the backward's
+    optional ReLU mask zeroes where the pooled input was <= 0."""
+    from paper_1808_05567_b200 import _lib
+    import ctypes as C
+
+    lib = _lib.lib()
+    N, C_, H, W = 2, 20, 15, 17
+    P, Q = (H - 1) // 2 + 1, (W - 1) // 2 + 1
+    x = torch.from_numpy(orc.random_f32(41, (N, C_, H, W))).cuda().to(dtype)
+    xb = dconv.to_blocked_activation(x.float(), 16, 0, 0, dtype=dtype)
+    yb = dconv.BlockedActivation(N, C_, P, Q, 16, 0, 0, dtype)
+    arg = torch.empty(yb.data.numel(), dtype=torch.uint8, device="cuda")
+    api = dconv.api
+    api._check(lib.dconv_maxpool_fwd(C.byref(xb.to_c()), C.byref(yb.to_c()), arg.data_ptr(), 0))
+    xr = x.float().requires_grad_(True)
+    yr = torch.nn.functional.max_pool2d(xr, 3, 2, 1)
+    assert torch.equal(dconv.from_blocked_activation(yb).float(), yr.detach())
+    g = torch.from_numpy(orc.random_f32(42, (N, C_, P, Q))).cuda().to(dtype)
+    gb = dconv.to_blocked_activation(g.float(), 16, 0, 0, dtype=dtype)
+    gi = dconv.BlockedActivation(N, C_, H, W, 16, 0, 0, dtype)
+    api._check(lib.dconv_maxpool_bwd(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()), None, 0))
+    yr.backward(g.float())
+    ref = xr.grad
+    got = dconv.from_blocked_activation(gi).float()
+    assert torch.allclose(got, ref.to(dtype).float(), rtol=1e-2 if dtype == torch.bfloat16 else 0, atol=1e-2 if dtype == torch.bfloat16 else 1e-6)
+    api._check(lib.dconv_maxpool_bwd(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()), xb.data.data_ptr(), 0))
+    got_m = dconv.from_blocked_activation(gi).float()
+    assert torch.equal(got_m, torch.where(x.float() > 0, got, torch.zeros_like(got)))
