@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "lib", "libdconv_b200.so")
 SOURCES = [os.path.join(CSRC, "dconv_capi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "kernels", f) for f in os.listdir(os.path.join(CSRC, "kernels"))] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h"))] + [
+    os.path.join(CSRC, "kernels", f) for f in os.listdir(os.path.join(CSRC, "kernels"))] + [
     os.path.join(ROOT, "include", "dconv_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -8,6 +8,10 @@
 //
 // Included at the end of dconv_capi.cu (shares its error plumbing).
 #pragma once
+#include <algorithm>
+#include <map>
+#include <set>
+#include <vector>
 
 struct dconv_host_step {
   dconv_spec_t spec;  // whole-batch layer
@@ -15,13 +19,14 @@ struct dconv_host_step {
   int chunk;  // images per chunk
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr, ev_w = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
-  // per chunk-size plans (full chunk and remainder)
+  // plans per chunk size (the schedule ramps 1, 2, 4, ... images up and down)
   struct Plans {
     int n = 0, y_hh = -1, y_hw = -1;
     dconv_fwd_plan_t f = nullptr;
     dconv_bwd_plan_t b = nullptr;
     dconv_upd_plan_t u = nullptr;
-  } plans[2];
+  };
+  std::map<int, Plans> plans;
   // device staging: two slots per streamed tensor, one weight / weight-gradient buffer
   void* slot[4][2] = {};  // x, dy, y, dx
   size_t slot_bytes[4] = {};
@@ -41,12 +46,13 @@ size_t act_bytes_per_image(const dconv_act_t& a) {
 }
 
 void hs_free(dconv_host_step& h) {
-  for (auto& pl : h.plans) {
+  for (auto& kv : h.plans) {
+    auto& pl = kv.second;
     if (pl.f) dconv_fwd_plan_destroy(pl.f);
     if (pl.b) dconv_bwd_plan_destroy(pl.b);
     if (pl.u) dconv_upd_plan_destroy(pl.u);
-    pl = dconv_host_step::Plans{};
   }
+  h.plans.clear();
   for (auto& s : h.slot)
     for (auto& p : s) {
       if (p) cudaFree(p);
@@ -136,11 +142,43 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
       fail(DCONV_ERR_SHAPE_MISMATCH, "host_step: weights do not match the layer spec");
     if (w && dw && w->dtype != dw->dtype) fail(DCONV_ERR_INVALID_ARGUMENT, "host_step: w / dw dtypes differ");
 
+    // chunk schedule: ramp 1, 2, 4, ... images up to the chunk size and back down,
+    // so the link's fill (first H2D) and drain (last D2H) move small chunks while
+    // the middle of the step runs both directions at once
+    std::vector<int> sched;
+    if (const char* env = getenv("DCONV_HOST_SCHED")) {  // debug: explicit comma-separated chunk sizes
+      int tot = 0;
+      for (const char* q = env; *q;) {
+        const int v = std::atoi(q);
+        if (v > 0) sched.push_back(v), tot += v;
+        while (*q && *q != ',') ++q;
+        if (*q) ++q;
+      }
+      if (tot != s.N) sched.clear();
+    }
+    if (sched.empty()) {
+      std::vector<int> up;
+      for (int r = 1; r < h->chunk; r *= 2) up.push_back(r);
+      int ramp = 0;
+      for (int r : up) ramp += 2 * r;
+      if (ramp < s.N) {
+        sched = up;
+        for (int mid = s.N - ramp; mid > 0;) {
+          const int c = std::min(h->chunk, mid);
+          sched.push_back(c);
+          mid -= c;
+        }
+        sched.insert(sched.end(), up.rbegin(), up.rend());
+      } else {
+        for (int n0 = 0; n0 < s.N; n0 += h->chunk) sched.push_back(std::min(h->chunk, s.N - n0));
+      }
+    }
+    const int max_chunk = *std::max_element(sched.begin(), sched.end());
     // staging buffers (two slots per streamed tensor)
     const dconv_act_t* acts[4] = {x, dy, y, dx};
     for (int t = 0; t < 4; ++t)
       if (acts[t]) {
-        const size_t want = act_bytes_per_image(*acts[t]) * h->chunk;
+        const size_t want = act_bytes_per_image(*acts[t]) * max_chunk;
         if (want > h->slot_bytes[t] || !h->slot[t][0]) {
           size_t have0 = h->slot_bytes[t], have1 = h->slot_bytes[t];
           ensure(h->slot[t][0], have0, want);
@@ -158,11 +196,10 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
       }
     }
 
-    // plans per chunk size (the last chunk may be short)
-    const int n_chunks = cdiv(s.N, h->chunk);
+    const int n_chunks = static_cast<int>(sched.size());
     const int yhh = y ? y->halo_h : 0, yhw = y ? y->halo_w : 0;
     auto plans_for = [&](int n) -> dconv_host_step::Plans& {
-      dconv_host_step::Plans& pl = h->plans[n == h->chunk ? 0 : 1];
+      dconv_host_step::Plans& pl = h->plans[n];
       if (pl.n != n || pl.y_hh != yhh || pl.y_hw != yhw) {
         if (pl.f) dconv_fwd_plan_destroy(pl.f);
         if (pl.b) dconv_bwd_plan_destroy(pl.b);
@@ -187,8 +224,7 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
     };
     // workspace: max over the passes and chunk sizes
     size_t ws_need = 256;
-    for (int i = 0; i < std::min(n_chunks, 2); ++i) {
-      const int n = i == 0 ? h->chunk : s.N - (n_chunks - 1) * h->chunk;
+    for (int n : std::set<int>(sched.begin(), sched.end())) {
       dconv_host_step::Plans& pl = plans_for(n);
       if (do_f) ws_need = std::max(ws_need, dconv_fwd_workspace_bytes(pl.f));
       if (do_b) ws_need = std::max(ws_need, dconv_bwd_workspace_bytes(pl.b));
@@ -222,12 +258,24 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
     cuda_check(cudaStreamWaitEvent(cs, h->ev_w, 0), "stream wait");
 
     int launches = 0;
-    for (int i = 0; i < n_chunks; ++i) {
+    // debug timeline (DCONV_HOST_STEP_TRACE=1): timing events around every copy / compute
+    static const bool trace = getenv("DCONV_HOST_STEP_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      tev.push_back(e);
+    };
+    mark(cs);
+    for (int i = 0, n0 = 0; i < n_chunks; n0 += sched[i], ++i) {
       const int b = i & 1;
-      const int n0 = i * h->chunk, n = std::min(h->chunk, s.N - n0);
+      const int n = sched[i];
       dconv_host_step::Plans& pl = plans_for(n);
       // the slot's previous chunk (i-2) must be done computing before its inputs are overwritten
       if (i >= 2) cuda_check(cudaStreamWaitEvent(h->h2d, h->ev_comp[b], 0), "stream wait");
+      mark(h->h2d);
       for (int t = 0; t < 2; ++t)
         if (acts[t]) {
           const size_t per = act_bytes_per_image(*acts[t]);
@@ -235,6 +283,7 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
                                      cudaMemcpyHostToDevice, h->h2d),
                      "H2D chunk");
         }
+      mark(h->h2d);
       cuda_check(cudaEventRecord(h->ev_in[b], h->h2d), "event record");
       cuda_check(cudaStreamWaitEvent(cs, h->ev_in[b], 0), "stream wait");
       // ... and its outputs (i-2) must have left the device before they are overwritten
@@ -244,6 +293,7 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
       if (dy) dyc = chunk_act(dy, h->slot[1][b], n);
       if (y) yc = chunk_act(y, h->slot[2][b], n);
       if (dx) dxc = chunk_act(dx, h->slot[3][b], n);
+      mark(cs);
       if (do_f) {
         ck(dconv_forward(pl.f, &xc, &wd, &yc, h->ws, stream));
         launches += dconv_fwd_launches(pl.f);
@@ -256,8 +306,10 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
         ck(dconv_weight_update(pl.u, &xc, &dyc, &dwd, i > 0 ? 1 : 0, h->ws, stream));
         launches += dconv_upd_launches(pl.u, &xc, &dyc);
       }
+      mark(cs);
       cuda_check(cudaEventRecord(h->ev_comp[b], cs), "event record");
       cuda_check(cudaStreamWaitEvent(h->d2h, h->ev_comp[b], 0), "stream wait");
+      mark(h->d2h);
       for (int t = 2; t < 4; ++t)
         if (acts[t]) {
           const size_t per = act_bytes_per_image(*acts[t]);
@@ -265,12 +317,29 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
                                      cudaMemcpyDeviceToHost, h->d2h),
                      "D2H chunk");
         }
+      mark(h->d2h);
       cuda_check(cudaEventRecord(h->ev_out[b], h->d2h), "event record");
     }
     if (do_u)
       cuda_check(cudaMemcpyAsync(dw->data, h->dw_dev, wbytes, cudaMemcpyDeviceToHost, cs), "D2H weight gradient");
     // the caller's stream completes after every copy of this step
     for (int b = 0; b < std::min(n_chunks, 2); ++b) cuda_check(cudaStreamWaitEvent(cs, h->ev_out[b], 0), "stream wait");
+    mark(cs);
+    if (trace) {
+      cudaStreamSynchronize(cs);
+      auto rel = [&](size_t k) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tev[0], tev[k]);
+        return ms * 1e3f;
+      };
+      for (int i = 0; i < n_chunks; ++i) {
+        const size_t k = 1 + 6 * i;
+        std::fprintf(stderr, "chunk %d (%d img): h2d %.0f-%.0f  comp %.0f-%.0f  d2h %.0f-%.0f us\n", i, sched[i],
+                     rel(k), rel(k + 1), rel(k + 2), rel(k + 3), rel(k + 4), rel(k + 5));
+      }
+      std::fprintf(stderr, "end %.0f us\n", rel(tev.size() - 1));
+      for (auto e : tev) cudaEventDestroy(e);
+    }
     h->last_launches = launches;
   });
 }
