@@ -1265,12 +1265,16 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
     bool first = true;
     int n_conv = 0, conv_i = 0;
     for (auto& ph : plan->phases) n_conv += ph.zero ? 0 : 1;
+    // 1x1 / stride 2: the single tap phase (0, 0) writes the whole dI (its lattice
+    // values and the three zero neighbours of each) instead of zero-phase passes
+    const bool fill = !accumulate && s.stride == 2 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 &&
+                      n_conv == 1;
     for (auto& ph : plan->phases) {
       if (!first) desc += ",";
       first = false;
       if (ph.zero) {
-        if (accumulate) {  // adding zeros: nothing to do
-          desc += "\"skip\"";
+        if (accumulate || fill) {  // adding zeros, or written by the tap phase
+          desc += accumulate ? "\"skip\"" : "\"filled\"";
           continue;
         }
         const int planes = s.N * cb;
@@ -1313,6 +1317,9 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
         p.mask = ep->mask;
         p.relu = ep->relu ? 1 : 0;
       }
+      p.out_fill = fill ? 1 : 0;
+      p.fill_h_end = grad_in->halo_h + s.H;
+      p.fill_w_end = grad_in->halo_w + s.W;
       launch_fwd(L, cs, 1, conv_i == 0, conv_i == n_conv - 1);
       ++conv_i;
       desc += json_tile(L);

@@ -901,6 +901,17 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
               continue;
             }
             if (!(p.dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
+            if (p.out_fill) {
+              // 1x1 / stride-2 backward: this lattice pixel (2y', 2x') owns the three
+              // off-lattice neighbours, which are exactly zero (acceptance.cpp:106-117);
+              // writing them here replaces a separate zero pass over dI
+              const long long row = (plane * p.out_hp + y) * p.out_wp;
+              if (x + 1 < p.fill_w_end) store16_zero(obase + (row + x + 1) * 16LL * esz, p.out_bf16);
+              if (y + 1 < p.fill_h_end) {
+                store16_zero(obase + (row + p.out_wp + x) * 16LL * esz, p.out_bf16);
+                if (x + 1 < p.fill_w_end) store16_zero(obase + (row + p.out_wp + x + 1) * 16LL * esz, p.out_bf16);
+              }
+            }
             if (p.out_halo_h | p.out_halo_w) {
               // zero the halo pixels whose clamp onto the interior is this pixel
               const int dy0 = pp == 0 ? -p.out_halo_h : 0, dy1 = pp == p.P - 1 ? p.out_halo_h : 0;

@@ -43,6 +43,8 @@ struct FwdParams {
   int kc;              // input channel blocks per pipeline stage (single-tap TS plans; else 1)
   int w_resident;      // 1: the CTA's whole weight slice stays in smem (loaded once)
   int tma_store;       // 1: epilogue stages 32-pixel slabs in smem and TMA-stores them (dense outputs)
+  int out_fill;        // 1: stride-2 lattice output that also writes the zero pixels it owns
+  int fill_h_end, fill_w_end;  // interior row / column ends (padded coordinates) for out_fill
   int n_taps;          // total taps (phase-sorted) in the prepared weights
   int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
   const void* wprep;   // prepared bf16 weights [pc][cb][ntile][tap][2nb][16][8]
