@@ -29,6 +29,7 @@
 // products with i + j <= 2: fp32-accurate (~2^-24 relative per product).
 #pragma once
 #include <cuda_bf16.h>
+#include <type_traits>
 
 #include "conv_params.h"
 #include "sm100_ptx.cuh"
@@ -682,6 +683,10 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     const uint32_t slot_bytes = 2u * 32u * 16u * esz;
     const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
     uint8_t* stg0 = smem + L.epi_off + (warp % 4) * 2u * 4096u;
+    // FUSED = residual add / ReLU-backward mask present: the plain variant has no
+    // per-pixel addressing or extra loads in its loop (smaller, faster code)
+    auto lean = [&](auto fused_tag) {
+      constexpr bool FUSED = decltype(fused_tag)::value;
     uint32_t n_st = 0, tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
@@ -719,10 +724,10 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
             // dense output: pixel v of plane (n, kb) at ((n*out_cb + kb)*P*Q + v)*16 lanes
-            const int v = v0 + mb * 128 + qrow + lane;
-            const bool live = v < v_end && kb < p.kb_out;
-            const long long px_off = ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz;
-            if (p.add != nullptr && live) {  // residual add / gradient sum
+            const int v = FUSED ? v0 + mb * 128 + qrow + lane : 0;
+            const bool live = FUSED && v < v_end && kb < p.kb_out;
+            const long long px_off = FUSED ? ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz : 0;
+            if (FUSED && p.add != nullptr && live) {  // residual add / gradient sum
               float a[16];
               load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
 #pragma unroll
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
             }
-            if (p.mask != nullptr && live) {  // ReLU backward through the forward activation
+            if (FUSED && p.mask != nullptr && live) {  // ReLU backward through the forward activation
               float m[16];
               load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
 #pragma unroll
@@ -766,6 +771,11 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
+    };
+    if (p.add != nullptr || p.mask != nullptr)
+      lean(std::true_type{});
+    else
+      lean(std::false_type{});
     if (lane == 0) bulk_wait_group0();
     if (dbg && threadIdx.x == kEpiWarp0 * 32) {
       dbg[6] = c_a;
@@ -779,11 +789,6 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     const int v_end = p.P * p.wsub;
     const int esz = p.out_bf16 ? 2 : 4;
     uint8_t* obase = reinterpret_cast<uint8_t*>(p.out);
-    // TMA-store staging: a ring of kEpiSlots [32 px][16 lanes] slabs per warp
-    // (SWIZZLE_64B fp32 / 32B bf16), one bulk store per (32 pixels, block)
-    const uint32_t slab = 32u * 16u * esz;
-    uint8_t* stg0 = smem + L.epi_off + (warp % 4) * kEpiSlots * 2048u;
-    uint32_t n_st = 0;
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
@@ -791,10 +796,9 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
       const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
       mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
-      if (!(p.dbg_mode & 16)) tc_fence_after();
-      long long t_e0 = dbg ? clock64() : 0;
+      tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
-      for (int mb = 0; mb < ((p.dbg_mode & 32) ? 0 : p.mb); ++mb) {
+      for (int mb = 0; mb < p.mb; ++mb) {
         int v = v0 + mb * 128 + qrow + lane;
         int nn = n;
         bool valid;
@@ -815,7 +819,6 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
           // two 16-column TMEM loads in flight, one wait
           const int ng = min(2, g_hi - g0);
           uint32_t r[2][16], rl[2][16];
-          const long long t_l0 = dbg ? clock64() : 0;
 #pragma unroll
           for (int k = 0; k < 2; ++k)
             if (k < ng && !(p.dbg_mode & 2)) {
@@ -823,13 +826,10 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
               if (PIECES == 3) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
             }
           tmem_ld_wait();
-          if (dbg) c_c += clock64() - t_l0;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             const int kb = ntile * p.nb + g0 + k;
-            if (k >= ng) continue;
-            if (!p.tma_store && (!valid || kb >= p.kb_out)) continue;
-            const long long tv0 = dbg ? clock64() : 0;
+            if (k >= ng || !valid || kb >= p.kb_out) continue;
             float vals[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
@@ -841,8 +841,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
             }
             const long long plane = static_cast<long long>(nn) * p.out_cb + kb;
             const long long px_off = ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz;
-            const bool live = valid && kb < p.kb_out;  // rows / blocks the TMA store clips anyway
-            if (p.add != nullptr && live) {  // residual add / gradient sum
+            if (p.add != nullptr) {  // residual add / gradient sum
               float a[16];
               load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
 #pragma unroll
@@ -852,53 +851,11 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = vals[e] > 0.0f ? vals[e] : 0.0f;
             }
-            if (p.mask != nullptr && live) {  // ReLU backward: gradient through the forward activation
+            if (p.mask != nullptr) {  // ReLU backward: gradient through the forward activation
               float m[16];
               load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
-            }
-            if (p.tma_store) {
-              if (kb >= p.kb_out) continue;  // blocks of the next n-tile belong to another CTA
-              uint8_t* stg = stg0 + (n_st % kEpiSlots) * 2048u;
-              const long long tq0 = dbg ? clock64() : 0;
-              if (n_st >= kEpiSlots) {  // that slab's previous store must have left smem
-                if (lane == 0) bulk_wait_group_read<kEpiSlots - 1>();
-                __syncwarp();
-              }
-              const long long tq1 = dbg ? clock64() : 0;
-              if (dbg) c_g += tq0 - tv0;
-              const uint32_t row = static_cast<uint32_t>(lane);
-              if (p.out_bf16) {
-                const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
-                const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
-                *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
-                *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
-              } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                  *reinterpret_cast<float4*>(stg + sw64(row, c)) =
-                      make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
-              }
-              // dense output: box {16 lanes, 32 pixels, 1 block, 1 image}; rows past
-              // P*Q are clipped by the tensor bounds
-              const long long tq2 = dbg ? clock64() : 0;
-              fence_proxy_async_smem();
-              __syncwarp();
-              const long long tq3 = dbg ? clock64() : 0;
-              if (lane == 0) {
-                tma_store_4d(&map_out, stg, 0, v0 + mb * 128 + qrow, kb, n);
-                bulk_commit_group();
-              }
-              if (dbg) {
-                c_d += tq1 - tq0;
-                c_e += tq3 - tq2;
-                c_f += clock64() - tq3;
-                c_h += tq2 - tq1;
-              }
-              ++n_st;
-              (void)slab;
-              continue;
             }
             if (!(p.dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
             if (p.out_fill) {
@@ -924,8 +881,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
           }
         }
       }
-      if (dbg) c_b += clock64() - t_e0;
-      if (!(p.dbg_mode & 16)) tc_fence_before();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
@@ -933,17 +889,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     if (dbg && threadIdx.x == kEpiWarp0 * 32) {
       dbg[6] = c_a;
       dbg[7] = clock64() - t_start - c_a;
-      dbg[11] = c_b;  // tile bodies (TMEM loads .. stores)
-      dbg[12] = c_c;  // of which TMEM loads + wait
-      dbg[13] = c_d;  // TMA-store slab waits
-      dbg[14] = c_e;  // proxy fence + syncwarp
-      dbg[15] = c_f;  // TMA issue
-      if (p.dbg) {
-        p.dbg[gridDim.x * 16 + 2048 + blockIdx.x * 2] = c_g;      // vals .. relu
-        p.dbg[gridDim.x * 16 + 2048 + blockIdx.x * 2 + 1] = c_h;  // staging writes
-      }
-    }
-  }
+    }  }
   tc_fence_before();
   __syncthreads();
   if (dbg && threadIdx.x == 0) {

@@ -11,6 +11,29 @@ using namespace dconv_sm100;
 
 constexpr int kPlanes = 512, kHW = 3136, kCb = 16;  // 32 images x 16 channel blocks x 56x56
 
+// TMA tile stores of 2 KB slabs {16 fp32, 32 px, 1 plane} from a smem ring (the lean epilogue's pattern)
+__global__ void writer(const __grid_constant__ CUtensorMap map, int n_slabs_per_cta, int planes_total) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < n_slabs_per_cta; ++i) {
+    const int slab = blockIdx.x + i * gridDim.x;
+    const int plane = slab % planes_total, v = (slab / planes_total) * 32;
+    if (i >= 4) bulk_wait_group_read<3>();
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(&map)),
+                 "r"(smem_u32(smem + (i % 4) * 2048)), "r"(0), "r"(v), "r"(plane)
+                 : "memory");
+    bulk_commit_group();
+  }
+  bulk_wait_group0();
+}
+
+// plain vectorised stores for comparison
+__global__ void stg_writer(float4* __restrict__ x, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = make_float4(1.f, 2.f, 3.f, 4.f);
+}
+
 // plain vectorised loads for comparison
 __global__ void ldg_reader(const float4* __restrict__ x, size_t n, float* out) {
   float acc = 0.f;
@@ -91,6 +114,45 @@ int main() {
       }
       printf("ldg reader %d blocks, %s flush: %.1f us %.0f GB/s\n", blocks, clean ? "write+read" : "write", best * 1e3, bytes / (best * 1e-3) / 1e9);
     }
+  }
+  {
+    // write bandwidth: TMA slab stores vs plain stores, 103 MB
+    CUtensorMap wmap;
+    cuuint64_t dims[3] = {16, (cuuint64_t)kHW, (cuuint64_t)kPlanes};
+    cuuint64_t st[2] = {64, (cuuint64_t)kHW * 64};
+    cuuint32_t box[3] = {16, 32, 1}, es[3] = {1, 1, 1};
+    enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, x, dims, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int slabs = kPlanes * (kHW / 32);
+    cudaFuncSetAttribute(writer, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192);
+    for (int ctas : {148, 296, 592}) {
+      float best = 1e9;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(flush, rep, 256 << 20);
+        ldg_reader<<<148 * 8, 512>>>((const float4*)flush, (256 << 20) / 16, (float*)flush);
+        cudaEventRecord(a);
+        writer<<<ctas, 32, 8192>>>(wmap, slabs / ctas, kPlanes);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      printf("TMA slab store %d ctas: %.1f us  %.0f GB/s %s\n", ctas, best * 1e3,
+             (double)slabs / ctas * ctas * 2048 / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
+    float best = 1e9;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaMemset(flush, rep, 256 << 20);
+      cudaEventRecord(a);
+      stg_writer<<<148 * 8, 512>>>((float4*)x, bytes / 16);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (ms < best) best = ms;
+    }
+    printf("plain stores: %.1f us %.0f GB/s\n", best * 1e3, bytes / (best * 1e-3) / 1e9);
   }
   const int shapes[][2] = {{128, 4}, {128, 2}};
   float* o2;
