@@ -685,8 +685,9 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     uint8_t* stg0 = smem + L.epi_off + (warp % 4) * 2u * 4096u;
     // FUSED = residual add / ReLU-backward mask present: the plain variant has no
     // per-pixel addressing or extra loads in its loop (smaller, faster code)
-    auto lean = [&](auto fused_tag) {
+    auto lean = [&](auto fused_tag, auto ops_tag) {
       constexpr bool FUSED = decltype(fused_tag)::value;
+      constexpr bool OPS = decltype(ops_tag)::value;  // bias / ReLU present
     uint32_t n_st = 0, tl = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       int n, v0, ntile;
@@ -719,7 +720,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
             for (int e = 0; e < 16; ++e)
               vals[e] = PIECES == 3 ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
                                     : __uint_as_float(r[16 * j + e]);
-            if (p.bias != nullptr && kb < p.kb_out) {
+            if (OPS && p.bias != nullptr && kb < p.kb_out) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += a[e];
             }
-            if (p.relu) {
+            if (OPS && p.relu) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
             }
@@ -773,9 +774,11 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     }
     };
     if (p.add != nullptr || p.mask != nullptr)
-      lean(std::true_type{});
+      lean(std::true_type{}, std::true_type{});
+    else if (p.bias != nullptr || p.relu)
+      lean(std::false_type{}, std::true_type{});
     else
-      lean(std::false_type{});
+      lean(std::false_type{}, std::false_type{});
     if (lane == 0) bulk_wait_group0();
     if (dbg && threadIdx.x == kEpiWarp0 * 32) {
       dbg[6] = c_a;
