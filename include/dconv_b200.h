@@ -218,6 +218,21 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
                         const dconv_wt_t* grad_w, int accumulate, void* workspace, dconv_stream_t stream);
 int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out);
 
+/* ---------------------------------------------------------------- plan validation */
+/* validate_plan (kernel_streams.cpp:461-617) analog: re-derives the plan's tile
+ * schedule for these tensors on the host and checks that every output element
+ * is written exactly once (tiles, CTA striding, lattices, zero fills), that the
+ * staged boxes cover every row the MMAs read, and the smem / TMEM / ring / box
+ * limits; UPD: split ranges and tap groups partition their index spaces.
+ * DCONV_ERR_INVALID_DESCRIPTOR on the first violation; `report` (may be null)
+ * receives a JSON summary. No device work. */
+int dconv_fwd_plan_validate(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_act_t* out, char* report,
+                            size_t len);
+int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, const dconv_act_t* grad_in,
+                            char* report, size_t len);
+int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out,
+                            char* report, size_t len);
+
 /* ---------------------------------------------------------------- host-buffer step */
 /* One layer step on HOST tensors (pinned for overlap), the reference's
  * execute contract (propagation.cpp:56-61 forward_into, :237-261 backward_with,

@@ -61,7 +61,8 @@ EXPORTS = [
     "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
     "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms", "dconv_forward_ex", "dconv_backward_data_ex",
     "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_sgd", "dconv_host_step_create", "dconv_host_step_destroy",
-    "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches",
+    "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches", "dconv_fwd_plan_validate",
+    "dconv_bwd_plan_validate", "dconv_upd_plan_validate",
 ]
 
 
@@ -120,6 +121,9 @@ def _bind(lib):
         "dconv_host_step_chunk": (i, [vp]),
         "dconv_host_step_run": (i, [vp, P(Act), P(Wt), P(Act), P(Act), P(Act), P(Wt), vp]),
         "dconv_host_step_launches": (i, [vp]),
+        "dconv_fwd_plan_validate": (i, [vp, P(Act), P(Act), C.c_char_p, sz]),
+        "dconv_bwd_plan_validate": (i, [vp, P(Act), P(Act), C.c_char_p, sz]),
+        "dconv_upd_plan_validate": (i, [vp, P(Act), P(Act), C.c_char_p, sz]),
         "dconv_profile_last_ms": (C.c_float, [i]),
     }
     for name, (res, args) in sig.items():

@@ -388,6 +388,15 @@ class _Workspace:
         return self.buf.data_ptr()
 
 
+def _validate(fn, handle, a, b) -> dict:
+    """validate_plan analog (kernel_streams.cpp:461-617): raises InvalidDescriptor
+    on a violated property, else returns the validator's JSON summary."""
+    buf = C.create_string_buffer(1 << 16)
+    st = fn(handle, C.byref(a.to_c()), C.byref(b.to_c()), buf, len(buf))
+    _check(st)
+    return json.loads(buf.value.decode() or "{}")
+
+
 def _describe(fn, handle) -> dict:
     buf = C.create_string_buffer(4096)
     fn(handle, buf, len(buf))
@@ -431,6 +440,9 @@ class ExecutionPlan:
 
     def launches(self) -> int:
         return _lib.lib().dconv_fwd_launches(self._h)
+
+    def validate(self, inp: BlockedActivation, out: BlockedActivation) -> dict:
+        return _validate(_lib.lib().dconv_fwd_plan_validate, self._h, inp, out)
 
     def execute(self, inp: BlockedActivation, wt: BlockedWeight, out: BlockedActivation) -> None:
         ws = self._ws.get(_lib.lib().dconv_fwd_workspace_bytes(self._h), inp.data.device)
@@ -539,6 +551,9 @@ class BackwardContext:
     def launches(self) -> int:
         return _lib.lib().dconv_bwd_launches(self._h)
 
+    def validate(self, grad_out: BlockedActivation, grad_in: BlockedActivation) -> dict:
+        return _validate(_lib.lib().dconv_bwd_plan_validate, self._h, grad_out, grad_in)
+
     def execute(self, wt: BlockedWeight, grad_out: BlockedActivation, grad_in: BlockedActivation) -> None:
         ws = self._ws.get(_lib.lib().dconv_bwd_workspace_bytes(self._h), grad_out.data.device)
         _check(_lib.lib().dconv_backward_data(self._h, C.byref(wt.to_c()), C.byref(grad_out.to_c()),
@@ -626,6 +641,9 @@ class UpdatePlan:
 
     def launches(self, inp, grad_out) -> int:
         return _lib.lib().dconv_upd_launches(self._h, C.byref(inp.to_c()), C.byref(grad_out.to_c()))
+
+    def validate(self, inp: BlockedActivation, grad_out: BlockedActivation) -> dict:
+        return _validate(_lib.lib().dconv_upd_plan_validate, self._h, inp, grad_out)
 
     def execute(self, inp: BlockedActivation, grad_out: BlockedActivation, dw: BlockedWeight, accumulate=False):
         a, g = inp.to_c(), grad_out.to_c()

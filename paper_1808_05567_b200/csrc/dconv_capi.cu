@@ -1911,3 +1911,4 @@ int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t
 }  // extern "C"
 
 #include "host_step.cuh"
+#include "validate.cuh"

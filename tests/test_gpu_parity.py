@@ -385,3 +385,43 @@ def test_maxpool_3x3s2_matches_torch(dconv, orc, dtype):
     api._check(lib.dconv_maxpool_bwd(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()), xb.data.data_ptr(), 0))
     got_m = dconv.from_blocked_activation(gi).float()
     assert torch.equal(got_m, torch.where(x.float() > 0, got, torch.zeros_like(got)))
+
+
+# ------------------------------------------------------------------ plan validation (validate_plan analog)
+
+VALIDATE_SHAPES = [r[1:] + (-1, -1) for r in TABLE_I] + [
+    (c, k, h, w, r, s, st, ph, pw) for (c, k, h, w, r, s, st, ph, pw) in CFG5] + [
+    (17, 33, 9, 13, 3, 3, 1, 1, 1), (3, 40, 30, 31, 7, 7, 2, 3, 3), (48, 24, 7, 7, 1, 1, 1, -1, -1),
+    (32, 48, 5, 9, 5, 3, 1, 2, 1)]
+
+
+@pytest.mark.parametrize("shape", VALIDATE_SHAPES, ids=[f"v{i}" for i in range(len(VALIDATE_SHAPES))])
+@pytest.mark.parametrize("math", [0, 1])
+def test_plans_validate(dconv, shape, math):
+    """Every F / B / U plan the tile selector builds passes the exactly-once
+    coverage and geometry validator for its tensors (N=3: multi-image and tail tiles)."""
+    C_, K, H, W, R, S, st, ph, pw = shape
+    N = 3
+    spec = (dconv.make_layer_spec(N, C_, K, H, W, R, S, st, ph, pw, 16) if ph >= 0
+            else dconv.make_layer_spec(N, C_, K, H, W, R, S, st))
+    P, Q = dconv.derive_output_shape(spec)
+    dt = torch.float32 if math == 0 else torch.bfloat16
+    x = dconv.BlockedActivation(N, C_, H, W, 16, spec.pad_h, spec.pad_w, dt)
+    y = dconv.BlockedActivation(N, K, P, Q, 16, 0, 0, dt)
+    g = dconv.BlockedActivation(N, K, P, Q, 16, 0, 0, dt)
+    gi = dconv.BlockedActivation(N, C_, H, W, 16, 0, 0, dt)
+    w = dconv.BlockedWeight(K, C_, R, S, 16, dt)
+    r = dconv.make_forward_plan(spec, 1, None, None, math).validate(x, y)
+    assert r["ok"] and r["writes"] == r["outputs"] == N * P * Q * spec.kb()
+    rb = dconv.prepare_backward(spec, w, 1, None, math).validate(g, gi)
+    assert rb["ok"] and rb["writes"] == rb["outputs"]
+    ru = dconv.UpdatePlan(spec, None, math).validate(x, g)
+    assert ru["ok"]
+
+
+def test_plan_validate_rejects_foreign_tensors(dconv):
+    spec = dconv.make_layer_spec(2, 32, 16, 10, 10, 3, 3, 1)
+    plan = dconv.make_forward_plan(spec, 1, None, None, 0)
+    x = dconv.BlockedActivation(2, 32, 10, 10, 16, 1, 1)
+    with pytest.raises(dconv.ShapeMismatch):
+        plan.validate(x, dconv.BlockedActivation(2, 16, 9, 10, 16, 0, 0))
