@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
   // group wait on a phase two ahead (parity aliasing), so it falls back to one group
   const int cvt_groups = (raw_stages >= 2 && pc_stages >= 2) ? 2 : 1;
   const int cvt_group_warps = TS ? 4 : kCvtWarps / cvt_groups;
+  // bf16 smem-staged plans have idle converter warps: with the lean TMA-store
+  // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
+  // doubling the loads in flight for fused residual adds / ReLU masks
+  const bool epi2 = !RAW_F32 && !TS && p.tma_store;
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
   constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kEpiWarps);
+      mbar_init(&acc_empty[a], kEpiWarps * (epi2 ? 2 : 1));
     }
     fence_barrier_init();
   }
@@ -539,6 +543,118 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       dbg[4] = c_a;
       dbg[5] = c_b;
     }
+  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) ||
+                              (epi2 && warp >= kCvtWarp0 && warp < kCvtWarp0 + 4))) {
+    // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
+    // two output blocks per step: one 32-column TMEM load per accumulator, one
+    // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
+    const int qrow = (warp % 4) * 32;
+    const uint32_t esz = p.out_bf16 ? 2u : 4u;
+    const uint32_t slot_bytes = 2u * 32u * 16u * esz;
+    const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
+    const int eg = warp >= kCvtWarp0 ? 1 : 0, n_eg = epi2 ? 2 : 1;  // epilogue group
+    uint8_t* stg0 = smem + L.epi_off + (eg * 4 + warp % 4) * 2u * 4096u;
+    // FUSED = residual add / ReLU-backward mask present: the plain variant has no
+    // per-pixel addressing or extra loads in its loop (smaller, faster code)
+    auto lean = [&](auto fused_tag, auto ops_tag) {
+      constexpr bool FUSED = decltype(fused_tag)::value;
+      constexpr bool OPS = decltype(ops_tag)::value;  // bias / ReLU present
+    uint32_t n_st = 0, tl = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      int n, v0, ntile;
+      tile_coords(t, n, v0, ntile);
+      const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+      const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+      mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
+      tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
+      for (int mb = 0; mb < p.mb; ++mb) {
+        for (int g0 = 2 * eg; g0 < p.nb; g0 += 2 * n_eg) {
+          const int kb0 = ntile * p.nb + g0;
+          if (kb0 >= p.kb_out) break;
+          const bool pair = g0 + 1 < p.nb;
+          uint32_t r[32], rl[32];
+          tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
+          if (PIECES == 3) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
+          tmem_ld_wait();
+          uint8_t* stg = stg0 + (n_st & 1u) * 4096u;
+          if (n_st >= 2) {  // this slot's previous store must have left smem
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j == 1 && !pair) break;
+            const int kb = kb0 + j;
+            float vals[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              vals[e] = PIECES == 3 ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
+                                    : __uint_as_float(r[16 * j + e]);
+            if (OPS && p.bias != nullptr && kb < p.kb_out) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
+            }
+            // dense output: pixel v of plane (n, kb) at ((n*out_cb + kb)*P*Q + v)*16 lanes
+            const int v = FUSED ? v0 + mb * 128 + qrow + lane : 0;
+            const bool live = FUSED && v < v_end && kb < p.kb_out;
+            const long long px_off = FUSED ? ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz : 0;
+            if (FUSED && p.add != nullptr && live) {  // residual add / gradient sum
+              float a[16];
+              load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += a[e];
+            }
+            if (OPS && p.relu) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
+            }
+            if (FUSED && p.mask != nullptr && live) {  // ReLU backward through the forward activation
+              float m[16];
+              load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
+            }
+            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
+            if (p.out_bf16) {
+              const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
+              const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
+              *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
+              *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<float4*>(stg + sw64(row, c)) =
+                    make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            // rows past P*Q and blocks past K are clipped by the tensor bounds
+            tma_store_4d(pair ? &map_out2 : &map_out, stg, 0, v0 + mb * 128 + qrow, kb0, n);
+            bulk_commit_group();
+          }
+          ++n_st;
+          (void)slot_bytes;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+    };
+    if (p.add != nullptr || p.mask != nullptr)
+      lean(std::true_type{}, std::true_type{});
+    else if (p.bias != nullptr || p.relu)
+      lean(std::false_type{}, std::true_type{});
+    else
+      lean(std::false_type{}, std::false_type{});
+    if (lane == 0) bulk_wait_group0();
+    if (dbg && threadIdx.x == kEpiWarp0 * 32) {
+      dbg[6] = c_a;
+      dbg[7] = clock64() - t_start - c_a;
+    }
   } else if (TS && warp >= kCvtWarp0) {
     // ------------------------------------------------------------ TS converters (smem fp32 -> TMEM pieces)
     // group = (warp - 8) / 4 takes stages g % cvt_groups == group; a warp owns
@@ -673,116 +789,6 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
         dbg[2] = c_b;
         dbg[3] = clock64() - t_start - c_a - c_b;
       }
-    }
-  } else if (warp >= kEpiWarp0 && p.tma_store) {
-    // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
-    // two output blocks per step: one 32-column TMEM load per accumulator, one
-    // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
-    const int qrow = (warp % 4) * 32;
-    const uint32_t esz = p.out_bf16 ? 2u : 4u;
-    const uint32_t slot_bytes = 2u * 32u * 16u * esz;
-    const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
-    uint8_t* stg0 = smem + L.epi_off + (warp % 4) * 2u * 4096u;
-    // FUSED = residual add / ReLU-backward mask present: the plain variant has no
-    // per-pixel addressing or extra loads in its loop (smaller, faster code)
-    auto lean = [&](auto fused_tag, auto ops_tag) {
-      constexpr bool FUSED = decltype(fused_tag)::value;
-      constexpr bool OPS = decltype(ops_tag)::value;  // bias / ReLU present
-    uint32_t n_st = 0, tl = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
-      int n, v0, ntile;
-      tile_coords(t, n, v0, ntile);
-      const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
-      const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
-      mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
-      tc_fence_after();
-      const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
-      for (int mb = 0; mb < p.mb; ++mb) {
-        for (int g0 = 0; g0 < p.nb; g0 += 2) {
-          const int kb0 = ntile * p.nb + g0;
-          if (kb0 >= p.kb_out) break;
-          const bool pair = g0 + 1 < p.nb;
-          uint32_t r[32], rl[32];
-          tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
-          if (PIECES == 3) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
-          tmem_ld_wait();
-          uint8_t* stg = stg0 + (n_st & 1u) * 4096u;
-          if (n_st >= 2) {  // this slot's previous store must have left smem
-            if (lane == 0) bulk_wait_group_read<1>();
-            __syncwarp();
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j == 1 && !pair) break;
-            const int kb = kb0 + j;
-            float vals[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-              vals[e] = PIECES == 3 ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
-                                    : __uint_as_float(r[16 * j + e]);
-            if (OPS && p.bias != nullptr && kb < p.kb_out) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
-            }
-            // dense output: pixel v of plane (n, kb) at ((n*out_cb + kb)*P*Q + v)*16 lanes
-            const int v = FUSED ? v0 + mb * 128 + qrow + lane : 0;
-            const bool live = FUSED && v < v_end && kb < p.kb_out;
-            const long long px_off = FUSED ? ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz : 0;
-            if (FUSED && p.add != nullptr && live) {  // residual add / gradient sum
-              float a[16];
-              load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
-#pragma unroll
-              for (int e = 0; e < 16; ++e) vals[e] += a[e];
-            }
-            if (OPS && p.relu) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
-            }
-            if (FUSED && p.mask != nullptr && live) {  // ReLU backward through the forward activation
-              float m[16];
-              load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
-#pragma unroll
-              for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
-            }
-            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
-            if (p.out_bf16) {
-              const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
-              const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
-              *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
-              *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
-            } else {
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<float4*>(stg + sw64(row, c)) =
-                    make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            // rows past P*Q and blocks past K are clipped by the tensor bounds
-            tma_store_4d(pair ? &map_out2 : &map_out, stg, 0, v0 + mb * 128 + qrow, kb0, n);
-            bulk_commit_group();
-          }
-          ++n_st;
-          (void)slot_bytes;
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
-    }
-    };
-    if (p.add != nullptr || p.mask != nullptr)
-      lean(std::true_type{}, std::true_type{});
-    else if (p.bias != nullptr || p.relu)
-      lean(std::false_type{}, std::true_type{});
-    else
-      lean(std::false_type{}, std::false_type{});
-    if (lane == 0) bulk_wait_group0();
-    if (dbg && threadIdx.x == kEpiWarp0 * 32) {
-      dbg[6] = c_a;
-      dbg[7] = clock64() - t_start - c_a;
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue (warps 4..7)

@@ -35,3 +35,22 @@ span = max(x.time_range.end for x in evs) - min(x.time_range.start for x in evs)
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"{v[1] / 1e3:8.2f} ms  x{v[0]:4d}  {k}")
 print(f"sum {tot / 1e3:.2f} ms, span {span / 1e3:.2f} ms")
+
+if os.environ.get("PER_LAUNCH"):
+    seq = sorted([x for x in evs if "conv_fwd_kernel" in x.name or "conv_upd" in x.name], key=lambda x: x.time_range.start)
+    names = [nd.name for nd in e.convs]
+    # forward: one conv_fwd launch per conv in order; backward: reverse order, BWD (if any) then UPD
+    i = 0
+    print("FWD")
+    for nm in names:
+        print(f"  {nm:8s} {seq[i].device_time:8.1f} us")
+        i += 1
+    print("BWD/UPD (reverse)")
+    for nm in reversed(names):
+        row = []
+        while i < len(seq) and len(row) < 2:
+            row.append(f"{seq[i].name.split('<')[0][-12:]} {seq[i].device_time:7.1f}")
+            i += 1
+            if "conv_upd" in row[-1]:
+                break
+        print(f"  {nm:8s} " + " | ".join(row))
