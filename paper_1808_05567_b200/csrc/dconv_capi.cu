@@ -409,11 +409,12 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           for (; kcx >= 1; kcx = kcx > 1 ? kcx / 2 : 0) {
             const FwdSmem lk = fwd_smem_layout(apx * kcx, wt * kcx, nb, pieces, raw_f32, 1, 1);
             int wsk = std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lk.w_slot)));
-            int left = kFwdBudget - 2 * static_cast<int>(kEpiStagingBytes) - wsk * static_cast<int>(lk.w_slot);
+            // room for three epilogue groups' TMA-store staging (bf16 slabs: 3 x 16 KB)
+            int left = kFwdBudget - 3 * 16384 - wsk * static_cast<int>(lk.w_slot);
             pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
             if (pcs < want_pc && wsk > 2) {
               wsk = 2;
-              left = kFwdBudget - 2 * static_cast<int>(kEpiStagingBytes) - wsk * static_cast<int>(lk.w_slot);
+              left = kFwdBudget - 3 * 16384 - wsk * static_cast<int>(lk.w_slot);
               pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
             }
             if (kcx == 1 && pcs < want_pc) {  // no room for the TMA-store staging: plain budget
@@ -526,8 +527,9 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
   // the epilogue stages 32-pixel slabs in smem and TMA-stores them
   FwdParams& p = L.p;
   const int esz = p.out_bf16 ? 2 : 4;
-  // bf16 smem-staged plans run two epilogue groups (twice the staging)
-  const size_t staging = kEpiStagingBytes * ((!L.raw_f32 && !L.ts) ? 2 : 1);
+  // 4 warps x 2 slabs of {16 lanes, 32 px, 2 blocks} per epilogue group; bf16
+  // smem-staged plans run three groups
+  const size_t staging = static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
   size_t smem = L.smem;
   p.tma_store = 0;
   CUtensorMap map_out, map_out2;
@@ -579,7 +581,7 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
     else
       go(conv_fwd_kernel<true, 1>, kFwdThreadsP);
   } else {
-    go(conv_fwd_kernel<false, 1>, kFwdThreadsP);
+    go(conv_fwd_kernel<false, 1>, kFwdThreadsTS);  // 16 warps: three epilogue groups
   }
   cuda_check(cudaGetLastError(), "conv_fwd_kernel launch");
 }

@@ -238,7 +238,7 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 }
 
 template <bool RAW_F32, int PIECES, bool TS = false>
-__global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
+__global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreadsP, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_out,
                     const __grid_constant__ CUtensorMap map_out2, const __grid_constant__ FwdParams p, int raw_stages,
                     int pc_stages, int w_stages) {
@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
   // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
   // doubling the loads in flight for fused residual adds / ReLU masks
   const bool epi2 = !RAW_F32 && !TS && p.tma_store;
+  const int n_epi_groups = epi2 ? 3 : 1;  // bf16: warps 4..7, 8..11, 12..15
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
   constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kEpiWarps * (epi2 ? 2 : 1));
+      mbar_init(&acc_empty[a], kEpiWarps * n_epi_groups);
     }
     fence_barrier_init();
   }
@@ -543,8 +544,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
       dbg[4] = c_a;
       dbg[5] = c_b;
     }
-  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) ||
-                              (epi2 && warp >= kCvtWarp0 && warp < kCvtWarp0 + 4))) {
+  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) || (epi2 && warp >= kCvtWarp0))) {
     // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
     // two output blocks per step: one 32-column TMEM load per accumulator, one
     // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
@@ -552,8 +552,8 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
     const uint32_t esz = p.out_bf16 ? 2u : 4u;
     const uint32_t slot_bytes = 2u * 32u * 16u * esz;
     const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
-    const int eg = warp >= kCvtWarp0 ? 1 : 0, n_eg = epi2 ? 2 : 1;  // epilogue group
-    uint8_t* stg0 = smem + L.epi_off + (eg * 4 + warp % 4) * 2u * 4096u;
+    const int eg = (warp - kEpiWarp0) / 4, n_eg = n_epi_groups;  // epilogue group
+    uint8_t* stg0 = smem + L.epi_off + (eg * 4 + warp % 4) * 2u * slot_bytes;
     // FUSED = residual add / ReLU-backward mask present: the plain variant has no
     // per-pixel addressing or extra loads in its loop (smaller, faster code)
     auto lean = [&](auto fused_tag, auto ops_tag) {
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(TS ? kFwdThreadsTS : kFwdThreadsP, 1)
           tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
           if (PIECES == 3) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
           tmem_ld_wait();
-          uint8_t* stg = stg0 + (n_st & 1u) * 4096u;
+          uint8_t* stg = stg0 + (n_st & 1u) * slot_bytes;
           if (n_st >= 2) {  // this slot's previous store must have left smem
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
