@@ -1389,7 +1389,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   p.linear = linear ? 1 : 0;
   // tap stacking for narrow inputs (< 8 channel blocks, e.g. the 3-channel stem)
   const bool stacked = !linear && cb < 8 && s.R * s.S > 1;
-  p.stack = stacked ? 8 / cb : 1;
+  // C <= 8 (the 3-channel stem): only the first 8-lane chunk of each pixel is
+  // non-zero, so a tap slot is one chunk and 16 taps share the 128 MMA rows
+  p.half = (stacked && s.C <= 8) ? 1 : 0;
+  p.stack = stacked ? (p.half ? 16 : 8 / cb) : 1;
   p.cb_eff = stacked ? cb : 8;
   // k tile
   int n_kt = cdiv(kb, 16);
@@ -1590,8 +1593,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     const char* base = reinterpret_cast<const char*>(data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 32;
     const uint64_t dims[5] = {8, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), 2, planes};
     const uint64_t strides[4] = {32, static_cast<uint64_t>(wp) * 32, 16, static_cast<uint64_t>(wp) * hp * 32};
-    const uint32_t box_in[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st), 2,
-                                static_cast<uint32_t>(p.cb_eff)};
+    const uint32_t box_in[5] = {8, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st),
+                                p.half ? 1u : 2u, static_cast<uint32_t>(p.cb_eff)};
     const uint32_t box_do[5] = {8, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps), 2,
                                 static_cast<uint32_t>(p.nb)};
     const uint32_t estr_in[5] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1, 1};

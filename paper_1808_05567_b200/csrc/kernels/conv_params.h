@@ -98,6 +98,7 @@ struct UpdParams {
   // `stack` taps x cb_eff channel blocks, each slot staged by its own shifted box
   int stack;               // 1 = shared-tile mode (taps via descriptor shifts)
   int cb_eff;
+  int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
   int tap_ph[kMaxTaps], tap_r2[kMaxTaps], tap_s2[kMaxTaps];
   int n_taps;
   float* partial;      // [split][tap(RS)][c_pad][k_pad]

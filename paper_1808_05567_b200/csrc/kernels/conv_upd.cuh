@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int band = stage % p.stages_per_img;
         uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
         const uint32_t a_bytes =
-            p.stack > 1 ? static_cast<uint32_t>(ntaps * 2 * p.cb_eff) * L.a_plane : L.a_piece;
+            p.stack > 1 ? static_cast<uint32_t>(ntaps * (p.half ? 1 : 2 * p.cb_eff)) * L.a_plane : L.a_piece;
         mbar_arrive_expect_tx(&full_bar[s], PA * a_bytes + PB * L.b_piece);
         for (int pc = 0; pc < PA; ++pc) {
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             // one shifted box per stacked tap: slot j = tap tap0 + j, cb_eff blocks
             for (int j = 0; j < ntaps; ++j) {
               const int tp = tap0 + j, tph = p.tap_ph[tp];
-              tma_load_5d(a_dst + j * 2 * p.cb_eff * L.a_plane, &map_in, &full_bar[s], 0,
+              tma_load_5d(a_dst + j * (p.half ? 1 : 2 * p.cb_eff) * L.a_plane, &map_in, &full_bar[s], 0,
                           p.in_col0 + p.phase_col[tph] + p.stride * p.tap_s2[tp],
                           p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]), 0, pa);
             }
@@ -186,8 +186,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int n_acc = p.stack > 1 ? 1 : ntaps;
     for (int t = 0; t < n_acc; ++t) {
       // stacked: TMEM row = (slot j, channel c) of tap tap0 + j
-      const int slot = p.stack > 1 ? (qrow + lane) / (16 * p.cb_eff) : 0;
-      const int c_row = p.stack > 1 ? (qrow + lane) % (16 * p.cb_eff) : c_glob;
+      const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
+      const int slot = p.stack > 1 ? (qrow + lane) / rows_slot : 0;
+      const int c_row = p.stack > 1 ? (qrow + lane) % rows_slot : c_glob;
       const bool row_ok = p.stack > 1 ? slot < ntaps : true;
       const int rs = p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : t)];
       float* dst_row =
@@ -410,7 +411,8 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
     // index math is hoisted out of the stage loop; a warp's lanes walk the
     // plane's pixels 32 at a time (conflict-free swizzled reads, contiguous writes).
     const int cw = warp - kUpdCvtWarp0;
-    const int a_cps = a_boxes * a_planes * 2, b_cps = 2 * p.nb;
+    // half-block stacking: one chunk plane (channels 0..7, half 0) per tap slot
+    const int a_cps = p.half ? a_boxes : a_boxes * a_planes * 2, b_cps = 2 * p.nb;
     // slots 0-1: A chunk planes cw, cw + 8; slots 2-5: dO chunk planes cw + 8 j (npx = 0: unused)
     uint32_t src_base[6], dst_base[6], piece_str[6], cp_rows0[6], cp_c0[6];
     int cp_npx[6];
@@ -420,9 +422,9 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       const int cp = cw + kUpdCvtWarps * (is_a ? u : u - 2);
       const bool ok = cp < (is_a ? a_cps : b_cps);
       cp_npx[u] = ok ? (is_a ? p.a_px : p.vs) : 0;
-      cp_c0[u] = 2u * (cp & 1);
+      cp_c0[u] = (is_a && p.half) ? 0u : 2u * (cp & 1);
       if (is_a) {
-        const int pl = (cp >> 1) % a_planes, box = (cp >> 1) / a_planes;
+        const int pl = p.half ? 0 : (cp >> 1) % a_planes, box = p.half ? cp : (cp >> 1) / a_planes;
         src_base[u] = box * R.a_sub;
         cp_rows0[u] = pl * p.a_px;
         dst_base[u] = static_cast<uint32_t>(cp) * S.a_plane;
@@ -493,8 +495,9 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       if (warp == kUpdCvtWarp0 && lane == 0) pdl_launch_dependents();  // the reduce may get scheduled
       const int n_acc = stacked ? 1 : ntaps;
       for (int t = 0; t < n_acc; ++t) {
-        const int slot = stacked ? (qrow + lane) / (16 * p.cb_eff) : 0;
-        const int c_row = stacked ? (qrow + lane) % (16 * p.cb_eff) : c_glob;
+        const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
+        const int slot = stacked ? (qrow + lane) / rows_slot : 0;
+        const int c_row = stacked ? (qrow + lane) % rows_slot : c_glob;
         const bool row_ok = stacked ? slot < ntaps : true;
         const int rs = p.tap_src[tap0 + (stacked ? (row_ok ? slot : 0) : t)];
         float* dst_row =
