@@ -18,8 +18,12 @@ def launches(path, out):
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 ks.append((d["Kernel Name"], float(d["Metric Value"].replace(",", ""))))
-    last = max(i for i, k in enumerate(ks) if "spin_kernel" in k[0])
-    step = ks[last + 1:]
+    first = min(i for i, k in enumerate(ks) if "spin_kernel" in k[0])
+    step = []
+    for n, t in ks[first + 1:]:
+        if "spin_kernel" in n or "FillFunctor" in n or "reduce_kernel_impl" in n or "at::native" in n:
+            break
+        step.append((n, t))
     tot = sum(t for _, t in step)
     with open(out, "w") as f:
         f.write("# r01 launch list: one bench.py step (cfg2 fp32-accurate F+B+U), "
