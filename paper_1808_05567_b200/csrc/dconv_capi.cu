@@ -272,6 +272,13 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     p.phase_tap0[i] = taps.phase_tap0[i];
   }
   p.taps_box = taps.taps_box;
+  // fp32-accurate: the tensor core rounds the fp32 accumulator per MMA, so long
+  // reductions keep hi*hi apart from the five correction products (Table I
+  // layer 18, 4608-long, reached 1.27e-4 with one accumulator); reductions of
+  // <= 1024 (<= 384 accumulation steps) stay well inside the gate with one
+  const int red_len = pb.cb_red * 16 * static_cast<int>(taps.r.size());
+  p.split_acc = (pieces == 3 && red_len > 1024) ? 1 : 0;
+  const int n_acc = (pieces == 3 && p.split_acc) ? 2 : 1;
   // linear mode: the halo'd physical plane is the virtual grid
   const bool linear = st == 1 && -pb.row_off == in.halo_h && -pb.col_off == in.halo_w;
   p.linear = linear ? 1 : 0;
@@ -306,7 +313,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     for (int want_bufs : {2, 1}) {
       for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
         const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
-        const int acc_cols = (pieces == 3 ? 2 : 1) * 16 * nb;
+        const int acc_cols = n_acc * 16 * nb;
         const int left = 512 - want_bufs * acc_cols;
         // channel blocks per stage: amortise the per-stage barrier / issue cost
         int kcx = std::min(4, pb.cb_red);
@@ -365,7 +372,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
       for (int mb : {2, 1}) {
         if (want_mb && mb != want_mb) continue;
         // accumulators: (pieces == 3 ? 2 : 1) x mb x 16nb columns, double-buffered when they fit
-        const int acc_cols = (pieces == 3 ? 2 : 1) * mb * 16 * nb;
+        const int acc_cols = n_acc * mb * 16 * nb;
         if (acc_cols > 512) continue;
         const int bufs = 2 * acc_cols <= 512 ? 2 : 1;
         if (bufs == 1 && mb == 2) continue;
@@ -614,11 +621,11 @@ std::string json_tile(const FwdLaunch& L) {
   std::snprintf(buf, sizeof(buf),
                 "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
                 "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d,"
-                "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d}",
+                "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d,\"split_acc\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
                 L.grid.x,
                 (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
-                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store);
+                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store, L.p.split_acc);
   return buf;
 }
 

@@ -264,7 +264,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   // fp32-accurate mode keeps the a0*b0 products and the five correction
   // products in separate accumulators: the large sum then takes 6x fewer
   // (truncating) fp32 accumulation steps; the epilogue adds the two
-  constexpr uint32_t kAccs = PIECES == 3 ? 2u : 1u;
+  // (only long reductions need the split: short ones accumulate all six
+  // products in one accumulator, halving TMEM columns and epilogue loads)
+  const bool two_acc = PIECES == 3 && p.split_acc;
+  const uint32_t kAccs = two_acc ? 2u : 1u;
   const uint32_t acc_cols = kAccs * static_cast<uint32_t>(p.mb * NT);
   // two converter groups alternate stages; a 1-deep ring would let the second
   // group wait on a phase two ahead (parity aliasing), so it falls back to one group
@@ -510,8 +513,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                   const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
                   const uint64_t bd =
                       make_smem_desc(wst + ib * L.w_piece + ((w_kk0 + kk) * nt + tp) * w_tap, 128, 256);
-                  const uint32_t acc_in = pr == 0 ? (first ? 0u : 1u) : ((first && pr == 1) ? 0u : 1u);
-                  const uint32_t d_t = pr == 0 ? d_hi : d_lo;
+                  const uint32_t acc_in = pr == 0 ? (first ? 0u : 1u)
+                                                  : ((two_acc && first && pr == 1) ? 0u : 1u);
+                  const uint32_t d_t = (pr == 0 || !two_acc) ? d_hi : d_lo;
                   if (p.dbg_mode & 8) {
                     // ablation: no MMAs
                   } else if (TS) {
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           const bool pair = g0 + 1 < p.nb;
           uint32_t r[32], rl[32];
           tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
-          if (PIECES == 3) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
+          if (two_acc) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
           tmem_ld_wait();
           uint8_t* stg = stg0 + (n_st & 1u) * slot_bytes;
           if (n_st >= 2) {  // this slot's previous store must have left smem
@@ -589,8 +593,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             float vals[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              vals[e] = PIECES == 3 ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
-                                    : __uint_as_float(r[16 * j + e]);
+              vals[e] = two_acc ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
+                                : __uint_as_float(r[16 * j + e]);
             if (OPS && p.bias != nullptr && kb < p.kb_out) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
@@ -832,7 +836,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           for (int k = 0; k < 2; ++k)
             if (k < ng && !(p.dbg_mode & 2)) {
               tmem_ld16(d_base + static_cast<uint32_t>(mb * NT + (g0 + k) * 16), r[k]);
-              if (PIECES == 3) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
+              if (two_acc) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
             }
           tmem_ld_wait();
 #pragma unroll
@@ -842,7 +846,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             float vals[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              vals[e] = PIECES == 3 ? __uint_as_float(r[k][e]) + __uint_as_float(rl[k][e]) : __uint_as_float(r[k][e]);
+              vals[e] = two_acc ? __uint_as_float(r[k][e]) + __uint_as_float(rl[k][e]) : __uint_as_float(r[k][e]);
             // APPLY after the final reduction step (kernel_streams.cpp:96-120)
             if (p.bias != nullptr && kb < p.kb_out) {
 #pragma unroll

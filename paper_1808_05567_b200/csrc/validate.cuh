@@ -98,7 +98,7 @@ void check_geometry(const FwdLaunch& L, int maxshift, VReport& r) {
   r.fail_if(L.stages < 1 || L.stages > kMaxStages || L.raw_stages > kMaxStages || L.w_stages > kMaxStages,
             "ring depth outside 1..kMaxStages");
   r.fail_if(L.smem > static_cast<size_t>(kSmemBudget), "shared memory " + std::to_string(L.smem) + " > budget");
-  const int acc_cols = (L.pieces == 3 ? 2 : 1) * p.mb * 16 * p.nb;
+  const int acc_cols = ((L.pieces == 3 && p.split_acc) ? 2 : 1) * p.mb * 16 * p.nb;
   const int ring = L.ts ? L.stages * L.pieces * 8 * p.kc : 0;
   r.fail_if(p.acc_bufs * acc_cols + ring > 512, "TMEM columns > 512");
   r.fail_if(p.kc < 1 || (p.kc > 1 && p.n_taps != 1), "multi-block stages need a single-tap problem");
