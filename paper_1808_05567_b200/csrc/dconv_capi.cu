@@ -1762,6 +1762,7 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     if (L0.split_in) launch_split(*in, in_pc, plan->pieces, cs);
     if (L0.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
     UpdLaunch L = plan_upd(*plan, *in, *grad_out, true, in_pc, do_pc, partial);
+    L.p.dbg_mode = g_fwd_dbg_mode;
     bool opened = false;  // profiling bracket opens right before the first conv kernel
     auto go = [&](auto kern, int a_base, int acc) {
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),

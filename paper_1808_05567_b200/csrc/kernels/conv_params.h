@@ -103,6 +103,7 @@ struct UpdParams {
   int tap_ph[kMaxTaps], tap_r2[kMaxTaps], tap_s2[kMaxTaps];
   int n_taps;
   float* partial;      // [split][tap(RS)][c_pad][k_pad]
+  int dbg_mode;        // ablation bits (debug only): 4 skip conversion, 8 skip MMAs
   int c_pad, k_pad;
 };
 

@@ -380,7 +380,9 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
                                         static_cast<uint32_t>(ks) * 256u,
                                     128, S.b_plane);
             };
-            if (CAT) {
+            if (p.dbg_mode & 8) {
+              // ablation: no MMAs
+            } else if (CAT) {
               // X|Y|Z += a0 [b0|b1|b2];  Y|Z += a1 [b0|b1];  Z += a2 b0
               mma_bf16(d_tmem, adesc(0), bdesc(0), make_idesc(1, 1, 1, 128, 3u * NT), first ? 0u : 1u);
               mma_bf16(d_tmem + NT, adesc(1), bdesc(0), make_idesc(1, 1, 1, 128, 2u * NT), 1u);
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
       uint8_t* pcs = smem + R.pc_off + static_cast<uint32_t>(ps) * R.pc_slot;
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
+      for (int u = 0; u < ((p.dbg_mode & 4) ? 0 : 6); ++u) {
         const uint32_t piece_stride = piece_str[u];
         const uint8_t* src0 = raw + src_base[u];
         uint8_t* dst0 = pcs + dst_base[u];
