@@ -18,7 +18,8 @@ struct dconv_host_step {
   int math;
   int chunk;  // images per chunk
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_w = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  static constexpr int kSlots = 3;  // staging depth: H2D of chunk i waits only for chunk i-3's compute
+  cudaEvent_t ev_start = nullptr, ev_w = nullptr, ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
   // plans per chunk size (the schedule ramps 1, 2, 4, ... images up and down)
   struct Plans {
     int n = 0, y_hh = -1, y_hw = -1;
@@ -28,7 +29,7 @@ struct dconv_host_step {
   };
   std::map<int, Plans> plans;
   // device staging: two slots per streamed tensor, one weight / weight-gradient buffer
-  void* slot[4][2] = {};  // x, dy, y, dx
+  void* slot[4][kSlots] = {};  // x, dy, y, dx
   size_t slot_bytes[4] = {};
   void* w_dev = nullptr;
   void* dw_dev = nullptr;
@@ -95,9 +96,11 @@ int dconv_host_step_create(const dconv_spec_t* spec, int math, int chunk_images,
     h->chunk = chunk_images > 0 ? std::min(chunk_images, spec->N) : std::max(1, spec->N / 4);
     cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
-    for (cudaEvent_t* e : {&h->ev_start, &h->ev_w, &h->ev_in[0], &h->ev_in[1], &h->ev_comp[0], &h->ev_comp[1],
-                           &h->ev_out[0], &h->ev_out[1]})
+    for (cudaEvent_t* e : {&h->ev_start, &h->ev_w})
       cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    for (int b = 0; b < dconv_host_step::kSlots; ++b)
+      for (cudaEvent_t* e : {&h->ev_in[b], &h->ev_comp[b], &h->ev_out[b]})
+        cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     *out = h;
   });
 }
@@ -106,8 +109,10 @@ void dconv_host_step_destroy(dconv_host_step_t h) {
   if (!h) return;
   cudaDeviceSynchronize();
   hs_free(*h);
-  for (cudaEvent_t e : {h->ev_start, h->ev_w, h->ev_in[0], h->ev_in[1], h->ev_comp[0], h->ev_comp[1], h->ev_out[0],
-                        h->ev_out[1]})
+  for (cudaEvent_t e : {h->ev_start, h->ev_w})
+    if (e) cudaEventDestroy(e);
+  for (int b = 0; b < dconv_host_step::kSlots; ++b)
+    for (cudaEvent_t e : {h->ev_in[b], h->ev_comp[b], h->ev_out[b]})
     if (e) cudaEventDestroy(e);
   if (h->h2d) cudaStreamDestroy(h->h2d);
   if (h->d2h) cudaStreamDestroy(h->d2h);
@@ -180,9 +185,10 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
       if (acts[t]) {
         const size_t want = act_bytes_per_image(*acts[t]) * max_chunk;
         if (want > h->slot_bytes[t] || !h->slot[t][0]) {
-          size_t have0 = h->slot_bytes[t], have1 = h->slot_bytes[t];
-          ensure(h->slot[t][0], have0, want);
-          ensure(h->slot[t][1], have1, want);
+          for (int b = 0; b < dconv_host_step::kSlots; ++b) {
+            size_t have = h->slot_bytes[t];
+            ensure(h->slot[t][b], have, want);
+          }
           h->slot_bytes[t] = want;
         }
       }
@@ -270,11 +276,11 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
     };
     mark(cs);
     for (int i = 0, n0 = 0; i < n_chunks; n0 += sched[i], ++i) {
-      const int b = i & 1;
+      const int b = i % dconv_host_step::kSlots;
       const int n = sched[i];
       dconv_host_step::Plans& pl = plans_for(n);
       // the slot's previous chunk (i-2) must be done computing before its inputs are overwritten
-      if (i >= 2) cuda_check(cudaStreamWaitEvent(h->h2d, h->ev_comp[b], 0), "stream wait");
+      if (i >= dconv_host_step::kSlots) cuda_check(cudaStreamWaitEvent(h->h2d, h->ev_comp[b], 0), "stream wait");
       mark(h->h2d);
       for (int t = 0; t < 2; ++t)
         if (acts[t]) {
@@ -287,7 +293,7 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
       cuda_check(cudaEventRecord(h->ev_in[b], h->h2d), "event record");
       cuda_check(cudaStreamWaitEvent(cs, h->ev_in[b], 0), "stream wait");
       // ... and its outputs (i-2) must have left the device before they are overwritten
-      if (i >= 2) cuda_check(cudaStreamWaitEvent(cs, h->ev_out[b], 0), "stream wait");
+      if (i >= dconv_host_step::kSlots) cuda_check(cudaStreamWaitEvent(cs, h->ev_out[b], 0), "stream wait");
       dconv_act_t xc{}, dyc{}, yc{}, dxc{};
       if (x) xc = chunk_act(x, h->slot[0][b], n);
       if (dy) dyc = chunk_act(dy, h->slot[1][b], n);
@@ -323,7 +329,8 @@ int dconv_host_step_run(dconv_host_step_t h, const dconv_act_t* x, const dconv_w
     if (do_u)
       cuda_check(cudaMemcpyAsync(dw->data, h->dw_dev, wbytes, cudaMemcpyDeviceToHost, cs), "D2H weight gradient");
     // the caller's stream completes after every copy of this step
-    for (int b = 0; b < std::min(n_chunks, 2); ++b) cuda_check(cudaStreamWaitEvent(cs, h->ev_out[b], 0), "stream wait");
+    for (int b = 0; b < std::min(n_chunks, dconv_host_step::kSlots); ++b)
+      cuda_check(cudaStreamWaitEvent(cs, h->ev_out[b], 0), "stream wait");
     mark(cs);
     if (trace) {
       cudaStreamSynchronize(cs);
