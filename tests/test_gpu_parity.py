@@ -425,3 +425,39 @@ def test_plan_validate_rejects_foreign_tensors(dconv):
     x = dconv.BlockedActivation(2, 32, 10, 10, 16, 1, 1)
     with pytest.raises(dconv.ShapeMismatch):
         plan.validate(x, dconv.BlockedActivation(2, 16, 9, 10, 16, 0, 0))
+
+
+# ------------------------------------------------------------------ single-tap (TMEM-staged) edge shapes
+
+EDGE_1x1 = [  # N, C, K, H, W, stride: channel tails, tiny / odd planes, multi-image tiles, one image
+    (1, 20, 36, 5, 7, 1), (3, 17, 33, 9, 9, 1), (2, 48, 80, 1, 1, 1), (5, 64, 16, 7, 7, 1), (1, 256, 64, 56, 56, 1),
+    (3, 40, 24, 11, 13, 2), (2, 16, 16, 12, 12, 2), (4, 96, 200, 14, 14, 1),
+]
+
+
+@pytest.mark.parametrize("shape", EDGE_1x1, ids=[f"e{i}" for i in range(len(EDGE_1x1))])
+@pytest.mark.parametrize("math", [0, 1])
+def test_single_tap_edge_shapes(dconv, orc, shape, math):
+    N, C_, K, H, W, st = shape
+    s = orc.spec(N, C_, K, H, W, 1, 1, st, 0, 0, 16)
+    spec = dconv.make_layer_spec(N, C_, K, H, W, 1, 1, st, 0, 0, 16)
+    P, Q = orc.output_shape(s)
+    x = orc.uniform(51, (N, C_, H, W))
+    w = orc.he_normal(52, (K, C_, 1, 1), C_)
+    g = orc.uniform(53, (N, K, P, Q))
+    fb = run_fwd(dconv, spec, x, w, math)
+    # tail lanes of the last output block stay exactly zero (test_propagation.cpp:90-102)
+    if K % 16:
+        assert not fb.view5()[:, -1, :, :, K % 16:].any()
+    gate(orc, orc.conv_forward(s, x, w), dconv.from_blocked_activation(fb).cpu().numpy(), math)
+    gi = dconv.from_blocked_activation(run_bwd(dconv, spec, g, w, math)).cpu().numpy()
+    rb = orc.conv_backward(s, g, w)
+    if st == 2:
+        mask = np.ones_like(gi, bool)
+        mask[:, :, ::2, ::2] = False
+        assert not gi[mask].any()
+        gate(orc, np.ascontiguousarray(rb[:, :, ::2, ::2]), np.ascontiguousarray(gi[:, :, ::2, ::2]), math)
+    else:
+        gate(orc, rb, gi, math)
+    gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(run_upd(dconv, spec, x, g, math)).cpu().numpy(),
+         math)
