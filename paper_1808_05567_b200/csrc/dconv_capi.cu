@@ -1359,6 +1359,7 @@ struct UpdLaunch {
   bool split_in, split_do;
   // fp32 operands converted in shared memory (conv_upd_raw_kernel)
   bool raw = false, cat = false;
+  bool tsa = false;  // single tap: A operand staged in TMEM (conv_upd_ts_kernel)
   int raw_stages = 0, pc_stages = 0;
 };
 
@@ -1488,6 +1489,29 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       if (pl.has_cfg && pl.cfg.stages > 0) L.raw_stages = std::max(2, std::min(L.raw_stages, pl.cfg.stages));
     }
   }
+  // single-tap layers: A (activations) converted straight into a TMEM ring, so only
+  // the raw boxes and the dO pieces occupy shared memory
+  const char* tsa_env = getenv("DCONV_UPD_TSA");
+  if (want_raw && !stacked && taps.r.size() == 1 && !(tsa_env && tsa_env[0] == '0')) {
+    const int acc_w = (pieces == 3 && 3 * NT <= 256) ? 3 * NT : NT;
+    const int want_vs = tsa_env ? std::atoi(tsa_env) : 0;  // > 1: force the stage band (experiments)
+    for (auto& cd : cands) {
+      if (cd.passes != 1 || (want_vs > 1 && cd.vs != want_vs)) continue;
+      const UpdRawLayout rl = upd_raw_layout(cd.a_px, cd.vs, p.nb, pieces, 1, 8, 1);
+      const int ring = pieces * cd.vs / 2;
+      const int ps = std::min(4, (512 - acc_w) / ring);
+      if (ps < 2) continue;
+      const int64_t left = static_cast<int64_t>(kSmemBudget) - static_cast<int64_t>(ps) * upd_ts_pc_slot(cd.vs, p.nb, pieces);
+      const int rr = left > 0 ? static_cast<int>(std::min<int64_t>(kMaxStages, left / rl.raw_slot)) : 0;
+      if (rr < 3) continue;
+      best = &cd;
+      L.raw = L.tsa = true;
+      L.raw_stages = rr;
+      L.pc_stages = ps;
+      if (pl.has_cfg && pl.cfg.stages > 0) L.raw_stages = std::max(2, std::min(L.raw_stages, pl.cfg.stages));
+      break;
+    }
+  }
   if (!best) fail(DCONV_ERR_PLAN_INFEASIBLE, "no weight-update tile fits shared memory / TMA box limits");
   if (L.raw) L.split_in = L.split_do = false;
   p.wsub = best->wsub;
@@ -1581,7 +1605,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   L.smem = static_cast<size_t>(stages) * layout.bytes;
   if (L.raw) {
     const UpdRawLayout rl = upd_raw_layout(p.a_px, p.vs, p.nb, pieces, stacked ? p.stack : 1, p.cb_eff, L.raw_stages);
-    L.smem = static_cast<size_t>(rl.pc_off) + static_cast<size_t>(L.pc_stages) * rl.pc_slot;
+    L.smem = static_cast<size_t>(rl.pc_off) +
+             static_cast<size_t>(L.pc_stages) * (L.tsa ? upd_ts_pc_slot(p.vs, p.nb, pieces) : rl.pc_slot);
   }
   L.ws_in = L.split_in ? align256(static_cast<size_t>(pieces) * act_elems(in) * 2) : 0;
   L.ws_do = L.split_do ? align256(static_cast<size_t>(pieces) * act_elems(dout) * 2) : 0;
@@ -1778,7 +1803,14 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
       kern<<<L.grid, kUpdRawWarps * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages, L.pc_stages);
       cuda_check(cudaGetLastError(), "conv_upd_raw_kernel launch");
     };
-    if (L.raw) {
+    if (L.tsa) {
+      if (plan->pieces == 1)
+        go_raw(conv_upd_ts_kernel<1, false>);
+      else if (L.cat)
+        go_raw(conv_upd_ts_kernel<3, true>);
+      else
+        go_raw(conv_upd_ts_kernel<3, false>);
+    } else if (L.raw) {
       if (plan->pieces == 1)
         go_raw(conv_upd_raw_kernel<1, false>);
       else if (L.cat)
@@ -1821,10 +1853,10 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     std::snprintf(buf, sizeof(buf),
                   "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
                   "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
-                  "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d}",
+                  "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d,\"a_in_tmem\":%d}",
                   L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
                   L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces, L.passes,
-                  L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0);
+                  L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0);
     plan->last_desc = buf;
   });
 }

@@ -226,6 +226,12 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8])
                "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
+// same store without a memory clobber: ordinary shared-memory loads may be
+// scheduled across it (the values are in registers; tmem_st_wait orders it)
+__device__ __forceinline__ void tmem_st8_nc(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // D[tmem] (+)= A[tmem] * B[smem] (A: lane = row, 8 columns = 16 packed bf16, low half = even k)
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -271,7 +277,13 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   const uint32_t acc_cols = kAccs * static_cast<uint32_t>(p.mb * NT);
   // two converter groups alternate stages; a 1-deep ring would let the second
   // group wait on a phase two ahead (parity aliasing), so it falls back to one group
-  const int cvt_groups = (raw_stages >= 2 && pc_stages >= 2) ? 2 : 1;
+  // Two converter groups alternate stages. Each waits its piece slot first: that
+  // proves every stage <= g - pc_stages was converted, hence its raw fill landed,
+  // so the raw_full parity wait for g cannot be satisfied by the fill of
+  // g - 2 raw_stages (TMA fills may land out of order) as long as the slot's
+  // previous fill is ours (raw_stages even) or <= g - pc_stages.
+  const int cvt_groups =
+      (raw_stages >= 2 && pc_stages >= 2 && (raw_stages % 2 == 0 || raw_stages >= pc_stages)) ? 2 : 1;
   const int cvt_group_warps = TS ? 4 : kCvtWarps / cvt_groups;
   // bf16 smem-staged plans have idle converter warps: with the lean TMA-store
   // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     dbg[9] = static_cast<long long>(gt);
   }
-  long long c_a = 0, c_b = 0, c_c = 0, c_d = 0, c_e = 0, c_f = 0, c_g = 0, c_h = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
+  long long c_a = 0, c_b = 0, c_c = 0, c_d = 0, c_e = 0, c_f = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
 
   // tile t -> (n, v0, ntile); output-channel tiles innermost so consecutive
   // CTAs share the activation tile through L2
@@ -689,11 +701,11 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         if (ph == 0) ++cbi;
         if (static_cast<int>(g & static_cast<uint32_t>(cvt_groups - 1)) != grp) continue;
         const int rs = rr.idx, ps = pr.idx;
-        mbar_wait_bt(&raw_full[rs], rr.ph, dbg ? &c_a : nullptr);
         long long* ctr = (dbg && blockIdx.x == 0 && g < 256 && lane == 0 && q == 0) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
-        if (ctr) ctr[3] = clock64() - t_start;
         mbar_wait_bt(&pc_empty[ps], pr.ph ^ 1u, dbg ? &c_b : nullptr);
         if (ctr) ctr[4] = clock64() - t_start;
+        mbar_wait_bt(&raw_full[rs], rr.ph, dbg ? &c_a : nullptr);
+        if (ctr) ctr[3] = clock64() - t_start;
         tc_fence_after();
         const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
         const int kc_eff = min(p.kc, p.cb_in - cbi * p.kc);
@@ -757,8 +769,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         for (int it = 0; it < k_iters; ++it, ++g, rr.adv(raw_stages), pr.adv(pc_stages)) {
           if (static_cast<int>(g & static_cast<uint32_t>(cvt_groups - 1)) != grp) continue;
           const int rs = rr.idx, ps = pr.idx;
+          mbar_wait_t(&pc_empty[ps], pr.ph ^ 1u, dbg ? &c_b : nullptr);  // first: see cvt_groups
           mbar_wait_t(&raw_full[rs], rr.ph, dbg ? &c_a : nullptr);
-          mbar_wait_t(&pc_empty[ps], pr.ph ^ 1u, dbg ? &c_b : nullptr);
           const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
           uint8_t* pcs = smem + ps * L.pc_slot;
           for (int i = ct; i < items; i += cvt_group_warps * 32) {

@@ -261,6 +261,11 @@ __host__ __device__ inline UpdRawLayout upd_raw_layout(int a_px, int vs, int nb,
   return L;
 }
 
+// dO piece ring slot of conv_upd_ts_kernel (A lives in TMEM)
+__host__ __device__ inline uint32_t upd_ts_pc_slot(int vs, int nb, int pieces) {
+  return (static_cast<uint32_t>(pieces) * 2u * nb * vs * 16u + 1023u) & ~1023u;
+}
+
 // 16 B chunk k of row j of a SWIZZLE_64B box whose start is 1 KiB aligned
 __device__ __forceinline__ uint32_t sw64_row(uint32_t j, uint32_t k) { return j * 64u + ((k ^ ((j >> 1) & 3u)) << 4); }
 
@@ -528,6 +533,267 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
             }
             d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
           }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);
+}
+
+// ---------------------------------------------------------------------------
+// Single-tap fp32 UPD with the A operand (input activations) in TENSOR memory.
+// The in-smem variant above is shared-memory-bandwidth bound (TMA raw writes,
+// converter reads + piece writes and the MMA's A / B reads ~170 KB per 32-pixel
+// stage against ~128 B/cycle). Here a converter thread owns one TMEM lane = one
+// input channel: it reads that channel's fp32 values of the stage's pixels from
+// the raw box (SWIZZLE_64B, 16 lanes per 64 B row: a warp's 32 channels are two
+// contiguous rows, conflict-free), splits them into bf16 pieces packed two
+// pixels per column and tcgen05.st's them into a TMEM ring; the MMA reads A
+// from TMEM (K = pixels along columns) and only dO pieces go through smem.
+// Two converter groups of four warps (one per TMEM lane quarter) alternate
+// stages; within a stage the group also converts the dO chunk planes.
+template <int PIECES, bool CAT>
+__global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
+    conv_upd_ts_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
+                       const __grid_constant__ UpdParams p, int raw_stages, int pc_stages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int NT = 16 * p.nb;
+  const int ctile = blockIdx.x;  // single tap: one tap group
+  const int ktile = blockIdx.y;
+  const int split = blockIdx.z;
+  const int per = (p.stages_total + p.splits - 1) / p.splits;
+  const int s_begin = split * per;
+  const int s_end = min(p.stages_total, s_begin + per);
+  const int iters = s_end > s_begin ? s_end - s_begin : 0;
+  // raw slot: A box (8 planes x a_px x 64 B) then the dO box; piece slot: dO pieces only
+  const UpdRawLayout R = upd_raw_layout(p.a_px, p.vs, p.nb, PIECES, 1, 8, raw_stages);
+  const uint32_t b_plane = static_cast<uint32_t>(p.vs) * 16u, b_piece = 2u * p.nb * b_plane;
+  const uint32_t pc_slot = upd_ts_pc_slot(p.vs, p.nb, PIECES);
+  const uint32_t smem0 = smem_u32(smem);
+  constexpr int kGroups = CAT ? 3 : 1;
+  const uint32_t acc_w = static_cast<uint32_t>(kGroups * NT);
+  const uint32_t a_cols = static_cast<uint32_t>(p.vs) / 2u;  // TMEM columns per piece per stage
+  const uint32_t ring_slot = PIECES * a_cols;
+  // alternating converter groups: same ordering argument as conv_fwd_kernel's
+  // (measured: all eight warps on every stage is slower than alternating groups)
+  const int cvt_groups =
+      (raw_stages >= 2 && pc_stages >= 2 && (raw_stages % 2 == 0 || raw_stages >= pc_stages)) ? 2 : 1;
+  const uint32_t cvt_arrivals = 4u;
+
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < acc_w + static_cast<uint32_t>(pc_stages) * ring_slot) tmem_cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_in);
+    tma_prefetch_desc(&map_do);
+    for (int s = 0; s < raw_stages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], cvt_arrivals);
+    }
+    for (int s = 0; s < pc_stages; ++s) {
+      mbar_init(&pc_full[s], cvt_arrivals);
+      mbar_init(&pc_empty[s], 1);
+    }
+    mbar_init(&accum_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (fp32 boxes)
+    if (lane == 0) {
+      const uint32_t a_bytes = 8u * p.a_px * 64u, b_bytes = static_cast<uint32_t>(p.nb) * p.vs * 64u;
+      for (int it = 0; it < iters; ++it) {
+        const int s = it % raw_stages;
+        mbar_wait(&raw_empty[s], (static_cast<uint32_t>(it / raw_stages) & 1u) ^ 1u);
+        const int stage = s_begin + it;
+        const int n = stage / p.stages_per_img, band = stage % p.stages_per_img;
+        uint8_t* st = smem + static_cast<uint32_t>(s) * R.raw_slot;
+        mbar_arrive_expect_tx(&raw_full[s], a_bytes + b_bytes);
+        const int pa = n * p.in_cb + ctile * 8, pb = n * p.do_cb + ktile * p.nb;
+        if (p.linear) {
+          tma_load_3d(st, &map_in, &raw_full[s], 0, band * p.vs, pa);
+          tma_load_3d(st + R.a_raw, &map_do, &raw_full[s], 0, band * p.vs, pb);
+        } else {
+          tma_load_4d(st, &map_in, &raw_full[s], 0, p.in_col0 + p.phase_col[0],
+                      p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[0], pa);
+          tma_load_4d(st + R.a_raw, &map_do, &raw_full[s], 0, 0, band * p.rows_ps, pb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (A from TMEM, B from smem)
+    const int ksteps = p.vs / 16;
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % pc_stages;
+      mbar_wait(&pc_full[s], static_cast<uint32_t>(it / pc_stages) & 1u);
+      tc_fence_after();
+      const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * pc_slot;
+      const uint32_t a_t = tmem_base + acc_w + static_cast<uint32_t>(s) * ring_slot;
+      if (elect_one()) {
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const bool first = it == 0 && ks == 0;
+          auto atm = [&](int ia) { return a_t + static_cast<uint32_t>(ia) * a_cols + static_cast<uint32_t>(ks) * 8u; };
+          auto bdesc = [&](int ib) {
+            return make_smem_desc(st + static_cast<uint32_t>(ib) * b_piece + static_cast<uint32_t>(ks) * 256u, 128,
+                                  b_plane);
+          };
+          if (p.dbg_mode & 8) {
+            // ablation: no MMAs
+          } else if (CAT) {
+            mma_bf16_ts(tmem_base, atm(0), bdesc(0), make_idesc(1, 0, 1, 128, 3u * NT), first ? 0u : 1u);
+            mma_bf16_ts(tmem_base + NT, atm(1), bdesc(0), make_idesc(1, 0, 1, 128, 2u * NT), 1u);
+            mma_bf16_ts(tmem_base + 2 * NT, atm(2), bdesc(0), make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT)),
+                        1u);
+          } else {
+            const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
+#pragma unroll
+            for (int ia = 0; ia < PIECES; ++ia)
+#pragma unroll
+              for (int ib = 0; ib < PIECES; ++ib) {
+                if (ia + ib > 2) continue;
+                mma_bf16_ts(tmem_base, atm(ia), bdesc(ib), idesc, (first && ia == 0 && ib == 0) ? 0u : 1u);
+              }
+          }
+        }
+        mma_commit(&pc_empty[s]);
+        if (it == iters - 1) mma_commit(&accum_bar);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= kUpdCvtWarp0) {
+    // ------------------------------------------------------------ converters
+    const int grp = (warp - kUpdCvtWarp0) / 4;
+    const uint32_t q = static_cast<uint32_t>(warp % 4);
+    const int row = static_cast<int>(q) * 32 + lane;  // TMEM lane = input channel of the c-tile
+    const int pl = row / 16, ln = row % 16;           // raw plane, lane within the 64 B row
+    // a warp's lanes 0-15 / 16-31 read two planes a_px rows apart: with a_px even
+    // both rows sit on the same 16 banks, so the upper half reads the pixel pair
+    // in swapped order (rows of opposite parity -> disjoint bank halves)
+    const uint32_t swap = ((lane >> 4) & ~p.a_px) & 1u;
+    const uint32_t kq = static_cast<uint32_t>(ln >> 2), lo4 = static_cast<uint32_t>(ln & 3) * 4u;
+    const uint32_t a_row0 = static_cast<uint32_t>(pl * p.a_px + p.tap_shift[0]);
+    // dO chunk planes 0 .. 2nb-1: warp q of the group takes q, q + 4, ...
+    for (int it = 0; it < iters; ++it) {
+      if ((it % cvt_groups) != grp) continue;
+      const int rs = it % raw_stages, ps = it % pc_stages;
+      mbar_wait_backoff(&pc_empty[ps], (static_cast<uint32_t>(it / pc_stages) & 1u) ^ 1u);  // first: see cvt_groups
+      mbar_wait_backoff(&raw_full[rs], static_cast<uint32_t>(it / raw_stages) & 1u);
+      tc_fence_after();
+      const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
+      if (!(p.dbg_mode & 4)) {
+        // A: this channel's values over the stage's pixels -> pieces, 2 pixels per column
+        const uint32_t col0 = tmem_base + (q * 32u << 16) + acc_w + static_cast<uint32_t>(ps) * ring_slot;
+        // 16-pixel units; the next unit's values are loaded before this unit's
+        // tcgen05.st so shared-memory latency overlaps the split arithmetic
+        const int px_end = (p.dbg_mode & 64) ? 0 : p.vs;
+        float xa[16];
+        auto load_unit = [&](int px0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t r0 = a_row0 + static_cast<uint32_t>(px0 + 2 * e);
+            xa[2 * e] = *reinterpret_cast<const float*>(raw + sw64_row(r0 + swap, kq) + lo4);
+            xa[2 * e + 1] = *reinterpret_cast<const float*>(raw + sw64_row(r0 + 1u - swap, kq) + lo4);
+          }
+        };
+        if (px_end > 0) load_unit(0);
+        for (int px0 = 0; px0 < px_end; px0 += 16) {
+          uint32_t h[8], m[8], l[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float va = xa[2 * e], vb = xa[2 * e + 1];
+            const float x0 = swap ? vb : va, x1 = swap ? va : vb;
+            h[e] = cvt2(x0, x1);
+            if (PIECES == 3) {
+              const float ra = x0 - lo_f(h[e]), rb = x1 - hi_f(h[e]);
+              m[e] = cvt2(ra, rb);
+              l[e] = cvt2(ra - lo_f(m[e]), rb - hi_f(m[e]));
+            }
+          }
+          if (px0 + 16 < px_end) load_unit(px0 + 16);
+          const uint32_t c = col0 + static_cast<uint32_t>(px0 / 2);
+          tmem_st8_nc(c, h);
+          if (PIECES == 3) {
+            tmem_st8_nc(c + a_cols, m);
+            tmem_st8_nc(c + 2 * a_cols, l);
+          }
+        }
+        // dO: chunk planes (8 k-channels) -> MN-major pieces in smem
+        uint8_t* pcs = smem + R.pc_off + static_cast<uint32_t>(ps) * pc_slot;
+        for (int cp = static_cast<int>(q); cp < ((p.dbg_mode & 128) ? 0 : 2 * p.nb); cp += 4) {
+          const uint32_t c0 = 2u * (cp & 1), rbase = static_cast<uint32_t>((cp >> 1) * p.vs);
+          for (int px = lane; px < p.vs; px += 32) {
+            const uint32_t off = sw64_row(rbase + px, c0);
+            const float4 a = *reinterpret_cast<const float4*>(raw + R.a_raw + off);
+            const float4 b = *reinterpret_cast<const float4*>(raw + R.a_raw + (off ^ 16u));
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint8_t* dst = pcs + static_cast<uint32_t>(cp) * b_plane + px * 16;
+            if (PIECES == 3) {
+              uint4 hh, mm, ll;
+              split8(v, hh, mm, ll);
+              *reinterpret_cast<uint4*>(dst) = hh;
+              *reinterpret_cast<uint4*>(dst + b_piece) = mm;
+              *reinterpret_cast<uint4*>(dst + 2 * b_piece) = ll;
+            } else {
+              *reinterpret_cast<uint4*>(dst) = cast8(v);
+            }
+          }
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rs]);
+        mbar_arrive(&pc_full[ps]);
+      }
+    }
+    if (warp < kUpdCvtWarp0 + 4) {
+      // -------------------------------------------------------- epilogue (w4..w7: TMEM lane quarters)
+      const int qrow = (warp % 4) * 32;
+      if (iters > 0) {
+        mbar_wait(&accum_bar, 0);
+        tc_fence_after();
+      }
+      if (warp == kUpdCvtWarp0 && lane == 0) pdl_launch_dependents();
+      float* dst_row = p.partial + ((static_cast<long long>(split) * p.n_taps + p.tap_src[0]) * p.c_pad +
+                                    ctile * 128 + qrow + lane) * p.k_pad + ktile * NT;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16);
+      for (int g = 0; g < p.nb; ++g) {
+        uint32_t r[16], ry[16], rz[16];
+        tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
+        if (CAT) {
+          tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
+          tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
+        }
+        tmem_ld_wait();
+        float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
+        const bool live = iters > 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int qq = 4 * e + u;
+            vv[u] = CAT ? __uint_as_float(r[qq]) + (__uint_as_float(ry[qq]) + __uint_as_float(rz[qq]))
+                        : __uint_as_float(r[qq]);
+            if (!live) vv[u] = 0.0f;
+          }
+          d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
         }
       }
     }

@@ -461,3 +461,27 @@ def test_single_tap_edge_shapes(dconv, orc, shape, math):
         gate(orc, rb, gi, math)
     gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(run_upd(dconv, spec, x, g, math)).cpu().numpy(),
          math)
+
+
+@pytest.mark.parametrize("shape", EDGE_1x1, ids=[f"e{i}" for i in range(len(EDGE_1x1))])
+@pytest.mark.parametrize("math", [0, 1])
+def test_update_tmem_and_smem_staging_agree(dconv, orc, shape, math, monkeypatch):
+    """Single-tap fp32 UPD: the TMEM-staged kernel (conv_upd_ts_kernel, default) and
+    the shared-memory-staged one (DCONV_UPD_TSA=0) both pass the gate."""
+    N, C_, K, H, W, st = shape
+    s = orc.spec(N, C_, K, H, W, 1, 1, st, 0, 0, 16)
+    spec = dconv.make_layer_spec(N, C_, K, H, W, 1, 1, st, 0, 0, 16)
+    P, Q = orc.output_shape(s)
+    x = orc.uniform(61, (N, C_, H, W))
+    g = orc.uniform(62, (N, K, P, Q))
+    ref = orc.conv_update(s, x, g)
+    ib = dconv.to_blocked_activation(dev(x), spec)
+    gb = dconv.to_blocked_activation(dev(g), 16, 0, 0)
+    for env, flag in (("1", 1), ("0", 0)):
+        monkeypatch.setenv("DCONV_UPD_TSA", env)
+        up = dconv.UpdatePlan(spec, None, math)
+        dw = dconv.BlockedWeight(K, C_, 1, 1)
+        up.execute(ib, gb, dw)
+        torch.cuda.synchronize()
+        assert up.blocking["a_in_tmem"] == flag, up.blocking
+        gate(orc, ref, dconv.from_blocked_weight(dw).cpu().numpy(), math)

@@ -19,7 +19,7 @@ dw = d.BlockedWeight(64, 256, 1, 1)
 up = d.UpdatePlan(spec, None, d.Math.F32)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 lib.dconv_profile(1)
-for mode in (0, 4, 8, 12):
+for mode in [int(m) for m in os.environ.get("MODES", "0 4 8 12").split()]:
     lib.dconv_debug_mode(mode)
     ts = []
     for i in range(8):
@@ -32,3 +32,4 @@ for mode in (0, 4, 8, 12):
     ts.sort()
     print("mode", mode, "upd kernel us", round(ts[len(ts) // 2], 1))
 lib.dconv_debug_mode(0)
+print(up.blocking)
