@@ -44,6 +44,12 @@ for label, run in (("fwd", lambda: fp.execute(ib, wb, out)), ("bwd", lambda: bc.
     print(label, "CTA start us: min %.2f max %.2f | end us: min %.2f max %.2f | total kcyc max %.1f" % (
         starts.min().item(), starts.max().item(), ends.min().item(), ends.max().item(), per[:, 8].max().item() / 1e3),
         "epi bodies kcyc %.1f (tmem ld %.1f slab-wait %.1f fence %.1f tma %.1f)" % tuple(per[:, i].double().mean().item() / 1e3 for i in (11, 12, 13, 14, 15)))
+    if os.environ.get("ENDS"):
+        e = ends.tolist()
+        order = sorted(range(148), key=lambda i: e[i])
+        print(label, "fastest CTAs", [(i, round(e[i], 1)) for i in order[:8]])
+        print(label, "slowest CTAs", [(i, round(e[i], 1)) for i in order[-12:]])
+        print(label, "ends by CTA id (x10):", [round(sum(e[i:i + 10]) / len(e[i:i + 10]), 1) for i in range(0, 148, 10)])
     ex = buf[148 * 16 + 2048:148 * 16 + 2048 + 296].view(148, 2).double().mean(0) / 1e3
     mm = buf[148 * 16 + 2048 + 296:].view(148, 5).double().mean(0) / 1e3
     print(label, "MMA warp kcyc: wait %.1f misc %.1f fence %.1f issue %.1f commit %.1f" % tuple(mm.tolist()))

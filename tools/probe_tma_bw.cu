@@ -76,6 +76,37 @@ __global__ void reader(const __grid_constant__ CUtensorMap map, int ring, int bo
   (void)dummy;
 }
 
+// wide-row variant: box {W floats, rows, 4 planes}; tile = 128 pixels = 128*16/W rows
+__global__ void reader_wide(const __grid_constant__ CUtensorMap map, int ring, int rows, int n_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[16];
+  const uint32_t slot = 32768;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ring; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int tiles_per_img = (kHW + 127) / 128;
+  const int stages_per_tile = kCb / 4;
+  auto issue = [&](int g) {
+    const int t = blockIdx.x + (g / stages_per_tile) * gridDim.x;
+    const int it = g % stages_per_tile;
+    const int n = t / tiles_per_img, r0 = (t % tiles_per_img) * rows;
+    const int s = g % ring;
+    mbar_arrive_expect_tx(&full[s], slot);
+    tma_load_3d(smem + s * slot, &map, &full[s], 0, r0, n * kCb + it * 4);
+  };
+  const int my_tiles = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int total = my_tiles * stages_per_tile;
+  int issued = 0;
+  for (; issued < ring && issued < total; ++issued) issue(issued);
+  for (int done = 0; done < total; ++done) {
+    mbar_wait(&full[done % ring], (done / ring) & 1);
+    if (issued < total) issue(issued++);
+  }
+}
+
 typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -153,6 +184,34 @@ int main() {
       if (ms < best) best = ms;
     }
     printf("plain stores: %.1f us %.0f GB/s\n", best * 1e3, bytes / (best * 1e-3) / 1e9);
+  }
+  {
+    // same bytes per stage, but described with wide rows: a plane's pixels are
+    // contiguous, so {256 floats (16 px), hw/16, planes} boxes {W, 128*16/W, 4}
+    cudaFuncSetAttribute(reader_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int wide : {256, 128, 64, 32, 16}) {
+      CUtensorMap map;
+      cuuint64_t dims[3] = {(cuuint64_t)wide, (cuuint64_t)kHW * 16 / wide, (cuuint64_t)kPlanes};
+      cuuint64_t st[2] = {(cuuint64_t)wide * 4, (cuuint64_t)kHW * 64};
+      cuuint32_t box[3] = {(cuuint32_t)wide, (cuuint32_t)(128 * 16 / wide), 4}, es[3] = {1, 1, 1};
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, x, dims, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const int n_tiles = 32 * ((kHW + 127) / 128);
+      float best = 1e9;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(flush, rep, 256 << 20);
+        ldg_reader<<<148 * 8, 512>>>((const float4*)flush, (256 << 20) / 16, (float*)flush + 1);
+        cudaEventRecord(a);
+        reader_wide<<<148, 32, 3 * 32768>>>(map, 3, 128 * 16 / wide, n_tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      printf("wide rows %d B (enc %d) box {%d,%d,4} ring 3: %.1f us %.0f GB/s %s\n", wide * 4, (int)r, wide,
+             128 * 16 / wide, best * 1e3, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   const int shapes[][2] = {{128, 4}, {128, 2}};
   float* o2;
