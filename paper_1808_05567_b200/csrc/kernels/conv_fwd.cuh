@@ -509,7 +509,35 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           tc_fence_after();
           const uint32_t wst = smem0 + L.w_off + ws * L.w_slot;
           const int nt = min(p.w_taps, ntaps - t0);
-          if (elect_one()) {
+          if (TS && elect_one()) {
+            // single tap, one m-block: straight-line issue of the stage's kc x 6 (or kc)
+            // MMAs with precomputed operand addresses (the generic loop's index
+            // arithmetic cost ~50 cycles per MMA on the issuing thread)
+            const uint32_t w_pc = L.w_piece >> 4;  // descriptor start-address units (16 B)
+            const uint64_t bd0 = make_smem_desc(wst + static_cast<uint32_t>(w_kk0) * w_tap, 128, 256);
+            const uint32_t a0 = tmem_base + ring_col0 + static_cast<uint32_t>(s) * ring_slot;
+            const uint32_t d_hi = d_base, d_lo = d_base + static_cast<uint32_t>(NT);
+            const uint32_t d_x = two_acc ? d_lo : d_hi;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk >= kc_eff) break;
+              const uint64_t bk = bd0 + static_cast<uint64_t>((static_cast<uint32_t>(kk) * w_tap) >> 4);
+              const uint32_t ak = a0 + static_cast<uint32_t>(kk) * kRingCols;
+              const bool first = it == 0 && kk == 0;
+              if (p.dbg_mode & 8) continue;  // ablation: no MMAs
+              mma_bf16_ts(d_hi, ak, bk, idesc, first ? 0u : 1u);
+              if (PIECES == 3) {
+                mma_bf16_ts(d_x, ak, bk + w_pc, idesc, (two_acc && first) ? 0u : 1u);
+                mma_bf16_ts(d_x, ak + 8u, bk, idesc, 1u);
+                mma_bf16_ts(d_x, ak, bk + 2u * w_pc, idesc, 1u);
+                mma_bf16_ts(d_x, ak + 8u, bk + w_pc, idesc, 1u);
+                mma_bf16_ts(d_x, ak + 16u, bk, idesc, 1u);
+              }
+            }
+            if (!p.w_resident) mma_commit(&w_empty[ws]);
+            mma_commit(&pc_empty[s]);
+            if (it == k_iters - 1) mma_commit(&acc_full[acc]);
+          } else if (!TS && elect_one()) {
             for (int kk = 0; kk < kc_eff; ++kk)
             for (int tp = 0; tp < nt; ++tp) {
               const int shift = p.tap_shift[p.phase_tap0[ph] + t0 + tp];

@@ -46,3 +46,21 @@ for mode in modes:
     print(which, "mode", mode, "kernel us", round(ts[len(ts) // 2], 2), "min", round(ts[0], 2))
 lib.dconv_debug_mode(0)
 print(plan.blocking)
+if os.environ.get("PROBE"):
+    import ctypes as C
+    pl = C.CDLL(os.path.join(os.path.dirname(__file__), "probe_lib", "libprobe_reader.so"))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for ring, variant in ((3, 0), (3, 1), (3, 2)):
+        ts = []
+        for i in range(10):
+            flush.fill_(i)
+            flush.view(torch.int32).sum()
+            torch.cuda._sleep(2_000_000)
+            s.record()
+            pl.probe_read(C.c_void_p(x.data.data_ptr()), N, 16, 56 * 56, ring, 4, variant,
+                          C.c_void_p(torch.cuda.current_stream().cuda_stream))
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) * 1e3)
+        ts.sort()
+        print("probe reader on x, ring", ring, "variant", variant, "us", round(ts[len(ts) // 2], 2), "min", round(ts[0], 2))

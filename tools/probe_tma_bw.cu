@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include "../paper_1808_05567_b200/csrc/kernels/sm100_ptx.cuh"
 using namespace dconv_sm100;
@@ -44,8 +45,10 @@ __global__ void ldg_reader(const float4* __restrict__ x, size_t n, float* out) {
   if (acc == 12345.f) out[0] = acc;
 }
 
+__device__ long long g_trace[2 * 64];
 __global__ void reader(const __grid_constant__ CUtensorMap map, int ring, int box_px, int box_planes, int n_tiles,
                        int dummy) {
+  const long long t0 = clock64();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16];
   const uint32_t slot = box_px * box_planes * 64;
@@ -54,7 +57,7 @@ __global__ void reader(const __grid_constant__ CUtensorMap map, int ring, int bo
     fence_barrier_init();
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x == 0) {
   const int tiles_per_img = (kHW + box_px - 1) / box_px;
   const int stages_per_tile = kCb / box_planes;
   int issued = 0, done = 0;
@@ -65,14 +68,18 @@ __global__ void reader(const __grid_constant__ CUtensorMap map, int ring, int bo
     const int s = g % ring;
     mbar_arrive_expect_tx(&full[s], slot);
     tma_load_3d(smem + s * slot, &map, &full[s], 0, v0, n * kCb + it * box_planes);
+    if (blockIdx.x == 0 && g < 64) g_trace[2 * g] = clock64() - t0;
   };
   const int my_tiles = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int total = my_tiles * stages_per_tile;
   for (; issued < ring && issued < total; ++issued) issue(issued);
   for (; done < total; ++done) {
     mbar_wait(&full[done % ring], (done / ring) & 1);
+    if (blockIdx.x == 0 && done < 64) g_trace[2 * done + 1] = clock64() - t0;
     if (issued < total) issue(issued++);
   }
+  }
+  __syncthreads();  // the other warps of a 512-thread CTA idle here (FWD-kernel shape)
   (void)dummy;
 }
 
@@ -116,12 +123,21 @@ int main() {
   void* x;
   cudaMalloc(&x, bytes);
   cudaMemset(x, 0, bytes);
+  if (getenv("RANDOM_X")) {  // non-zero payload (rules out any zero-data shortcut)
+    std::vector<float> h(bytes / 4);
+    uint32_t st = 12345u;
+    for (auto& v : h) {
+      st = st * 1664525u + 1013904223u;
+      v = static_cast<float>(st >> 8) * (1.0f / 16777216.0f) - 0.5f;
+    }
+    cudaMemcpy(x, h.data(), bytes, cudaMemcpyHostToDevice);
+  }
   void* flush;
   cudaMalloc(&flush, 256 << 20);
   Enc enc;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
-  cudaFuncSetAttribute(reader, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(reader, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -213,14 +229,15 @@ int main() {
              128 * 16 / wide, best * 1e3, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
   }
-  const int shapes[][2] = {{128, 4}, {128, 2}};
+  const int shapes[][2] = {{128, 2}, {128, 4}};
   float* o2;
   cudaMalloc(&o2, 4);
-  for (int clean = 0; clean < 2; ++clean)
+  for (int big = 0; big < 2; ++big)
+  for (int clean = 1; clean < 2; ++clean)
   for (int ctas_per_sm : {1})
   for (auto& sh : shapes)
     for (int promo = 0; promo < 1; ++promo)
-      for (int ring : {3, 6}) {
+      for (int ring : {6, 3}) {
         const int box_px = sh[0], box_planes = sh[1];
         if ((size_t)ring * box_px * box_planes * 64 * ctas_per_sm > 200 * 1024) continue;
         CUtensorMap map;
@@ -236,7 +253,10 @@ int main() {
           cudaMemset(flush, rep, 256 << 20);
           if (clean) ldg_reader<<<148 * 8, 512>>>((const float4*)flush, (256 << 20) / 16, o2);
           cudaEventRecord(a);
-          reader<<<148 * ctas_per_sm, 32, ring * box_px * box_planes * 64>>>(map, ring, box_px, box_planes, n_tiles, 0);
+          if (big)
+            reader<<<148, 512, 208 * 1024>>>(map, ring, box_px, box_planes, n_tiles, 0);
+          else
+            reader<<<148 * ctas_per_sm, 32, ring * box_px * box_planes * 64>>>(map, ring, box_px, box_planes, n_tiles, 0);
           cudaEventRecord(b);
           cudaEventSynchronize(b);
           float ms;
@@ -244,10 +264,16 @@ int main() {
           if (ms < best) best = ms;
         }
         const cudaError_t e = cudaGetLastError();
-        printf("%s flush ctas/SM %d box {16,%d,%d} ring %d (%zu KB in flight): %.1f us  %.0f GB/s %s\n",
-               clean ? "write+read" : "write", ctas_per_sm, box_px, box_planes, ring,
+        printf("%s%s flush ctas/SM %d box {16,%d,%d} ring %d (%zu KB in flight): %.1f us  %.0f GB/s %s\n",
+               big ? "[512 thr, 208 KB] " : "", clean ? "write+read" : "write", ctas_per_sm, box_px, box_planes, ring,
                (size_t)ring * box_px * box_planes * 64 / 1024, best * 1e3, bytes / (best * 1e-3) / 1e9,
                e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
+  {
+    long long tr[128];
+    cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr));
+    printf("last reader run, CTA 0: stage issue -> landed (cycles)\n");
+    for (int i = 0; i < 24; ++i) printf("%d %lld %lld (lat %lld)\n", i, tr[2 * i], tr[2 * i + 1], tr[2 * i + 1] - tr[2 * i]);
+  }
   return 0;
 }
