@@ -1800,7 +1800,8 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
       cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
                  "smem attribute");
       if (!opened) prof_begin(2, cs), opened = true;
-      kern<<<L.grid, kUpdRawWarps * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages, L.pc_stages);
+      kern<<<L.grid, (L.tsa ? kUpdTsWarps : kUpdRawWarps) * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages,
+                                                                             L.pc_stages);
       cuda_check(cudaGetLastError(), "conv_upd_raw_kernel launch");
     };
     if (L.tsa) {

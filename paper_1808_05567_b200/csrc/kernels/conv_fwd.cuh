@@ -424,11 +424,18 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         for (int ks = 0; ks < kc_stages; ++ks) {
           const int cb0 = ks * p.kc, cb1 = min(p.cb_in, cb0 + p.kc);
           mbar_arrive_expect_tx(&w_full[ks], PIECES * (cb1 - cb0) * w_tap);
-          for (int cb = cb0; cb < cb1; ++cb)
+          if (p.n_ntiles == 1) {  // the stage's blocks are contiguous per piece: one copy each
             for (int pc = 0; pc < PIECES; ++pc)
-              bulk_load(dst + pc * L.w_piece + cb * w_tap,
-                        wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_tap, w_tap,
+              bulk_load(dst + pc * L.w_piece + cb0 * w_tap,
+                        wsrc + (static_cast<long long>(pc) * p.cb_in + cb0) * w_tap, (cb1 - cb0) * w_tap,
                         &w_full[ks]);
+          } else {
+            for (int cb = cb0; cb < cb1; ++cb)
+              for (int pc = 0; pc < PIECES; ++pc)
+                bulk_load(dst + pc * L.w_piece + cb * w_tap,
+                          wsrc + ((static_cast<long long>(pc) * p.cb_in + cb) * p.n_ntiles + ntile) * w_tap, w_tap,
+                          &w_full[ks]);
+          }
         }
       }
     } else if (lane == 0) {

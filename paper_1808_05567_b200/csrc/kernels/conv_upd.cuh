@@ -554,8 +554,13 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
 // from TMEM (K = pixels along columns) and only dO pieces go through smem.
 // Two converter groups of four warps (one per TMEM lane quarter) alternate
 // stages; within a stage the group also converts the dO chunk planes.
+// warps: w0 TMA producer, w1 MMA issuer, w4.. converter groups of four (w4..w7 then
+// run the epilogue); w2, w3 idle
+constexpr int kUpdTsCvtGroups = 2;  // (3 measured slower)
+constexpr int kUpdTsWarps = 4 + 4 * kUpdTsCvtGroups;
+
 template <int PIECES, bool CAT>
-__global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
+__global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
     conv_upd_ts_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
                        const __grid_constant__ UpdParams p, int raw_stages, int pc_stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -583,10 +588,13 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
   const uint32_t acc_w = static_cast<uint32_t>(kGroups * NT);
   const uint32_t a_cols = static_cast<uint32_t>(p.vs) / 2u;  // TMEM columns per piece per stage
   const uint32_t ring_slot = PIECES * a_cols;
-  // alternating converter groups: same ordering argument as conv_fwd_kernel's
-  // (measured: all eight warps on every stage is slower than alternating groups)
-  const int cvt_groups =
-      (raw_stages >= 2 && pc_stages >= 2 && (raw_stages % 2 == 0 || raw_stages >= pc_stages)) ? 2 : 1;
+  // converter groups take stages round-robin: same ordering argument as
+  // conv_fwd_kernel's (pc_stages >= groups keeps the piece-slot parity wait
+  // unambiguous); measured: all warps on every stage is slower than rotating groups
+  const int cvt_groups = (raw_stages >= 2 && pc_stages >= kUpdTsCvtGroups &&
+                          (raw_stages % kUpdTsCvtGroups == 0 || raw_stages >= pc_stages))
+                             ? kUpdTsCvtGroups
+                             : 1;
   const uint32_t cvt_arrivals = 4u;
 
   uint32_t tmem_cols = 32;
@@ -644,28 +652,27 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * pc_slot;
       const uint32_t a_t = tmem_base + acc_w + static_cast<uint32_t>(s) * ring_slot;
       if (elect_one()) {
-        for (int ks = 0; ks < ksteps; ++ks) {
+        // operand addresses advance by constants per k-step: no descriptor packing in the loop
+        const uint64_t b0 = make_smem_desc(st, 128, b_plane);
+        const uint64_t b_pc = b_piece >> 4;
+        const uint32_t id3 = make_idesc(1, 0, 1, 128, 3u * NT), id2 = make_idesc(1, 0, 1, 128, 2u * NT),
+                       id1 = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
+        for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
           const bool first = it == 0 && ks == 0;
-          auto atm = [&](int ia) { return a_t + static_cast<uint32_t>(ia) * a_cols + static_cast<uint32_t>(ks) * 8u; };
-          auto bdesc = [&](int ib) {
-            return make_smem_desc(st + static_cast<uint32_t>(ib) * b_piece + static_cast<uint32_t>(ks) * 256u, 128,
-                                  b_plane);
-          };
-          if (p.dbg_mode & 8) {
-            // ablation: no MMAs
-          } else if (CAT) {
-            mma_bf16_ts(tmem_base, atm(0), bdesc(0), make_idesc(1, 0, 1, 128, 3u * NT), first ? 0u : 1u);
-            mma_bf16_ts(tmem_base + NT, atm(1), bdesc(0), make_idesc(1, 0, 1, 128, 2u * NT), 1u);
-            mma_bf16_ts(tmem_base + 2 * NT, atm(2), bdesc(0), make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT)),
-                        1u);
+          const uint32_t ak = a_t + static_cast<uint32_t>(ks) * 8u;
+          const uint64_t bk = b0 + static_cast<uint64_t>(ks) * 16u;  // 256 B per k-step
+          if (CAT) {
+            mma_bf16_ts(tmem_base, ak, bk, id3, first ? 0u : 1u);
+            mma_bf16_ts(tmem_base + NT, ak + a_cols, bk, id2, 1u);
+            mma_bf16_ts(tmem_base + 2 * NT, ak + 2u * a_cols, bk, id1, 1u);
           } else {
-            const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
 #pragma unroll
             for (int ia = 0; ia < PIECES; ++ia)
 #pragma unroll
               for (int ib = 0; ib < PIECES; ++ib) {
                 if (ia + ib > 2) continue;
-                mma_bf16_ts(tmem_base, atm(ia), bdesc(ib), idesc, (first && ia == 0 && ib == 0) ? 0u : 1u);
+                mma_bf16_ts(tmem_base, ak + static_cast<uint32_t>(ia) * a_cols, bk + static_cast<uint64_t>(ib) * b_pc,
+                            id1, (first && ia == 0 && ib == 0) ? 0u : 1u);
               }
           }
         }
