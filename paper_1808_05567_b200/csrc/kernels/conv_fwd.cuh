@@ -254,6 +254,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   __shared__ __align__(8) uint64_t w_full[kMaxStages], w_empty[kMaxStages];
   __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
+  // per-phase / per-tap tables copied out of the parameter block (the hot loops
+  // index them dynamically; shared memory keeps those reads off the constant cache)
+  __shared__ int s_phase_row[kMaxPhases], s_phase_col[kMaxPhases], s_phase_ntaps[kMaxPhases],
+      s_phase_tap0[kMaxPhases], s_tap_shift[kMaxTaps];
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -320,6 +324,15 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     }
     fence_barrier_init();
   }
+  if (warp == 3) {
+    for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
+    if (lane < kMaxPhases) {
+      s_phase_row[lane] = p.phase_row[lane];
+      s_phase_col[lane] = p.phase_col[lane];
+      s_phase_ntaps[lane] = p.phase_ntaps[lane];
+      s_phase_tap0[lane] = p.phase_tap0[lane];
+    }
+  }
   if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
   tc_fence_before();
   __syncthreads();
@@ -379,8 +392,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               for (int i = 0; i < p.lin_boxes; ++i)
                 tma_load_3d(dst + i * 128 * 64, &map_a, &raw_full[s], 0, a_px0 + i * 128, plane);
             } else {
-              tma_load_4d(dst, &map_a, &raw_full[s], 0, p.in_col0 + p.phase_col[ph],
-                          p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
+              tma_load_4d(dst, &map_a, &raw_full[s], 0, p.in_col0 + s_phase_col[ph],
+                          p.in_row0 + p.stride * row0 + s_phase_row[ph], plane);
             }
           } else {
             const int s = rp.idx;
@@ -398,8 +411,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                 for (int i = 0; i < p.lin_boxes; ++i)
                   tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, a_px0 + i * 128, plane);
             } else {
-              tma_load_4d(dst, &map_a, &pc_full[s], 0, p.in_col0 + p.phase_col[ph],
-                          p.in_row0 + p.stride * row0 + p.phase_row[ph], plane);
+              tma_load_4d(dst, &map_a, &pc_full[s], 0, p.in_col0 + s_phase_col[ph],
+                          p.in_row0 + p.stride * row0 + s_phase_row[ph], plane);
             }
           }
         }
@@ -453,8 +466,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             ++cb;
           }
           const int kc_eff = min(p.kc, p.cb_in - cb * p.kc);
-          for (int t0 = 0; t0 < p.phase_ntaps[ph]; t0 += p.w_taps, ++g, wp.adv(w_stages)) {
-            const int nt = min(p.w_taps, p.phase_ntaps[ph] - t0);
+          for (int t0 = 0; t0 < s_phase_ntaps[ph]; t0 += p.w_taps, ++g, wp.adv(w_stages)) {
+            const int nt = min(p.w_taps, s_phase_ntaps[ph] - t0);
             const int s = wp.idx;
             mbar_wait(&w_empty[s], wp.ph ^ 1u);
             if (p.dbg && blockIdx.x == 0 && g < 256) p.dbg[gridDim.x * 16 + g * 8 + 7] = clock64() - t_start;
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               for (int pc = 0; pc < PIECES; ++pc)
                 bulk_load(dst + pc * L.w_piece + kk * w_bytes,
                           wsrc + ((static_cast<long long>(pc) * p.cb_in + cb * p.kc + kk) * p.n_ntiles + ntile) * w_blk +
-                              static_cast<long long>(p.phase_tap0[ph] + t0) * w_tap,
+                              static_cast<long long>(s_phase_tap0[ph] + t0) * w_tap,
                           w_bytes, &w_full[s]);
           }
         }
@@ -501,7 +514,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           mbar_wait_t(&pc_full[s], par, dbg ? &c_a : nullptr);
         if (trace && lane == 0) trace[0] = clock64() - t_start;
         const uint32_t st = smem0 + s * L.pc_slot;
-        const int ntaps = p.phase_ntaps[ph];
+        const int ntaps = s_phase_ntaps[ph];
         const int kc_eff = min(p.kc, p.cb_in - cbi * p.kc);
         const int w_kk0 = p.w_resident ? cbi * p.kc : 0;  // resident slice: channel block index
         for (int t0 = 0; t0 < ntaps; t0 += p.w_taps, wpp.adv(w_stages)) {
@@ -545,41 +558,36 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             mma_commit(&pc_empty[s]);
             if (it == k_iters - 1) mma_commit(&acc_full[acc]);
           } else if (!TS && elect_one()) {
+            // operand descriptors are packed once per stage; per MMA only the 16 B-unit
+            // start-address field advances (no repacking, no parameter reads)
+            const uint64_t a_base = RAW_F32 ? make_smem_desc(st, L.a_plane, 128) : make_smem_desc_sw32(st);
+            const uint64_t b_base = make_smem_desc(wst, 128, 256);
+            const uint32_t a_pc = RAW_F32 ? (2u * L.a_plane) >> 4 : 0u, w_pc = L.w_piece >> 4;
+            const int tap0 = s_phase_tap0[ph] + t0;
             for (int kk = 0; kk < kc_eff; ++kk)
-            for (int tp = 0; tp < nt; ++tp) {
-              const int shift = p.tap_shift[p.phase_tap0[ph] + t0 + tp];
-              for (int mb = 0; mb < p.mb; ++mb) {
-                const uint32_t a_off = static_cast<uint32_t>(v_off + mb * 128 + shift) * 16u;
-                const uint32_t d_hi = d_base + static_cast<uint32_t>(mb * NT);
-                const uint32_t d_lo = d_hi + static_cast<uint32_t>(p.mb * NT);
-                const bool first = it == 0 && t0 == 0 && tp == 0 && kk == 0;
-#pragma unroll
-                for (int pr = 0; pr < (PIECES == 3 ? 6 : 1); ++pr) {
-                  // products (ia, ib) with ia + ib <= 2
-                  const int ia = pr == 2 ? 1 : pr == 4 ? 1 : pr == 5 ? 2 : 0;
-                  const int ib = pr == 1 ? 1 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
-                  const uint64_t bd =
-                      make_smem_desc(wst + ib * L.w_piece + ((w_kk0 + kk) * nt + tp) * w_tap, 128, 256);
-                  const uint32_t acc_in = pr == 0 ? (first ? 0u : 1u)
-                                                  : ((two_acc && first && pr == 1) ? 0u : 1u);
-                  const uint32_t d_t = (pr == 0 || !two_acc) ? d_hi : d_lo;
-                  if (p.dbg_mode & 8) {
-                    // ablation: no MMAs
-                  } else if (TS) {
-                    mma_bf16_ts(d_t,
-                                tmem_base + ring_col0 + static_cast<uint32_t>(s) * ring_slot +
-                                    static_cast<uint32_t>(kk) * kRingCols + ia * 8u,
-                                bd, idesc, acc_in);
-                  } else {
-                    const uint64_t ad =
-                        RAW_F32
-                            ? make_smem_desc(st + static_cast<uint32_t>(ia) * 2u * L.a_plane + a_off, L.a_plane, 128)
-                            : make_smem_desc_sw32(st + static_cast<uint32_t>(kk * p.a_px + v_off + mb * 128 + shift) * 32u);
-                    mma_bf16(d_t, ad, bd, idesc, acc_in);
+              for (int tp = 0; tp < nt; ++tp) {
+                const int shift = s_tap_shift[tap0 + tp];
+                const uint32_t b_off = ((static_cast<uint32_t>(w_kk0 + kk) * nt + tp) * w_tap) >> 4;
+                for (int mb = 0; mb < p.mb; ++mb) {
+                  const uint32_t rows = static_cast<uint32_t>(v_off + mb * 128 + shift);
+                  // MN-major pieces: 16 B per pixel row; SW32 K-major bf16: 32 B per pixel row
+                  const uint32_t a_off = RAW_F32 ? rows : 2u * (static_cast<uint32_t>(kk * p.a_px) + rows);
+                  const uint32_t d_hi = d_base + static_cast<uint32_t>(mb * NT);
+                  const uint32_t d_lo = d_hi + static_cast<uint32_t>(p.mb * NT);
+                  const uint32_t d_x = two_acc ? d_lo : d_hi;
+                  const bool first = it == 0 && t0 == 0 && tp == 0 && kk == 0;
+                  const uint64_t ad = a_base + a_off, bd = b_base + b_off;
+                  if (p.dbg_mode & 8) continue;  // ablation: no MMAs
+                  mma_bf16(d_hi, ad, bd, idesc, first ? 0u : 1u);
+                  if (PIECES == 3) {  // products (ia, ib) with ia + ib <= 2
+                    mma_bf16(d_x, ad, bd + w_pc, idesc, (two_acc && first) ? 0u : 1u);
+                    mma_bf16(d_x, ad + a_pc, bd, idesc, 1u);
+                    mma_bf16(d_x, ad, bd + 2u * w_pc, idesc, 1u);
+                    mma_bf16(d_x, ad + a_pc, bd + w_pc, idesc, 1u);
+                    mma_bf16(d_x, ad + 2u * a_pc, bd, idesc, 1u);
                   }
                 }
               }
-            }
             if (!p.w_resident) mma_commit(&w_empty[ws]);
             if (t0 + p.w_taps >= ntaps) {
               mma_commit(&pc_empty[s]);
