@@ -57,9 +57,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t accum_bar;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int s_tap_shift[kMaxTaps];  // off the constant cache in the issue loop
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (warp == 2)
+    for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
   const int NT = 16 * p.nb;
   const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB);
   const uint32_t smem0 = smem_u32(smem);
@@ -149,23 +152,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t st = smem0 + static_cast<uint32_t>(s) * L.bytes;
       if (elect_one()) {
         const int n_acc = p.stack > 1 ? 1 : ntaps;  // stacked: one accumulator holds all the group's taps
+        // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels.
+        // Descriptors are packed once per stage; per MMA only the start address (16 B units) advances.
+        const uint64_t a0 = make_smem_desc(st, 128, L.a_plane);
+        const uint64_t b0 = make_smem_desc(st + L.b_off, 128, L.b_plane);
+        const uint32_t a_pc = L.a_piece >> 4, b_pc = L.b_piece >> 4;
         for (int t = 0; t < n_acc; ++t) {
-          const int shift = p.stack > 1 ? 0 : p.tap_shift[tap0 + t];
+          const int shift = p.stack > 1 ? 0 : s_tap_shift[tap0 + t];
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * NT);
           for (int ks = 0; ks < ksteps; ++ks) {
+            const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift);  // 16 B per pixel row
+            const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u;          // 256 B per k-step
 #pragma unroll
             for (int ia = 0; ia < PA; ++ia) {
 #pragma unroll
               for (int ib = 0; ib < PB; ++ib) {
                 if (a_base + ia + ib > 2) continue;
-                // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels
-                const uint64_t ad = make_smem_desc(
-                    st + static_cast<uint32_t>(ia) * L.a_piece + static_cast<uint32_t>(ks * 16 + shift) * 16u, 128,
-                    L.a_plane);
-                const uint64_t bd = make_smem_desc(
-                    st + L.b_off + static_cast<uint32_t>(ib) * L.b_piece + static_cast<uint32_t>(ks) * 256u, 128,
-                    L.b_plane);
-                mma_bf16(d_tmem, ad, bd, idesc, (it > 0 || ks > 0 || ia > 0 || ib > 0) ? 1u : 0u);
+                mma_bf16(d_tmem, ak + static_cast<uint32_t>(ia) * a_pc, bk + static_cast<uint32_t>(ib) * b_pc, idesc,
+                         (it > 0 || ks > 0 || ia > 0 || ib > 0) ? 1u : 0u);
               }
             }
           }
@@ -278,9 +282,12 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
   __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_empty[kMaxStages];
   __shared__ __align__(8) uint64_t accum_bar;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int s_tap_shift[kMaxTaps];  // off the constant cache in the issue loop
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (warp == 2)
+    for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
   const int NT = 16 * p.nb;
   const int ctile = blockIdx.x / p.n_tgroups;
   const int tgrp = blockIdx.x % p.n_tgroups;
@@ -369,38 +376,32 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * R.pc_slot;
       if (elect_one()) {
         const int n_acc = stacked ? 1 : ntaps;
+        // descriptors packed once per stage; per MMA only the 16 B-unit start address advances
+        const uint64_t a0 = make_smem_desc(st, 128, S.a_plane);
+        const uint64_t b0 = make_smem_desc(st + S.b_off, 128, S.b_plane);
+        const uint32_t a_pc = S.a_piece >> 4, b_pc = S.b_piece >> 4;
+        const uint32_t id3 = make_idesc(1, 1, 1, 128, 3u * NT), id2 = make_idesc(1, 1, 1, 128, 2u * NT),
+                       id1 = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
         for (int t = 0; t < n_acc; ++t) {
-          const int shift = stacked ? 0 : p.tap_shift[tap0 + t];
+          const int shift = stacked ? 0 : s_tap_shift[tap0 + t];
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * acc_w);
-          for (int ks = 0; ks < ksteps; ++ks) {
+          for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
             const bool first = it == 0 && ks == 0;
-            // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels
-            auto adesc = [&](int ia) {
-              return make_smem_desc(st + static_cast<uint32_t>(ia) * S.a_piece +
-                                        static_cast<uint32_t>(ks * 16 + shift) * 16u,
-                                    128, S.a_plane);
-            };
-            auto bdesc = [&](int ib) {
-              return make_smem_desc(st + S.b_off + static_cast<uint32_t>(ib) * S.b_piece +
-                                        static_cast<uint32_t>(ks) * 256u,
-                                    128, S.b_plane);
-            };
-            if (p.dbg_mode & 8) {
-              // ablation: no MMAs
-            } else if (CAT) {
+            const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift);  // 16 B per pixel row
+            const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u;          // 256 B per k-step
+            if (CAT) {
               // X|Y|Z += a0 [b0|b1|b2];  Y|Z += a1 [b0|b1];  Z += a2 b0
-              mma_bf16(d_tmem, adesc(0), bdesc(0), make_idesc(1, 1, 1, 128, 3u * NT), first ? 0u : 1u);
-              mma_bf16(d_tmem + NT, adesc(1), bdesc(0), make_idesc(1, 1, 1, 128, 2u * NT), 1u);
-              mma_bf16(d_tmem + 2 * NT, adesc(2), bdesc(0), make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT)),
-                       1u);
+              mma_bf16(d_tmem, ak, bk, id3, first ? 0u : 1u);
+              mma_bf16(d_tmem + NT, ak + a_pc, bk, id2, 1u);
+              mma_bf16(d_tmem + 2 * NT, ak + 2u * a_pc, bk, id1, 1u);
             } else {
-              const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
 #pragma unroll
               for (int ia = 0; ia < PIECES; ++ia)
 #pragma unroll
                 for (int ib = 0; ib < PIECES; ++ib) {
                   if (ia + ib > 2) continue;
-                  mma_bf16(d_tmem, adesc(ia), bdesc(ib), idesc, (first && ia == 0 && ib == 0) ? 0u : 1u);
+                  mma_bf16(d_tmem, ak + static_cast<uint32_t>(ia) * a_pc, bk + static_cast<uint32_t>(ib) * b_pc, id1,
+                           (first && ia == 0 && ib == 0) ? 0u : 1u);
                 }
             }
           }
