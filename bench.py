@@ -377,8 +377,9 @@ def run_ours(args):
     dom = max(avg, key=avg.get) if avg else "fwd"
     achieved = byts[dom] / (avg.get(dom, float("nan")) * 1e-3) / 1e9
     traffic = ncu_traffic(dom) if math == d.Math.F32 else None
+    upd_kernel = "conv_upd_ts_kernel" if uplan.blocking.get("a_in_tmem") else "conv_upd_raw_kernel"
     roofline = {"bound": "hbm", "kernel": {"fwd": "conv_fwd_kernel", "bwd": "conv_fwd_kernel (dual)",
-                                           "upd": "conv_upd_raw_kernel"}[dom],
+                                           "upd": upd_kernel}[dom],
                 "pass": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "traffic_source": "profiles/r01_ncu_full_cfg2.json (dram read+write bytes of one ncu --set full launch)"

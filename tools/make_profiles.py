@@ -46,7 +46,7 @@ def full(path, out):
             "launch__block_size", "lts__t_sector_hit_rate.pct", "sm__issue_active.avg.pct_of_peak_sustained_elapsed"]
     ks = []
     roles = ["fwd (conv_fwd_kernel<1,3,1>: A pieces in TMEM)", "bwd (same kernel on the dual problem)",
-             "upd (conv_upd_raw_kernel<3,1>)"]
+             "upd (conv_upd_ts_kernel<3,1>: activations in TMEM)"]
     for v, role in zip(r, roles):
         d = dict(zip(h, v))
         e = {"Kernel Name": d["Kernel Name"].split("(")[0], "pass": role}
