@@ -241,6 +241,7 @@ struct FwdLaunch {
   bool raw_f32;
   int pieces;
   bool ts = false;  // A pieces staged in tensor memory (single-tap fp32 problems)
+  size_t raw_slot = 0;  // bytes per raw-ring slot
 };
 
 // Decide staging mode, tile and pipeline depth; encode TMA maps.
@@ -483,6 +484,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   L.raw_stages = raw_st;
   L.w_stages = w_st;
   L.smem = static_cast<size_t>(layout.raw_off) + static_cast<size_t>(raw_st) * layout.raw_slot + kEpiStageBytes;
+  L.raw_slot = layout.raw_slot;
   const int n_tiles = (p.mimg > 0 ? cdiv(in.n, p.mimg) : in.n * p.tiles_per_img) * cdiv(kb_total, tile.nb);
   L.grid = dim3(static_cast<unsigned>(std::min(n_tiles, sm_count())), 1, 1);
 
@@ -536,7 +538,19 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
   const int esz = p.out_bf16 ? 2 : 4;
   // 4 warps x 2 slabs of {16 lanes, 32 px, 2 blocks} per epilogue group; bf16
   // smem-staged plans run three groups
-  const size_t staging = static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
+  // TS plans with one stage per tile: a second epilogue group (the stores dominate)
+  const int kiters = cdiv(p.cb_in, p.kc) * p.n_phases;
+  p.ts_epi2 = (L.ts && kiters == 1 && p.nb >= 4 && !getenv("DCONV_NO_TS_EPI2")) ? 1 : 0;
+  auto staging_bytes = [&] {
+    return static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : p.ts_epi2 ? 2 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
+  };
+  // its staging comes out of the raw ring when needed (these plans load 1/4 of what they store)
+  while (p.ts_epi2 && L.smem + staging_bytes() > static_cast<size_t>(kSmemBudget) && L.raw_stages > 3) {
+    --L.raw_stages;
+    L.smem -= L.raw_slot;
+  }
+  if (L.smem + staging_bytes() > static_cast<size_t>(kSmemBudget)) p.ts_epi2 = 0;
+  const size_t staging = staging_bytes();
   size_t smem = L.smem;
   p.tma_store = 0;
   CUtensorMap map_out, map_out2;
@@ -621,11 +635,13 @@ std::string json_tile(const FwdLaunch& L) {
   std::snprintf(buf, sizeof(buf),
                 "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
                 "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d,"
-                "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d,\"split_acc\":%d}",
+                "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d,\"split_acc\":%d,"
+                "\"epi_groups\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
                 L.grid.x,
                 (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
-                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store, L.p.split_acc);
+                L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store, L.p.split_acc,
+                (!L.raw_f32 && !L.ts && L.p.tma_store) ? 3 : (L.p.ts_epi2 && L.p.tma_store) ? 2 : 1);
   return buf;
 }
 

@@ -286,14 +286,17 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   // so the raw_full parity wait for g cannot be satisfied by the fill of
   // g - 2 raw_stages (TMA fills may land out of order) as long as the slot's
   // previous fill is ours (raw_stages even) or <= g - pc_stages.
+  // TS plans whose tiles are one stage (output-heavy, e.g. the dual BWD of a
+  // channel-expanding 1x1) give the second converter group to the epilogue
+  const bool ts_epi2 = TS && p.tma_store && p.ts_epi2;
   const int cvt_groups =
-      (raw_stages >= 2 && pc_stages >= 2 && (raw_stages % 2 == 0 || raw_stages >= pc_stages)) ? 2 : 1;
+      (!ts_epi2 && raw_stages >= 2 && pc_stages >= 2 && (raw_stages % 2 == 0 || raw_stages >= pc_stages)) ? 2 : 1;
   const int cvt_group_warps = TS ? 4 : kCvtWarps / cvt_groups;
   // bf16 smem-staged plans have idle converter warps: with the lean TMA-store
   // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
   // doubling the loads in flight for fused residual adds / ReLU masks
   const bool epi2 = !RAW_F32 && !TS && p.tma_store;
-  const int n_epi_groups = epi2 ? 3 : 1;  // bf16: warps 4..7, 8..11, 12..15
+  const int n_epi_groups = epi2 ? 3 : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
   constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
@@ -603,7 +606,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       dbg[4] = c_a;
       dbg[5] = c_b;
     }
-  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) || (epi2 && warp >= kCvtWarp0))) {
+  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) || (epi2 && warp >= kCvtWarp0) ||
+                             (ts_epi2 && warp >= kCvtWarp0 + 4))) {
     // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
     // two output blocks per step: one 32-column TMEM load per accumulator, one
     // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     const uint32_t esz = p.out_bf16 ? 2u : 4u;
     const uint32_t slot_bytes = 2u * 32u * 16u * esz;
     const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
-    const int eg = (warp - kEpiWarp0) / 4, n_eg = n_epi_groups;  // epilogue group
+    const int eg = ts_epi2 ? (warp >= kCvtWarp0 ? 1 : 0) : (warp - kEpiWarp0) / 4, n_eg = n_epi_groups;
     uint8_t* stg0 = smem + L.epi_off + (eg * 4 + warp % 4) * 2u * slot_bytes;
     // FUSED = residual add / ReLU-backward mask present: the plain variant has no
     // per-pixel addressing or extra loads in its loop (smaller, faster code)

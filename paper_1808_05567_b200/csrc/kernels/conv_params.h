@@ -45,6 +45,7 @@ struct FwdParams {
   int tma_store;       // 1: epilogue stages 32-pixel slabs in smem and TMA-stores them (dense outputs)
   int out_fill;        // 1: stride-2 lattice output that also writes the zero pixels it owns
   int split_acc;       // fp32-accurate: 1 = hi*hi and corrections in separate accumulators (long reductions)
+  int ts_epi2;         // TS plans with one stage per tile: warps 12..15 are a second epilogue group
   int fill_h_end, fill_w_end;  // interior row / column ends (padded coordinates) for out_fill
   int n_taps;          // total taps (phase-sorted) in the prepared weights
   int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
