@@ -393,7 +393,8 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         }
         // weight stage <= 32 KB
         int wt = taps.taps_box;
-        while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > 32 * 1024)
+        const int w_cap = getenv("DCONV_WCAP") ? atoi(getenv("DCONV_WCAP")) * 1024 : 32 * 1024;  // debug sweep
+        while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > w_cap)
           wt = (wt + 1) / 2;
         const FwdSmem lay = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1);
         int pcs, rws = 0, wss;
@@ -440,6 +441,12 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
               kc = kcx;
               break;
             }
+          }
+          if (const char* e = getenv("DCONV_WST")) {  // debug: weight-ring depth sweep
+            const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
+            wss = atoi(e);
+            pcs = std::min<int>(kMaxStages, (kFwdBudget - 3 * 16384 - wss * static_cast<int>(lk.w_slot)) /
+                                                static_cast<int>(lk.pc_slot));
           }
           if (pcs < want_pc) continue;
           if (kc > 1 && linear && !mimg_ok) lb = 1;  // one box of Lpx pixels x kc blocks
@@ -541,6 +548,7 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
   // TS plans with one stage per tile: a second epilogue group (the stores dominate)
   const int kiters = cdiv(p.cb_in, p.kc) * p.n_phases;
   p.ts_epi2 = (L.ts && kiters == 1 && p.nb >= 4 && !getenv("DCONV_NO_TS_EPI2")) ? 1 : 0;
+  p.epi_groups = getenv("DCONV_EPI_GROUPS") ? atoi(getenv("DCONV_EPI_GROUPS")) : 3;
   auto staging_bytes = [&] {
     return static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : p.ts_epi2 ? 2 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
   };
@@ -1632,6 +1640,28 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   auto act_map = [&](const dconv_act_t& a, const void* data, int chans_blocks, bool is_in) {
     const int hp = a.h + 2 * a.halo_h, wp = a.w + 2 * a.halo_w;
     const uint64_t planes = static_cast<uint64_t>(is_in ? pieces : pieces) * a.n * chans_blocks;
+    if (p.sw32) {  // bf16 tensors in place: 32 B pixel rows, SWIZZLE_32B (MN-major SW32 operands)
+      const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_32B;
+      if (linear) {
+        const uint64_t dims[3] = {16, static_cast<uint64_t>(a.h) * a.w, planes};
+        const uint64_t strides[2] = {32, static_cast<uint64_t>(a.h) * a.w * 32};
+        const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs), static_cast<uint32_t>(is_in ? 8 : p.nb)};
+        return encode(1, 3, data, dims, strides, box, nullptr, is_in ? "upd input linear sw32" : "upd dO linear sw32",
+                      swz);
+      }
+      const char* base = reinterpret_cast<const char*>(data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 32;
+      const uint64_t dims[4] = {16, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), planes};
+      const uint64_t strides3[3] = {32, static_cast<uint64_t>(wp) * 32, static_cast<uint64_t>(wp) * hp * 32};
+      if (is_in) {
+        const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st),
+                                 static_cast<uint32_t>(p.cb_eff)};
+        const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
+        return encode(1, 4, base, dims, strides3, box, estr, "upd input rows sw32", swz);
+      }
+      const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps),
+                               static_cast<uint32_t>(p.nb)};
+      return encode(1, 4, base, dims, strides3, box, nullptr, "upd dO rows sw32", swz);
+    }
     if (linear) {
       const uint64_t dims[4] = {8, static_cast<uint64_t>(a.h) * a.w, 2, planes};
       const uint64_t strides[3] = {32, 16, static_cast<uint64_t>(a.h) * a.w * 32};
@@ -1679,6 +1709,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     L.map_do = raw_map(dout, false);
     return L;
   }
+  p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !getenv("DCONV_UPD_NO_SW32")) ? 1 : 0;
   L.map_in = act_map(in, in_pieces, cb, true);
   L.map_do = act_map(dout, do_pieces, kb, false);
   return L;

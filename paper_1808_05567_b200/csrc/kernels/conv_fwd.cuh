@@ -38,6 +38,7 @@ namespace dconv_sm100 {
 
 constexpr int kFwdThreads = 256;
 constexpr int kMaxStages = 8;
+constexpr int kFastTaps = 16;  // taps per weight stage issued by the unrolled MMA path
 constexpr int kConvWarp0 = 2;
 constexpr int kConvThreads = 192;  // warps 2..7
 
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
   // doubling the loads in flight for fused residual adds / ReLU masks
   const bool epi2 = !RAW_F32 && !TS && p.tma_store;
-  const int n_epi_groups = epi2 ? 3 : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
+  const int n_epi_groups = epi2 ? max(1, min(3, p.epi_groups)) : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
   constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
@@ -402,6 +403,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             const int s = rp.idx;
             mbar_wait_t(&pc_empty[s], rp.ph ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
+            if (p.dbg_mode & 256) {  // ablation: no activation loads
+              mbar_arrive(&pc_full[s]);
+              continue;
+            }
             mbar_arrive_expect_tx(&pc_full[s], a_bytes);
             // bf16 pixels as SWIZZLE_32B rows: the MMA reads them in place
             if (p.mimg > 0) {
@@ -475,6 +480,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             mbar_wait(&w_empty[s], wp.ph ^ 1u);
             if (p.dbg && blockIdx.x == 0 && g < 256) p.dbg[gridDim.x * 16 + g * 8 + 7] = clock64() - t_start;
             const uint32_t w_bytes = static_cast<uint32_t>(nt) * w_tap;
+            if (p.dbg_mode & 128) {  // ablation: no weight loads
+              mbar_arrive(&w_full[s]);
+              continue;
+            }
             mbar_arrive_expect_tx(&w_full[s], PIECES * kc_eff * w_bytes);
             uint8_t* dst = smem + L.w_off + s * L.w_slot;
             // slot layout [piece][kk][tap]: piece stride w_piece = kc * w_taps taps
@@ -560,7 +569,46 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             if (!p.w_resident) mma_commit(&w_empty[ws]);
             mma_commit(&pc_empty[s]);
             if (it == k_iters - 1) mma_commit(&acc_full[acc]);
-          } else if (!TS && elect_one()) {
+          } else if (!TS && PIECES == 1 && nt <= kFastTaps && p.mb <= 2 && elect_one()) {
+            // single-piece multi-tap stage, fully unrolled: the stage's tap shifts are
+            // read into registers with independent loads, then every MMA is one
+            // address add away (the generic loop below serialises a shared-memory
+            // load and its index arithmetic per tap: ~125 cycles per MMA, 2x the
+            // tensor time of a 128x128x16 MMA)
+            const uint64_t a_base = RAW_F32 ? make_smem_desc(st, L.a_plane, 128) : make_smem_desc_sw32(st);
+            const uint64_t b_base = make_smem_desc(wst, 128, 256);
+            const int tap0 = s_phase_tap0[ph] + t0;
+            constexpr uint32_t kRow = RAW_F32 ? 1u : 2u;  // descriptor units (16 B) per pixel row
+            uint32_t sh[kFastTaps];
+#pragma unroll
+            for (int i = 0; i < kFastTaps; ++i) sh[i] = i < nt ? kRow * static_cast<uint32_t>(s_tap_shift[tap0 + i]) : 0u;
+            const uint32_t b_tap = w_tap >> 4;
+            const bool do_mma = !(p.dbg_mode & 8);  // ablation: no MMAs
+            for (int kk = 0; kk < kc_eff; ++kk) {
+              const uint64_t ak = a_base + (RAW_F32 ? static_cast<uint32_t>(v_off)
+                                                    : 2u * static_cast<uint32_t>(kk * p.a_px + v_off));
+              const uint64_t bk = b_base + ((static_cast<uint32_t>(w_kk0 + kk) * nt * w_tap) >> 4);
+              const bool first_k = it == 0 && t0 == 0 && kk == 0;
+#pragma unroll
+              for (int tp = 0; tp < kFastTaps; ++tp) {
+                if (tp >= nt) break;
+#pragma unroll
+                for (int mb = 0; mb < 2; ++mb) {
+                  if (mb >= p.mb) break;
+                  if (do_mma)
+                    mma_bf16(d_base + static_cast<uint32_t>(mb * NT), ak + (sh[tp] + kRow * 128u * mb),
+                             bk + static_cast<uint32_t>(tp) * b_tap, idesc, (first_k && tp == 0) ? 0u : 1u);
+                }
+              }
+            }
+            if (trace) trace[3] = clock64() - t_start;
+            if (!p.w_resident) mma_commit(&w_empty[ws]);
+            if (trace) trace[4] = clock64() - t_start;
+            if (t0 + p.w_taps >= ntaps) {
+              mma_commit(&pc_empty[s]);
+              if (it == k_iters - 1) mma_commit(&acc_full[acc]);
+            }
+          } else if (!TS && !(PIECES == 1 && nt <= kFastTaps && p.mb <= 2) && elect_one()) {
             // operand descriptors are packed once per stage; per MMA only the 16 B-unit
             // start-address field advances (no repacking, no parameter reads)
             const uint64_t a_base = RAW_F32 ? make_smem_desc(st, L.a_plane, 128) : make_smem_desc_sw32(st);
@@ -591,7 +639,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                   }
                 }
               }
+            if (trace) trace[3] = clock64() - t_start;
             if (!p.w_resident) mma_commit(&w_empty[ws]);
+            if (trace) trace[4] = clock64() - t_start;
             if (t0 + p.w_taps >= ntaps) {
               mma_commit(&pc_empty[s]);
               if (it == k_iters - 1) mma_commit(&acc_full[acc]);
@@ -606,7 +656,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       dbg[4] = c_a;
       dbg[5] = c_b;
     }
-  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) || (epi2 && warp >= kCvtWarp0) ||
+  } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) ||
+                             (epi2 && warp >= kCvtWarp0 && warp < kEpiWarp0 + 4 * n_epi_groups) ||
                              (ts_epi2 && warp >= kCvtWarp0 + 4))) {
     // ------------------------------------------------------------ lean TMA-store epilogue (warps 4..7)
     // two output blocks per step: one 32-column TMEM load per accumulator, one

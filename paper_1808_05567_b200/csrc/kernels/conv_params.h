@@ -46,6 +46,7 @@ struct FwdParams {
   int out_fill;        // 1: stride-2 lattice output that also writes the zero pixels it owns
   int split_acc;       // fp32-accurate: 1 = hi*hi and corrections in separate accumulators (long reductions)
   int ts_epi2;         // TS plans with one stage per tile: warps 12..15 are a second epilogue group
+  int epi_groups;      // bf16 smem-staged plans with the lean epilogue: epilogue warp groups (1..3)
   int fill_h_end, fill_w_end;  // interior row / column ends (padded coordinates) for out_fill
   int n_taps;          // total taps (phase-sorted) in the prepared weights
   int n_ntiles;        // output-channel tiles (prepared weights are tiled by nb)
@@ -101,6 +102,7 @@ struct UpdParams {
   int stack;               // 1 = shared-tile mode (taps via descriptor shifts)
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
+  int sw32;                // bf16 operands staged as SWIZZLE_32B 32 B pixel rows (MN-major SW32 descriptors)
   int tap_ph[kMaxTaps], tap_r2[kMaxTaps], tap_s2[kMaxTaps];
   int n_taps;
   float* partial;      // [split][tap(RS)][c_pad][k_pad]

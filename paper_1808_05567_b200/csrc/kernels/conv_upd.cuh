@@ -116,7 +116,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int pc = 0; pc < PA; ++pc) {
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
           uint8_t* a_dst = st + pc * L.a_piece;
-          if (p.stack > 1) {
+          if (p.sw32) {  // 32 B pixel rows: {16, px[, rows], planes} boxes
+            if (p.stack > 1) {
+              for (int j = 0; j < ntaps; ++j) {
+                const int tp = tap0 + j, tph = p.tap_ph[tp];
+                tma_load_4d(a_dst + j * 2 * p.cb_eff * L.a_plane, &map_in, &full_bar[s], 0,
+                            p.in_col0 + p.phase_col[tph] + p.stride * p.tap_s2[tp],
+                            p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]), pa);
+              }
+            } else if (p.linear) {
+              tma_load_3d(a_dst, &map_in, &full_bar[s], 0, band * p.vs, pa);
+            } else {
+              tma_load_4d(a_dst, &map_in, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
+                          p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], pa);
+            }
+          } else if (p.stack > 1) {
             // one shifted box per stacked tap: slot j = tap tap0 + j, cb_eff blocks
             for (int j = 0; j < ntaps; ++j) {
               const int tp = tap0 + j, tph = p.tap_ph[tp];
@@ -134,7 +148,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int pc = 0; pc < PB; ++pc) {
           const int pb = pc * do_planes + n * p.do_cb + ktile * p.nb;
           uint8_t* b_dst = st + L.b_off + pc * L.b_piece;
-          if (p.linear)
+          if (p.sw32) {
+            if (p.linear)
+              tma_load_3d(b_dst, &map_do, &full_bar[s], 0, band * p.vs, pb);
+            else
+              tma_load_4d(b_dst, &map_do, &full_bar[s], 0, 0, band * p.rows_ps, pb);
+          } else if (p.linear)
             tma_load_4d(b_dst, &map_do, &full_bar[s], 0, band * p.vs, 0, pb);
           else
             tma_load_5d(b_dst, &map_do, &full_bar[s], 0, 0, band * p.rows_ps, 0, pb);
@@ -154,15 +173,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int n_acc = p.stack > 1 ? 1 : ntaps;  // stacked: one accumulator holds all the group's taps
         // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels.
         // Descriptors are packed once per stage; per MMA only the start address (16 B units) advances.
-        const uint64_t a0 = make_smem_desc(st, 128, L.a_plane);
-        const uint64_t b0 = make_smem_desc(st + L.b_off, 128, L.b_plane);
+        const uint64_t a0 = p.sw32 ? make_smem_desc_mn_sw32(st, 2 * L.a_plane) : make_smem_desc(st, 128, L.a_plane);
+        const uint64_t b0 =
+            p.sw32 ? make_smem_desc_mn_sw32(st + L.b_off, 2 * L.b_plane) : make_smem_desc(st + L.b_off, 128, L.b_plane);
         const uint32_t a_pc = L.a_piece >> 4, b_pc = L.b_piece >> 4;
+        const uint32_t row_u = p.sw32 ? 2u : 1u;  // descriptor units (16 B) per pixel row
         for (int t = 0; t < n_acc; ++t) {
           const int shift = p.stack > 1 ? 0 : s_tap_shift[tap0 + t];
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * NT);
           for (int ks = 0; ks < ksteps; ++ks) {
-            const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift);  // 16 B per pixel row
-            const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u;          // 256 B per k-step
+            const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift) * row_u;
+            const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u * row_u;
 #pragma unroll
             for (int ia = 0; ia < PA; ++ia) {
 #pragma unroll

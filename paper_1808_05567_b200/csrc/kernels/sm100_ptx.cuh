@@ -231,6 +231,22 @@ __device__ __forceinline__ uint64_t make_smem_desc_sw32(uint32_t saddr) {
   return d;
 }
 
+// MN-major SWIZZLE_32B canonical layout ((2,n),(8,k)):((1,LBO),(2,SBO)) in 16 B
+// units: 16 MN elements (one pixel's 16 bf16 channels) per 32 B row, K rows
+// (pixels) at 32 B, 8-row groups at SBO = 256 B, 16-element MN groups (channel
+// blocks) at LBO = the plane stride. Same TMA-written rows as the K-major
+// SW32 FWD operand; pixel shifts of the start address stay valid (the swizzle
+// is on absolute address bits).
+__device__ __forceinline__ uint64_t make_smem_desc_mn_sw32(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>(256 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(6) << 61;  // SWIZZLE_32B
+  return d;
+}
+
 // a_fmt/b_fmt: 1 = BF16, 2 = TF32; majors: 0 = K-major, 1 = MN-major
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t fmt, uint32_t a_major, uint32_t b_major, uint32_t M,
                                                   uint32_t N) {

@@ -485,3 +485,52 @@ def test_update_tmem_and_smem_staging_agree(dconv, orc, shape, math, monkeypatch
         torch.cuda.synchronize()
         assert up.blocking["a_in_tmem"] == flag, up.blocking
         gate(orc, ref, dconv.from_blocked_weight(dw).cpu().numpy(), math)
+
+
+# ------------------------------------------------------------------ bf16 storage (the executor's tensors)
+
+BF16_STORAGE = [TABLE_I[i - 1][1:] + ((TABLE_I[i - 1][5] - 1) // 2, (TABLE_I[i - 1][6] - 1) // 2)
+                for i in (1, 2, 4, 5, 6, 8, 11, 13, 16, 18, 20)] + [
+    (c, k, h, w, r, s, st, ph, pw) for (c, k, h, w, r, s, st, ph, pw) in CFG5]
+
+
+@pytest.mark.parametrize("row", BF16_STORAGE, ids=[f"{r[0]}to{r[1]}_{r[4]}x{r[5]}s{r[6]}_{r[2]}" for r in BF16_STORAGE])
+@pytest.mark.parametrize("halo", [0, 1])
+def test_bf16_storage_all_passes(dconv, orc, row, halo):
+    """bf16 activations / output-gradients stored in place (SWIZZLE_32B staging
+    of the 32 B pixel rows: K-major for FWD / BWD, MN-major for UPD), input halo
+    0 (rows mode) or = pad, against the oracle on the same bf16-rounded
+    operands (only fp32 accumulation and output rounding differ)."""
+    C_, K, H, W, R, S, st, ph, pw = row
+    if halo and (ph, pw) == (0, 0):
+        pytest.skip("no padding")
+    N = 2
+    s = orc.spec(N, C_, K, H, W, R, S, st, ph, pw, 16)
+    spec = dconv.make_layer_spec(N, C_, K, H, W, R, S, st, ph, pw, 16)
+    P, Q = orc.output_shape(s)
+    rnd = lambda a: torch.from_numpy(a).bfloat16().float().numpy()  # noqa: E731
+    x = rnd(orc.uniform(11, (N, C_, H, W)))
+    w = rnd(orc.he_normal(12, (K, C_, R, S), C_ * R * S))
+    g = rnd(orc.uniform(13, (N, K, P, Q)))
+    bf = torch.bfloat16
+    ib = dconv.to_blocked_activation(dev(x), 16, ph if halo else 0, pw if halo else 0, dtype=bf)
+    gb = dconv.to_blocked_activation(dev(g), 16, 0, 0, dtype=bf)
+    wb = dconv.to_blocked_weight(dev(w), spec)
+    M = dconv.Math.BF16
+    plan = dconv.make_forward_plan(spec, 1, None, None, M)
+    out = dconv.BlockedActivation(N, K, P, Q, 16, 0, 0, bf)
+    plan.execute(ib, wb, out)
+    gate(orc, orc.conv_forward(s, x, w), dconv.from_blocked_activation(out, dtype=torch.float32).cpu().numpy(), M)
+    dx = dconv.BlockedActivation(N, C_, H, W, 16, 0, 0, bf)
+    dconv.prepare_backward(spec, wb, 1, None, M).execute(wb, gb, dx)
+    gi = dconv.from_blocked_activation(dx, dtype=torch.float32).cpu().numpy()
+    rb = orc.conv_backward(s, g, w)
+    if R == 1 and S == 1 and st == 2:  # structural zeros off the lattice; gate over the lattice
+        mask = np.ones_like(gi, bool)
+        mask[:, :, ::2, ::2] = False
+        assert not gi[mask].any()
+        rb, gi = np.ascontiguousarray(rb[:, :, ::2, ::2]), np.ascontiguousarray(gi[:, :, ::2, ::2])
+    gate(orc, rb, gi, M)
+    dw = dconv.BlockedWeight(K, C_, R, S)
+    dconv.UpdatePlan(spec, None, M).execute(ib, gb, dw)
+    gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(dw).cpu().numpy(), M)
