@@ -295,8 +295,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
 
   FwdTile tile;
   const int kb_total = pb.kb_out;
-  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : 0;
-  const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16) : 0;
+  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : getenv("DCONV_FWD_MB") ? atoi(getenv("DCONV_FWD_MB")) : 0;
+  const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16)
+                     : getenv("DCONV_FWD_NB") ? std::min(atoi(getenv("DCONV_FWD_NB")), 16) : 0;
   int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0, w_st = 0, acc_bufs = 2;
   FwdSmem layout;
   bool found = false;
@@ -370,13 +371,14 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     const int want_bufs = (tier % 2 == 0) ? 2 : 1;
     for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
       const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
-      for (int mb : {2, 1}) {
+      for (int mb : {4, 2, 1}) {
         if (want_mb && mb != want_mb) continue;
+        if (mb == 4 && !want_mb) continue;  // 512-row tiles: explicit override only (DCONV_FWD_MB / tile_mb)
         // accumulators: (pieces == 3 ? 2 : 1) x mb x 16nb columns, double-buffered when they fit
         const int acc_cols = n_acc * mb * 16 * nb;
         if (acc_cols > 512) continue;
         const int bufs = 2 * acc_cols <= 512 ? 2 : 1;
-        if (bufs == 1 && mb == 2) continue;
+        if (bufs == 1 && mb > 1 && !want_mb) continue;
         if (bufs < want_bufs) continue;
         const int Lpx = 128 * mb;
         int apx, lb = 0;
@@ -391,9 +393,11 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           if (p.wsub * st > 256 || rows_box * st > 256) continue;
           apx = rows_box * p.wsub;
         }
-        // weight stage <= 32 KB
+        // weight stage <= 32 KB (fp32 activations) / 80 KB (bf16: every tap of a (c_b,
+        // phase) in one stage for nb <= 16 -- fewer per-stage barriers and MMA-issue
+        // restarts; measured 1.2-1.5x on the 3x3 bf16 layers)
         int wt = taps.taps_box;
-        const int w_cap = getenv("DCONV_WCAP") ? atoi(getenv("DCONV_WCAP")) * 1024 : 32 * 1024;  // debug sweep
+        const int w_cap = getenv("DCONV_WCAP") ? atoi(getenv("DCONV_WCAP")) * 1024 : (raw_f32 ? 32 : 80) * 1024;
         while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > w_cap)
           wt = (wt + 1) / 2;
         const FwdSmem lay = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1);

@@ -569,14 +569,15 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             if (!p.w_resident) mma_commit(&w_empty[ws]);
             mma_commit(&pc_empty[s]);
             if (it == k_iters - 1) mma_commit(&acc_full[acc]);
-          } else if (!TS && PIECES == 1 && nt <= kFastTaps && p.mb <= 2 && elect_one()) {
-            // single-piece multi-tap stage, fully unrolled: the stage's tap shifts are
-            // read into registers with independent loads, then every MMA is one
-            // address add away (the generic loop below serialises a shared-memory
-            // load and its index arithmetic per tap: ~125 cycles per MMA, 2x the
-            // tensor time of a 128x128x16 MMA)
+          } else if (!TS && PIECES == 1 && nt <= kFastTaps && (p.mb == 1 || p.mb == 2 || p.mb == 4) && elect_one()) {
+            // single-piece multi-tap stage, fully unrolled for the tile's m-block count:
+            // the stage's tap shifts are read into registers with independent loads,
+            // then every MMA is one 32-bit address add away (the generic loop below
+            // serialises a shared-memory load and its index arithmetic per tap: ~125
+            // cycles per MMA, 2x the tensor time of a 128x128x16 MMA)
             const uint64_t a_base = RAW_F32 ? make_smem_desc(st, L.a_plane, 128) : make_smem_desc_sw32(st);
             const uint64_t b_base = make_smem_desc(wst, 128, 256);
+            const uint32_t a_hi = static_cast<uint32_t>(a_base >> 32), b_hi = static_cast<uint32_t>(b_base >> 32);
             const int tap0 = s_phase_tap0[ph] + t0;
             constexpr uint32_t kRow = RAW_F32 ? 1u : 2u;  // descriptor units (16 B) per pixel row
             uint32_t sh[kFastTaps];
@@ -584,23 +585,30 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             for (int i = 0; i < kFastTaps; ++i) sh[i] = i < nt ? kRow * static_cast<uint32_t>(s_tap_shift[tap0 + i]) : 0u;
             const uint32_t b_tap = w_tap >> 4;
             const bool do_mma = !(p.dbg_mode & 8);  // ablation: no MMAs
-            for (int kk = 0; kk < kc_eff; ++kk) {
-              const uint64_t ak = a_base + (RAW_F32 ? static_cast<uint32_t>(v_off)
-                                                    : 2u * static_cast<uint32_t>(kk * p.a_px + v_off));
-              const uint64_t bk = b_base + ((static_cast<uint32_t>(w_kk0 + kk) * nt * w_tap) >> 4);
-              const bool first_k = it == 0 && t0 == 0 && kk == 0;
+            auto issue = [&](auto mb_c) {
+              constexpr int MB = decltype(mb_c)::value;
+              for (int kk = 0; kk < kc_eff; ++kk) {
+                const uint32_t ak = static_cast<uint32_t>(a_base) +
+                                    (RAW_F32 ? static_cast<uint32_t>(v_off) : 2u * static_cast<uint32_t>(kk * p.a_px + v_off));
+                const uint32_t bk = static_cast<uint32_t>(b_base) + ((static_cast<uint32_t>(w_kk0 + kk) * nt * w_tap) >> 4);
+                const bool first_k = it == 0 && t0 == 0 && kk == 0;
 #pragma unroll
-              for (int tp = 0; tp < kFastTaps; ++tp) {
-                if (tp >= nt) break;
+                for (int tp = 0; tp < kFastTaps; ++tp) {
+                  if (tp >= nt) break;
 #pragma unroll
-                for (int mb = 0; mb < 2; ++mb) {
-                  if (mb >= p.mb) break;
-                  if (do_mma)
-                    mma_bf16(d_base + static_cast<uint32_t>(mb * NT), ak + (sh[tp] + kRow * 128u * mb),
-                             bk + static_cast<uint32_t>(tp) * b_tap, idesc, (first_k && tp == 0) ? 0u : 1u);
+                  for (int mb = 0; mb < MB; ++mb)
+                    if (do_mma)
+                      mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + kRow * 128u * mb, a_hi,
+                                  bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
                 }
               }
-            }
+            };
+            if (p.mb == 1)
+              issue(std::integral_constant<int, 1>{});
+            else if (p.mb == 2)
+              issue(std::integral_constant<int, 2>{});
+            else
+              issue(std::integral_constant<int, 4>{});
             if (trace) trace[3] = clock64() - t_start;
             if (!p.w_resident) mma_commit(&w_empty[ws]);
             if (trace) trace[4] = clock64() - t_start;
@@ -608,7 +616,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               mma_commit(&pc_empty[s]);
               if (it == k_iters - 1) mma_commit(&acc_full[acc]);
             }
-          } else if (!TS && !(PIECES == 1 && nt <= kFastTaps && p.mb <= 2) && elect_one()) {
+          } else if (!TS && !(PIECES == 1 && nt <= kFastTaps && (p.mb == 1 || p.mb == 2 || p.mb == 4)) && elect_one()) {
             // operand descriptors are packed once per stage; per MMA only the 16 B-unit
             // start-address field advances (no repacking, no parameter reads)
             const uint64_t a_base = RAW_F32 ? make_smem_desc(st, L.a_plane, 128) : make_smem_desc_sw32(st);
