@@ -497,6 +497,72 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         }
       }
     }
+  } else if (warp == 1 && !RAW_F32 && !TS && p.n_phases == 1 && p.w_taps == p.n_taps && !p.w_resident &&
+             p.n_taps <= kFastTaps && (p.mb == 1 || p.mb == 2 || p.mb == 4) && !p.dbg) {
+    // ------------------------------------------------------------ MMA issuer, bf16 single-phase stages
+    // One lane runs the whole loop: the tap shifts and descriptor high words are
+    // computed once per launch, so between the last MMA of a stage and the first of
+    // the next there are only the commits and the two barrier waits (the tensor
+    // pipe's queue is short: issue blocks at the tensor rate, and whatever the
+    // issuing thread does between stages is a bubble in the pipe).
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
+      const int nt = p.n_taps;
+      uint32_t sh[kFastTaps];
+#pragma unroll
+      for (int i = 0; i < kFastTaps; ++i) sh[i] = i < nt ? 2u * static_cast<uint32_t>(s_tap_shift[i]) : 0u;
+      const uint32_t a_hi = static_cast<uint32_t>(make_smem_desc_sw32(smem0) >> 32);
+      const uint32_t b_hi = static_cast<uint32_t>(make_smem_desc(smem0, 128, 256) >> 32);
+      const uint32_t a_lo0 = static_cast<uint32_t>(make_smem_desc_sw32(smem0));
+      const uint32_t b_lo0 = static_cast<uint32_t>(make_smem_desc(smem0 + L.w_off, 128, 256));
+      const uint32_t pc_u = L.pc_slot >> 4, w_u = L.w_slot >> 4, b_tap = w_tap >> 4;
+      auto run = [&](auto mb_c) {
+        constexpr int MB = decltype(mb_c)::value;
+        uint32_t tl = 0;
+        RingPos pcp, wpp;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+          int n, v0, ntile;
+          tile_coords(t, n, v0, ntile);
+          const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
+          const uint32_t v_off2 = 2u * static_cast<uint32_t>(v0 - a_px0);
+          const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+          const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+          mbar_wait(&acc_empty[acc], apar ^ 1u);
+          tc_fence_after();
+          const uint32_t d_base = tmem_base + acc * acc_cols;
+          for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages)) {
+            mbar_wait(&pc_full[pcp.idx], pcp.ph);
+            mbar_wait(&w_full[wpp.idx], wpp.ph);
+            tc_fence_after();
+            const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
+            for (int kk = 0; kk < kc_eff; ++kk) {
+              const uint32_t ak = a_lo0 + static_cast<uint32_t>(pcp.idx) * pc_u +
+                                  2u * static_cast<uint32_t>(kk * p.a_px) + v_off2;
+              const uint32_t bk = b_lo0 + static_cast<uint32_t>(wpp.idx) * w_u + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
+              const bool first_k = it == 0 && kk == 0;
+#pragma unroll
+              for (int tp = 0; tp < kFastTaps; ++tp) {
+                if (tp >= nt) break;
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb)
+                  mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                              bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
+              }
+            }
+            mma_commit(&w_empty[wpp.idx]);
+            mma_commit(&pc_empty[pcp.idx]);
+          }
+          mma_commit(&acc_full[acc]);
+        }
+      };
+      if (p.mb == 1)
+        run(std::integral_constant<int, 1>{});
+      else if (p.mb == 2)
+        run(std::integral_constant<int, 2>{});
+      else
+        run(std::integral_constant<int, 4>{});
+    }
+    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
