@@ -1714,6 +1714,26 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     return L;
   }
   p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !getenv("DCONV_UPD_NO_SW32")) ? 1 : 0;
+  // cp.async loader warps in place of the TMA box loads: opt-in experiment only
+  // (DCONV_UPD_LSU=1). Measured 2-5x SLOWER than the TMA boxes on every ResNet-50
+  // layer (per-chunk address arithmetic on six warps, and the loaders share the
+  // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
+  // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
+  p.lsu = (p.sw32 && L.stages > kUpdLsuDepth && getenv("DCONV_UPD_LSU")) ? 1 : 0;
+  if (p.lsu) {
+    const int ihp = in.h + 2 * in.halo_h, iwp = in.w + 2 * in.halo_w;
+    const int dhp = dout.h + 2 * dout.halo_h, dwp = dout.w + 2 * dout.halo_w;
+    p.in_ptr = reinterpret_cast<const char*>(in_pieces) + (static_cast<int64_t>(in.halo_h) * iwp + in.halo_w) * 32;
+    p.do_ptr = reinterpret_cast<const char*>(do_pieces) + (static_cast<int64_t>(dout.halo_h) * dwp + dout.halo_w) * 32;
+    p.in_h = in.h;
+    p.in_w = in.w;
+    p.in_wp = iwp;
+    p.in_plane = static_cast<long long>(ihp) * iwp;
+    p.do_h = dout.h;
+    p.do_w = dout.w;
+    p.do_wp = dwp;
+    p.do_plane = static_cast<long long>(dhp) * dwp;
+  }
   L.map_in = act_map(in, in_pieces, cb, true);
   L.map_do = act_map(dout, do_pieces, kb, false);
   return L;

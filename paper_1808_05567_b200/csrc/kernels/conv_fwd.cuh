@@ -403,6 +403,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             const int s = rp.idx;
             mbar_wait_t(&pc_empty[s], rp.ph ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
+            if (dbg && blockIdx.x == 0 && g < 256) dbg[gridDim.x * 16 + g * 8 + 6] = clock64() - t_start;
             if (p.dbg_mode & 256) {  // ablation: no activation loads
               mbar_arrive(&pc_full[s]);
               continue;
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       }
     }
   } else if (warp == 1 && !RAW_F32 && !TS && p.n_phases == 1 && p.w_taps == p.n_taps && !p.w_resident &&
-             p.n_taps <= kFastTaps && (p.mb == 1 || p.mb == 2 || p.mb == 4) && !p.dbg) {
+             p.n_taps <= kFastTaps && (p.mb == 1 || p.mb == 2 || p.mb == 4)) {
     // ------------------------------------------------------------ MMA issuer, bf16 single-phase stages
     // One lane runs the whole loop: the tap shifts and descriptor high words are
     // computed once per launch, so between the last MMA of a stage and the first of
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       const uint32_t pc_u = L.pc_slot >> 4, w_u = L.w_slot >> 4, b_tap = w_tap >> 4;
       auto run = [&](auto mb_c) {
         constexpr int MB = decltype(mb_c)::value;
-        uint32_t tl = 0;
+        uint32_t tl = 0, g = 0;
         RingPos pcp, wpp;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
           int n, v0, ntile;
@@ -530,9 +531,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           mbar_wait(&acc_empty[acc], apar ^ 1u);
           tc_fence_after();
           const uint32_t d_base = tmem_base + acc * acc_cols;
-          for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages)) {
+          for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages), ++g) {
+            long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
             mbar_wait(&pc_full[pcp.idx], pcp.ph);
+            if (trace) trace[0] = clock64() - t_start;
             mbar_wait(&w_full[wpp.idx], wpp.ph);
+            if (trace) trace[1] = clock64() - t_start;
             tc_fence_after();
             const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
             for (int kk = 0; kk < kc_eff; ++kk) {
@@ -549,8 +553,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                               bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
               }
             }
+            if (trace) trace[3] = clock64() - t_start;
             mma_commit(&w_empty[wpp.idx]);
             mma_commit(&pc_empty[pcp.idx]);
+            if (trace) trace[2] = clock64() - t_start;
           }
           mma_commit(&acc_full[acc]);
         }

@@ -103,6 +103,15 @@ struct UpdParams {
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
   int sw32;                // bf16 operands staged as SWIZZLE_32B 32 B pixel rows (MN-major SW32 descriptors)
+  // lsu = 1: the operand rows are staged by cp.async from loader warps (the TMA
+  // unit moves 32 B rows at ~27 B/clk/SM; 16 B cp.async from six warps ~2x that)
+  int lsu;
+  const void* in_ptr;      // interior pixel (0, 0) of plane 0 (halo offset applied)
+  const void* do_ptr;
+  int in_h, in_w, in_wp;   // interior extents, physical row pitch (pixels)
+  long long in_plane;      // pixels per physical plane
+  int do_h, do_w, do_wp;
+  long long do_plane;
   int tap_ph[kMaxTaps], tap_r2[kMaxTaps], tap_s2[kMaxTaps];
   int n_taps;
   float* partial;      // [split][tap(RS)][c_pad][k_pad]

@@ -43,6 +43,49 @@ __host__ __device__ inline UpdStage upd_stage_layout(int a_px, int vs, int nb, i
   return L;
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+constexpr int kUpdLoaderWarp0 = 2, kUpdLoaderWarps = 6;  // warps 2..7 stage operands (lsu plans)
+constexpr int kUpdLsuDepth = 2;                          // stages in flight per loader thread
+
+// One stage of the bf16 SW32 operand tiles by cp.async, exactly the boxes the
+// TMA path loads: rows `r` of `n_rows`, `cols` pixels per row (element stride
+// `st` in the source), 2 x 16 B per pixel, zero outside the interior; the
+// destination [plane][row][col][32 B] with the SWIZZLE_32B XOR (bit 4 ^= bit 7).
+__device__ __forceinline__ void lsu_box(uint32_t dst0, const uint8_t* src_plane0, long long plane_px, int n_planes,
+                                        int n_valid, int n_rows, int cols, int row0, int col0, int st, int h, int w,
+                                        int wp, int t, int nt) {
+  const int chunks = 2 * cols;
+  const int pairs = n_planes * n_rows;
+  for (int pr = t / chunks, c = t % chunks; pr < pairs;) {
+    const int pl = pr / n_rows, r = pr - pl * n_rows;
+    const int rg = row0 + st * r;
+    const uint8_t* rowp = src_plane0 + (static_cast<long long>(pl) * plane_px + static_cast<long long>(rg) * wp) * 32;
+    const uint32_t drow = dst0 + static_cast<uint32_t>((pl * n_rows + r) * cols) * 32u;
+    const bool row_ok = rg >= 0 && rg < h && pl < n_valid;  // planes past the tensor's channels: zero
+    for (; c < chunks; c += nt) {
+      const int col = c >> 1, cg = col0 + st * col;
+      const bool ok = row_ok && cg >= 0 && cg < w;
+      const uint32_t d = drow + static_cast<uint32_t>(c) * 16u;
+      cp_async16(d ^ ((d >> 3) & 16u), ok ? rowp + static_cast<long long>(cg) * 32 + (c & 1) * 16 : src_plane0,
+                 ok ? 16u : 0u);
+    }
+    // next (plane, row) pair this thread owns: advance by nt chunks overall
+    c -= chunks;
+    ++pr;
+    while (c >= chunks && pr < pairs) {
+      c -= chunks;
+      ++pr;
+    }
+  }
+}
+
 // PA / PB: operand pieces staged per stage. The products (ia, ib) with
 // a_base + ia + ib <= 2 are accumulated, so one launch with PA = PB = 3 (or
 // PA = PB = 1 for bf16) covers everything, and when three A pieces do not
@@ -87,7 +130,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch_desc(&map_in);
     tma_prefetch_desc(&map_do);
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], p.lsu ? kUpdLoaderWarps * 32 : 1);
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&accum_bar, 1);
@@ -99,9 +142,61 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
 
-  if (warp == 0) {
+  if (PA == 1 && PB == 1 && p.lsu && warp >= kUpdLoaderWarp0 && warp < kUpdLoaderWarp0 + kUpdLoaderWarps) {
+    // ------------------------------------------------------------ cp.async operand loaders
+    const int t = threadIdx.x - kUpdLoaderWarp0 * 32, nt = kUpdLoaderWarps * 32;
+    const uint8_t* in0 = static_cast<const uint8_t*>(p.in_ptr);
+    const uint8_t* do0 = static_cast<const uint8_t*>(p.do_ptr);
+    RingPos rp, fp;  // fill position, arrive position (kUpdLsuDepth behind)
+    const int a_valid = p.in_cb - ctile * 8, b_valid = p.do_cb - ktile * p.nb;
+    for (int it = 0; it < iters; ++it, rp.adv(n_stages)) {
+      mbar_wait(&empty_bar[rp.idx], rp.ph ^ 1u);
+      const int stage = s_begin + it;
+      const int n = stage / p.stages_per_img;
+      const int band = stage - n * p.stages_per_img;
+      const uint32_t st_a = smem0 + static_cast<uint32_t>(rp.idx) * L.bytes;
+      const uint8_t* in_n = in0 + (static_cast<long long>(n) * p.in_cb + ctile * 8) * p.in_plane * 32;
+      const uint8_t* do_n = do0 + (static_cast<long long>(n) * p.do_cb + ktile * p.nb) * p.do_plane * 32;
+      if (p.linear) {
+        // dense planes: pixels [band*vs, +vs) of cb_eff (A) / nb (B) planes
+        lsu_box(st_a, in_n, p.in_plane, 8, a_valid, 1, p.vs, 0, band * p.vs, 1, 1, p.in_h * p.in_w, 0, t, nt);
+        lsu_box(st_a + L.b_off, do_n, p.do_plane, p.nb, b_valid, 1, p.vs, 0, band * p.vs, 1, 1, p.do_h * p.do_w, 0, t,
+                nt);
+      } else {
+        if (p.stack > 1) {
+          for (int j = 0; j < ntaps; ++j) {
+            const int tp = tap0 + j, tph = p.tap_ph[tp];
+            lsu_box(st_a + static_cast<uint32_t>(j * 2 * p.cb_eff) * L.a_plane, in_n, p.in_plane, p.cb_eff, a_valid,
+                    p.in_rows,
+                    p.wsub, p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]),
+                    p.in_col0 + p.phase_col[tph] + p.stride * p.tap_s2[tp], p.stride, p.in_h, p.in_w, p.in_wp, t, nt);
+          }
+        } else {
+          lsu_box(st_a, in_n, p.in_plane, p.cb_eff, a_valid, p.in_rows, p.wsub,
+                  p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], p.in_col0 + p.phase_col[ph], p.stride,
+                  p.in_h, p.in_w, p.in_wp, t, nt);
+        }
+        lsu_box(st_a + L.b_off, do_n, p.do_plane, p.nb, b_valid, p.rows_ps, p.wsub, band * p.rows_ps, 0, 1, p.do_h,
+                p.do_w, p.do_wp, t, nt);
+      }
+      cp_async_commit();
+      if (it >= kUpdLsuDepth) {
+        cp_async_wait<kUpdLsuDepth>();
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        mbar_arrive(&full_bar[fp.idx]);
+        fp.adv(n_stages);
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int it = max(0, iters - kUpdLsuDepth); it < iters; ++it) {
+      mbar_arrive(&full_bar[fp.idx]);
+      fp.adv(n_stages);
+    }
+    // warps 4..7 continue as the epilogue below
+  } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    if (lane == 0 && !p.lsu) {
       const int in_planes = p.n_img * p.in_cb, do_planes = p.n_img * p.do_cb;
       for (int it = 0; it < iters; ++it) {
         const int s = it % n_stages;
@@ -160,6 +255,42 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
+  } else if (warp == 1 && PA == 1 && PB == 1 && p.sw32 && (p.stack > 1 ? 1 : ntaps) <= kFastTaps) {
+    // ------------------------------------------------------------ MMA issuer (bf16 SW32), one lane
+    // shifts and descriptor words hoisted out of the stage loop; between stages
+    // only the commit and the full-barrier wait (see conv_fwd_kernel)
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
+      const int ksteps = p.vs / 16;
+      const int n_acc = p.stack > 1 ? 1 : ntaps;
+      uint32_t sh[kFastTaps];
+#pragma unroll
+      for (int i = 0; i < kFastTaps; ++i)
+        sh[i] = (i < n_acc && p.stack == 1) ? 2u * static_cast<uint32_t>(s_tap_shift[tap0 + i]) : 0u;
+      const uint64_t a_d = make_smem_desc_mn_sw32(smem0, 2 * L.a_plane);
+      const uint64_t b_d = make_smem_desc_mn_sw32(smem0 + L.b_off, 2 * L.b_plane);
+      const uint32_t a_hi = static_cast<uint32_t>(a_d >> 32), b_hi = static_cast<uint32_t>(b_d >> 32);
+      const uint32_t a_lo0 = static_cast<uint32_t>(a_d), b_lo0 = static_cast<uint32_t>(b_d);
+      const uint32_t slot_u = L.bytes >> 4;
+      RingPos rp;
+      for (int it = 0; it < iters; ++it, rp.adv(n_stages)) {
+        mbar_wait(&full_bar[rp.idx], rp.ph);
+        tc_fence_after();
+        const uint32_t a_s = a_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
+        const uint32_t b_s = b_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
+        for (int ks = 0; ks < ksteps; ++ks) {
+#pragma unroll
+          for (int t = 0; t < kFastTaps; ++t) {
+            if (t >= n_acc) break;
+            mma_bf16_lo(tmem_base + static_cast<uint32_t>(t * NT), a_s + 32u * ks + sh[t], a_hi, b_s + 32u * ks, b_hi,
+                        idesc, (it > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(&empty_bar[rp.idx]);
+      }
+      if (iters > 0) mma_commit(&accum_bar);
+    }
+    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
@@ -200,8 +331,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       __syncwarp();
     }
-  } else if (warp >= 4) {
-    // ---------------------------------------------------------- epilogue
+  }
+  if (warp >= 4) {
+    // ---------------------------------------------------------- epilogue (lsu plans: after loading)
     const int qrow = (warp % 4) * 32;
     const int c_glob = ctile * 128 + qrow + lane;
     if (iters > 0) {

@@ -19,6 +19,7 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, uint64_
       : "memory");
 }
 
+__device__ int g_same;
 // mode 0: tensor box {inner, rows}; mode 1: 1-D bulk copy of box_bytes. `prod` warps issue, each its own ring.
 __global__ void reader(const __grid_constant__ CUtensorMap map, const uint8_t* src, int mode, int ring, int box_bytes,
                        int box_rows, int n_pos, int n_boxes, int prod) {
@@ -32,7 +33,7 @@ __global__ void reader(const __grid_constant__ CUtensorMap map, const uint8_t* s
   __syncthreads();
   if (threadIdx.x % 32 != 0 || w >= prod) return;
   uint8_t* base = smem + w * ring * box_bytes;
-  int pos = (blockIdx.x * 7919 + w * 131) % n_pos;
+  int pos = g_same ? (w * 131) % n_pos : (blockIdx.x * 7919 + w * 131) % n_pos;
   int s_issue = 0;
   auto issue = [&]() {
     mbar_arrive_expect_tx(&full[w][s_issue], box_bytes);
@@ -78,8 +79,10 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int n_boxes = 2400;
-  for (int inner : {16, 32, 64, 128}) {
-    for (int box_bytes : {2048, 4096, 8192, 16384, 32768}) {
+  for (int same : {0, 1})
+  for (int inner : {32, 128, 0}) {
+    cudaMemcpyToSymbol(g_same, &same, 4);
+    for (int box_bytes : {8192, 32768}) {
       const int rows = inner ? box_bytes / inner : 0;
       if (inner && rows > 256) continue;
       CUtensorMap map;
@@ -113,8 +116,8 @@ int main() {
             if (ms < best) best = ms;
           }
           const double gbs = 148.0 * n_boxes * box_bytes / (best * 1e-3) / 1e9;
-          printf("%s inner %3d box %5d prod %d ring %d: %7.1f us %6.0f GB/s %5.1f B/clk/SM  %.0f ns/box/SM %s\n",
-                 inner ? "tma " : "bulk", inner, box_bytes, prod, ring, best * 1e3, gbs, gbs / 148 / 1.965,
+          printf("same=%d %s inner %3d box %5d prod %d ring %d: %7.1f us %6.0f GB/s %5.1f B/clk/SM  %.0f ns/box/SM %s\n",
+                 same, inner ? "tma " : "bulk", inner, box_bytes, prod, ring, best * 1e3, gbs, gbs / 148 / 1.965,
                  best * 1e6 / n_boxes, cudaGetErrorString(cudaGetLastError()));
         }
     }
