@@ -198,6 +198,13 @@ int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argma
 /* mask (nullable, grad_in's geometry): ReLU backward of the pooled activation */
 int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in, const void* mask,
                       dconv_stream_t stream);
+/* space-to-depth for a stride-2 conv on a narrow input (the 7x7/s2/p3 stem):
+ * xs[n][i][j][(dy*2+dx)*C+c] = x[n][c][2i+dy-pad][2j+dx-pad], C <= 4 -> 4C
+ * channels; the conv becomes stride 1 with a ceil(R/2) x ceil(S/2) filter */
+int dconv_s2d_act(const dconv_act_t* x, const dconv_act_t* xs, int pad, dconv_stream_t stream);
+/* filter for that conv (inverse = 0: w -> w2) and its gradient back (inverse = 1:
+ * w2 -> w, i.e. dW from the stride-1 conv's dW2); fp32 blocked weights */
+int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_stream_t stream);
 /* w -= lr * g on fp32 blocked weights */
 int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t stream);
 

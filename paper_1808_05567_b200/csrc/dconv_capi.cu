@@ -299,6 +299,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16)
                      : getenv("DCONV_FWD_NB") ? std::min(atoi(getenv("DCONV_FWD_NB")), 16) : 0;
   int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0, w_st = 0, acc_bufs = 2;
+  bool w_all = false;
   FwdSmem layout;
   bool found = false;
   // widest N tile first (fewer activation re-reads), then the largest M tile;
@@ -454,6 +455,23 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           }
           if (pcs < want_pc) continue;
           if (kc > 1 && linear && !mimg_ok) lb = 1;  // one box of Lpx pixels x kc blocks
+          // one output-channel tile and every tap of a channel-block group in one stage:
+          // when all the stages' weights fit, each gets its own slot, loaded once per CTA
+          // (the stem, the 56x56 3x3 and 1x1 layers re-streamed them for every tile)
+          w_all = false;
+          if (nb >= kb_total && taps.n_phases == 1 && wt == taps.taps_box && !getenv("DCONV_NO_WALL")) {
+            const int kst = cdiv(pb.cb_red, kc);
+            const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
+            const int w_bytes = kst * static_cast<int>(lk.w_slot);
+            const int pcs2 = kst <= kMaxStages && w_bytes <= 112 * 1024
+                                 ? std::min<int>(kMaxStages, (kFwdBudget - 3 * 16384 - w_bytes) / static_cast<int>(lk.pc_slot))
+                                 : 0;
+            if (pcs2 >= 2) {
+              wss = kst;
+              pcs = pcs2;
+              w_all = true;
+            }
+          }
         }
         tile.mb = mb;
         tile.nb = nb;
@@ -481,6 +499,8 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.mb = tile.mb;
   p.nb = tile.nb;
   p.kc = kc;
+  // w_all is consumed only by the single-lane bf16 MMA loop (conv_fwd.cuh): same conditions
+  p.w_all = (w_all && (tile.mb == 1 || tile.mb == 2 || tile.mb == 4) && static_cast<int>(taps.r.size()) <= kFastTaps) ? 1 : 0;
   p.acc_bufs = acc_bufs;
   p.a_px = a_px;
   p.a_load_px = a_px;
@@ -2010,6 +2030,54 @@ int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dco
                                                            (const __nv_bfloat16*)mask, planes, grad_in->h,
                                                            grad_in->w, grad_out->h, grad_out->w);
     cuda_check(cudaGetLastError(), "maxpool_bwd");
+  });
+}
+
+int dconv_s2d_act(const dconv_act_t* x, const dconv_act_t* xs, int pad, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(x, "s2d input");
+    check_act(xs, "s2d output");
+    if (x->vlen != 16 || xs->vlen != 16 || x->c > 4 || xs->c != 4 * x->c || x->halo_h || x->halo_w ||
+        xs->halo_h || xs->halo_w || xs->n != x->n || xs->dtype != x->dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "s2d: halo-0 vlen-16 tensors, C <= 4 -> 4C channels");
+    const int g = grid1d(static_cast<int64_t>(x->n) * xs->h * xs->w);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    auto go = [&](auto c_tag) {
+      constexpr int Cc = decltype(c_tag)::value;
+      if (x->dtype == DCONV_F32)
+        s2d_act_kernel<float, Cc><<<g, 256, 0, cs>>>((const float*)x->data, (float*)xs->data, x->n, x->h, x->w,
+                                                     xs->h, xs->w, pad);
+      else
+        s2d_act_kernel<__nv_bfloat16, Cc><<<g, 256, 0, cs>>>((const __nv_bfloat16*)x->data,
+                                                             (__nv_bfloat16*)xs->data, x->n, x->h, x->w, xs->h,
+                                                             xs->w, pad);
+    };
+    switch (x->c) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 3: go(std::integral_constant<int, 3>{}); break;
+      default: go(std::integral_constant<int, 4>{}); break;
+    }
+    cuda_check(cudaGetLastError(), "s2d_act");
+  });
+}
+
+int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(w, "s2d weight");
+    check_wt(w2, "s2d weight'");
+    if (w->dtype != DCONV_F32 || w2->dtype != DCONV_F32 || w->vlen != 16 || w2->vlen != 16 || w->c > 4 ||
+        w2->c != 4 * w->c || w2->k != w->k || w2->r != (w->r + 1) / 2 || w2->s != (w->s + 1) / 2)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "s2d weights: fp32 [K][C<=4][R][S] <-> [K][4C][ceil(R/2)][ceil(S/2)]");
+    const int kb = cdiv(w->k, 16);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (!inverse)
+      s2d_wt_kernel<<<grid1d(static_cast<int64_t>(kb) * w2->r * w2->s * 256), 256, 0, cs>>>(
+          (const float*)w->data, (float*)w2->data, kb, w->c, w->r, w->s, w2->r, w2->s);
+    else
+      s2d_wt_grad_kernel<<<grid1d(static_cast<int64_t>(kb) * w->r * w->s * 256), 256, 0, cs>>>(
+          (const float*)w2->data, (float*)w->data, kb, w->c, w->r, w->s, w2->r, w2->s);
+    cuda_check(cudaGetLastError(), "s2d_wt");
   });
 }
 

@@ -297,7 +297,11 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   // epilogue, warps 8..11 form a second epilogue group (alternate block pairs),
   // doubling the loads in flight for fused residual adds / ReLU masks
   const bool epi2 = !RAW_F32 && !TS && p.tma_store;
-  const int n_epi_groups = epi2 ? max(1, min(3, p.epi_groups)) : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
+  // bf16 plans with the register epilogue (halo'd / strided / padded-row outputs: every
+  // rows-mode layer) split each tile's (m-block, block pair) items over the same
+  // groups: one warp per lane quarter is latency bound (dependent chains, no ILP)
+  const bool epi_reg3 = !RAW_F32 && !TS && !p.tma_store;
+  const int n_epi_groups = (epi2 || epi_reg3) ? max(1, min(3, p.epi_groups)) : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
   constexpr uint32_t kRingCols = PIECES * 8;  // per channel block
@@ -466,6 +470,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       uint32_t g = 0;
       RingPos wp;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        if (p.w_all && t != blockIdx.x) break;  // every stage has its own slot: loaded once
         int n, v0, ntile;
         tile_coords(t, n, v0, ntile);
         int cb = 0, ph = 0;
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
             mbar_wait(&pc_full[pcp.idx], pcp.ph);
             if (trace) trace[0] = clock64() - t_start;
-            mbar_wait(&w_full[wpp.idx], wpp.ph);
+            if (!p.w_all || tl == 0) mbar_wait(&w_full[wpp.idx], wpp.ph);
             if (trace) trace[1] = clock64() - t_start;
             tc_fence_after();
             const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
@@ -554,7 +559,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               }
             }
             if (trace) trace[3] = clock64() - t_start;
-            mma_commit(&w_empty[wpp.idx]);
+            if (!p.w_all) mma_commit(&w_empty[wpp.idx]);
             mma_commit(&pc_empty[pcp.idx]);
             if (trace) trace[2] = clock64() - t_start;
           }
@@ -935,7 +940,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       dbg[2] = c_b;
       dbg[3] = clock64() - t_start - c_a - c_b;
     }
-  } else if (warp >= kCvtWarp0) {
+  } else if (warp >= kCvtWarp0 && !epi_reg3) {
     // ------------------------------------------------------------ converters (smem fp32 -> bf16 pieces)
     if (RAW_F32) {
       const int grp = (warp - kCvtWarp0) / cvt_group_warps;  // this group converts stages g % cvt_groups == grp
@@ -984,10 +989,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         dbg[3] = clock64() - t_start - c_a - c_b;
       }
     }
-  } else if (warp >= kEpiWarp0) {
-    // ------------------------------------------------------------ epilogue (warps 4..7)
-    // warp -> TMEM lane quarter (warp % 4)
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 * n_epi_groups) {
+    // ------------------------------------------------------------ epilogue (warps 4..7 [, 8..15])
+    // warp -> TMEM lane quarter (warp % 4); group eg takes items eg, eg + n_groups, ...
     const int qrow = (warp % 4) * 32;
+    const int eg = (warp - kEpiWarp0) / 4;
+    const int n_pairs = (p.nb + 1) / 2;
     const int g_lo = 0, g_hi = p.nb;
     const int v_end = p.P * p.wsub;
     const int esz = p.out_bf16 ? 2 : 4;
@@ -1001,7 +1008,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
-      for (int mb = 0; mb < p.mb; ++mb) {
+      for (int item = eg; item < p.mb * n_pairs; item += n_epi_groups) {
+        const int mb = item / n_pairs;
         int v = v0 + mb * 128 + qrow + lane;
         int nn = n;
         bool valid;
@@ -1018,7 +1026,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         valid = valid && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
-        for (int g0 = g_lo; g0 < ((p.dbg_mode & 64) ? g_lo : g_hi); g0 += 2) {
+        for (int g0 = 2 * (item - mb * n_pairs); g0 < ((p.dbg_mode & 64) ? g_lo : g_hi); g0 += 2 * n_pairs) {
           // two 16-column TMEM loads in flight, one wait
           const int ng = min(2, g_hi - g0);
           uint32_t r[2][16], rl[2][16];

@@ -42,6 +42,7 @@ struct FwdParams {
   int w_taps;          // taps per weight pipeline stage (<= taps_box)
   int kc;              // input channel blocks per pipeline stage (single-tap TS plans; else 1)
   int w_resident;      // 1: the CTA's whole weight slice stays in smem (loaded once)
+  int w_all;           // bf16 single-phase plans, one output-channel tile: every weight stage has its own slot, loaded once
   int tma_store;       // 1: epilogue stages 32-pixel slabs in smem and TMA-stores them (dense outputs)
   int out_fill;        // 1: stride-2 lattice output that also writes the zero pixels it owns
   int split_acc;       // fp32-accurate: 1 = hi*hi and corrections in separate accumulators (long reductions)

@@ -367,6 +367,77 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __
   }
 }
 
+// Space-to-depth of a narrow (C <= 4), halo-0, one-block input for a stride-2
+// conv: xs[n][i][j][(dy*2+dx)*C + c] = x[n][c][2i+dy-pad][2j+dx-pad] (zero
+// outside; lanes >= 4C zero). A stride-2 RxS conv over x equals a stride-1
+// ceil(R/2) x ceil(S/2) conv over xs with the filter s2d_wt_kernel builds
+// (the 7x7/s2 ResNet stem becomes a 4x4/s1 conv over 12 of 16 lanes).
+template <typename T, int C>
+__global__ void s2d_act_kernel(const T* __restrict__ x, T* __restrict__ xs, int n, int h, int w, int hs, int ws,
+                               int pad) {
+  const long long total = static_cast<long long>(n) * hs * ws;
+  DCONV_GRID_STRIDE(e, total) {
+    const int j = static_cast<int>(e % ws);
+    const long long r = e / ws;
+    const int i = static_cast<int>(r % hs);
+    const long long img = r / hs;
+    T v[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) v[l] = from_f<T>(0.0f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int y = 2 * i + q / 2 - pad, xx = 2 * j + q % 2 - pad;
+      if (y < 0 || y >= h || xx < 0 || xx >= w) continue;
+      const T* px = x + ((img * h + y) * w + xx) * 16;
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) v[q * C + ch] = px[ch];
+    }
+    uint4* o = reinterpret_cast<uint4*>(xs + e * 16);
+    const uint4* vv = reinterpret_cast<const uint4*>(v);
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(16 * sizeof(T) / 16); ++k) o[k] = vv[k];
+  }
+}
+
+// W[k][c][r][s] (blocked, one c-block) -> W'[k][(dy*2+dx)*C + c][r'][s'] =
+// W[k][c][2r'+dy][2s'+dx] (zero past R / S); inverse = s2d_wt_grad_kernel
+__global__ void s2d_wt_kernel(const float* __restrict__ w, float* __restrict__ w2, int kb, int c, int R, int S,
+                              int R2, int S2) {
+  const long long total = static_cast<long long>(kb) * R2 * S2 * 256;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % 256);
+    const long long rr = e / 256;
+    const int s2 = static_cast<int>(rr % S2), r2 = static_cast<int>((rr / S2) % R2);
+    const long long kbi = rr / (static_cast<long long>(S2) * R2);
+    const int ci = lane / 16, ki = lane % 16;  // lane [c][k]
+    float v = 0.0f;
+    if (ci < 4 * c) {
+      const int q = ci / c, ch = ci % c, dy = q / 2, dx = q % 2;
+      const int r = 2 * r2 + dy, sx = 2 * s2 + dx;
+      if (r < R && sx < S) v = w[((kbi * R + r) * S + sx) * 256 + ch * 16 + ki];
+    }
+    w2[e] = v;
+  }
+}
+
+__global__ void s2d_wt_grad_kernel(const float* __restrict__ g2, float* __restrict__ g, int kb, int c, int R, int S,
+                                   int R2, int S2) {
+  const long long total = static_cast<long long>(kb) * R * S * 256;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % 256);
+    const long long rr = e / 256;
+    const int sx = static_cast<int>(rr % S), r = static_cast<int>((rr / S) % R);
+    const long long kbi = rr / (static_cast<long long>(S) * R);
+    const int ci = lane / 16, ki = lane % 16;
+    float v = 0.0f;
+    if (ci < c) {
+      const int q = (r % 2) * 2 + (sx % 2);
+      v = g2[((kbi * R2 + r / 2) * S2 + sx / 2) * 256 + (q * c + ci) * 16 + ki];
+    }
+    g[e] = v;
+  }
+}
+
 // SGD on fp32 master weights: w -= lr * g (blocked layouts, identical shapes)
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, long long n) {
   DCONV_GRID_STRIDE(e, n) { w[e] -= lr * g[e]; }

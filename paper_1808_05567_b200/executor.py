@@ -218,11 +218,30 @@ class ConvStackExecutor:
                    for i, nd in enumerate(self.convs)}
         self.bucketer = GradBucketer(self.flat, [self.slices[i] for i in order], bucket_bytes, group)
         self._bucket_index = {i: k for k, i in enumerate(order)}
+        # narrow stride-2 input convs (the 7x7/s2 stem, C=3) run as a stride-1 conv over a
+        # space-to-depth copy of their input: 4x4 taps over 12 of 16 lanes instead of
+        # 49 taps over 3 of 16 (the MMA K dimension is a 16-lane channel block)
+        self.s2d: Dict[str, dict] = {}
+        for nd in self.convs:
+            c, h, w = self.shapes[nd.src]
+            if nd.stride == 2 and nd.C * 4 <= 16 and nd.R > 1 and nd.S > 1:
+                _, P, Q = self.shapes[nd.out]
+                r2, s2 = (nd.R + 1) // 2, (nd.S + 1) // 2
+                hs, wsz = P + r2 - 1, Q + s2 - 1
+                spec2 = d.ConvLayerSpec(batch, 4 * nd.C, nd.K, hs, wsz, r2, s2, 1, 0, 0, 16)
+                spec2.validate()
+                self.s2d[nd.name] = {
+                    "spec": spec2,
+                    "x": d.BlockedActivation(batch, 4 * nd.C, hs, wsz, 16, 0, 0, act_dtype, self.dev),
+                    "w": d.BlockedWeight(nd.K, 4 * nd.C, r2, s2, 16, torch.float32, self.dev),
+                    "dw": d.BlockedWeight(nd.K, 4 * nd.C, r2, s2, 16, torch.float32, self.dev),
+                }
         # plans
-        self.fplan = {n: d.ExecutionPlan(s, None, None, self.math, 0, 0) for n, s in self.specs.items()}
+        self.pspec = {n: (self.s2d[n]["spec"] if n in self.s2d else s) for n, s in self.specs.items()}
+        self.fplan = {n: d.ExecutionPlan(s, None, None, self.math, 0, 0) for n, s in self.pspec.items()}
         self.bplan = {n: d.BackwardContext(s, None, 1, None, self.math) for n, s in self.specs.items()
                       if self._needs_bwd(n)}
-        self.uplan = {n: d.UpdatePlan(s, None, self.math) for n, s in self.specs.items()}
+        self.uplan = {n: d.UpdatePlan(s, None, self.math) for n, s in self.pspec.items()}
         self.comm_stream = torch.cuda.Stream(self.dev) if group is not None else None
         self._ev = {i: torch.cuda.Event() for i in range(len(self.convs))}
 
@@ -244,11 +263,32 @@ class ConvStackExecutor:
                 _check(self.lib.dconv_maxpool_fwd(C.byref(self.act[nd.src].to_c()), C.byref(self.act[nd.out].to_c()),
                                                   self.argmax[nd.name].data_ptr(), self._stream()))
                 continue
-            plan = self.fplan[nd.name]
-            ep = self._ep(add=self.act[nd.add] if nd.add else None, relu=nd.relu)
-            ws = plan._ws.get(self.lib.dconv_fwd_workspace_bytes(plan._h), self.dev)
-            _check(self.lib.dconv_forward_ex(plan._h, C.byref(self.act[nd.src].to_c()), C.byref(self.w[nd.name].to_c()),
-                                             C.byref(self.act[nd.out].to_c()), C.byref(ep), ws, self._stream()))
+            self.conv_forward(nd)
+
+    def conv_forward(self, nd: ConvNode):
+        plan = self.fplan[nd.name]
+        ep = self._ep(add=self.act[nd.add] if nd.add else None, relu=nd.relu)
+        ws = plan._ws.get(self.lib.dconv_fwd_workspace_bytes(plan._h), self.dev)
+        src, wt = self.act[nd.src], self.w[nd.name]
+        if nd.name in self.s2d:
+            sd = self.s2d[nd.name]
+            _check(self.lib.dconv_s2d_act(C.byref(src.to_c()), C.byref(sd["x"].to_c()), nd.pad, self._stream()))
+            _check(self.lib.dconv_s2d_wt(C.byref(wt.to_c()), C.byref(sd["w"].to_c()), 0, self._stream()))
+            src, wt = sd["x"], sd["w"]
+        _check(self.lib.dconv_forward_ex(plan._h, C.byref(src.to_c()), C.byref(wt.to_c()),
+                                         C.byref(self.act[nd.out].to_c()), C.byref(ep), ws, self._stream()))
+
+    def conv_update(self, nd: ConvNode):
+        up = self.uplan[nd.name]
+        src, dw = self.act[nd.src], self.dw[nd.name]
+        if nd.name in self.s2d:  # s2d copy of the input was made by the forward of this step
+            src, dw = self.s2d[nd.name]["x"], self.s2d[nd.name]["dw"]
+        a, g = src.to_c(), self.grad[nd.out].to_c()
+        ws = up._ws.get(self.lib.dconv_upd_workspace_bytes(up._h, C.byref(a), C.byref(g)), self.dev)
+        _check(self.lib.dconv_weight_update(up._h, C.byref(a), C.byref(g), C.byref(dw.to_c()), 0, ws,
+                                            self._stream()))
+        if nd.name in self.s2d:
+            _check(self.lib.dconv_s2d_wt(C.byref(self.dw[nd.name].to_c()), C.byref(dw.to_c()), 1, self._stream()))
 
     def backward(self, dtop: d.BlockedActivation):
         """Gradient buffers hold dL/dz (already through the ReLU of their tensor)."""
@@ -270,12 +310,7 @@ class ConvStackExecutor:
                 continue
             ci = self.convs.index(nd)
             g_out = self.grad[nd.out]  # = dL/dz of this conv (its epilogue's pre-activation)
-            # weight gradient
-            up = self.uplan[nd.name]
-            a, g = self.act[nd.src].to_c(), g_out.to_c()
-            ws = up._ws.get(self.lib.dconv_upd_workspace_bytes(up._h, C.byref(a), C.byref(g)), self.dev)
-            _check(self.lib.dconv_weight_update(up._h, C.byref(a), C.byref(g), C.byref(self.dw[nd.name].to_c()), 0,
-                                                ws, self._stream()))
+            self.conv_update(nd)  # weight gradient
             if self.group is not None:
                 self._ev[ci].record()
                 self.comm_stream.wait_event(self._ev[ci])
@@ -323,7 +358,10 @@ class ConvStackExecutor:
                 n += 2
                 continue
             n += self.fplan[nd.name].launches()
-            n += self.uplan[nd.name].launches(self.act[nd.src], self.grad[nd.out])
+            src = self.s2d[nd.name]["x"] if nd.name in self.s2d else self.act[nd.src]
+            n += self.uplan[nd.name].launches(src, self.grad[nd.out])
+            if nd.name in self.s2d:
+                n += 3  # input / filter space-to-depth, gradient back
             if nd.name in self.bplan:
                 n += self.bplan[nd.name].launches()
             n += 1  # sgd

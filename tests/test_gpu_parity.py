@@ -534,3 +534,45 @@ def test_bf16_storage_all_passes(dconv, orc, row, halo):
     dw = dconv.BlockedWeight(K, C_, R, S)
     dconv.UpdatePlan(spec, None, M).execute(ib, gb, dw)
     gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(dw).cpu().numpy(), M)
+
+
+@pytest.mark.parametrize("math", [0, 1])
+def test_space_to_depth_stem_matches_direct_conv(dconv, orc, math):
+    """The executor's stem: a 7x7/s2/p3 conv over C=3 computed as a 4x4/s1 conv
+    over the space-to-depth input (12 of 16 lanes) equals the oracle's 7x7/s2
+    forward and weight update."""
+    import ctypes as C
+
+    from paper_1808_05567_b200 import _lib
+
+    lib = _lib.lib()
+    M = dconv.Math(math)
+    N, Cn, K, H, R, st, pad = 2, 3, 64, 40, 7, 2, 3
+    s = orc.spec(N, Cn, K, H, H, R, R, st, pad, pad, 16)
+    P, Q = orc.output_shape(s)
+    x = orc.uniform(21, (N, Cn, H, H))
+    w = orc.he_normal(22, (K, Cn, R, R), Cn * R * R)
+    g = orc.uniform(23, (N, K, P, Q))
+    dt = torch.float32 if math == 0 else torch.bfloat16
+    if math == 1:  # same bf16-rounded operands on both sides
+        x = torch.from_numpy(x).bfloat16().float().numpy()
+        g = torch.from_numpy(g).bfloat16().float().numpy()
+    r2 = (R + 1) // 2
+    hs = P + r2 - 1
+    xb = dconv.to_blocked_activation(dev(x), 16, 0, 0, dtype=dt)
+    xs = dconv.BlockedActivation(N, 4 * Cn, hs, hs, 16, 0, 0, dt)
+    st_ = torch.cuda.current_stream().cuda_stream
+    assert lib.dconv_s2d_act(C.byref(xb.to_c()), C.byref(xs.to_c()), pad, st_) == 0
+    wb = dconv.to_blocked_weight(dev(w), dconv.make_layer_spec(N, Cn, K, H, H, R, R, st, pad, pad, 16))
+    w2 = dconv.BlockedWeight(K, 4 * Cn, r2, r2)
+    assert lib.dconv_s2d_wt(C.byref(wb.to_c()), C.byref(w2.to_c()), 0, st_) == 0
+    spec2 = dconv.make_layer_spec(N, 4 * Cn, K, hs, hs, r2, r2, 1, 0, 0, 16)
+    out = dconv.BlockedActivation(N, K, P, Q, 16, 0, 0, dt)
+    dconv.make_forward_plan(spec2, 1, None, None, M).execute(xs, w2, out)
+    gate(orc, orc.conv_forward(s, x, w), dconv.from_blocked_activation(out, dtype=torch.float32).cpu().numpy(), M)
+    gb = dconv.to_blocked_activation(dev(g), 16, 0, 0, dtype=dt)
+    dw2 = dconv.BlockedWeight(K, 4 * Cn, r2, r2)
+    dconv.UpdatePlan(spec2, None, M).execute(xs, gb, dw2)
+    dw = dconv.BlockedWeight(K, Cn, R, R)
+    assert lib.dconv_s2d_wt(C.byref(dw.to_c()), C.byref(dw2.to_c()), 1, st_) == 0
+    gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(dw).cpu().numpy(), M)

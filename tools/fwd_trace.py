@@ -16,11 +16,12 @@ lib = _lib.lib()
 lib.dconv_debug_counters.argtypes = [Ct.c_void_p]
 C, K, H, R = (int(v) for v in os.environ.get("LAYER", "128,128,28,3").split(","))
 N = int(os.environ.get("N", "256"))
-pad = (R - 1) // 2
+pad = int(os.environ.get("PAD", (R - 1) // 2))
 spec = d.make_layer_spec(N, C, K, H, H, R, R, 1, pad, pad, 16)
 x = d.BlockedActivation(N, C, H, H, 16, 0, 0, torch.bfloat16)
 x.data.uniform_(-1, 1)
-y = d.BlockedActivation(N, K, H, H, 16, 0, 0, torch.bfloat16)
+P_ = H + 2 * pad - R + 1
+y = d.BlockedActivation(N, K, P_, P_, 16, 0, 0, torch.bfloat16)
 w = d.BlockedWeight(K, C, R, R)
 w.data.normal_()
 fp = d.make_forward_plan(spec, 1, None, None, d.Math.BF16)

@@ -41,15 +41,8 @@ tot = {"F": 0.0, "B": 0.0, "U": 0.0}
 for nd in e.convs:
     s = e.specs[nd.name]
     fl = 2 * s.N * s.K * s.C * s.P() * s.Q() * s.R * s.S
-    plan = e.fplan[nd.name]
-    ws = plan._ws.get(lib.dconv_fwd_workspace_bytes(plan._h), e.dev)
-    tf = timed(lambda: _chk(lib.dconv_forward(plan._h, C.byref(e.act[nd.src].to_c()), C.byref(e.w[nd.name].to_c()),
-                                                  C.byref(e.act[nd.out].to_c()), ws, st.cuda_stream)))
-    up = e.uplan[nd.name]
-    a_, g_ = e.act[nd.src].to_c(), e.grad[nd.out].to_c()
-    wsu = up._ws.get(lib.dconv_upd_workspace_bytes(up._h, C.byref(a_), C.byref(g_)), e.dev)
-    tu = timed(lambda: _chk(lib.dconv_weight_update(up._h, C.byref(a_), C.byref(g_), C.byref(e.dw[nd.name].to_c()), 0,
-                                                        wsu, st.cuda_stream)))
+    tf = timed(lambda: e.conv_forward(nd))
+    tu = timed(lambda: e.conv_update(nd))
     tb = 0.0
     if nd.name in e.bplan:
         bp = e.bplan[nd.name]
