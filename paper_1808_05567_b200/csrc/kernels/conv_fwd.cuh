@@ -843,7 +843,125 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
     };
-    if (p.add != nullptr || p.mask != nullptr)
+    // bf16 residual add / ReLU mask: the two extra operand tiles are fetched one step
+    // AHEAD into registers (the first step of a tile before its accumulator wait),
+    // so their HBM latency overlaps the previous step instead of stalling every
+    // step (these epilogues move ~3x the bytes of their mainloop)
+    auto lean_fused_bf16 = [&](auto) {  // generic: instantiated only for the bf16-activation kernels
+      uint32_t n_st = 0, tl = 0;
+      const uint8_t* addp = reinterpret_cast<const uint8_t*>(p.add);
+      const uint8_t* maskp = reinterpret_cast<const uint8_t*>(p.mask);
+      auto fetch = [&](int n, int v0, int ntile, int s, int ng, uint4 (&b)[8]) {
+        const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - (s / ng) * ng);
+        const int kb0 = ntile * p.nb + g0;
+        const bool pair = g0 + 1 < p.nb;
+        const int v = v0 + mb * 128 + qrow + lane;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int kb = kb0 + j;
+          const bool live = v < v_end && kb < p.kb_out && (j == 0 || pair);
+          const long long off = ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 32LL;
+          const uint4 z = make_uint4(0, 0, 0, 0);
+          b[2 * j] = (addp && live) ? *reinterpret_cast<const uint4*>(addp + off) : z;
+          b[2 * j + 1] = (addp && live) ? *reinterpret_cast<const uint4*>(addp + off + 16) : z;
+          b[4 + 2 * j] = (maskp && live) ? *reinterpret_cast<const uint4*>(maskp + off) : z;
+          b[4 + 2 * j + 1] = (maskp && live) ? *reinterpret_cast<const uint4*>(maskp + off + 16) : z;
+        }
+      };
+      auto unpack = [](const uint4& a, const uint4& b, float (&f)[16]) {
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          f[2 * e] = __uint_as_float(w[e] << 16);
+          f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+        }
+      };
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+        int n, v0, ntile;
+        tile_coords(t, n, v0, ntile);
+        int ng = 0;  // this group's block pairs in the tile
+        for (int g0 = 2 * eg; g0 < p.nb && ntile * p.nb + g0 < p.kb_out; g0 += 2 * n_eg) ++ng;
+        const int total = p.mb * ng;
+        uint4 cur[8], nxt[8];
+        if (total > 0) fetch(n, v0, ntile, 0, ng, cur);
+        const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+        const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+        mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
+        tc_fence_after();
+        const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
+        for (int s = 0; s < total; ++s) {
+          if (s + 1 < total) fetch(n, v0, ntile, s + 1, ng, nxt);
+          const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - mb * ng);
+          const int kb0 = ntile * p.nb + g0;
+          const bool pair = g0 + 1 < p.nb;
+          uint32_t r[32], rl[32];
+          tmem_ld32(d_base + static_cast<uint32_t>(mb * NT + g0 * 16), r);
+          if (two_acc) tmem_ld32(d_base + static_cast<uint32_t>((p.mb + mb) * NT + g0 * 16), rl);
+          tmem_ld_wait();
+          uint8_t* stg = stg0 + (n_st & 1u) * slot_bytes;
+          if (n_st >= 2) {  // this slot's previous store must have left smem
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j == 1 && !pair) break;
+            const int kb = kb0 + j;
+            float vals[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              vals[e] = two_acc ? __uint_as_float(r[16 * j + e]) + __uint_as_float(rl[16 * j + e])
+                                : __uint_as_float(r[16 * j + e]);
+            if (p.bias != nullptr && kb < p.kb_out) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
+            }
+            if (addp) {
+              float a[16];
+              unpack(cur[2 * j], cur[2 * j + 1], a);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] += a[e];
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = fmaxf(vals[e], 0.0f);
+            }
+            if (maskp) {
+              float m[16];
+              unpack(cur[4 + 2 * j], cur[4 + 2 * j + 1], m);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
+            }
+            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
+            const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
+            const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
+            *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);
+            *reinterpret_cast<uint4*>(stg + sw32(row, 1)) = cast8(b8);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(pair ? &map_out2 : &map_out, stg, 0, v0 + mb * 128 + qrow, kb0, n);
+            bulk_commit_group();
+          }
+          ++n_st;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      }
+    };
+    bool done = false;
+    if constexpr (!RAW_F32) {
+      if ((p.add != nullptr || p.mask != nullptr) && p.out_bf16 && !(p.dbg_mode & 512)) {  // dbg 512: no prefetch
+        lean_fused_bf16(0);
+        done = true;
+      }
+    }
+    if (done) {
+    } else if (p.add != nullptr || p.mask != nullptr)
       lean(std::true_type{}, std::true_type{});
     else if (p.bias != nullptr || p.relu)
       lean(std::false_type{}, std::true_type{});
