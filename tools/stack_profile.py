@@ -27,13 +27,19 @@ rows = []
 st = torch.cuda.current_stream()
 
 
-def timed(fn):
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
+def timed(fn, reps=3):
+    """mean device time of `reps` back-to-back calls (queued behind a spin so host
+    launch gaps are not timed)"""
     fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(2_000_000)
+    a.record(st)
+    for _ in range(reps):
+        fn()
     b.record(st)
     b.synchronize()
-    return a.elapsed_time(b)
+    return a.elapsed_time(b) / reps
 
 
 peak = 1332.6
