@@ -1409,13 +1409,44 @@ struct UpdLaunch {
   bool raw = false, cat = false;
   bool tsa = false;  // single tap: A operand staged in TMEM (conv_upd_ts_kernel)
   int raw_stages = 0, pc_stages = 0;
+  double est_cycles = 0;  // bf16 plans: modelled SM-cycles of the whole launch (selection only)
 };
 
 // Tile selection for the split-K UPD (replaces choose_update_strategy /
 // choose_spatial_blocking, planner.cpp:107-173): virtual-pixel band per stage,
 // k-tile width, tap groups bounded by TMEM, split factor for >= 2 waves.
 UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_act_t& dout, bool encode_maps,
-                   const void* in_pieces, const void* do_pieces, float* partial) {
+                   const void* in_pieces, const void* do_pieces, float* partial, int force_nb = 0,
+                   int force_unstack = -1) {
+  // bf16 operands read in place: pick the k-tile width and (for < 8 channel blocks)
+  // tap stacking vs plain shifted-descriptor taps by the modelled time -- the TMA
+  // row rate (27 B/clk/SM for 32 B rows) against the MMA time of each choice
+  const bool bf16_ops = in.dtype == DCONV_BF16 && dout.dtype == DCONV_BF16 && pl.pieces == 1 &&
+                        !getenv("DCONV_UPD_NO_MODEL");
+  if (bf16_ops && force_unstack < 0 && !(pl.has_cfg && pl.cfg.tile_nb > 0)) {
+    const int kb0 = cdiv(pl.spec.K, 16), cb0 = cdiv(pl.spec.C, 16);
+    const int nb_def = cdiv(kb0, cdiv(kb0, 16));
+    // (un-stacked narrow multi-tap plans -- M rows past C idle, every tap through a shifted
+    // descriptor -- are modelled well but measured slower on the C=64 3x3 layer: opt-in)
+    const bool narrow_taps = cb0 < 8 && pl.spec.R * pl.spec.S > 1 && pl.spec.C > 8 && getenv("DCONV_UPD_UNSTACK");
+    double best = 1e30;
+    int b_nb = nb_def, b_un = 0;
+    for (int un = 0; un <= (narrow_taps ? 1 : 0); ++un)
+      for (int div : {1, 2, 4}) {
+        const int nbv = nb_def / div;
+        if (nbv < 1 || (div > 1 && nb_def % div)) continue;
+        try {
+          const UpdLaunch t = plan_upd(pl, in, dout, false, nullptr, nullptr, nullptr, nbv, un);
+          if (t.est_cycles > 0 && t.est_cycles < best * 0.97) {
+            best = t.est_cycles;
+            b_nb = nbv;
+            b_un = un;
+          }
+        } catch (...) {
+        }
+      }
+    return plan_upd(pl, in, dout, encode_maps, in_pieces, do_pieces, partial, b_nb, b_un);
+  }
   UpdLaunch L;
   std::memset(&L.p, 0, sizeof(L.p));
   UpdParams& p = L.p;
@@ -1444,16 +1475,19 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
                       in.halo_w == 0 && dout.halo_h == 0 && dout.halo_w == 0;
   p.linear = linear ? 1 : 0;
   // tap stacking for narrow inputs (< 8 channel blocks, e.g. the 3-channel stem)
-  const bool stacked = !linear && cb < 8 && s.R * s.S > 1;
+  const bool stacked = !linear && cb < 8 && s.R * s.S > 1 && force_unstack != 1;
   // C <= 8 (the 3-channel stem): only the first 8-lane chunk of each pixel is
   // non-zero, so a tap slot is one chunk and 16 taps share the 128 MMA rows
   p.half = (stacked && s.C <= 8) ? 1 : 0;
   p.stack = stacked ? (p.half ? 16 : 8 / cb) : 1;
-  p.cb_eff = stacked ? cb : 8;
+  // bf16 in place: a c-tile of a narrow layer loads only its cb planes (the MMA's
+  // rows past them read stale shared memory; those dW rows are never reduced)
+  p.cb_eff = stacked ? cb : ((bf16_ops && !p.half && !getenv("DCONV_UPD_NO_SW32")) ? std::min(8, cb) : 8);
   // k tile
   int n_kt = cdiv(kb, 16);
   p.nb = cdiv(kb, n_kt);
   if (pl.has_cfg && pl.cfg.tile_nb > 0) p.nb = std::min(pl.cfg.tile_nb, 16);
+  if (force_nb > 0) p.nb = force_nb;
   const int NT = 16 * p.nb;
   const int n_ktiles = cdiv(kb, p.nb);
   const int n_ctiles = cdiv(cb, 8);
@@ -1499,6 +1533,43 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     }
   }
   const Cand* best = nullptr;
+  // modelled cycles of one candidate over the whole launch (bf16 in-place plans)
+  auto cand_cycles = [&](const Cand& cd) -> double {
+    const int tgv = std::max(1, std::min(512 / NT, taps.taps_box));
+    std::vector<int> groups;  // taps per CTA accumulator group
+    if (stacked) {
+      for (int t0 = 0; t0 < static_cast<int>(taps.r.size()); t0 += p.stack)
+        groups.push_back(std::min(p.stack, static_cast<int>(taps.r.size()) - t0));
+    } else {
+      for (int ph = 0; ph < taps.n_phases; ++ph)
+        for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += tgv) groups.push_back(std::min(tgv, taps.phase_ntaps[ph] - t0));
+    }
+    const double b_bytes = 2.0 * p.nb * cd.lay.b_plane;
+    const double spi = linear ? cdiv(P * Q, cd.vs) : cdiv(P, cd.rows_ps);
+    // cycles per 128 x NT x 16 MMA: tensor time NT/2, or the shared-memory reads of its
+    // operands (4 KB of A + NT x 32 B of B at ~128 B/clk) when those are longer (NT < 128)
+    const double mma_unit = std::max(NT / 2.0, (4096.0 + 32.0 * NT) / 128.0);
+    double cyc = 0;
+    for (int g : groups) {
+      const double a_bytes = stacked ? static_cast<double>(g) * (p.half ? 1 : 2 * p.cb_eff) * cd.lay.a_plane
+                                     : 2.0 * p.cb_eff * cd.lay.a_plane;
+      const double mma = (stacked ? 1 : g) * (cd.vs / 16.0) * mma_unit;
+      cyc += std::max((a_bytes + b_bytes) / 27.0, mma) + 300.0;
+    }
+    return cyc * n_ctiles * n_ktiles * spi * s.N / sm_count();
+  };
+  if (bf16_ops) {
+    double bc = 1e30;
+    for (auto& cd : cands)
+      if (cd.passes == 1 && cd.stages >= 2) {
+        const double c = cand_cycles(cd) * (cd.stages >= 3 ? 1.0 : 1.15);
+        if (c < bc * 0.98) {
+          bc = c;
+          best = &cd;
+        }
+      }
+    if (best) L.est_cycles = bc;
+  }
   for (int tier = 0; tier < 4 && !best; ++tier) {
     const int want_passes = tier < 2 ? 1 : 3, want_stages = (tier % 2 == 0) ? 3 : 2;
     for (auto& cd : cands)
@@ -1669,7 +1740,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       if (linear) {
         const uint64_t dims[3] = {16, static_cast<uint64_t>(a.h) * a.w, planes};
         const uint64_t strides[2] = {32, static_cast<uint64_t>(a.h) * a.w * 32};
-        const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs), static_cast<uint32_t>(is_in ? 8 : p.nb)};
+        const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs), static_cast<uint32_t>(is_in ? p.cb_eff : p.nb)};
         return encode(1, 3, data, dims, strides, box, nullptr, is_in ? "upd input linear sw32" : "upd dO linear sw32",
                       swz);
       }

@@ -205,8 +205,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int n = stage / p.stages_per_img;
         const int band = stage % p.stages_per_img;
         uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
-        const uint32_t a_bytes =
-            p.stack > 1 ? static_cast<uint32_t>(ntaps * (p.half ? 1 : 2 * p.cb_eff)) * L.a_plane : L.a_piece;
+        const uint32_t a_bytes = p.stack > 1 ? static_cast<uint32_t>(ntaps * (p.half ? 1 : 2 * p.cb_eff)) * L.a_plane
+                                 : p.sw32     ? static_cast<uint32_t>(2 * p.cb_eff) * L.a_plane
+                                              : L.a_piece;
         mbar_arrive_expect_tx(&full_bar[s], PA * a_bytes + PB * L.b_piece);
         for (int pc = 0; pc < PA; ++pc) {
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
