@@ -418,7 +418,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         } else {
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
-          int kcx = (taps.r.size() == 1) ? std::min(4, pb.cb_red) : 1;
+          int kcx = (taps.r.size() == 1) ? std::min(getenv("DCONV_FWD_KC") ? atoi(getenv("DCONV_FWD_KC")) : 4, pb.cb_red) : 1;
           pcs = 0;
           for (; kcx >= 1; kcx = kcx > 1 ? kcx / 2 : 0) {
             const FwdSmem lk = fwd_smem_layout(apx * kcx, wt * kcx, nb, pieces, raw_f32, 1, 1);
