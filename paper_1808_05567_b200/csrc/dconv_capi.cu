@@ -419,16 +419,18 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
           int kcx = (taps.r.size() == 1) ? std::min(getenv("DCONV_FWD_KC") ? atoi(getenv("DCONV_FWD_KC")) : 4, pb.cb_red) : 1;
+          // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
+          const int stg_res = (taps.r.size() == 1 || getenv("DCONV_STG_RES")) ? 3 * 16384 : 0;
           pcs = 0;
           for (; kcx >= 1; kcx = kcx > 1 ? kcx / 2 : 0) {
             const FwdSmem lk = fwd_smem_layout(apx * kcx, wt * kcx, nb, pieces, raw_f32, 1, 1);
             int wsk = std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lk.w_slot)));
             // room for three epilogue groups' TMA-store staging (bf16 slabs: 3 x 16 KB)
-            int left = kFwdBudget - 3 * 16384 - wsk * static_cast<int>(lk.w_slot);
+            int left = kFwdBudget - stg_res - wsk * static_cast<int>(lk.w_slot);
             pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
             if (pcs < want_pc && wsk > 2) {
               wsk = 2;
-              left = kFwdBudget - 3 * 16384 - wsk * static_cast<int>(lk.w_slot);
+              left = kFwdBudget - stg_res - wsk * static_cast<int>(lk.w_slot);
               pcs = left > 0 ? std::min<int>(kMaxStages, left / static_cast<int>(lk.pc_slot)) : 0;
             }
             if (kcx == 1 && pcs < want_pc) {  // no room for the TMA-store staging: plain budget
@@ -450,7 +452,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           if (const char* e = getenv("DCONV_WST")) {  // debug: weight-ring depth sweep
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
             wss = atoi(e);
-            pcs = std::min<int>(kMaxStages, (kFwdBudget - 3 * 16384 - wss * static_cast<int>(lk.w_slot)) /
+            pcs = std::min<int>(kMaxStages, (kFwdBudget - stg_res - wss * static_cast<int>(lk.w_slot)) /
                                                 static_cast<int>(lk.pc_slot));
           }
           if (pcs < want_pc) continue;
@@ -464,7 +466,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
             const int w_bytes = kst * static_cast<int>(lk.w_slot);
             const int pcs2 = kst <= kMaxStages && w_bytes <= 112 * 1024
-                                 ? std::min<int>(kMaxStages, (kFwdBudget - 3 * 16384 - w_bytes) / static_cast<int>(lk.pc_slot))
+                                 ? std::min<int>(kMaxStages, (kFwdBudget - stg_res - w_bytes) / static_cast<int>(lk.pc_slot))
                                  : 0;
             if (pcs2 >= 2) {
               wss = kst;
