@@ -169,7 +169,7 @@ class GradBucketer:
 class ConvStackExecutor:
     def __init__(self, nodes: Sequence, batch: int, img: int = 224, math: d.Math = d.Math.BF16,
                  device: str = "cuda", group=None, lr: float = 1e-4, seed: int = 1, bucket_bytes: int = 8 << 20,
-                 act_dtype=torch.bfloat16):
+                 act_dtype=torch.bfloat16, overlap_upd: bool = True):
         self.nodes, self.N, self.img, self.math, self.dev = list(nodes), batch, img, d.Math(math), torch.device(device)
         self.group, self.lr, self.adt = group, lr, act_dtype
         self.lib = _lib.lib()
@@ -244,6 +244,12 @@ class ConvStackExecutor:
         self.uplan = {n: d.UpdatePlan(s, None, self.math) for n, s in self.pspec.items()}
         self.comm_stream = torch.cuda.Stream(self.dev) if group is not None else None
         self._ev = {i: torch.cuda.Event() for i in range(len(self.convs))}
+        # weight updates (+ their split reductions) run on a side stream, concurrent with the
+        # backward-data chain: each kernel's last-wave tail is filled by the other's CTAs and
+        # the small reduction kernels leave the critical path. A layer's update is forked
+        # once its output gradient is final; SGD joins.
+        self.upd_stream = torch.cuda.Stream(self.dev) if (self.dev.type == "cuda" and overlap_upd) else None
+        self._ev_gready = {i: torch.cuda.Event() for i in range(len(self.convs))}
 
     def _needs_bwd(self, name):
         nd = next(n for n in self.convs if n.name == name)
@@ -309,11 +315,20 @@ class ConvStackExecutor:
                 written.add(nd.src)
                 continue
             ci = self.convs.index(nd)
-            g_out = self.grad[nd.out]  # = dL/dz of this conv (its epilogue's pre-activation)
-            self.conv_update(nd)  # weight gradient
-            if self.group is not None:
-                self._ev[ci].record()
-                self.comm_stream.wait_event(self._ev[ci])
+            g_out = self.grad[nd.out]  # = dL/dz of this conv (its epilogue's pre-activation), final here
+            if self.upd_stream is not None:
+                self._ev_gready[ci].record()
+                self.upd_stream.wait_event(self._ev_gready[ci])
+                with torch.cuda.stream(self.upd_stream):
+                    self.conv_update(nd)  # weight gradient
+                    if self.group is not None:
+                        self._ev[ci].record()
+                        self.comm_stream.wait_event(self._ev[ci])
+            else:
+                self.conv_update(nd)
+                if self.group is not None:
+                    self._ev[ci].record()
+                    self.comm_stream.wait_event(self._ev[ci])
             self.bucketer.ready(self._bucket_index[ci], self.comm_stream)
             # residual branch: a projection shares this dz (aliased buffer); an identity
             # shortcut's contribution is folded into the input-gradient epilogue below
@@ -335,6 +350,8 @@ class ConvStackExecutor:
             _check(self.lib.dconv_backward_data_ex(bp._h, C.byref(self.w[nd.name].to_c()), C.byref(g_out.to_c()),
                                                    C.byref(gi.to_c()), C.byref(ep), ws, self._stream()))
             written.add(nd.src)
+        if self.upd_stream is not None:
+            torch.cuda.current_stream().wait_stream(self.upd_stream)  # join: every dW final
 
     def sgd(self):
         self.bucketer.finish()
