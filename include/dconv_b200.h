@@ -205,6 +205,11 @@ int dconv_s2d_act(const dconv_act_t* x, const dconv_act_t* xs, int pad, dconv_st
 /* filter for that conv (inverse = 0: w -> w2) and its gradient back (inverse = 1:
  * w2 -> w, i.e. dW from the stride-1 conv's dW2); fp32 blocked weights */
 int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_stream_t stream);
+/* same backward with the ReLU mask of the pooled INPUT taken from the pooled
+ * OUTPUT (grad_out's geometry): at the argmax the input equals the window max,
+ * so "input > 0" == "output > 0" -- a quarter of the mask bytes */
+int dconv_maxpool_bwd_pooled_mask(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in,
+                                   const dconv_act_t* pooled, dconv_stream_t stream);
 /* w -= lr * g on fp32 blocked weights */
 int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t stream);
 

@@ -2154,6 +2154,31 @@ int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_s
   });
 }
 
+int dconv_maxpool_bwd_pooled_mask(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in,
+                                   const dconv_act_t* pooled, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(grad_out, "maxpool grad_out");
+    check_act(grad_in, "maxpool grad_in");
+    check_act(pooled, "maxpool pooled mask");
+    if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
+    if (pooled->n != grad_out->n || pooled->c != grad_out->c || pooled->h != grad_out->h ||
+        pooled->w != grad_out->w || pooled->dtype != grad_out->dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "maxpool: pooled mask must match grad_out");
+    const int planes = grad_in->n * cdiv(grad_in->c, 16);
+    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (grad_in->dtype == DCONV_F32)
+      maxpool_bwd_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
+                                                   (float*)grad_in->data, nullptr, planes, grad_in->h, grad_in->w,
+                                                   grad_out->h, grad_out->w, (const float*)pooled->data);
+    else
+      maxpool_bwd_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>(
+          (const __nv_bfloat16*)grad_out->data, (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data, nullptr,
+          planes, grad_in->h, grad_in->w, grad_out->h, grad_out->w, (const __nv_bfloat16*)pooled->data);
+    cuda_check(cudaGetLastError(), "maxpool_bwd");
+  });
+}
+
 int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t stream) {
   return guarded([&] {
     check_wt(w, "sgd weight");

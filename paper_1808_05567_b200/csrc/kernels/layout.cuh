@@ -330,9 +330,13 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ in, T* __restrict__ out
 // gather form of the max-pool backward (deterministic, no atomics): each input
 // pixel-block sums the output gradients of the <= 4 windows whose argmax it is
 template <typename T>
+// pmask (nullable, gout's geometry): the POOLED output as the ReLU mask. The
+// argmax element of a window holds the window's max, so "input > 0" at the
+// argmax equals "pooled output > 0": the same mask as `mask` at a quarter of
+// the bytes (the pooled tensor instead of the full-resolution activation).
 __global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __restrict__ arg,
                                    T* __restrict__ gin, const T* __restrict__ mask, int planes, int h, int w, int p,
-                                   int q) {
+                                   int q, const T* __restrict__ pmask = nullptr) {
   const long long total = static_cast<long long>(planes) * h * w;
   DCONV_GRID_STRIDE(e, total) {
     const int ix = static_cast<int>(e % w);
@@ -352,6 +356,13 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __
         const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w};
         const uint32_t code = static_cast<uint32_t>(dy * 3 + dx);
         ld16f(gout + o * 16, g);
+        if (pmask != nullptr) {
+          float pm[16];
+          ld16f(pmask + o * 16, pm);
+#pragma unroll
+          for (int l = 0; l < 16; ++l)
+            if (!(pm[l] > 0.0f)) g[l] = 0.0f;
+        }
 #pragma unroll
         for (int l = 0; l < 16; ++l)
           if (((aw[l / 4] >> (8 * (l % 4))) & 0xFFu) == code) acc[l] += g[l];

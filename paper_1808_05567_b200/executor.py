@@ -216,6 +216,15 @@ class ConvStackExecutor:
         self.dw = {nd.name: d.BlockedWeight(nd.K, nd.C, nd.R, nd.S, 16, torch.float32, self.dev,
                                             data=self.flat[self.slices[i]])
                    for i, nd in enumerate(self.convs)}
+        # master weights in one flat buffer laid out like the gradients: SGD is ONE launch
+        self.wflat = torch.empty_like(self.flat)
+        for i, nd in enumerate(self.convs):
+            self.wflat[self.slices[i]].copy_(self.w[nd.name].data.reshape(-1))
+            self.w[nd.name] = d.BlockedWeight(nd.K, nd.C, nd.R, nd.S, 16, torch.float32, self.dev,
+                                              data=self.wflat[self.slices[i]])
+        n256 = self.flat.numel() // 256  # every blocked weight is a whole number of 16x16 lane blocks
+        self._wflat_view = d.BlockedWeight(16, 16, 1, n256, 16, torch.float32, self.dev, data=self.wflat)
+        self._gflat_view = d.BlockedWeight(16, 16, 1, n256, 16, torch.float32, self.dev, data=self.flat)
         self.bucketer = GradBucketer(self.flat, [self.slices[i] for i in order], bucket_bytes, group)
         self._bucket_index = {i: k for k, i in enumerate(order)}
         # narrow stride-2 input convs (the 7x7/s2 stem, C=3) run as a stride-1 conv over a
@@ -308,10 +317,14 @@ class ConvStackExecutor:
         for idx in reversed(range(len(self.nodes))):
             nd = self.nodes[idx]
             if isinstance(nd, PoolNode):
-                gm = self.act[nd.src] if nd.src in self.relu_out else None
-                _check(self.lib.dconv_maxpool_bwd(C.byref(self.grad[nd.out].to_c()), self.argmax[nd.name].data_ptr(),
-                                                  C.byref(self.grad[nd.src].to_c()),
-                                                  gm.data.data_ptr() if gm is not None else None, self._stream()))
+                if nd.src in self.relu_out:  # ReLU mask of the pooled input, read off the pooled output
+                    _check(self.lib.dconv_maxpool_bwd_pooled_mask(
+                        C.byref(self.grad[nd.out].to_c()), self.argmax[nd.name].data_ptr(),
+                        C.byref(self.grad[nd.src].to_c()), C.byref(self.act[nd.out].to_c()), self._stream()))
+                else:
+                    _check(self.lib.dconv_maxpool_bwd(C.byref(self.grad[nd.out].to_c()),
+                                                      self.argmax[nd.name].data_ptr(),
+                                                      C.byref(self.grad[nd.src].to_c()), None, self._stream()))
                 written.add(nd.src)
                 continue
             ci = self.convs.index(nd)
@@ -359,9 +372,8 @@ class ConvStackExecutor:
             import torch.distributed as dist
 
             self.flat.div_(dist.get_world_size(self.group))
-        for nd in self.convs:
-            _check(self.lib.dconv_sgd(C.byref(self.w[nd.name].to_c()), C.byref(self.dw[nd.name].to_c()), self.lr,
-                                      self._stream()))
+        _check(self.lib.dconv_sgd(C.byref(self._wflat_view.to_c()), C.byref(self._gflat_view.to_c()), self.lr,
+                                  self._stream()))
 
     def step(self, dtop: d.BlockedActivation):
         self.forward()
@@ -381,8 +393,7 @@ class ConvStackExecutor:
                 n += 3  # input / filter space-to-depth, gradient back
             if nd.name in self.bplan:
                 n += self.bplan[nd.name].launches()
-            n += 1  # sgd
-        return n
+        return n + 1  # one SGD launch over the flat weights
 
 
 def _check(st):

@@ -385,6 +385,16 @@ def test_maxpool_3x3s2_matches_torch(dconv, orc, dtype):
     api._check(lib.dconv_maxpool_bwd(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()), xb.data.data_ptr(), 0))
     got_m = dconv.from_blocked_activation(gi).float()
     assert torch.equal(got_m, torch.where(x.float() > 0, got, torch.zeros_like(got)))
+    # the executor's variant reads the ReLU mask off the pooled OUTPUT (a quarter of the
+    # bytes): identical on a post-ReLU input (zeros and ties included)
+    xp = torch.relu(x.float()).to(dtype)
+    xpb = dconv.to_blocked_activation(xp.float(), 16, 0, 0, dtype=dtype)
+    api._check(lib.dconv_maxpool_fwd(C.byref(xpb.to_c()), C.byref(yb.to_c()), arg.data_ptr(), 0))
+    api._check(lib.dconv_maxpool_bwd(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()), xpb.data.data_ptr(), 0))
+    full = gi.data.clone()
+    api._check(lib.dconv_maxpool_bwd_pooled_mask(C.byref(gb.to_c()), arg.data_ptr(), C.byref(gi.to_c()),
+                                                 C.byref(yb.to_c()), 0))
+    assert torch.equal(gi.data, full)
 
 
 # ------------------------------------------------------------------ plan validation (validate_plan analog)
