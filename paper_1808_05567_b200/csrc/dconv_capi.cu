@@ -644,17 +644,17 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
 // weight prep: src blocked weights -> bf16 pieces in the phase-sorted tap order
 // (tapmap_dev is uploaded once at plan creation so execute calls are graph-capturable)
 void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int nb,
-                        int n_ntiles, int dual, int pieces, cudaStream_t stream) {
+                        int n_ntiles, int dual, int pieces, int nt_major, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(cb_in) * n_ntiles * n_taps * 2 * nb * 128;
   const int kbs = cdiv(w.k, 16), cbs = cdiv(w.c, 16);
   if (w.dtype == DCONV_F32)
     weight_prep_kernel<float><<<grid1d(total), 256, 0, stream>>>(
         reinterpret_cast<const float*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
-        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces);
+        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major);
   else
     weight_prep_kernel<__nv_bfloat16><<<grid1d(total), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
-        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces);
+        tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major);
   cuda_check(cudaGetLastError(), "weight_prep launch");
 }
 
@@ -1164,7 +1164,8 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
     pb.row_off = -s.pad_h;
     pb.col_off = -s.pad_w;
     FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
-    launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces, cs);
+    launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces,
+                       L.raw_f32 ? 0 : 1, cs);
     FwdParams& p = L.p;
     p.out = out->data;
     p.out_bf16 = out->dtype == DCONV_BF16;
@@ -1356,7 +1357,7 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
       pb.in = *grad_out;
       FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
       launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, L.p.nb, L.p.n_ntiles, 1,
-                         plan->pieces, cs);
+                         plan->pieces, L.raw_f32 ? 0 : 1, cs);
       tap_off += static_cast<int>(ph.tapmap.size());
       FwdParams& p = L.p;
       p.out = grad_in->data;

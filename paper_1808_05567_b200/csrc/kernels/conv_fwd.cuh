@@ -450,6 +450,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         for (int ks = 0; ks < kc_stages; ++ks) {
           const int cb0 = ks * p.kc, cb1 = min(p.cb_in, cb0 + p.kc);
           mbar_arrive_expect_tx(&w_full[ks], PIECES * (cb1 - cb0) * w_tap);
+          // (fp32-activation plans: prepared weights [piece][c_b][n_tile][..], see weight_prep_kernel)
           if (p.n_ntiles == 1) {  // the stage's blocks are contiguous per piece: one copy each
             for (int pc = 0; pc < PIECES; ++pc)
               bulk_load(dst + pc * L.w_piece + cb0 * w_tap,
@@ -492,13 +493,36 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             }
             mbar_arrive_expect_tx(&w_full[s], PIECES * kc_eff * w_bytes);
             uint8_t* dst = smem + L.w_off + s * L.w_slot;
-            // slot layout [piece][kk][tap]: piece stride w_piece = kc * w_taps taps
-            for (int kk = 0; kk < kc_eff; ++kk)
-              for (int pc = 0; pc < PIECES; ++pc)
-                bulk_load(dst + pc * L.w_piece + kk * w_bytes,
-                          wsrc + ((static_cast<long long>(pc) * p.cb_in + cb * p.kc + kk) * p.n_ntiles + ntile) * w_blk +
-                              static_cast<long long>(s_phase_tap0[ph] + t0) * w_tap,
-                          w_bytes, &w_full[s]);
+            // (bf16-activation plans: prepared weights [piece][n_tile][c_b][tap][..], see weight_prep_kernel)
+            // slot layout [piece][kk][tap]: piece stride w_piece = kc * w_taps taps. A stage
+            // holding every tap of its kc blocks is one contiguous run of the prepared
+            // weights: one bulk copy per piece (each copy costs the issuing thread ~240
+            // cycles -- four per stage paced the 1x1 layers)
+            // (fp32-activation kernels keep the [piece][c_b][n_tile] layout and per-block copies:
+            // their code, and timing, is left exactly as it was)
+            if constexpr (!RAW_F32) {
+              if (p.n_phases == 1 && nt == p.n_taps) {
+                for (int pc = 0; pc < PIECES; ++pc)
+                  bulk_load(dst + pc * L.w_piece,
+                            wsrc + ((static_cast<long long>(pc) * p.n_ntiles + ntile) * p.cb_in + cb * p.kc) * w_blk,
+                            static_cast<uint32_t>(kc_eff) * w_bytes, &w_full[s]);
+              } else {
+                for (int kk = 0; kk < kc_eff; ++kk)
+                  for (int pc = 0; pc < PIECES; ++pc)
+                    bulk_load(dst + pc * L.w_piece + kk * w_bytes,
+                              wsrc + ((static_cast<long long>(pc) * p.n_ntiles + ntile) * p.cb_in + cb * p.kc + kk) *
+                                         w_blk +
+                                  static_cast<long long>(s_phase_tap0[ph] + t0) * w_tap,
+                              w_bytes, &w_full[s]);
+              }
+            } else {
+              for (int kk = 0; kk < kc_eff; ++kk)
+                for (int pc = 0; pc < PIECES; ++pc)
+                  bulk_load(dst + pc * L.w_piece + kk * w_bytes,
+                            wsrc + ((static_cast<long long>(pc) * p.cb_in + cb * p.kc + kk) * p.n_ntiles + ntile) * w_blk +
+                                static_cast<long long>(s_phase_tap0[ph] + t0) * w_tap,
+                            w_bytes, &w_full[s]);
+            }
           }
         }
       }

@@ -169,7 +169,7 @@ __global__ void rehalo_kernel(const T* __restrict__ src, T* __restrict__ dst, in
 template <typename S>
 __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
                                    int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps, int cb_in,
-                                   int nb, int n_ntiles, int dual, int pieces) {
+                                   int nb, int n_ntiles, int dual, int pieces, int nt_major) {
   // the conv kernel launched after this one (programmatic dependent launch) may
   // start its prologue and activation loads now; it waits before reading weights
   pdl_launch_dependents();
@@ -182,8 +182,11 @@ __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __r
     q /= (2 * nb);
     const int t = static_cast<int>(q % n_taps);
     q /= n_taps;
-    const int nt = static_cast<int>(q % n_ntiles);
-    const int cbi = static_cast<int>(q / n_ntiles);
+    // nt_major: [piece][n_tile][c_b][tap][2nb][16][8] -- one n-tile's channel blocks are
+    // contiguous, so a streamed stage's kc blocks (all taps) are ONE bulk copy. Otherwise
+    // [piece][c_b][n_tile][tap][..] (the fp32-activation plans keep the original layout)
+    const int cbi = nt_major ? static_cast<int>(q % cb_in) : static_cast<int>(q / n_ntiles);
+    const int nt = nt_major ? static_cast<int>(q / cb_in) : static_cast<int>(q % n_ntiles);
     const int ob = nt * nb + ng / 2, ol = (ng % 2) * 8 + kk;  // out block / lane
     const int ib = cbi, il = ci;                    // in block / lane
     const int rs = tapmap[t];

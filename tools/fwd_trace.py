@@ -25,6 +25,17 @@ y = d.BlockedActivation(N, K, P_, P_, 16, 0, 0, torch.bfloat16)
 w = d.BlockedWeight(K, C, R, R)
 w.data.normal_()
 fp = d.make_forward_plan(spec, 1, None, None, d.Math.BF16)
+if os.environ.get("ADD"):  # the executor's fused residual-add + ReLU epilogue
+    from paper_1808_05567_b200._lib import Epilogue
+    res = d.BlockedActivation(N, K, P_, P_, 16, 0, 0, torch.bfloat16)
+    res.data.uniform_(-1, 1)
+    ep = Epilogue(res.data.data_ptr(), None, 1)
+    ws = fp._ws.get(lib.dconv_fwd_workspace_bytes(fp._h), torch.device("cuda"))
+
+    def _fwd(a, b, c):
+        d.api._check(lib.dconv_forward_ex(fp._h, Ct.byref(a.to_c()), Ct.byref(b.to_c()), Ct.byref(c.to_c()), Ct.byref(ep),
+                                      ws, torch.cuda.current_stream().cuda_stream))
+    fp.execute = _fwd
 print(fp.blocking)
 buf = torch.zeros(148 * 16 + 8 * 256 + 2 * 148 + 5 * 148, dtype=torch.int64, device="cuda")
 lib.dconv_debug_mode(int(os.environ.get("DBG", "0")))
