@@ -532,12 +532,8 @@ def run_stack(args):
     loss_pin = torch.zeros(1, dtype=torch.float32).pin_memory()
     stream = torch.cuda.current_stream()
 
-    import ctypes
-
-    from paper_1808_05567_b200 import api as dapi
-
     def pack_input():
-        dapi._check(lib.dconv_pack_act(x_dev.data_ptr(), 0, ctypes.byref(e.act["x"].to_c()), stream.cuda_stream))
+        e.load_input_nchw(x_dev)
 
     x_dev.copy_(x_pin)
     pack_input()
@@ -608,7 +604,7 @@ def run_stack(args):
     def e2e_step(i, last):
         b = i % 2
         stream.wait_event(copied[b])
-        dapi._check(lib.dconv_pack_act(x_bufs[b].data_ptr(), 0, ctypes.byref(e.act["x"].to_c()), stream.cuda_stream))
+        e.load_input_nchw(x_bufs[b])
         consumed[b].record(stream)
         if not last:
             issue_copy(i + 1)

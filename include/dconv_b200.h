@@ -202,6 +202,10 @@ int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dco
  * xs[n][i][j][(dy*2+dx)*C+c] = x[n][c][2i+dy-pad][2j+dx-pad], C <= 4 -> 4C
  * channels; the conv becomes stride 1 with a ceil(R/2) x ceil(S/2) filter */
 int dconv_s2d_act(const dconv_act_t* x, const dconv_act_t* xs, int pad, dconv_stream_t stream);
+/* the NCHW fp32 image (C <= 4) packed straight into that space-to-depth layout
+ * (input packing and dconv_s2d_act in one pass) */
+int dconv_pack_s2d(const float* nchw, int n, int c, int h, int w, const dconv_act_t* xs, int pad,
+                   dconv_stream_t stream);
 /* filter for that conv (inverse = 0: w -> w2) and its gradient back (inverse = 1:
  * w2 -> w, i.e. dW from the stride-1 conv's dW2); fp32 blocked weights */
 int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_stream_t stream);

@@ -60,7 +60,7 @@ EXPORTS = [
     "dconv_backward_data", "dconv_bwd_launches", "dconv_upd_plan_create", "dconv_upd_plan_destroy",
     "dconv_upd_splits", "dconv_upd_plan_describe", "dconv_upd_workspace_bytes", "dconv_weight_update",
     "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms", "dconv_forward_ex", "dconv_backward_data_ex",
-    "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_maxpool_bwd_pooled_mask", "dconv_sgd", "dconv_s2d_act", "dconv_s2d_wt", "dconv_host_step_create", "dconv_host_step_destroy",
+    "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_maxpool_bwd_pooled_mask", "dconv_sgd", "dconv_s2d_act", "dconv_s2d_wt", "dconv_pack_s2d", "dconv_host_step_create", "dconv_host_step_destroy",
     "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches", "dconv_fwd_plan_validate",
     "dconv_bwd_plan_validate", "dconv_upd_plan_validate",
 ]
@@ -119,6 +119,7 @@ def _bind(lib):
         "dconv_maxpool_bwd_pooled_mask": (i, [P(Act), vp, P(Act), P(Act), vp]),
         "dconv_s2d_act": (i, [P(Act), P(Act), i, vp]),
         "dconv_s2d_wt": (i, [P(Wt), P(Wt), i, vp]),
+        "dconv_pack_s2d": (i, [vp, i, i, i, i, P(Act), i, vp]),
         "dconv_host_step_create": (i, [P(Spec), i, i, P(vp)]),
         "dconv_host_step_destroy": (None, [vp]),
         "dconv_host_step_chunk": (i, [vp]),

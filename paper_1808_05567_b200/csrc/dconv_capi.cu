@@ -2136,6 +2136,33 @@ int dconv_s2d_act(const dconv_act_t* x, const dconv_act_t* xs, int pad, dconv_st
   });
 }
 
+int dconv_pack_s2d(const float* nchw, int n, int c, int h, int w, const dconv_act_t* xs, int pad,
+                   dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(xs, "pack_s2d output");
+    if (!nchw) fail(DCONV_ERR_INVALID_ARGUMENT, "pack_s2d: null source");
+    if (c < 1 || c > 4 || xs->vlen != 16 || xs->c != 4 * c || xs->halo_h || xs->halo_w || xs->n != n)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "pack_s2d: NCHW C <= 4 -> halo-0 vlen-16 tensor of 4C channels");
+    const int g = grid1d(static_cast<int64_t>(n) * xs->h * xs->w);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    auto go = [&](auto c_tag) {
+      constexpr int Cc = decltype(c_tag)::value;
+      if (xs->dtype == DCONV_F32)
+        pack_s2d_kernel<float, Cc><<<g, 256, 0, cs>>>(nchw, (float*)xs->data, n, h, w, xs->h, xs->w, pad);
+      else
+        pack_s2d_kernel<__nv_bfloat16, Cc><<<g, 256, 0, cs>>>(nchw, (__nv_bfloat16*)xs->data, n, h, w, xs->h, xs->w,
+                                                              pad);
+    };
+    switch (c) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 3: go(std::integral_constant<int, 3>{}); break;
+      default: go(std::integral_constant<int, 4>{}); break;
+    }
+    cuda_check(cudaGetLastError(), "pack_s2d");
+  });
+}
+
 int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_stream_t stream) {
   return guarded([&] {
     check_wt(w, "s2d weight");

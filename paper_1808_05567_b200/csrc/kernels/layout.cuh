@@ -413,6 +413,34 @@ __global__ void s2d_act_kernel(const T* __restrict__ x, T* __restrict__ xs, int 
   }
 }
 
+// NCHW fp32 image straight into the space-to-depth blocked layout (the input pack
+// and dconv_s2d_act in one pass: no 16-lane full-resolution intermediate)
+template <typename T, int C>
+__global__ void pack_s2d_kernel(const float* __restrict__ x, T* __restrict__ xs, int n, int h, int w, int hs, int ws,
+                                int pad) {
+  const long long total = static_cast<long long>(n) * hs * ws;
+  DCONV_GRID_STRIDE(e, total) {
+    const int j = static_cast<int>(e % ws);
+    const long long r = e / ws;
+    const int i = static_cast<int>(r % hs);
+    const long long img = r / hs;
+    T v[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) v[l] = from_f<T>(0.0f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int y = 2 * i + q / 2 - pad, xx = 2 * j + q % 2 - pad;
+      if (y < 0 || y >= h || xx < 0 || xx >= w) continue;
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) v[q * C + ch] = from_f<T>(x[((img * C + ch) * h + y) * w + xx]);
+    }
+    uint4* o = reinterpret_cast<uint4*>(xs + e * 16);
+    const uint4* vv = reinterpret_cast<const uint4*>(v);
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(16 * sizeof(T) / 16); ++k) o[k] = vv[k];
+  }
+}
+
 // W[k][c][r][s] (blocked, one c-block) -> W'[k][(dy*2+dx)*C + c][r'][s'] =
 // W[k][c][2r'+dy][2s'+dx] (zero past R / S); inverse = s2d_wt_grad_kernel
 __global__ void s2d_wt_kernel(const float* __restrict__ w, float* __restrict__ w2, int kb, int c, int R, int S,

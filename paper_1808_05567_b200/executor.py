@@ -246,6 +246,7 @@ class ConvStackExecutor:
                     "dw": d.BlockedWeight(nd.K, 4 * nd.C, r2, s2, 16, torch.float32, self.dev),
                 }
         # plans
+        self.input_s2d = False  # set by load_input_nchw: the stem's s2d input is packed directly
         self.pspec = {n: (self.s2d[n]["spec"] if n in self.s2d else s) for n, s in self.specs.items()}
         self.fplan = {n: d.ExecutionPlan(s, None, None, self.math, 0, 0) for n, s in self.pspec.items()}
         self.bplan = {n: d.BackwardContext(s, None, 1, None, self.math) for n, s in self.specs.items()
@@ -287,11 +288,26 @@ class ConvStackExecutor:
         src, wt = self.act[nd.src], self.w[nd.name]
         if nd.name in self.s2d:
             sd = self.s2d[nd.name]
-            _check(self.lib.dconv_s2d_act(C.byref(src.to_c()), C.byref(sd["x"].to_c()), nd.pad, self._stream()))
+            if not (nd.src == "x" and self.input_s2d):  # load_input_nchw packed it already
+                _check(self.lib.dconv_s2d_act(C.byref(src.to_c()), C.byref(sd["x"].to_c()), nd.pad, self._stream()))
             _check(self.lib.dconv_s2d_wt(C.byref(wt.to_c()), C.byref(sd["w"].to_c()), 0, self._stream()))
             src, wt = sd["x"], sd["w"]
         _check(self.lib.dconv_forward_ex(plan._h, C.byref(src.to_c()), C.byref(wt.to_c()),
                                          C.byref(self.act[nd.out].to_c()), C.byref(ep), ws, self._stream()))
+
+    def load_input_nchw(self, nchw: torch.Tensor):
+        """Pack this step's images (N, 3, H, W fp32 on the device) into the executor's
+        input: straight into the stem's space-to-depth layout when the stem runs that
+        way (one pass, no full-resolution 16-lane copy), else the blocked tensor 'x'.
+        Steps after this skip the stem's own space-to-depth."""
+        stem = next((nd for nd in self.convs if nd.src == "x"), None)
+        if stem is not None and stem.name in self.s2d:
+            n, c, h, w = nchw.shape
+            _check(self.lib.dconv_pack_s2d(nchw.data_ptr(), n, c, h, w, C.byref(self.s2d[stem.name]["x"].to_c()),
+                                           stem.pad, self._stream()))
+            self.input_s2d = True
+        else:
+            _check(self.lib.dconv_pack_act(nchw.data_ptr(), 0, C.byref(self.act["x"].to_c()), self._stream()))
 
     def conv_update(self, nd: ConvNode):
         up = self.uplan[nd.name]

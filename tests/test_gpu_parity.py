@@ -586,3 +586,24 @@ def test_space_to_depth_stem_matches_direct_conv(dconv, orc, math):
     dw = dconv.BlockedWeight(K, Cn, R, R)
     assert lib.dconv_s2d_wt(C.byref(dw.to_c()), C.byref(dw2.to_c()), 1, st_) == 0
     gate(orc, orc.conv_update(s, x, g), dconv.from_blocked_weight(dw).cpu().numpy(), M)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_pack_s2d_equals_pack_then_s2d(dconv, orc, dtype):
+    """dconv_pack_s2d (NCHW image straight into the space-to-depth layout) is bitwise
+    the blocked pack followed by dconv_s2d_act."""
+    import ctypes as C
+
+    from paper_1808_05567_b200 import _lib
+
+    lib = _lib.lib()
+    N, Cn, H, pad, P = 2, 3, 37, 3, 19
+    hs = P + 3
+    x = torch.from_numpy(orc.uniform(31, (N, Cn, H, H))).cuda()
+    xb = dconv.to_blocked_activation(x, 16, 0, 0, dtype=dtype)
+    a = dconv.BlockedActivation(N, 4 * Cn, hs, hs, 16, 0, 0, dtype)
+    b = dconv.BlockedActivation(N, 4 * Cn, hs, hs, 16, 0, 0, dtype)
+    assert lib.dconv_s2d_act(C.byref(xb.to_c()), C.byref(a.to_c()), pad, 0) == 0
+    assert lib.dconv_pack_s2d(x.data_ptr(), N, Cn, H, H, C.byref(b.to_c()), pad, 0) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(a.data, b.data)
