@@ -1420,7 +1420,7 @@ struct UpdLaunch {
 // k-tile width, tap groups bounded by TMEM, split factor for >= 2 waves.
 UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_act_t& dout, bool encode_maps,
                    const void* in_pieces, const void* do_pieces, float* partial, int force_nb = 0,
-                   int force_unstack = -1) {
+                   int force_unstack = -1, int force_mc = 1) {
   // bf16 operands read in place: pick the k-tile width and (for < 8 channel blocks)
   // tap stacking vs plain shifted-descriptor taps by the modelled time -- the TMA
   // row rate (27 B/clk/SM for 32 B rows) against the MMA time of each choice
@@ -1432,23 +1432,28 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     // (un-stacked narrow multi-tap plans -- M rows past C idle, every tap through a shifted
     // descriptor -- are modelled well but measured slower on the C=64 3x3 layer: opt-in)
     const bool narrow_taps = cb0 < 8 && pl.spec.R * pl.spec.S > 1 && pl.spec.C > 8 && getenv("DCONV_UPD_UNSTACK");
+    // single-tap layers with >= 2 c-tiles: a CTA may also take two c-tiles (two
+    // accumulators), staging each dO tile once for both
+    const bool mc_ok = pl.spec.R * pl.spec.S == 1 && cb0 % 16 == 0 && !getenv("DCONV_UPD_NO_MC");
     double best = 1e30;
-    int b_nb = nb_def, b_un = 0;
+    int b_nb = nb_def, b_un = 0, b_mc = 1;
     for (int un = 0; un <= (narrow_taps ? 1 : 0); ++un)
-      for (int div : {1, 2, 4}) {
-        const int nbv = nb_def / div;
-        if (nbv < 1 || (div > 1 && nb_def % div)) continue;
-        try {
-          const UpdLaunch t = plan_upd(pl, in, dout, false, nullptr, nullptr, nullptr, nbv, un);
-          if (t.est_cycles > 0 && t.est_cycles < best * 0.97) {
-            best = t.est_cycles;
-            b_nb = nbv;
-            b_un = un;
+      for (int mcv = 1; mcv <= (mc_ok ? 2 : 1); ++mcv)
+        for (int div : {1, 2, 4}) {
+          const int nbv = nb_def / div;
+          if (nbv < 1 || (div > 1 && nb_def % div) || mcv * 16 * nbv > 512) continue;
+          try {
+            const UpdLaunch t = plan_upd(pl, in, dout, false, nullptr, nullptr, nullptr, nbv, un, mcv);
+            if (t.est_cycles > 0 && t.est_cycles < best * 0.97) {
+              best = t.est_cycles;
+              b_nb = nbv;
+              b_un = un;
+              b_mc = mcv;
+            }
+          } catch (...) {
           }
-        } catch (...) {
         }
-      }
-    return plan_upd(pl, in, dout, encode_maps, in_pieces, do_pieces, partial, b_nb, b_un);
+    return plan_upd(pl, in, dout, encode_maps, in_pieces, do_pieces, partial, b_nb, b_un, b_mc);
   }
   UpdLaunch L;
   std::memset(&L.p, 0, sizeof(L.p));
@@ -1494,6 +1499,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   const int NT = 16 * p.nb;
   const int n_ktiles = cdiv(kb, p.nb);
   const int n_ctiles = cdiv(cb, 8);
+  // c-tiles per CTA (see the selector above); only the bf16 SW32 single-tap kernel path
+  const int mc = (force_mc == 2 && bf16_ops && !stacked && taps.r.size() == 1 && cb % 16 == 0 && !p.half &&
+                  !getenv("DCONV_UPD_NO_SW32")) ? 2 : 1;
+  p.mc = mc;
   // geometry and pipeline depth
   const int maxshift_rows = taps.r2max, s2max = taps.s2max;
   // Candidate (virtual pitch, band) geometries in preference order. A single
@@ -1509,7 +1518,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     if (linear && vs > 256) return;
     for (int passes : {1, 3}) {
       if (passes == 3 && pieces == 1) continue;
-      const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, p.nb, pieces, pieces)
+      const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, p.nb, pieces, pieces, mc)
                                        : upd_stage_layout(a_px, vs, p.nb, 1, 3);
       const int stg = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
       if (stg >= 2) cands.push_back({wsub, rows_ps, in_rows, vs, a_px, stg, passes, lay});
@@ -1555,11 +1564,11 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     double cyc = 0;
     for (int g : groups) {
       const double a_bytes = stacked ? static_cast<double>(g) * (p.half ? 1 : 2 * p.cb_eff) * cd.lay.a_plane
-                                     : 2.0 * p.cb_eff * cd.lay.a_plane;
-      const double mma = (stacked ? 1 : g) * (cd.vs / 16.0) * mma_unit;
+                                     : 2.0 * p.cb_eff * mc * cd.lay.a_plane;
+      const double mma = (stacked ? 1 : g * mc) * (cd.vs / 16.0) * mma_unit;
       cyc += std::max((a_bytes + b_bytes) / 27.0, mma) + 300.0;
     }
-    return cyc * n_ctiles * n_ktiles * spi * s.N / sm_count();
+    return cyc * (n_ctiles / mc) * n_ktiles * spi * s.N / sm_count();
   };
   if (bf16_ops) {
     double bc = 1e30;
@@ -1692,10 +1701,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   // trade-off of partial-copy traffic against parallelism, for 148 SMs):
   // minimise max(MMA time over the busy SMs, HBM time of operands + partials
   // written and re-read by the reduce); one CTA per SM (smem-bound)
-  const int tiles = n_ctiles * p.n_tgroups * n_ktiles;
+  const int tiles = (n_ctiles / mc) * p.n_tgroups * n_ktiles;
   const int sms = sm_count();
   const double op_bytes = (in.dtype == DCONV_BF16 ? 2.0 : 4.0) * (static_cast<double>(act_elems(in)) +
-                                                                  static_cast<double>(act_elems(dout)) * n_ctiles);
+                                                                  static_cast<double>(act_elems(dout)) * (n_ctiles / mc));
   const double dw_part = 4.0 * p.n_taps * (n_ctiles * 128.0) * (n_ktiles * NT);
   const double mma_flops = 2.0 * (n_ctiles * 128.0) * (n_ktiles * NT) * p.n_taps * static_cast<double>(p.stages_total) *
                            p.vs * (pieces == 3 ? 6.0 : 1.0);
@@ -1721,7 +1730,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   p.c_pad = n_ctiles * 128;
   p.k_pad = n_ktiles * NT;
   p.partial = partial;
-  L.grid = dim3(static_cast<unsigned>(n_ctiles * p.n_tgroups), static_cast<unsigned>(n_ktiles),
+  L.grid = dim3(static_cast<unsigned>((n_ctiles / mc) * p.n_tgroups), static_cast<unsigned>(n_ktiles),
                 static_cast<unsigned>(splits));
   L.stages = stages;
   L.smem = static_cast<size_t>(stages) * layout.bytes;
@@ -1743,7 +1752,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       if (linear) {
         const uint64_t dims[3] = {16, static_cast<uint64_t>(a.h) * a.w, planes};
         const uint64_t strides[2] = {32, static_cast<uint64_t>(a.h) * a.w * 32};
-        const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs), static_cast<uint32_t>(is_in ? p.cb_eff : p.nb)};
+        const uint32_t box[3] = {16, static_cast<uint32_t>(p.vs),
+                                 static_cast<uint32_t>(is_in ? p.cb_eff * p.mc : p.nb)};
         return encode(1, 3, data, dims, strides, box, nullptr, is_in ? "upd input linear sw32" : "upd dO linear sw32",
                       swz);
       }
@@ -1752,7 +1762,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       const uint64_t strides3[3] = {32, static_cast<uint64_t>(wp) * 32, static_cast<uint64_t>(wp) * hp * 32};
       if (is_in) {
         const uint32_t box[4] = {16, static_cast<uint32_t>(p.wsub * st), static_cast<uint32_t>(p.in_rows * st),
-                                 static_cast<uint32_t>(p.cb_eff)};
+                                 static_cast<uint32_t>(p.cb_eff * p.mc)};
         const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
         return encode(1, 4, base, dims, strides3, box, estr, "upd input rows sw32", swz);
       }
@@ -1813,7 +1823,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   // layer (per-chunk address arithmetic on six warps, and the loaders share the
   // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
   // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
-  p.lsu = (p.sw32 && L.stages > kUpdLsuDepth && getenv("DCONV_UPD_LSU")) ? 1 : 0;
+  p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && getenv("DCONV_UPD_LSU")) ? 1 : 0;
   if (p.lsu) {
     const int ihp = in.h + 2 * in.halo_h, iwp = in.w + 2 * in.halo_w;
     const int dhp = dout.h + 2 * dout.halo_h, dwp = dout.w + 2 * dout.halo_w;

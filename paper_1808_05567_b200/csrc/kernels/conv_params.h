@@ -104,6 +104,7 @@ struct UpdParams {
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
   int sw32;                // bf16 operands staged as SWIZZLE_32B 32 B pixel rows (MN-major SW32 descriptors)
+  int mc;                  // single-tap sw32 plans: 128-channel c-tiles per CTA (2: the dO tile is staged once for both)
   // lsu = 1: the operand rows are staged by cp.async from loader warps (the TMA
   // unit moves 32 B rows at ~27 B/clk/SM; 16 B cp.async from six warps ~2x that)
   int lsu;

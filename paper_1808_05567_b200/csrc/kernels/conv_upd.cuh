@@ -32,11 +32,11 @@ struct UpdStage {
   uint32_t b_off, bytes;
 };
 
-__host__ __device__ inline UpdStage upd_stage_layout(int a_px, int vs, int nb, int pa, int pb) {
+__host__ __device__ inline UpdStage upd_stage_layout(int a_px, int vs, int nb, int pa, int pb, int mc = 1) {
   UpdStage L;
   L.a_plane = static_cast<uint32_t>(a_px) * 16u;
   L.b_plane = static_cast<uint32_t>(vs) * 16u;
-  L.a_piece = 16u * L.a_plane;
+  L.a_piece = 16u * static_cast<uint32_t>(mc) * L.a_plane;  // mc c-tiles of 8 channel blocks
   L.b_piece = 2u * nb * L.b_plane;
   L.b_off = static_cast<uint32_t>(pa) * L.a_piece;
   L.bytes = (L.b_off + static_cast<uint32_t>(pb) * L.b_piece + 1023u) & ~1023u;
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 2)
     for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
   const int NT = 16 * p.nb;
-  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB);
+  const int mc = p.mc > 1 ? p.mc : 1;
+  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB, mc);
   const uint32_t smem0 = smem_u32(smem);
 
   // CTA coordinates: x = c-tile * n_tgroups + tap group, y = k-tile, z = split
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int ntaps = p.tg_ntaps[tgrp];
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(p.tg * NT)) tmem_cols <<= 1;
+  while (tmem_cols < static_cast<uint32_t>(max(p.tg, mc) * NT)) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_in);
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int band = stage % p.stages_per_img;
         uint8_t* st = smem + static_cast<uint32_t>(s) * L.bytes;
         const uint32_t a_bytes = p.stack > 1 ? static_cast<uint32_t>(ntaps * (p.half ? 1 : 2 * p.cb_eff)) * L.a_plane
-                                 : p.sw32     ? static_cast<uint32_t>(2 * p.cb_eff) * L.a_plane
+                                 : p.sw32     ? static_cast<uint32_t>(2 * p.cb_eff * mc) * L.a_plane
                                               : L.a_piece;
         mbar_arrive_expect_tx(&full_bar[s], PA * a_bytes + PB * L.b_piece);
         for (int pc = 0; pc < PA; ++pc) {
-          const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8;
+          const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8 * mc;
           uint8_t* a_dst = st + pc * L.a_piece;
           if (p.sw32) {  // 32 B pixel rows: {16, px[, rows], planes} boxes
             if (p.stack > 1) {
@@ -256,18 +257,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && PA == 1 && PB == 1 && p.sw32 && (p.stack > 1 ? 1 : ntaps) <= kFastTaps) {
+  } else if (warp == 1 && PA == 1 && PB == 1 && p.sw32 && (p.stack > 1 ? 1 : max(ntaps, mc)) <= kFastTaps) {
     // ------------------------------------------------------------ MMA issuer (bf16 SW32), one lane
     // shifts and descriptor words hoisted out of the stage loop; between stages
     // only the commit and the full-barrier wait (see conv_fwd_kernel)
     if (lane == 0) {
       const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
       const int ksteps = p.vs / 16;
-      const int n_acc = p.stack > 1 ? 1 : ntaps;
+      // accumulators: one per tap of the group, or (single-tap, mc > 1) one per c-tile,
+      // whose A rows are the next 8 channel-block planes (a_piece / mc bytes on)
+      const int n_acc = p.stack > 1 ? 1 : (mc > 1 ? mc : ntaps);
       uint32_t sh[kFastTaps];
 #pragma unroll
       for (int i = 0; i < kFastTaps; ++i)
-        sh[i] = (i < n_acc && p.stack == 1) ? 2u * static_cast<uint32_t>(s_tap_shift[tap0 + i]) : 0u;
+        sh[i] = (i < n_acc && p.stack == 1)
+                    ? (mc > 1 ? static_cast<uint32_t>(i) * ((L.a_piece / mc) >> 4)
+                              : 2u * static_cast<uint32_t>(s_tap_shift[tap0 + i]))
+                    : 0u;
       const uint64_t a_d = make_smem_desc_mn_sw32(smem0, 2 * L.a_plane);
       const uint64_t b_d = make_smem_desc_mn_sw32(smem0 + L.b_off, 2 * L.b_plane);
       const uint32_t a_hi = static_cast<uint32_t>(a_d >> 32), b_hi = static_cast<uint32_t>(b_d >> 32);
@@ -336,19 +342,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp >= 4) {
     // ---------------------------------------------------------- epilogue (lsu plans: after loading)
     const int qrow = (warp % 4) * 32;
-    const int c_glob = ctile * 128 + qrow + lane;
     if (iters > 0) {
       mbar_wait(&accum_bar, 0);
       tc_fence_after();
     }
-    const int n_acc = p.stack > 1 ? 1 : ntaps;
+    const int n_acc = p.stack > 1 ? 1 : (mc > 1 ? mc : ntaps);
     for (int t = 0; t < n_acc; ++t) {
+      const int c_glob = (ctile * mc + (mc > 1 ? t : 0)) * 128 + qrow + lane;
       // stacked: TMEM row = (slot j, channel c) of tap tap0 + j
       const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
       const int slot = p.stack > 1 ? (qrow + lane) / rows_slot : 0;
       const int c_row = p.stack > 1 ? (qrow + lane) % rows_slot : c_glob;
       const bool row_ok = p.stack > 1 ? slot < ntaps : true;
-      const int rs = p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : t)];
+      const int rs = p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : (mc > 1 ? 0 : t))];
       float* dst_row =
           p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
       for (int g = 0; g < p.nb; ++g) {

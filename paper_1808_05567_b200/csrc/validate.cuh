@@ -230,7 +230,9 @@ int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const 
     const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
     const UpdParams& p = L.p;
     VReport r;
-    const int n_ctiles = static_cast<int>(L.grid.x) / p.n_tgroups, n_ktiles = static_cast<int>(L.grid.y);
+    // a CTA covers p.mc consecutive 128-channel c-tiles
+    const int n_ctiles = static_cast<int>(L.grid.x) / p.n_tgroups * (p.mc > 1 ? p.mc : 1),
+              n_ktiles = static_cast<int>(L.grid.y);
     r.tiles = static_cast<long long>(L.grid.x) * L.grid.y * L.grid.z;
     // split ranges partition [0, stages_total) exactly once
     std::vector<uint8_t> st(static_cast<size_t>(p.stages_total), 0);
