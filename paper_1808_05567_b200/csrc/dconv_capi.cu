@@ -21,6 +21,10 @@
 using namespace dconv_sm100;
 
 namespace {
+// Debug / experiment overrides (DCONV_*) are read once per process, not per
+// plan or execute call: each call site caches its own lookup.
+#define DCONV_ENV(name) ([]() -> const char* { static const char* v_ = std::getenv(name); return v_; }())
+
 
 thread_local std::string g_err;
 
@@ -295,9 +299,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
 
   FwdTile tile;
   const int kb_total = pb.kb_out;
-  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : getenv("DCONV_FWD_MB") ? atoi(getenv("DCONV_FWD_MB")) : 0;
+  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : DCONV_ENV("DCONV_FWD_MB") ? atoi(DCONV_ENV("DCONV_FWD_MB")) : 0;
   const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16)
-                     : getenv("DCONV_FWD_NB") ? std::min(atoi(getenv("DCONV_FWD_NB")), 16) : 0;
+                     : DCONV_ENV("DCONV_FWD_NB") ? std::min(atoi(DCONV_ENV("DCONV_FWD_NB")), 16) : 0;
   int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0, w_st = 0, acc_bufs = 2;
   bool w_all = false;
   FwdSmem layout;
@@ -337,7 +341,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           const int grid_est = std::min(m_tiles * n_nt_tiles, sm_count());
           const int res_bytes = pb.cb_red * pieces * nb * 512;
           const bool resident = grid_est % n_nt_tiles == 0 && res_bytes <= 120 * 1024 &&
-                                cdiv(pb.cb_red, kcx) <= kMaxStages && !getenv("DCONV_NO_RESIDENT");
+                                cdiv(pb.cb_red, kcx) <= kMaxStages && !DCONV_ENV("DCONV_NO_RESIDENT");
           const FwdSmem lay = fwd_smem_layout(apx_rows * kcx, resident ? pb.cb_red : kcx, nb, pieces, true, 0, 1);
           int wss = resident ? 1
                              : std::max(2, std::min<int>(kMaxStages, (kFwdBudget / 4) / static_cast<int>(lay.w_slot)));
@@ -398,7 +402,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         // phase) in one stage for nb <= 16 -- fewer per-stage barriers and MMA-issue
         // restarts; measured 1.2-1.5x on the 3x3 bf16 layers)
         int wt = taps.taps_box;
-        const int w_cap = getenv("DCONV_WCAP") ? atoi(getenv("DCONV_WCAP")) * 1024 : (raw_f32 ? 32 : 80) * 1024;
+        const int w_cap = DCONV_ENV("DCONV_WCAP") ? atoi(DCONV_ENV("DCONV_WCAP")) * 1024 : (raw_f32 ? 32 : 80) * 1024;
         while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > w_cap)
           wt = (wt + 1) / 2;
         const FwdSmem lay = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1);
@@ -418,9 +422,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         } else {
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
-          int kcx = (taps.r.size() == 1) ? std::min(getenv("DCONV_FWD_KC") ? atoi(getenv("DCONV_FWD_KC")) : 4, pb.cb_red) : 1;
+          int kcx = (taps.r.size() == 1) ? std::min(DCONV_ENV("DCONV_FWD_KC") ? atoi(DCONV_ENV("DCONV_FWD_KC")) : 4, pb.cb_red) : 1;
           // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
-          const int stg_res = (taps.r.size() == 1 || getenv("DCONV_STG_RES")) ? 3 * 16384 : 0;
+          const int stg_res = (taps.r.size() == 1 || DCONV_ENV("DCONV_STG_RES")) ? 3 * 16384 : 0;
           pcs = 0;
           for (; kcx >= 1; kcx = kcx > 1 ? kcx / 2 : 0) {
             const FwdSmem lk = fwd_smem_layout(apx * kcx, wt * kcx, nb, pieces, raw_f32, 1, 1);
@@ -458,7 +462,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
               break;
             }
           }
-          if (const char* e = getenv("DCONV_WST")) {  // debug: weight-ring depth sweep
+          if (const char* e = DCONV_ENV("DCONV_WST")) {  // debug: weight-ring depth sweep
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
             wss = atoi(e);
             pcs = std::min<int>(kMaxStages, (kFwdBudget - stg_res - wss * static_cast<int>(lk.w_slot)) /
@@ -470,7 +474,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // when all the stages' weights fit, each gets its own slot, loaded once per CTA
           // (the stem, the 56x56 3x3 and 1x1 layers re-streamed them for every tile)
           w_all = false;
-          if (nb >= kb_total && taps.n_phases == 1 && wt == taps.taps_box && !getenv("DCONV_NO_WALL")) {
+          if (nb >= kb_total && taps.n_phases == 1 && wt == taps.taps_box && !DCONV_ENV("DCONV_NO_WALL")) {
             const int kst = cdiv(pb.cb_red, kc);
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
             const int w_bytes = kst * static_cast<int>(lk.w_slot);
@@ -582,8 +586,8 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
   // smem-staged plans run three groups
   // TS plans with one stage per tile: a second epilogue group (the stores dominate)
   const int kiters = cdiv(p.cb_in, p.kc) * p.n_phases;
-  p.ts_epi2 = (L.ts && kiters == 1 && p.nb >= 4 && !getenv("DCONV_NO_TS_EPI2")) ? 1 : 0;
-  p.epi_groups = getenv("DCONV_EPI_GROUPS") ? atoi(getenv("DCONV_EPI_GROUPS")) : 3;
+  p.ts_epi2 = (L.ts && kiters == 1 && p.nb >= 4 && !DCONV_ENV("DCONV_NO_TS_EPI2")) ? 1 : 0;
+  p.epi_groups = DCONV_ENV("DCONV_EPI_GROUPS") ? atoi(DCONV_ENV("DCONV_EPI_GROUPS")) : 3;
   auto staging_bytes = [&] {
     return static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : p.ts_epi2 ? 2 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
   };
@@ -1434,16 +1438,16 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   // tap stacking vs plain shifted-descriptor taps by the modelled time -- the TMA
   // row rate (27 B/clk/SM for 32 B rows) against the MMA time of each choice
   const bool bf16_ops = in.dtype == DCONV_BF16 && dout.dtype == DCONV_BF16 && pl.pieces == 1 &&
-                        !getenv("DCONV_UPD_NO_MODEL");
+                        !DCONV_ENV("DCONV_UPD_NO_MODEL");
   if (bf16_ops && force_unstack < 0 && !(pl.has_cfg && pl.cfg.tile_nb > 0)) {
     const int kb0 = cdiv(pl.spec.K, 16), cb0 = cdiv(pl.spec.C, 16);
     const int nb_def = cdiv(kb0, cdiv(kb0, 16));
     // (un-stacked narrow multi-tap plans -- M rows past C idle, every tap through a shifted
     // descriptor -- are modelled well but measured slower on the C=64 3x3 layer: opt-in)
-    const bool narrow_taps = cb0 < 8 && pl.spec.R * pl.spec.S > 1 && pl.spec.C > 8 && getenv("DCONV_UPD_UNSTACK");
+    const bool narrow_taps = cb0 < 8 && pl.spec.R * pl.spec.S > 1 && pl.spec.C > 8 && DCONV_ENV("DCONV_UPD_UNSTACK");
     // single-tap layers with >= 2 c-tiles: a CTA may also take two c-tiles (two
     // accumulators), staging each dO tile once for both
-    const bool mc_ok = pl.spec.R * pl.spec.S == 1 && cb0 % 16 == 0 && !getenv("DCONV_UPD_NO_MC");
+    const bool mc_ok = pl.spec.R * pl.spec.S == 1 && cb0 % 16 == 0 && !DCONV_ENV("DCONV_UPD_NO_MC");
     double best = 1e30;
     int b_nb = nb_def, b_un = 0, b_mc = 1;
     for (int un = 0; un <= (narrow_taps ? 1 : 0); ++un)
@@ -1499,7 +1503,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   p.stack = stacked ? (p.half ? 16 : 8 / cb) : 1;
   // bf16 in place: a c-tile of a narrow layer loads only its cb planes (the MMA's
   // rows past them read stale shared memory; those dW rows are never reduced)
-  p.cb_eff = stacked ? cb : ((bf16_ops && !p.half && !getenv("DCONV_UPD_NO_SW32")) ? std::min(8, cb) : 8);
+  p.cb_eff = stacked ? cb : ((bf16_ops && !p.half && !DCONV_ENV("DCONV_UPD_NO_SW32")) ? std::min(8, cb) : 8);
   // k tile
   int n_kt = cdiv(kb, 16);
   p.nb = cdiv(kb, n_kt);
@@ -1510,7 +1514,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   const int n_ctiles = cdiv(cb, 8);
   // c-tiles per CTA (see the selector above); only the bf16 SW32 single-tap kernel path
   const int mc = (force_mc == 2 && bf16_ops && !stacked && taps.r.size() == 1 && cb % 16 == 0 && !p.half &&
-                  !getenv("DCONV_UPD_NO_SW32")) ? 2 : 1;
+                  !DCONV_ENV("DCONV_UPD_NO_SW32")) ? 2 : 1;
   p.mc = mc;
   // geometry and pipeline depth
   const int maxshift_rows = taps.r2max, s2max = taps.s2max;
@@ -1631,7 +1635,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   }
   // single-tap layers: A (activations) converted straight into a TMEM ring, so only
   // the raw boxes and the dO pieces occupy shared memory
-  const char* tsa_env = getenv("DCONV_UPD_TSA");
+  const char* tsa_env = std::getenv("DCONV_UPD_TSA");  // live: tests toggle it per plan
   if (want_raw && !stacked && taps.r.size() == 1 && !(tsa_env && tsa_env[0] == '0')) {
     const int acc_w = (pieces == 3 && 3 * NT <= 256) ? 3 * NT : NT;
     const int want_vs = tsa_env ? std::atoi(tsa_env) : 0;  // > 1: force the stage band (experiments)
@@ -1826,13 +1830,13 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     L.map_do = raw_map(dout, false);
     return L;
   }
-  p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !getenv("DCONV_UPD_NO_SW32")) ? 1 : 0;
+  p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !DCONV_ENV("DCONV_UPD_NO_SW32")) ? 1 : 0;
   // cp.async loader warps in place of the TMA box loads: opt-in experiment only
   // (DCONV_UPD_LSU=1). Measured 2-5x SLOWER than the TMA boxes on every ResNet-50
   // layer (per-chunk address arithmetic on six warps, and the loaders share the
   // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
   // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
-  p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && getenv("DCONV_UPD_LSU")) ? 1 : 0;
+  p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && DCONV_ENV("DCONV_UPD_LSU")) ? 1 : 0;
   if (p.lsu) {
     const int ihp = in.h + 2 * in.halo_h, iwp = in.w + 2 * in.halo_w;
     const int dhp = dout.h + 2 * dout.halo_h, dwp = dout.w + 2 * dout.halo_w;
