@@ -12,6 +12,9 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
+#include <mutex>
+#include <array>
 
 #include "../../include/dconv_b200.h"
 #include "kernels/conv_fwd.cuh"
@@ -749,6 +752,10 @@ struct dconv_upd_plan {
   bool has_cfg;
   Taps taps;
   std::string last_desc;
+  // modelled bf16 variant choice (k-tile width, stacking, c-tiles per CTA) per operand
+  // geometry: computed once, not on every execute (the search evaluates ~10 plans)
+  mutable std::mutex sel_mu;
+  mutable std::map<std::array<int, 12>, std::array<int, 3>> sel_cache;
 };
 
 extern "C" {
@@ -1448,6 +1455,15 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     // single-tap layers with >= 2 c-tiles: a CTA may also take two c-tiles (two
     // accumulators), staging each dO tile once for both
     const bool mc_ok = pl.spec.R * pl.spec.S == 1 && cb0 % 16 == 0 && !DCONV_ENV("DCONV_UPD_NO_MC");
+    const std::array<int, 12> key = {in.n,   in.c,     in.h,       in.w,   in.halo_h, in.halo_w,
+                                     dout.h, dout.w, dout.halo_h, dout.halo_w, in.dtype, dout.dtype};
+    {
+      std::lock_guard<std::mutex> lk(pl.sel_mu);
+      const auto it = pl.sel_cache.find(key);
+      if (it != pl.sel_cache.end())
+        return plan_upd(pl, in, dout, encode_maps, in_pieces, do_pieces, partial, it->second[0], it->second[1],
+                        it->second[2]);
+    }
     double best = 1e30;
     int b_nb = nb_def, b_un = 0, b_mc = 1;
     for (int un = 0; un <= (narrow_taps ? 1 : 0); ++un)
@@ -1466,6 +1482,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
           } catch (...) {
           }
         }
+    {
+      std::lock_guard<std::mutex> lk(pl.sel_mu);
+      pl.sel_cache[key] = {b_nb, b_un, b_mc};
+    }
     return plan_upd(pl, in, dout, encode_maps, in_pieces, do_pieces, partial, b_nb, b_un, b_mc);
   }
   UpdLaunch L;

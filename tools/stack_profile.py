@@ -27,19 +27,23 @@ rows = []
 st = torch.cuda.current_stream()
 
 
-def timed(fn, reps=3):
-    """mean device time of `reps` back-to-back calls (queued behind a spin so host
-    launch gaps are not timed)"""
+def timed(fn, reps=3, trials=3):
+    """device time per call: mean of `reps` back-to-back calls queued behind a spin
+    (host launch gaps not timed), best of `trials` (a host stall longer than the
+    spin would otherwise be timed as device idle)"""
     fn()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda._sleep(2_000_000)
-    a.record(st)
-    for _ in range(reps):
-        fn()
-    b.record(st)
-    b.synchronize()
-    return a.elapsed_time(b) / reps
+    best = float("inf")
+    for _ in range(trials):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(4_000_000)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) / reps)
+    return best
 
 
 peak = 1332.6
