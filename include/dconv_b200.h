@@ -162,7 +162,13 @@ typedef struct dconv_epilogue {
   const void* add;
   const void* mask;
   int relu;
+  /* DCONV_EP_PREP_ONLY: only prepare the weights into `workspace` (they depend on
+   * the weights alone: a caller may run this on another stream, ahead of time);
+   * DCONV_EP_WEIGHTS_READY: the workspace already holds them, skip the preparation */
+  int flags;
 } dconv_epilogue_t;
+#define DCONV_EP_WEIGHTS_READY 1
+#define DCONV_EP_PREP_ONLY 2
 int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
                      const dconv_epilogue_t* ep, void* workspace, dconv_stream_t stream);
 

@@ -30,8 +30,12 @@ class Fusion(C.Structure):
     _fields_ = [("kind", C.c_int), ("bias", C.POINTER(C.c_float)), ("bias_len", C.c_int)]
 
 
+EP_WEIGHTS_READY = 1  # dconv_epilogue_t.flags (include/dconv_b200.h)
+EP_PREP_ONLY = 2
+
+
 class Epilogue(C.Structure):
-    _fields_ = [("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int)]
+    _fields_ = [("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int), ("flags", C.c_int)]
 
 
 class EngineCfg(C.Structure):

@@ -383,8 +383,11 @@ class _Workspace:
 
     def get(self, nbytes: int, device) -> int:
         nbytes = max(int(nbytes), 256)
-        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
-            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None:  # "cuda" == the current device: compare like with like
+            dev = torch.device("cuda", torch.cuda.current_device())
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != dev:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         return self.buf.data_ptr()
 
 

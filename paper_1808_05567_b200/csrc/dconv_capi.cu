@@ -1184,8 +1184,11 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
     pb.row_off = -s.pad_h;
     pb.col_off = -s.pad_w;
     FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
-    launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces,
-                       L.raw_f32 ? 0 : 1, cs);
+    const int ep_flags = ep ? ep->flags : 0;
+    if (!(ep_flags & DCONV_EP_WEIGHTS_READY))
+      launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces,
+                         L.raw_f32 ? 0 : 1, cs);
+    if (ep_flags & DCONV_EP_PREP_ONLY) return;
     FwdParams& p = L.p;
     p.out = out->data;
     p.out_bf16 = out->dtype == DCONV_BF16;
@@ -1350,9 +1353,11 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
     // values and the three zero neighbours of each) instead of zero-phase passes
     const bool fill = !accumulate && s.stride == 2 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 &&
                       n_conv == 1;
+    const int ep_flags = ep ? ep->flags : 0;
     for (auto& ph : plan->phases) {
       if (!first) desc += ",";
       first = false;
+      if (ph.zero && (ep_flags & DCONV_EP_PREP_ONLY)) continue;
       if (ph.zero) {
         if (accumulate || fill) {  // adding zeros, or written by the tap phase
           desc += accumulate ? "\"skip\"" : "\"filled\"";
@@ -1376,9 +1381,11 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
       ConvProblem pb = ph.pb;
       pb.in = *grad_out;
       FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
-      launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, L.p.nb, L.p.n_ntiles, 1,
-                         plan->pieces, L.raw_f32 ? 0 : 1, cs);
+      if (!(ep_flags & DCONV_EP_WEIGHTS_READY))
+        launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, L.p.nb, L.p.n_ntiles, 1,
+                           plan->pieces, L.raw_f32 ? 0 : 1, cs);
       tap_off += static_cast<int>(ph.tapmap.size());
+      if (ep_flags & DCONV_EP_PREP_ONLY) continue;
       FwdParams& p = L.p;
       p.out = grad_in->data;
       p.out_bf16 = grad_in->dtype == DCONV_BF16;
@@ -1406,6 +1413,7 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
       desc += json_tile(L);
     }
     desc += "]}";
+    if (ep_flags & DCONV_EP_PREP_ONLY) return;
     if (s.stride != 1) {
       const int r = dconv_zero_halo(grad_in, stream);
       if (r != DCONV_OK) fail(r, g_err);
