@@ -997,15 +997,24 @@ __global__ void __launch_bounds__(256)
   float sum = 0.0f;
   if (live) {
     const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
+    // up to 12 independent loads in flight per thread before the (fixed-order) adds:
+    // the partials were just written by the update kernel, so this is L2 latency bound
     int sp = y;
-    for (; sp + 3 * G < splits; sp += 4 * G) {
-      float v[4];
+    for (; sp + 11 * G < splits; sp += 12 * G) {
+      float v[12];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (sp + u * G) * split_stride);
+      for (int u = 0; u < 12; ++u) v[u] = __ldg(src + (sp + u * G) * split_stride);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) sum += v[u];
+      for (int u = 0; u < 12; ++u) sum += v[u];
     }
-    for (; sp < splits; sp += G) sum += __ldg(src + sp * split_stride);
+    {
+      float v[12];
+#pragma unroll
+      for (int u = 0; u < 12; ++u) v[u] = (sp + u * G < splits) ? __ldg(src + (sp + u * G) * split_stride) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 12; ++u)
+        if (sp + u * G < splits) sum += v[u];
+    }
   }
   if (G > 1) {
     red[y * (TX + 1) + threadIdx.x] = sum;
