@@ -24,9 +24,11 @@
 using namespace dconv_sm100;
 
 namespace {
-// Debug / experiment overrides (DCONV_*) are read once per process, not per
-// plan or execute call: each call site caches its own lookup.
-#define DCONV_ENV(name) ([]() -> const char* { static const char* v_ = std::getenv(name); return v_; }())
+// Debug / experiment overrides (DCONV_*): read where the plan is formed, so a
+// sweep (tools/fwd_sweep.py) can vary them between plans in one process. Unset in
+// production; a lookup costs ~0.1 us of host time per execute call (nothing
+// inside a CUDA graph).
+#define DCONV_ENV(name) (std::getenv(name))
 
 
 thread_local std::string g_err;
