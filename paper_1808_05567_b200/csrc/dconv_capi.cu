@@ -1769,6 +1769,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     }
   }
   if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
+  if (DCONV_ENV("DCONV_UPD_SPLITS")) splits = std::max(1, std::min(std::atoi(DCONV_ENV("DCONV_UPD_SPLITS")), p.stages_total));
   p.splits = splits;
   p.c_pad = n_ctiles * 128;
   p.k_pad = n_ktiles * NT;
