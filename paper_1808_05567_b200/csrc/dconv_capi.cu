@@ -1771,6 +1771,35 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
   if (DCONV_ENV("DCONV_UPD_SPLITS")) splits = std::max(1, std::min(std::atoi(DCONV_ENV("DCONV_UPD_SPLITS")), p.stages_total));
   p.splits = splits;
+  // fp32-accurate: bound the accumulation chain per TMEM accumulator (the tensor
+  // core truncates each fp32 accumulate; a 1-split cfg2 chain of 6272 k-steps drifted
+  // to 4.8e-4 of the output RMS, 74 splits = 85 k-steps to 5e-6). Longer chains are
+  // cut into periods of <= kDrainKsteps k-steps whose sums are added in fp32.
+  {
+    // (counted in accumulate steps into the hi*hi accumulator: one per k-step when the
+    // hi*hi product has its own column group (CAT), six when all six products share one)
+    constexpr int kDrainSteps = 96;
+    const int steps = (p.vs / 16) * (L.cat ? 1 : 6);
+    const int per_split = cdiv(p.stages_total, splits);
+    p.drain = 0;
+    p.drain_bufs = 1;
+    if (pieces == 3 && per_split * steps > kDrainSteps) {
+      p.drain = std::max(1, kDrainSteps / steps);
+      const int acc_w = (L.cat ? 3 : 1) * NT;
+      if (L.tsa) {
+        const int ring = pieces * p.vs / 2;
+        const int ps2 = std::min(4, (512 - 2 * acc_w) / ring);
+        if (ps2 >= 2) {
+          p.drain_bufs = 2;
+          L.pc_stages = std::min(L.pc_stages, ps2);
+        }
+      } else if (L.raw) {
+        if (2 * p.tg * acc_w <= 512) p.drain_bufs = 2;
+      } else if (2 * std::max(p.tg, mc) * NT <= 512) {
+        p.drain_bufs = 2;
+      }
+    }
+  }
   p.c_pad = n_ctiles * 128;
   p.k_pad = n_ktiles * NT;
   p.partial = partial;

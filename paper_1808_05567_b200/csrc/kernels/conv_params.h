@@ -119,6 +119,13 @@ struct UpdParams {
   float* partial;      // [split][tap(RS)][c_pad][k_pad]
   int dbg_mode;        // ablation bits (debug only): 4 skip conversion, 8 skip MMAs
   int c_pad, k_pad;
+  // fp32-accurate accumulation periods: the tensor core's fp32 accumulate truncates
+  // per MMA, so a long chain drifts (~ chain x 2^-24 relative, biased). Every `drain`
+  // stages the TMEM accumulator is added (RNE, fp32) into the CTA's partial slice
+  // and restarted; `drain_bufs` = 2 alternates two accumulators so the MMA never
+  // waits on the drain. drain = 0: one period (no drains).
+  int drain;
+  int drain_bufs;
 };
 
 }  // namespace dconv_sm100

@@ -26,6 +26,22 @@
 
 namespace dconv_sm100 {
 
+// Accumulation periods of the fp32-accurate UPD kernels (UpdParams::drain): the
+// stages [j*drain, (j+1)*drain) of a CTA accumulate in TMEM buffer j % bufs;
+// when period j ends the MMA commits acc_full[buf], the drainers add the
+// buffer into the CTA's fp32 partial slice (round to nearest) and arrive
+// acc_drained[buf]; period j + bufs waits for that before reusing the buffer.
+struct AccPeriods {
+  int drain, bufs;
+  __device__ __forceinline__ int period(int it) const { return drain ? it / drain : 0; }
+  __device__ __forceinline__ bool starts(int it) const { return drain ? (it % drain == 0) : it == 0; }
+  __device__ __forceinline__ bool ends(int it, int iters) const {
+    return it == iters - 1 || (drain && (it + 1) % drain == 0);
+  }
+  __device__ __forceinline__ int buf(int j) const { return j % bufs; }
+  __device__ __forceinline__ uint32_t par(int j) const { return static_cast<uint32_t>(j / bufs) & 1u; }
+};
+
 struct UpdStage {
   uint32_t a_plane, b_plane;  // bytes per 16B-chunk plane
   uint32_t a_piece, b_piece;  // bytes per operand piece (16 / 2*nb planes)
@@ -98,7 +114,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
-  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ __align__(8) uint64_t acc_full[2], acc_drained[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_tap_shift[kMaxTaps];  // off the constant cache in the issue loop
 
@@ -108,6 +124,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
   const int NT = 16 * p.nb;
   const int mc = p.mc > 1 ? p.mc : 1;
+  // accumulation periods (fp32-accurate long chains, see AccPeriods); the bf16 paths keep drain = 0
+  const AccPeriods per_acc{(PA == 1 && PB == 1) ? 0 : p.drain, p.drain_bufs > 1 ? 2 : 1};
   const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB, mc);
   const uint32_t smem0 = smem_u32(smem);
 
@@ -124,8 +142,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int tap0 = p.tg_tap0[tgrp];
   const int ntaps = p.tg_ntaps[tgrp];
 
+  const uint32_t buf_cols = static_cast<uint32_t>(max(p.tg, mc) * NT);
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(max(p.tg, mc) * NT)) tmem_cols <<= 1;
+  while (tmem_cols < static_cast<uint32_t>(per_acc.bufs) * buf_cols) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_in);
@@ -134,7 +153,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&full_bar[s], p.lsu ? kUpdLoaderWarps * 32 : 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(&accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_drained[b], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
@@ -295,7 +317,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         mma_commit(&empty_bar[rp.idx]);
       }
-      if (iters > 0) mma_commit(&accum_bar);
+      if (iters > 0) mma_commit(&acc_full[0]);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -304,9 +326,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int ksteps = p.vs / 16;
     for (int it = 0; it < iters; ++it) {
       const int s = it % n_stages;
+      const int jp = per_acc.period(it);
+      const bool p_first = per_acc.starts(it);
+      if (p_first && jp >= per_acc.bufs)
+        mbar_wait(&acc_drained[per_acc.buf(jp)], static_cast<uint32_t>(jp / per_acc.bufs - 1) & 1u);
       mbar_wait(&full_bar[s], static_cast<uint32_t>(it / n_stages) & 1u);
       tc_fence_after();
       const uint32_t st = smem0 + static_cast<uint32_t>(s) * L.bytes;
+      const uint32_t acc0 = tmem_base + static_cast<uint32_t>(per_acc.buf(jp)) * buf_cols;
       if (elect_one()) {
         const int n_acc = p.stack > 1 ? 1 : ntaps;  // stacked: one accumulator holds all the group's taps
         // MN-major: 16B rows = 8 channels, K rows = pixels; SBO = chunk-plane stride, LBO = 8 pixels.
@@ -318,7 +345,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t row_u = p.sw32 ? 2u : 1u;  // descriptor units (16 B) per pixel row
         for (int t = 0; t < n_acc; ++t) {
           const int shift = p.stack > 1 ? 0 : s_tap_shift[tap0 + t];
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * NT);
+          const uint32_t d_tmem = acc0 + static_cast<uint32_t>(t * NT);
           for (int ks = 0; ks < ksteps; ++ks) {
             const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift) * row_u;
             const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u * row_u;
@@ -328,24 +355,30 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               for (int ib = 0; ib < PB; ++ib) {
                 if (a_base + ia + ib > 2) continue;
                 mma_bf16(d_tmem, ak + static_cast<uint32_t>(ia) * a_pc, bk + static_cast<uint32_t>(ib) * b_pc, idesc,
-                         (it > 0 || ks > 0 || ia > 0 || ib > 0) ? 1u : 0u);
+                         (!p_first || ks > 0 || ia > 0 || ib > 0) ? 1u : 0u);
               }
             }
           }
         }
         mma_commit(&empty_bar[s]);
-        if (it == iters - 1) mma_commit(&accum_bar);
+        if (per_acc.ends(it, iters)) mma_commit(&acc_full[per_acc.buf(jp)]);
       }
       __syncwarp();
     }
   }
   if (warp >= 4) {
     // ---------------------------------------------------------- epilogue (lsu plans: after loading)
+    // one pass per accumulation period: every period's buffer is added into the
+    // partial slice (the first one overwrites it unless the launch accumulates)
     const int qrow = (warp % 4) * 32;
-    if (iters > 0) {
-      mbar_wait(&accum_bar, 0);
-      tc_fence_after();
-    }
+    const int n_periods = iters > 0 ? per_acc.period(iters - 1) + 1 : 1;
+    for (int jd = 0; jd < n_periods; ++jd) {
+      if (iters > 0) {
+        mbar_wait(&acc_full[per_acc.buf(jd)], per_acc.par(jd));
+        tc_fence_after();
+      }
+      const uint32_t acc_col0 = static_cast<uint32_t>(per_acc.buf(jd)) * buf_cols;
+      const bool add_old = accumulate || jd > 0;
     const int n_acc = p.stack > 1 ? 1 : (mc > 1 ? mc : ntaps);
     for (int t = 0; t < n_acc; ++t) {
       const int c_glob = (ctile * mc + (mc > 1 ? t : 0)) * 128 + qrow + lane;
@@ -359,7 +392,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
       for (int g = 0; g < p.nb; ++g) {
         uint32_t r[16];
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(t * NT + g * 16), r);
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + acc_col0 + static_cast<uint32_t>(t * NT + g * 16), r);
         tmem_ld_wait();
         if (!row_ok) continue;
         float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
@@ -369,15 +402,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           float4 v = live ? make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
                                         __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (accumulate) {
+          if (add_old) {
             const float4 o = d[e];
-            v.x += o.x;
-            v.y += o.y;
-            v.z += o.z;
-            v.w += o.w;
+            v.x = o.x + v.x;
+            v.y = o.y + v.y;
+            v.z = o.z + v.z;
+            v.w = o.w + v.w;
           }
           d[e] = v;
         }
+      }
+    }
+      if (jd + 1 < n_periods) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_drained[per_acc.buf(jd)]);
       }
     }
   }
@@ -433,6 +472,7 @@ __host__ __device__ inline uint32_t upd_ts_pc_slot(int vs, int nb, int pieces) {
 // 16 B chunk k of row j of a SWIZZLE_64B box whose start is 1 KiB aligned
 __device__ __forceinline__ uint32_t sw64_row(uint32_t j, uint32_t k) { return j * 64u + ((k ^ ((j >> 1) & 3u)) << 4); }
 
+
 template <int PIECES, bool CAT>
 __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
     conv_upd_raw_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
@@ -440,7 +480,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
   __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_empty[kMaxStages];
-  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ __align__(8) uint64_t acc_full[2], acc_drained[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_tap_shift[kMaxTaps];  // off the constant cache in the issue loop
 
@@ -449,6 +489,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
   if (warp == 2)
     for (int i = lane; i < kMaxTaps; i += 32) s_tap_shift[i] = p.tap_shift[i];
   const int NT = 16 * p.nb;
+  const AccPeriods per_acc{p.drain, p.drain_bufs > 1 ? 2 : 1};
   const int ctile = blockIdx.x / p.n_tgroups;
   const int tgrp = blockIdx.x % p.n_tgroups;
   const int ktile = blockIdx.y;
@@ -468,9 +509,10 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
   const uint32_t smem0 = smem_u32(smem);
   constexpr int kGroups = CAT ? 3 : 1;  // accumulator column groups per tap
   const int acc_w = kGroups * NT;
+  const uint32_t buf_cols = static_cast<uint32_t>(p.tg * acc_w);  // one accumulation buffer
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(p.tg * acc_w)) tmem_cols <<= 1;
+  while (tmem_cols < static_cast<uint32_t>(per_acc.bufs) * buf_cols) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_in);
@@ -483,7 +525,10 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       mbar_init(&pc_full[s], kUpdCvtWarps);
       mbar_init(&pc_empty[s], 1);
     }
-    mbar_init(&accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_drained[b], 4);  // the four epilogue warps
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
@@ -531,9 +576,15 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
     const int ksteps = p.vs / 16;
     for (int it = 0; it < iters; ++it) {
       const int s = it % pc_stages;
+      const int jp = per_acc.period(it);
+      const bool p_first = per_acc.starts(it);
+      if (p_first && jp >= per_acc.bufs) {  // the buffer's previous period has been drained
+        mbar_wait(&acc_drained[per_acc.buf(jp)], static_cast<uint32_t>(jp / per_acc.bufs - 1) & 1u);
+      }
       mbar_wait(&pc_full[s], static_cast<uint32_t>(it / pc_stages) & 1u);
       tc_fence_after();
       const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * R.pc_slot;
+      const uint32_t acc0 = tmem_base + static_cast<uint32_t>(per_acc.buf(jp)) * buf_cols;
       if (elect_one()) {
         const int n_acc = stacked ? 1 : ntaps;
         // descriptors packed once per stage; per MMA only the 16 B-unit start address advances
@@ -544,9 +595,9 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
                        id1 = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
         for (int t = 0; t < n_acc; ++t) {
           const int shift = stacked ? 0 : s_tap_shift[tap0 + t];
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(t * acc_w);
+          const uint32_t d_tmem = acc0 + static_cast<uint32_t>(t * acc_w);
           for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
-            const bool first = it == 0 && ks == 0;
+            const bool first = p_first && ks == 0;
             const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift);  // 16 B per pixel row
             const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u;          // 256 B per k-step
             if (CAT) {
@@ -567,12 +618,62 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
           }
         }
         mma_commit(&pc_empty[s]);
-        if (it == iters - 1) mma_commit(&accum_bar);
+        if (per_acc.ends(it, iters)) mma_commit(&acc_full[per_acc.buf(jp)]);
       }
       __syncwarp();
     }
   } else if (warp >= kUpdCvtWarp0) {
     // ------------------------------------------------------------ converters (fp32 raw -> bf16 pieces)
+    // w4..w7 (one per TMEM lane quarter) also write the partials: after the last
+    // period, and (drain > 0) at every period boundary, where they add the
+    // finished accumulation buffer into the CTA's partial slice
+    const bool epi_warp = warp < kUpdCvtWarp0 + 4;
+    const int qrow = (warp % 4) * 32;
+    auto write_partial = [&](uint32_t acc_col0, bool add_old) {
+      const int c_glob = ctile * 128 + qrow + lane;
+      const int n_acc = stacked ? 1 : ntaps;
+      for (int t = 0; t < n_acc; ++t) {
+        const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
+        const int slot = stacked ? (qrow + lane) / rows_slot : 0;
+        const int c_row = stacked ? (qrow + lane) % rows_slot : c_glob;
+        const bool row_ok = stacked ? slot < ntaps : true;
+        const int rs = p.tap_src[tap0 + (stacked ? (row_ok ? slot : 0) : t)];
+        float* dst_row =
+            p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
+        const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16) + acc_col0 + static_cast<uint32_t>(t * acc_w);
+        for (int g = 0; g < p.nb; ++g) {
+          uint32_t r[16], ry[16], rz[16];
+          tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
+          if (CAT) {
+            tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
+            tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
+          }
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
+          const bool live = iters > 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int q = 4 * e + u;
+              vv[u] = CAT ? __uint_as_float(r[q]) + (__uint_as_float(ry[q]) + __uint_as_float(rz[q]))
+                          : __uint_as_float(r[q]);
+              if (!live) vv[u] = 0.0f;
+            }
+            if (add_old) {
+              const float4 o = d[e];
+              vv[0] = o.x + vv[0];
+              vv[1] = o.y + vv[1];
+              vv[2] = o.z + vv[2];
+              vv[3] = o.w + vv[3];
+            }
+            d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+          }
+        }
+      }
+    };
     // Work unit = one 16 B-chunk plane (8 channels) of one operand: A has
     // a_boxes * a_planes * 2 <= 16 of them, dO 2 * nb <= 32. Warp cw owns chunk
     // planes cw, cw + 8, ... of each operand for the whole kernel, so all
@@ -607,6 +708,15 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
     int rs = 0, ps = 0;
     uint32_t rph = 0, pph = 0;
     for (int it = 0; it < iters; ++it) {
+      if (epi_warp && it > 0 && per_acc.drain && per_acc.starts(it)) {
+        const int jd = per_acc.period(it) - 1;  // the period that just ended
+        mbar_wait(&acc_full[per_acc.buf(jd)], per_acc.par(jd));
+        tc_fence_after();
+        write_partial(static_cast<uint32_t>(per_acc.buf(jd)) * buf_cols, jd > 0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_drained[per_acc.buf(jd)]);
+      }
       mbar_wait(&raw_full[rs], rph);
       mbar_wait(&pc_empty[ps], pph ^ 1u);
       const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
@@ -652,50 +762,15 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
         pph ^= 1u;
       }
     }
-    if (warp < kUpdCvtWarp0 + 4) {
+    if (epi_warp) {
       // -------------------------------------------------------- epilogue (w4..w7: TMEM lane quarters)
-      const int qrow = (warp % 4) * 32;
-      const int c_glob = ctile * 128 + qrow + lane;
+      const int jl = iters > 0 ? per_acc.period(iters - 1) : 0;
       if (iters > 0) {
-        mbar_wait(&accum_bar, 0);
+        mbar_wait(&acc_full[per_acc.buf(jl)], per_acc.par(jl));
         tc_fence_after();
       }
       if (warp == kUpdCvtWarp0 && lane == 0) pdl_launch_dependents();  // the reduce may get scheduled
-      const int n_acc = stacked ? 1 : ntaps;
-      for (int t = 0; t < n_acc; ++t) {
-        const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
-        const int slot = stacked ? (qrow + lane) / rows_slot : 0;
-        const int c_row = stacked ? (qrow + lane) % rows_slot : c_glob;
-        const bool row_ok = stacked ? slot < ntaps : true;
-        const int rs = p.tap_src[tap0 + (stacked ? (row_ok ? slot : 0) : t)];
-        float* dst_row =
-            p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
-        const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(t * acc_w);
-        for (int g = 0; g < p.nb; ++g) {
-          uint32_t r[16], ry[16], rz[16];
-          tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
-          if (CAT) {
-            tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
-            tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
-          }
-          tmem_ld_wait();
-          if (!row_ok) continue;
-          float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
-          const bool live = iters > 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float vv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int q = 4 * e + u;
-              vv[u] = CAT ? __uint_as_float(r[q]) + (__uint_as_float(ry[q]) + __uint_as_float(rz[q]))
-                          : __uint_as_float(r[q]);
-              if (!live) vv[u] = 0.0f;
-            }
-            d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-          }
-        }
-      }
+      write_partial(static_cast<uint32_t>(per_acc.buf(jl)) * buf_cols, jl > 0);
     }
   }
   tc_fence_before();
@@ -727,12 +802,13 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t raw_full[kMaxStages], raw_empty[kMaxStages];
   __shared__ __align__(8) uint64_t pc_full[kMaxStages], pc_empty[kMaxStages];
-  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ __align__(8) uint64_t acc_full[2], acc_drained[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int NT = 16 * p.nb;
+  const AccPeriods per_acc{p.drain, p.drain_bufs > 1 ? 2 : 1};
   const int ctile = blockIdx.x;  // single tap: one tap group
   const int ktile = blockIdx.y;
   const int split = blockIdx.z;
@@ -747,6 +823,7 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
   const uint32_t smem0 = smem_u32(smem);
   constexpr int kGroups = CAT ? 3 : 1;
   const uint32_t acc_w = static_cast<uint32_t>(kGroups * NT);
+  const uint32_t acc_all = static_cast<uint32_t>(per_acc.bufs) * acc_w;  // accumulation buffers, then the A ring
   const uint32_t a_cols = static_cast<uint32_t>(p.vs) / 2u;  // TMEM columns per piece per stage
   const uint32_t ring_slot = PIECES * a_cols;
   // converter groups take stages round-robin: same ordering argument as
@@ -759,7 +836,7 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
   const uint32_t cvt_arrivals = 4u;
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < acc_w + static_cast<uint32_t>(pc_stages) * ring_slot) tmem_cols <<= 1;
+  while (tmem_cols < acc_all + static_cast<uint32_t>(pc_stages) * ring_slot) tmem_cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_in);
@@ -772,7 +849,10 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
       mbar_init(&pc_full[s], cvt_arrivals);
       mbar_init(&pc_empty[s], 1);
     }
-    mbar_init(&accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_drained[b], 4);  // the four epilogue warps
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, tmem_cols);
@@ -808,10 +888,15 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
     const int ksteps = p.vs / 16;
     for (int it = 0; it < iters; ++it) {
       const int s = it % pc_stages;
+      const int jp = per_acc.period(it);
+      const bool p_first = per_acc.starts(it);
+      if (p_first && jp >= per_acc.bufs)  // the buffer's previous period has been drained
+        mbar_wait(&acc_drained[per_acc.buf(jp)], static_cast<uint32_t>(jp / per_acc.bufs - 1) & 1u);
       mbar_wait(&pc_full[s], static_cast<uint32_t>(it / pc_stages) & 1u);
       tc_fence_after();
       const uint32_t st = smem0 + R.pc_off + static_cast<uint32_t>(s) * pc_slot;
-      const uint32_t a_t = tmem_base + acc_w + static_cast<uint32_t>(s) * ring_slot;
+      const uint32_t a_t = tmem_base + acc_all + static_cast<uint32_t>(s) * ring_slot;
+      const uint32_t dacc = tmem_base + static_cast<uint32_t>(per_acc.buf(jp)) * acc_w;
       if (elect_one()) {
         // operand addresses advance by constants per k-step: no descriptor packing in the loop
         const uint64_t b0 = make_smem_desc(st, 128, b_plane);
@@ -819,26 +904,26 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
         const uint32_t id3 = make_idesc(1, 0, 1, 128, 3u * NT), id2 = make_idesc(1, 0, 1, 128, 2u * NT),
                        id1 = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
         for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
-          const bool first = it == 0 && ks == 0;
+          const bool first = p_first && ks == 0;
           const uint32_t ak = a_t + static_cast<uint32_t>(ks) * 8u;
           const uint64_t bk = b0 + static_cast<uint64_t>(ks) * 16u;  // 256 B per k-step
           if (CAT) {
-            mma_bf16_ts(tmem_base, ak, bk, id3, first ? 0u : 1u);
-            mma_bf16_ts(tmem_base + NT, ak + a_cols, bk, id2, 1u);
-            mma_bf16_ts(tmem_base + 2 * NT, ak + 2u * a_cols, bk, id1, 1u);
+            mma_bf16_ts(dacc, ak, bk, id3, first ? 0u : 1u);
+            mma_bf16_ts(dacc + NT, ak + a_cols, bk, id2, 1u);
+            mma_bf16_ts(dacc + 2 * NT, ak + 2u * a_cols, bk, id1, 1u);
           } else {
 #pragma unroll
             for (int ia = 0; ia < PIECES; ++ia)
 #pragma unroll
               for (int ib = 0; ib < PIECES; ++ib) {
                 if (ia + ib > 2) continue;
-                mma_bf16_ts(tmem_base, ak + static_cast<uint32_t>(ia) * a_cols, bk + static_cast<uint64_t>(ib) * b_pc,
+                mma_bf16_ts(dacc, ak + static_cast<uint32_t>(ia) * a_cols, bk + static_cast<uint64_t>(ib) * b_pc,
                             id1, (first && ia == 0 && ib == 0) ? 0u : 1u);
               }
           }
         }
         mma_commit(&pc_empty[s]);
-        if (it == iters - 1) mma_commit(&accum_bar);
+        if (per_acc.ends(it, iters)) mma_commit(&acc_full[per_acc.buf(jp)]);
       }
       __syncwarp();
     }
@@ -854,8 +939,57 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
     const uint32_t swap = ((lane >> 4) & ~p.a_px) & 1u;
     const uint32_t kq = static_cast<uint32_t>(ln >> 2), lo4 = static_cast<uint32_t>(ln & 3) * 4u;
     const uint32_t a_row0 = static_cast<uint32_t>(pl * p.a_px + p.tap_shift[0]);
+    // group 0 (w4..w7, one warp per TMEM lane quarter) writes the partials: after the
+    // last period and, when drain > 0, at every period boundary (adding the finished
+    // buffer into the CTA's partial slice)
+    const bool epi_warp = warp < kUpdCvtWarp0 + 4;
+    const int qrow = (warp % 4) * 32;
+    auto write_partial = [&](uint32_t acc_col0, bool add_old) {
+      float* dst_row = p.partial + ((static_cast<long long>(split) * p.n_taps + p.tap_src[0]) * p.c_pad +
+                                    ctile * 128 + qrow + lane) * p.k_pad + ktile * NT;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16) + acc_col0;
+      for (int g = 0; g < p.nb; ++g) {
+        uint32_t r[16], ry[16], rz[16];
+        tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
+        if (CAT) {
+          tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
+          tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
+        }
+        tmem_ld_wait();
+        float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
+        const bool live = iters > 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int qq = 4 * e + u;
+            vv[u] = CAT ? __uint_as_float(r[qq]) + (__uint_as_float(ry[qq]) + __uint_as_float(rz[qq]))
+                        : __uint_as_float(r[qq]);
+            if (!live) vv[u] = 0.0f;
+          }
+          if (add_old) {
+            const float4 o = d[e];
+            vv[0] = o.x + vv[0];
+            vv[1] = o.y + vv[1];
+            vv[2] = o.z + vv[2];
+            vv[3] = o.w + vv[3];
+          }
+          d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        }
+      }
+    };
     // dO chunk planes 0 .. 2nb-1: warp q of the group takes q, q + 4, ...
     for (int it = 0; it < iters; ++it) {
+      if (epi_warp && it > 0 && per_acc.drain && per_acc.starts(it)) {
+        const int jd = per_acc.period(it) - 1;  // the period that just ended
+        mbar_wait_backoff(&acc_full[per_acc.buf(jd)], per_acc.par(jd));
+        tc_fence_after();
+        write_partial(static_cast<uint32_t>(per_acc.buf(jd)) * acc_w, jd > 0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_drained[per_acc.buf(jd)]);
+      }
       if ((it % cvt_groups) != grp) continue;
       const int rs = it % raw_stages, ps = it % pc_stages;
       mbar_wait_backoff(&pc_empty[ps], (static_cast<uint32_t>(it / pc_stages) & 1u) ^ 1u);  // first: see cvt_groups
@@ -864,7 +998,7 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
       const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
       if (!(p.dbg_mode & 4)) {
         // A: this channel's values over the stage's pixels -> pieces, 2 pixels per column
-        const uint32_t col0 = tmem_base + (q * 32u << 16) + acc_w + static_cast<uint32_t>(ps) * ring_slot;
+        const uint32_t col0 = tmem_base + (q * 32u << 16) + acc_all + static_cast<uint32_t>(ps) * ring_slot;
         // 16-pixel units; the next unit's values are loaded before this unit's
         // tcgen05.st so shared-memory latency overlaps the split arithmetic
         const int px_end = (p.dbg_mode & 64) ? 0 : p.vs;
@@ -930,40 +1064,15 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
         mbar_arrive(&pc_full[ps]);
       }
     }
-    if (warp < kUpdCvtWarp0 + 4) {
+    if (epi_warp) {
       // -------------------------------------------------------- epilogue (w4..w7: TMEM lane quarters)
-      const int qrow = (warp % 4) * 32;
+      const int jl = iters > 0 ? per_acc.period(iters - 1) : 0;
       if (iters > 0) {
-        mbar_wait(&accum_bar, 0);
+        mbar_wait(&acc_full[per_acc.buf(jl)], per_acc.par(jl));
         tc_fence_after();
       }
       if (warp == kUpdCvtWarp0 && lane == 0) pdl_launch_dependents();
-      float* dst_row = p.partial + ((static_cast<long long>(split) * p.n_taps + p.tap_src[0]) * p.c_pad +
-                                    ctile * 128 + qrow + lane) * p.k_pad + ktile * NT;
-      const uint32_t tb = tmem_base + (static_cast<uint32_t>(qrow) << 16);
-      for (int g = 0; g < p.nb; ++g) {
-        uint32_t r[16], ry[16], rz[16];
-        tmem_ld16(tb + static_cast<uint32_t>(g * 16), r);
-        if (CAT) {
-          tmem_ld16(tb + static_cast<uint32_t>(NT + g * 16), ry);
-          tmem_ld16(tb + static_cast<uint32_t>(2 * NT + g * 16), rz);
-        }
-        tmem_ld_wait();
-        float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
-        const bool live = iters > 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float vv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int qq = 4 * e + u;
-            vv[u] = CAT ? __uint_as_float(r[qq]) + (__uint_as_float(ry[qq]) + __uint_as_float(rz[qq]))
-                        : __uint_as_float(r[qq]);
-            if (!live) vv[u] = 0.0f;
-          }
-          d[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-        }
-      }
+      write_partial(static_cast<uint32_t>(per_acc.buf(jl)) * acc_w, jl > 0);
     }
   }
   tc_fence_before();
