@@ -255,6 +255,23 @@ int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, 
 int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out,
                             char* report, size_t len);
 
+/* ---------------------------------------------------------------- plan serialization */
+/* save_plan / load_plan (kernel_streams.cpp:619-788; KSPL v1) analog, text
+ * format "DCPL 1": the plan descriptor plus every launch the plan has resolved
+ * (tile shapes, ring depths, grid, split-K factor, tap tables, epilogue) per
+ * tensor geometry. save: writes a NUL-terminated text into buf (len bytes;
+ * buf = NULL only reports the size in *needed). load: rebuilds the plan and
+ * seeds its launch cache, so the reloaded plan executes exactly the saved
+ * tiles (bitwise-identical results); validate != 0 runs the plan validator on
+ * every loaded launch (DCONV_ERR_INVALID_DESCRIPTOR if one fails). Malformed
+ * text: DCONV_ERR_PARSE (errors.hpp:54). */
+int dconv_fwd_plan_save(dconv_fwd_plan_t plan, char* buf, size_t len, size_t* needed);
+int dconv_fwd_plan_load(const char* text, size_t len, int validate, dconv_fwd_plan_t* plan);
+int dconv_bwd_plan_save(dconv_bwd_plan_t plan, char* buf, size_t len, size_t* needed);
+int dconv_bwd_plan_load(const char* text, size_t len, int validate, dconv_bwd_plan_t* plan);
+int dconv_upd_plan_save(dconv_upd_plan_t plan, char* buf, size_t len, size_t* needed);
+int dconv_upd_plan_load(const char* text, size_t len, int validate, dconv_upd_plan_t* plan);
+
 /* ---------------------------------------------------------------- host-buffer step */
 /* One layer step on HOST tensors (pinned for overlap), the reference's
  * execute contract (propagation.cpp:56-61 forward_into, :237-261 backward_with,
@@ -271,6 +288,12 @@ int dconv_host_step_run(dconv_host_step_t step, const dconv_act_t* x, const dcon
                         const dconv_act_t* y, const dconv_act_t* dx, const dconv_wt_t* dw, dconv_stream_t stream);
 /* kernels launched by the last run */
 int dconv_host_step_launches(dconv_host_step_t step);
+
+/* ---------------------------------------------------------------- developer mode */
+/* on != 0: the DCONV_* experiment variables of tools/ (tile / ring / split
+ * overrides) take effect and plan caches are bypassed. Off by default: the
+ * environment cannot change a production plan. */
+int dconv_set_dev_mode(int on);
 
 /* ---------------------------------------------------------------- profiling */
 /* enable != 0: bracket each pass's main conv kernel(s) with CUDA events on the

@@ -66,7 +66,8 @@ EXPORTS = [
     "dconv_upd_launches", "dconv_profile", "dconv_profile_last_ms", "dconv_forward_ex", "dconv_backward_data_ex",
     "dconv_maxpool_fwd", "dconv_maxpool_bwd", "dconv_maxpool_bwd_pooled_mask", "dconv_sgd", "dconv_s2d_act", "dconv_s2d_wt", "dconv_pack_s2d", "dconv_host_step_create", "dconv_host_step_destroy",
     "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches", "dconv_fwd_plan_validate",
-    "dconv_bwd_plan_validate", "dconv_upd_plan_validate",
+    "dconv_bwd_plan_validate", "dconv_upd_plan_validate", "dconv_set_dev_mode", "dconv_fwd_plan_save",
+    "dconv_fwd_plan_load", "dconv_bwd_plan_save", "dconv_bwd_plan_load", "dconv_upd_plan_save", "dconv_upd_plan_load",
 ]
 
 
@@ -133,6 +134,13 @@ def _bind(lib):
         "dconv_bwd_plan_validate": (i, [vp, P(Act), P(Act), C.c_char_p, sz]),
         "dconv_upd_plan_validate": (i, [vp, P(Act), P(Act), C.c_char_p, sz]),
         "dconv_profile_last_ms": (C.c_float, [i]),
+        "dconv_set_dev_mode": (i, [i]),
+        "dconv_fwd_plan_save": (i, [vp, C.c_char_p, sz, P(sz)]),
+        "dconv_fwd_plan_load": (i, [C.c_char_p, sz, i, P(vp)]),
+        "dconv_bwd_plan_save": (i, [vp, C.c_char_p, sz, P(sz)]),
+        "dconv_bwd_plan_load": (i, [C.c_char_p, sz, i, P(vp)]),
+        "dconv_upd_plan_save": (i, [vp, C.c_char_p, sz, P(sz)]),
+        "dconv_upd_plan_load": (i, [C.c_char_p, sz, i, P(vp)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -400,6 +400,38 @@ def _validate(fn, handle, a, b) -> dict:
     return json.loads(buf.value.decode() or "{}")
 
 
+def _save(fn, handle) -> str:
+    """save_plan (kernel_streams.cpp:619-688) analog: the plan and its resolved launches as DCPL text."""
+    need = C.c_size_t()
+    _check(fn(handle, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check(fn(handle, buf, len(buf), C.byref(need)))
+    return buf.value.decode()
+
+
+def _plan_header(text: str) -> dict:
+    rec = {}
+    for line in text.splitlines():
+        parts = line.split()
+        if parts and parts[0] in ("kind", "spec", "math", "out_halo") and parts[0] not in rec:
+            rec[parts[0]] = parts[1:]
+        if parts and parts[0] == "entries":
+            break
+    if "spec" not in rec:
+        raise ParseError("load_plan: no spec record")
+    return rec
+
+
+def _load(fn, text: str, validate: bool):
+    """load_plan (kernel_streams.cpp:690-788) analog; validate=True also runs the plan validator."""
+    h = C.c_void_p()
+    raw = text.encode()
+    _check(fn(raw, len(raw), int(validate), C.byref(h)))
+    rec = _plan_header(text)
+    spec = ConvLayerSpec(*[int(v) for v in rec["spec"]])
+    return h, spec, Math(int(rec["math"][0])), rec
+
+
 def _describe(fn, handle) -> dict:
     buf = C.create_string_buffer(4096)
     fn(handle, buf, len(buf))
@@ -446,6 +478,18 @@ class ExecutionPlan:
 
     def validate(self, inp: BlockedActivation, out: BlockedActivation) -> dict:
         return _validate(_lib.lib().dconv_fwd_plan_validate, self._h, inp, out)
+
+    def save(self) -> str:
+        return _save(_lib.lib().dconv_fwd_plan_save, self._h)
+
+    @classmethod
+    def load(cls, text: str, validate: bool = True) -> "ExecutionPlan":
+        h, spec, math, rec = _load(_lib.lib().dconv_fwd_plan_load, text, validate)
+        self = cls.__new__(cls)
+        self.spec, self.fusion, self.math, self.threads = spec, None, math, 1
+        self.out_halo_h, self.out_halo_w = (int(v) for v in rec["out_halo"])
+        self._h, self._bias_keep, self._ws = h, None, _Workspace()
+        return self
 
     def execute(self, inp: BlockedActivation, wt: BlockedWeight, out: BlockedActivation) -> None:
         ws = self._ws.get(_lib.lib().dconv_fwd_workspace_bytes(self._h), inp.data.device)
@@ -557,6 +601,18 @@ class BackwardContext:
     def validate(self, grad_out: BlockedActivation, grad_in: BlockedActivation) -> dict:
         return _validate(_lib.lib().dconv_bwd_plan_validate, self._h, grad_out, grad_in)
 
+    def save(self) -> str:
+        return _save(_lib.lib().dconv_bwd_plan_save, self._h)
+
+    @classmethod
+    def load(cls, text: str, validate: bool = True, wt: Optional[BlockedWeight] = None) -> "BackwardContext":
+        h, spec, math, _ = _load(_lib.lib().dconv_bwd_plan_load, text, validate)
+        self = cls.__new__(cls)
+        self.spec, self.wt, self.threads, self.math = spec, wt, 1, math
+        self._h, self._ws = h, _Workspace()
+        self.route = BackwardRoute(_lib.lib().dconv_bwd_route(self._h))
+        return self
+
     def execute(self, wt: BlockedWeight, grad_out: BlockedActivation, grad_in: BlockedActivation) -> None:
         ws = self._ws.get(_lib.lib().dconv_bwd_workspace_bytes(self._h), grad_out.data.device)
         _check(_lib.lib().dconv_backward_data(self._h, C.byref(wt.to_c()), C.byref(grad_out.to_c()),
@@ -647,6 +703,17 @@ class UpdatePlan:
 
     def validate(self, inp: BlockedActivation, grad_out: BlockedActivation) -> dict:
         return _validate(_lib.lib().dconv_upd_plan_validate, self._h, inp, grad_out)
+
+    def save(self) -> str:
+        return _save(_lib.lib().dconv_upd_plan_save, self._h)
+
+    @classmethod
+    def load(cls, text: str, validate: bool = True) -> "UpdatePlan":
+        h, spec, math, _ = _load(_lib.lib().dconv_upd_plan_load, text, validate)
+        self = cls.__new__(cls)
+        self.spec, self.math = spec, math
+        self._h, self._ws = h, _Workspace()
+        return self
 
     def execute(self, inp: BlockedActivation, grad_out: BlockedActivation, dw: BlockedWeight, accumulate=False):
         a, g = inp.to_c(), grad_out.to_c()

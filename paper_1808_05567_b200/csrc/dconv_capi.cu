@@ -24,11 +24,15 @@
 using namespace dconv_sm100;
 
 namespace {
-// Debug / experiment overrides (DCONV_*): read where the plan is formed, so a
-// sweep (tools/fwd_sweep.py) can vary them between plans in one process. Unset in
-// production; a lookup costs ~0.1 us of host time per execute call (nothing
-// inside a CUDA graph).
-#define DCONV_ENV(name) (std::getenv(name))
+// Experiment overrides (DCONV_* environment variables, read by the tile selectors
+// of tools/*_sweep.py). They are inert unless developer mode is switched on with
+// dconv_set_dev_mode(1): a stray variable cannot change a production plan. In
+// developer mode the plan caches are bypassed (every execute re-plans, so a sweep
+// can vary them between calls in one process) and malformed numbers are an error.
+bool g_dev_mode = false;
+
+const char* dev_env(const char* name) { return g_dev_mode ? std::getenv(name) : nullptr; }
+#define DCONV_ENV(name) dev_env(name)
 
 
 thread_local std::string g_err;
@@ -44,6 +48,17 @@ struct Fail {
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(DCONV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// developer-mode integer override: `dflt` when unset, an error when malformed
+int env_int(const char* name, int dflt) {
+  const char* v = dev_env(name);
+  if (!v) return dflt;
+  char* end = nullptr;
+  const long x = std::strtol(v, &end, 10);
+  if (end == v || *end != 0 || x < -(1L << 30) || x > (1L << 30))
+    fail(DCONV_ERR_INVALID_ARGUMENT, std::string(name) + ": not an integer: '" + v + "'");
+  return static_cast<int>(x);
 }
 
 template <class F>
@@ -84,7 +99,6 @@ int64_t act_elems(const dconv_act_t& a) {
 int64_t wt_elems(const dconv_wt_t& w) {
   return static_cast<int64_t>(cdiv(w.k, w.vlen)) * cdiv(w.c, w.vlen) * w.r * w.s * w.vlen * w.vlen;
 }
-int esize(int dtype) { return dtype == DCONV_BF16 ? 2 : 4; }
 
 void check_dtype(int dt) {
   if (dt != DCONV_F32 && dt != DCONV_BF16) fail(DCONV_ERR_INVALID_ARGUMENT, "dtype must be DCONV_F32 or DCONV_BF16");
@@ -251,6 +265,9 @@ struct FwdLaunch {
   int pieces;
   bool ts = false;  // A pieces staged in tensor memory (single-tap fp32 problems)
   size_t raw_slot = 0;  // bytes per raw-ring slot
+  // resolved by finalize_fwd() for a given output surface (epilogue staging)
+  CUtensorMap map_out, map_out2;
+  size_t smem_launch = 0;  // dynamic smem of the launch (rings + epilogue staging)
 };
 
 // Decide staging mode, tile and pipeline depth; encode TMA maps.
@@ -266,7 +283,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   L.raw_f32 = raw_f32;
   L.pieces = pieces;
   const int st = pb.stride;
-  const int hp = in.h + 2 * in.halo_h, wp = in.w + 2 * in.halo_w;
+  const int wp = in.w + 2 * in.halo_w;
   p.n_img = in.n;
   p.in_cb = cdiv(in.c, 16);
   p.cb_in = pb.cb_red;
@@ -304,9 +321,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
 
   FwdTile tile;
   const int kb_total = pb.kb_out;
-  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : DCONV_ENV("DCONV_FWD_MB") ? atoi(DCONV_ENV("DCONV_FWD_MB")) : 0;
+  const int want_mb = (cfg && cfg->tile_mb > 0) ? cfg->tile_mb : env_int("DCONV_FWD_MB", 0);
   const int want_nb = (cfg && cfg->tile_nb > 0) ? std::min(cfg->tile_nb, 16)
-                     : DCONV_ENV("DCONV_FWD_NB") ? std::min(atoi(DCONV_ENV("DCONV_FWD_NB")), 16) : 0;
+                     : std::min(env_int("DCONV_FWD_NB", 0), 16);
   int a_px = 0, lin_boxes = 0, pc_st = 0, raw_st = 0, w_st = 0, acc_bufs = 2;
   bool w_all = false;
   FwdSmem layout;
@@ -407,7 +424,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         // phase) in one stage for nb <= 16 -- fewer per-stage barriers and MMA-issue
         // restarts; measured 1.2-1.5x on the 3x3 bf16 layers)
         int wt = taps.taps_box;
-        const int w_cap = DCONV_ENV("DCONV_WCAP") ? atoi(DCONV_ENV("DCONV_WCAP")) * 1024 : (raw_f32 ? 32 : 80) * 1024;
+        const int w_cap = env_int("DCONV_WCAP", raw_f32 ? 32 : 80) * 1024;
         while (wt > 1 && static_cast<int>(fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1).w_slot) > w_cap)
           wt = (wt + 1) / 2;
         const FwdSmem lay = fwd_smem_layout(apx, wt, nb, pieces, raw_f32, 1, 1);
@@ -427,7 +444,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         } else {
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
-          int kcx = (taps.r.size() == 1) ? std::min(DCONV_ENV("DCONV_FWD_KC") ? atoi(DCONV_ENV("DCONV_FWD_KC")) : 4, pb.cb_red) : 1;
+          int kcx = (taps.r.size() == 1) ? std::min(env_int("DCONV_FWD_KC", 4), pb.cb_red) : 1;
           // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
           const int stg_res = (taps.r.size() == 1 || DCONV_ENV("DCONV_STG_RES")) ? 3 * 16384 : 0;
           pcs = 0;
@@ -467,9 +484,9 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
               break;
             }
           }
-          if (const char* e = DCONV_ENV("DCONV_WST")) {  // debug: weight-ring depth sweep
+          if (DCONV_ENV("DCONV_WST")) {  // debug: weight-ring depth sweep
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
-            wss = atoi(e);
+            wss = std::max(1, std::min(kMaxStages, env_int("DCONV_WST", 2)));
             pcs = std::min<int>(kMaxStages, (kFwdBudget - stg_res - wss * static_cast<int>(lk.w_slot)) /
                                                 static_cast<int>(lk.pc_slot));
           }
@@ -543,8 +560,18 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.w_taps = w_taps;
   p.n_ntiles = cdiv(kb_total, tile.nb);
   p.wprep = wprep;
-  // activation map: fp32 as 64 B pixel rows (SWIZZLE_64B, converted to pieces in smem),
-  // bf16 as 32 B pixel rows (SWIZZLE_32B, read in place by the MMA)
+  return L;
+}
+
+// activation tensor map of a resolved forward launch for input `in`
+// (fp32 as 64 B pixel rows, SWIZZLE_64B, converted to pieces on chip; bf16 as
+// 32 B pixel rows, SWIZZLE_32B, read in place by the MMA)
+void encode_fwd_act_map(FwdLaunch& L, const dconv_act_t& in) {
+  const FwdParams& p = L.p;
+  const bool raw_f32 = L.raw_f32;
+  const int st = p.stride, kc = p.kc, a_px = p.a_px;
+  const int hp = in.h + 2 * in.halo_h, wp = in.w + 2 * in.halo_w;
+  const int hw = in.h * in.w;
   const uint64_t planes = static_cast<uint64_t>(in.n) * p.in_cb;
   const uint64_t pix = raw_f32 ? 64 : 32;
   const CUtensorMapSwizzle swz = raw_f32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -557,7 +584,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     const uint32_t box[4] = {16, static_cast<uint32_t>(hw), static_cast<uint32_t>(L.ts ? kc : 1),
                              static_cast<uint32_t>(p.mimg)};
     L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation multi-image", swz);
-  } else if (linear) {
+  } else if (p.linear) {
     const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
     const uint64_t strides[2] = {pix, pix * hp * wp};
     const uint32_t box[3] = {16, static_cast<uint32_t>(kc > 1 ? a_px : 128), static_cast<uint32_t>(kc)};
@@ -571,28 +598,25 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     const uint32_t estr[4] = {1, static_cast<uint32_t>(st), static_cast<uint32_t>(st), 1};
     L.map_a = encode(!raw_f32, 4, base, dims, strides, box, estr, "activation rows", swz);
   }
-  return L;
 }
 
 long long* g_fwd_dbg = nullptr;  // dconv_debug_counters(): per-CTA role cycle counters
 int g_fwd_dbg_mode = 0;
 
-// prof_slot >= 0: bracket the kernel launch with the profiling events (after
-// all host-side encoding, so the interval is device time of the kernel)
-void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof_open = true,
-                bool prof_close = true) {
-  L.p.dbg = g_fwd_dbg;
-  L.p.dbg_mode = g_fwd_dbg_mode;
-  // dense outputs (no halo / lattice / padding columns / multi-image rows):
-  // the epilogue stages 32-pixel slabs in smem and TMA-stores them
+// Epilogue decisions of a forward launch for its output surface (p.out_* set):
+// dense outputs (no halo / lattice / padding columns / multi-image rows) stage
+// 32-pixel slabs in smem and TMA-store them. Resolved once per cached launch.
+void finalize_fwd(FwdLaunch& L) {
   FwdParams& p = L.p;
+  p.dbg = g_fwd_dbg;
+  p.dbg_mode = g_fwd_dbg_mode;
   const int esz = p.out_bf16 ? 2 : 4;
   // 4 warps x 2 slabs of {16 lanes, 32 px, 2 blocks} per epilogue group; bf16
   // smem-staged plans run three groups
   // TS plans with one stage per tile: a second epilogue group (the stores dominate)
   const int kiters = cdiv(p.cb_in, p.kc) * p.n_phases;
   p.ts_epi2 = (L.ts && kiters == 1 && p.nb >= 4 && !DCONV_ENV("DCONV_NO_TS_EPI2")) ? 1 : 0;
-  p.epi_groups = DCONV_ENV("DCONV_EPI_GROUPS") ? atoi(DCONV_ENV("DCONV_EPI_GROUPS")) : 3;
+  p.epi_groups = env_int("DCONV_EPI_GROUPS", 3);
   auto staging_bytes = [&] {
     return static_cast<size_t>((!L.raw_f32 && !L.ts) ? 3 : p.ts_epi2 ? 2 : 1) * 4 * 2 * (2 * 32 * 16 * esz);
   };
@@ -603,35 +627,61 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
   }
   if (L.smem + staging_bytes() > static_cast<size_t>(kSmemBudget)) p.ts_epi2 = 0;
   const size_t staging = staging_bytes();
-  size_t smem = L.smem;
+  L.smem_launch = L.smem;
   p.tma_store = 0;
-  CUtensorMap map_out, map_out2;
-  std::memset(&map_out, 0, sizeof(map_out));
-  std::memset(&map_out2, 0, sizeof(map_out2));
   if (p.mimg == 0 && p.out_halo_h == 0 && p.out_halo_w == 0 && p.out_scale == 1 && p.out_y0 == 0 &&
       p.out_x0 == 0 && p.out_hp == p.P && p.out_wp == p.Q && p.wsub == p.Q && !(p.dbg_mode & 1) &&
       L.smem + staging <= static_cast<size_t>(kSmemBudget)) {
-    const uint64_t pq = static_cast<uint64_t>(p.P) * p.Q;
-    const uint64_t dims[4] = {16, pq, static_cast<uint64_t>(p.out_cb), static_cast<uint64_t>(p.n_img)};
-    const uint64_t strides[3] = {16ull * esz, pq * 16 * esz, pq * 16 * esz * p.out_cb};
-    const uint32_t box[4] = {16, 32, 1, 1};
-    map_out = encode(p.out_bf16, 4, p.out, dims, strides, box, nullptr, "output slab",
-                     p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
-    const uint32_t box2[4] = {16, 32, 2, 1};
-    map_out2 = encode(p.out_bf16, 4, p.out, dims, strides, box2, nullptr, "output slab pair",
-                      p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
     p.tma_store = 1;
-    smem = L.smem + staging;
+    L.smem_launch = L.smem + staging;
   }
+}
+
+// output slab maps of a TMA-store launch (p.out set)
+void encode_fwd_out_maps(FwdLaunch& L) {
+  std::memset(&L.map_out, 0, sizeof(L.map_out));
+  std::memset(&L.map_out2, 0, sizeof(L.map_out2));
+  const FwdParams& p = L.p;
+  if (!p.tma_store) return;
+  const int esz = p.out_bf16 ? 2 : 4;
+  const uint64_t pq = static_cast<uint64_t>(p.P) * p.Q;
+  const uint64_t dims[4] = {16, pq, static_cast<uint64_t>(p.out_cb), static_cast<uint64_t>(p.n_img)};
+  const uint64_t strides[3] = {16ull * esz, pq * 16 * esz, pq * 16 * esz * p.out_cb};
+  const uint32_t box[4] = {16, 32, 1, 1};
+  L.map_out = encode(p.out_bf16, 4, p.out, dims, strides, box, nullptr, "output slab",
+                     p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+  const uint32_t box2[4] = {16, 32, 2, 1};
+  L.map_out2 = encode(p.out_bf16, 4, p.out, dims, strides, box2, nullptr, "output slab pair",
+                      p.out_bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize, raised once per kernel (not per launch)
+std::mutex g_attr_mu;
+std::map<const void*, int> g_attr_smem;
+template <class K>
+void ensure_smem(K kern, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& cur = g_attr_smem[reinterpret_cast<const void*>(kern)];
+  if (cur >= static_cast<int>(smem)) return;
+  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+             "smem attribute");
+  cur = static_cast<int>(smem);
+}
+
+// Launch a resolved forward launch (maps encoded, pointers patched).
+// pdl: programmatic dependent launch -- only when the weight prep was launched
+// on this stream immediately before (its weight producer waits on
+// griddepcontrol.wait; every other role reads data the prep's predecessors wrote).
+// prof_slot >= 0: bracket the kernel launch with the profiling events.
+void launch_fwd(const FwdLaunch& L, cudaStream_t stream, bool pdl, int prof_slot = -1, bool prof_open = true,
+                bool prof_close = true) {
+  const size_t smem = L.smem_launch;
   auto go = [&](auto kern, int threads) {
-    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "smem attribute");
+    ensure_smem(kern, smem);
     if (prof_slot >= 0 && prof_open) prof_begin(prof_slot, stream);
-    // programmatic dependent launch: the kernel starts while the weight prep that
-    // precedes it finishes (its weight producer waits on griddepcontrol.wait)
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr.val.programmaticStreamSerializationAllowed = (prof_slot >= 0 && prof_open) ? 0 : 1;
+    attr.val.programmaticStreamSerializationAllowed = (pdl && !(prof_slot >= 0 && prof_open)) ? 1 : 0;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = L.grid;
     lc.blockDim = dim3(threads, 1, 1);
@@ -639,7 +689,8 @@ void launch_fwd(FwdLaunch& L, cudaStream_t stream, int prof_slot = -1, bool prof
     lc.stream = stream;
     lc.attrs = &attr;
     lc.numAttrs = 1;
-    cuda_check(cudaLaunchKernelEx(&lc, kern, L.map_a, map_out, map_out2, L.p, L.raw_stages, L.stages, L.w_stages),
+    cuda_check(cudaLaunchKernelEx(&lc, kern, L.map_a, L.map_out, L.map_out2, L.p, L.raw_stages, L.stages,
+                                  L.w_stages),
                "conv_fwd_kernel launch");
     if (prof_slot >= 0 && prof_close) prof_end(prof_slot, stream);
   };
@@ -713,6 +764,25 @@ void copy_out(const std::string& s, char* buf, size_t len) {
 }  // namespace
 
 // ====================================================================== plans
+// Resolved launches are cached per tensor geometry (the reference builds its
+// ExecutionPlan once per layer, propagation.cpp:42-54): the tile search, the
+// epilogue decisions and the descriptor JSON happen on the first execute of a
+// geometry; the tensor maps are re-encoded only when a tensor address changes.
+using GeoKey = std::array<int, 16>;
+
+GeoKey geo_key(const dconv_act_t& a, const dconv_act_t& b, int extra = 0) {
+  return {a.n, a.c, a.h, a.w, a.halo_h, a.halo_w, a.dtype, b.n, b.c, b.h, b.w, b.halo_h, b.halo_w, b.dtype,
+          extra, 0};
+}
+
+struct FwdEntry {
+  std::vector<FwdLaunch> L;  // one per launched phase (forward: one)
+  const void* in_ptr = nullptr;
+  const void* out_ptr = nullptr;
+  bool maps = false;
+  std::string desc;
+};
+
 struct dconv_fwd_plan {
   dconv_spec_t spec;
   int math, pieces;
@@ -723,7 +793,9 @@ struct dconv_fwd_plan {
   bool has_cfg;
   Taps taps;
   int* tapmap_dev = nullptr;
-  std::string last_desc;
+  std::mutex mu;
+  std::map<GeoKey, FwdEntry> cache;
+  const std::string* last_desc = nullptr;
 };
 
 struct BwdPhase {
@@ -744,8 +816,12 @@ struct dconv_bwd_plan {
   std::vector<BwdPhase> phases;
   int* tapmap_dev = nullptr;  // concatenated tap maps
   size_t ws_bytes = 0;
-  std::string last_desc;
+  std::mutex mu;
+  std::map<GeoKey, FwdEntry> cache;  // key: (grad_out, grad_in, accumulate)
+  const std::string* last_desc = nullptr;
 };
+
+struct UpdEntry;
 
 struct dconv_upd_plan {
   dconv_spec_t spec;
@@ -753,7 +829,9 @@ struct dconv_upd_plan {
   dconv_engine_config_t cfg;
   bool has_cfg;
   Taps taps;
-  std::string last_desc;
+  std::mutex mu;
+  std::map<GeoKey, UpdEntry*> cache;
+  const std::string* last_desc = nullptr;
   // modelled bf16 variant choice (k-tile width, stacking, c-tiles per CTA) per operand
   // geometry: computed once, not on every execute (the search evaluates ~10 plans)
   mutable std::mutex sel_mu;
@@ -1140,8 +1218,8 @@ size_t dconv_fwd_workspace_bytes(dconv_fwd_plan_t plan) {
 int dconv_fwd_plan_describe(dconv_fwd_plan_t plan, char* buf, size_t len) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
-    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
-             len);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    copy_out(plan->last_desc ? *plan->last_desc : std::string("{\"tile\":\"chosen at first execute\"}"), buf, len);
   });
 }
 
@@ -1151,6 +1229,49 @@ int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t
                   void* workspace, dconv_stream_t stream) {
   return dconv_forward_ex(plan, in, wt, out, nullptr, workspace, stream);
 }
+
+}  // extern "C"
+
+namespace {
+// the forward plan's resolved launch for (in, out) geometry (caller holds plan->mu)
+FwdEntry& fwd_entry(dconv_fwd_plan* plan, const dconv_act_t& in, const dconv_act_t& out) {
+  const GeoKey key = geo_key(in, out);
+  auto it = plan->cache.find(key);
+  if (it != plan->cache.end() && !g_dev_mode) return it->second;
+  const dconv_spec_t& s = plan->spec;
+  const int P = out_P(s), Q = out_Q(s);
+  const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
+  ConvProblem pb;
+  pb.in = in;
+  pb.cb_red = cb;
+  pb.kb_out = kb;
+  pb.P = P;
+  pb.Q = Q;
+  pb.R = s.R;
+  pb.S = s.S;
+  pb.stride = s.stride;
+  pb.row_off = -s.pad_h;
+  pb.col_off = -s.pad_w;
+  FwdLaunch L = plan_fwd_launch(pb, plan->taps, nullptr, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
+  FwdParams& p = L.p;
+  p.out_bf16 = out.dtype == DCONV_BF16;
+  p.out_cb = kb;
+  p.out_hp = P + 2 * out.halo_h;
+  p.out_wp = Q + 2 * out.halo_w;
+  p.out_y0 = out.halo_h;
+  p.out_x0 = out.halo_w;
+  p.out_scale = 1;
+  p.out_halo_h = out.halo_h;
+  p.out_halo_w = out.halo_w;
+  finalize_fwd(L);
+  FwdEntry e;
+  e.L.push_back(L);
+  e.desc = json_tile(L);
+  return plan->cache[key] = std::move(e);
+}
+}  // namespace
+
+extern "C" {
 
 int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
                      const dconv_epilogue_t* ep, void* workspace, dconv_stream_t stream) {
@@ -1172,46 +1293,44 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
     if (out->halo_h != plan->out_halo_h || out->halo_w != plan->out_halo_w)
       fail(DCONV_ERR_PLAN_TENSOR_MISMATCH, "forward: output halo differs from the plan's output surface");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-    const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
-    // weights -> bf16 pieces, phase-sorted taps
-    ConvProblem pb;
-    pb.in = *in;
-    pb.cb_red = cb;
-    pb.kb_out = kb;
-    pb.P = P;
-    pb.Q = Q;
-    pb.R = s.R;
-    pb.S = s.S;
-    pb.stride = s.stride;
-    pb.row_off = -s.pad_h;
-    pb.col_off = -s.pad_w;
-    FwdLaunch L = plan_fwd_launch(pb, plan->taps, workspace, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
-    const int ep_flags = ep ? ep->flags : 0;
-    if (!(ep_flags & DCONV_EP_WEIGHTS_READY))
-      launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev, workspace, cb, L.p.nb, L.p.n_ntiles, 0, plan->pieces,
-                         L.raw_f32 ? 0 : 1, cs);
-    if (ep_flags & DCONV_EP_PREP_ONLY) return;
+    const int cb = cdiv(s.C, 16);
+    FwdLaunch L;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      FwdEntry& e = fwd_entry(plan, *in, *out);
+      FwdLaunch& c = e.L[0];
+      if (!e.maps || e.in_ptr != in->data || e.out_ptr != out->data) {
+        encode_fwd_act_map(c, *in);
+        c.p.out = out->data;
+        encode_fwd_out_maps(c);
+        e.in_ptr = in->data;
+        e.out_ptr = out->data;
+        e.maps = true;
+      }
+      L = c;
+      plan->last_desc = &e.desc;
+    }
     FwdParams& p = L.p;
+    p.wprep = workspace;
     p.out = out->data;
-    p.out_bf16 = out->dtype == DCONV_BF16;
-    p.out_cb = kb;
-    p.out_hp = P + 2 * out->halo_h;
-    p.out_wp = Q + 2 * out->halo_w;
-    p.out_y0 = out->halo_h;
-    p.out_x0 = out->halo_w;
-    p.out_scale = 1;
-    p.out_halo_h = out->halo_h;
-    p.out_halo_w = out->halo_w;
     p.bias = (plan->fuse_kind == DCONV_FUSE_BIAS_ADD || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? plan->bias_dev
                                                                                                   : nullptr;
     p.relu = (plan->fuse_kind == DCONV_FUSE_RELU || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? 1 : 0;
+    p.add = nullptr;
+    p.mask = nullptr;
     if (ep) {
       p.add = ep->add;
       p.mask = ep->mask;
       p.relu |= ep->relu ? 1 : 0;
     }
-    launch_fwd(L, cs, 0);
-    plan->last_desc = json_tile(L);
+    // weights -> bf16 pieces, phase-sorted taps
+    const int ep_flags = ep ? ep->flags : 0;
+    const bool prep = !(ep_flags & DCONV_EP_WEIGHTS_READY);
+    if (prep)
+      launch_weight_prep(*wt, p.n_taps, plan->tapmap_dev, workspace, cb, p.nb, p.n_ntiles, 0, plan->pieces,
+                         L.raw_f32 ? 0 : 1, cs);
+    if (ep_flags & DCONV_EP_PREP_ONLY) return;
+    launch_fwd(L, cs, prep, 0);
   });
 }
 
@@ -1307,8 +1426,8 @@ size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan) { return plan ? std::max
 int dconv_bwd_plan_describe(dconv_bwd_plan_t plan, char* buf, size_t len) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
-    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
-             len);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    copy_out(plan->last_desc ? *plan->last_desc : std::string("{\"tile\":\"chosen at first execute\"}"), buf, len);
   });
 }
 int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
@@ -1322,6 +1441,67 @@ int dconv_bwd_launches(dconv_bwd_plan_t plan) {
   for (auto& ph : plan->phases) n += ph.zero ? 1 : 2;
   return n;
 }
+
+}  // extern "C"
+
+namespace {
+// 1x1 / stride 2 without accumulation: the single tap phase (0, 0) writes the whole
+// dI (its lattice values and the three zero neighbours of each) instead of zero passes
+bool bwd_fill(const dconv_bwd_plan* plan, bool accumulate) {
+  const dconv_spec_t& s = plan->spec;
+  int n_conv = 0;
+  for (auto& ph : plan->phases) n_conv += ph.zero ? 0 : 1;
+  return !accumulate && s.stride == 2 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 && n_conv == 1;
+}
+
+// the backward plan's resolved phase launches for (grad_out, grad_in) geometry
+// and the accumulate mode (caller holds plan->mu)
+FwdEntry& bwd_entry(dconv_bwd_plan* plan, const dconv_act_t& grad_out, const dconv_act_t& grad_in,
+                    bool accumulate) {
+  const GeoKey key = geo_key(grad_out, grad_in, accumulate ? 1 : 0);
+  auto it = plan->cache.find(key);
+  if (it != plan->cache.end() && !g_dev_mode) return it->second;
+  const dconv_spec_t& s = plan->spec;
+  const int cb = cdiv(s.C, 16);
+  const int hp = s.H + 2 * grad_in.halo_h, wp = s.W + 2 * grad_in.halo_w;
+  const bool fill = bwd_fill(plan, accumulate);
+  FwdEntry e;
+  e.desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
+  bool first = true;
+  for (auto& ph : plan->phases) {
+    if (!first) e.desc += ",";
+    first = false;
+    if (ph.zero) {
+      e.desc += accumulate ? "\"skip\"" : fill ? "\"filled\"" : "\"zero\"";
+      continue;
+    }
+    ConvProblem pb = ph.pb;
+    pb.in = grad_out;
+    FwdLaunch L = plan_fwd_launch(pb, ph.taps, nullptr, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
+    FwdParams& p = L.p;
+    p.out_bf16 = grad_in.dtype == DCONV_BF16;
+    p.out_cb = cb;
+    p.out_hp = hp;
+    p.out_wp = wp;
+    p.out_y0 = grad_in.halo_h + ph.a;
+    p.out_x0 = grad_in.halo_w + ph.b;
+    p.out_scale = s.stride;
+    const bool single = s.stride == 1;
+    p.out_halo_h = single ? grad_in.halo_h : 0;
+    p.out_halo_w = single ? grad_in.halo_w : 0;
+    p.out_fill = fill ? 1 : 0;
+    p.fill_h_end = grad_in.halo_h + s.H;
+    p.fill_w_end = grad_in.halo_w + s.W;
+    finalize_fwd(L);
+    e.desc += json_tile(L);
+    e.L.push_back(L);
+  }
+  e.desc += "]}";
+  return plan->cache[key] = std::move(e);
+}
+}  // namespace
+
+extern "C" {
 
 int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv_act_t* grad_out,
                            const dconv_act_t* grad_in, const dconv_epilogue_t* ep, void* workspace,
@@ -1346,25 +1526,31 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
     const bool accumulate = ep && ep->add && ep->add == grad_in->data;
     if (ep && ep->add && !accumulate && s.stride != 1)
       fail(DCONV_ERR_UNSUPPORTED, "backward_data_ex: strided layers accept add == grad_in only");
-    std::string desc = "{\"route\":" + std::to_string(plan->route) + ",\"phases\":[";
-    int tap_off = 0;
-    bool first = true;
-    int n_conv = 0, conv_i = 0;
-    for (auto& ph : plan->phases) n_conv += ph.zero ? 0 : 1;
-    // 1x1 / stride 2: the single tap phase (0, 0) writes the whole dI (its lattice
-    // values and the three zero neighbours of each) instead of zero-phase passes
-    const bool fill = !accumulate && s.stride == 2 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 &&
-                      n_conv == 1;
-    const int ep_flags = ep ? ep->flags : 0;
-    for (auto& ph : plan->phases) {
-      if (!first) desc += ",";
-      first = false;
-      if (ph.zero && (ep_flags & DCONV_EP_PREP_ONLY)) continue;
-      if (ph.zero) {
-        if (accumulate || fill) {  // adding zeros, or written by the tap phase
-          desc += accumulate ? "\"skip\"" : "\"filled\"";
-          continue;
+    const bool fill = bwd_fill(plan, accumulate);
+    std::vector<FwdLaunch> Ls;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      FwdEntry& e = bwd_entry(plan, *grad_out, *grad_in, accumulate);
+      if (!e.maps || e.in_ptr != grad_out->data || e.out_ptr != grad_in->data) {
+        for (auto& c : e.L) {
+          encode_fwd_act_map(c, *grad_out);
+          c.p.out = grad_in->data;
+          encode_fwd_out_maps(c);
         }
+        e.in_ptr = grad_out->data;
+        e.out_ptr = grad_in->data;
+        e.maps = true;
+      }
+      Ls = e.L;
+      plan->last_desc = &e.desc;
+    }
+    const int ep_flags = ep ? ep->flags : 0;
+    const bool prep = !(ep_flags & DCONV_EP_WEIGHTS_READY);
+    const int n_conv = static_cast<int>(Ls.size());
+    int tap_off = 0, conv_i = 0;
+    for (auto& ph : plan->phases) {
+      if (ph.zero) {
+        if (accumulate || fill || (ep_flags & DCONV_EP_PREP_ONLY)) continue;  // adding zeros / written by the tap phase
         const int planes = s.N * cb;
         const int ly = cdiv(s.H - ph.a, s.stride), lx = cdiv(s.W - ph.b, s.stride);
         const int g = grid1d(static_cast<int64_t>(planes) * ly * lx * 16);
@@ -1376,51 +1562,38 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
                                                                 wp, grad_in->halo_h, grad_in->halo_w, s.stride, ph.a,
                                                                 ph.b);
         cuda_check(cudaGetLastError(), "zero_lattice");
-        desc += "\"zero\"";
         continue;
       }
+      FwdLaunch& L = Ls[conv_i];
       void* wprep = reinterpret_cast<char*>(workspace) + ph.ws_off;
-      ConvProblem pb = ph.pb;
-      pb.in = *grad_out;
-      FwdLaunch L = plan_fwd_launch(pb, ph.taps, wprep, plan->pieces, plan->has_cfg ? &plan->cfg : nullptr);
-      if (!(ep_flags & DCONV_EP_WEIGHTS_READY))
-        launch_weight_prep(*wt, L.p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, L.p.nb, L.p.n_ntiles, 1,
-                           plan->pieces, L.raw_f32 ? 0 : 1, cs);
-      tap_off += static_cast<int>(ph.tapmap.size());
-      if (ep_flags & DCONV_EP_PREP_ONLY) continue;
       FwdParams& p = L.p;
+      p.wprep = wprep;
+      if (prep)
+        launch_weight_prep(*wt, p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, p.nb, p.n_ntiles, 1, plan->pieces,
+                           L.raw_f32 ? 0 : 1, cs);
+      tap_off += static_cast<int>(ph.tapmap.size());
+      if (ep_flags & DCONV_EP_PREP_ONLY) {
+        ++conv_i;
+        continue;
+      }
       p.out = grad_in->data;
-      p.out_bf16 = grad_in->dtype == DCONV_BF16;
-      p.out_cb = cb;
-      p.out_hp = hp;
-      p.out_wp = wp;
-      p.out_y0 = grad_in->halo_h + ph.a;
-      p.out_x0 = grad_in->halo_w + ph.b;
-      p.out_scale = s.stride;
-      const bool single = s.stride == 1;
-      p.out_halo_h = single ? grad_in->halo_h : 0;
-      p.out_halo_w = single ? grad_in->halo_w : 0;
       p.bias = nullptr;
       p.relu = 0;
+      p.add = nullptr;
+      p.mask = nullptr;
       if (ep) {
         p.add = ep->add;
         p.mask = ep->mask;
         p.relu = ep->relu ? 1 : 0;
       }
-      p.out_fill = fill ? 1 : 0;
-      p.fill_h_end = grad_in->halo_h + s.H;
-      p.fill_w_end = grad_in->halo_w + s.W;
-      launch_fwd(L, cs, 1, conv_i == 0, conv_i == n_conv - 1);
+      launch_fwd(L, cs, prep, 1, conv_i == 0, conv_i == n_conv - 1);
       ++conv_i;
-      desc += json_tile(L);
     }
-    desc += "]}";
     if (ep_flags & DCONV_EP_PREP_ONLY) return;
     if (s.stride != 1) {
       const int r = dconv_zero_halo(grad_in, stream);
       if (r != DCONV_OK) fail(r, g_err);
     }
-    plan->last_desc = desc;
   });
 }
 
@@ -1445,6 +1618,9 @@ struct UpdLaunch {
   double est_cycles = 0;  // bf16 plans: modelled SM-cycles of the whole launch (selection only)
 };
 
+void encode_upd_maps(UpdLaunch& L, const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_act_t& dout,
+                     const void* in_pieces, const void* do_pieces);
+
 // Tile selection for the split-K UPD (replaces choose_update_strategy /
 // choose_spatial_blocking, planner.cpp:107-173): virtual-pixel band per stage,
 // k-tile width, tap groups bounded by TMEM, split factor for >= 2 waves.
@@ -1467,7 +1643,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     const bool mc_ok = pl.spec.R * pl.spec.S == 1 && cb0 % 16 == 0 && !DCONV_ENV("DCONV_UPD_NO_MC");
     const std::array<int, 12> key = {in.n,   in.c,     in.h,       in.w,   in.halo_h, in.halo_w,
                                      dout.h, dout.w, dout.halo_h, dout.halo_w, in.dtype, dout.dtype};
-    {
+    if (!g_dev_mode) {
       std::lock_guard<std::mutex> lk(pl.sel_mu);
       const auto it = pl.sel_cache.find(key);
       if (it != pl.sel_cache.end())
@@ -1665,10 +1841,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   }
   // single-tap layers: A (activations) converted straight into a TMEM ring, so only
   // the raw boxes and the dO pieces occupy shared memory
-  const char* tsa_env = std::getenv("DCONV_UPD_TSA");  // live: tests toggle it per plan
+  const char* tsa_env = dev_env("DCONV_UPD_TSA");  // developer mode: tests toggle it per plan
   if (want_raw && !stacked && taps.r.size() == 1 && !(tsa_env && tsa_env[0] == '0')) {
     const int acc_w = (pieces == 3 && 3 * NT <= 256) ? 3 * NT : NT;
-    const int want_vs = tsa_env ? std::atoi(tsa_env) : 0;  // > 1: force the stage band (experiments)
+    const int want_vs = env_int("DCONV_UPD_TSA", 0);  // > 1: force the stage band (experiments)
     for (auto& cd : cands) {
       if (cd.passes != 1 || (want_vs > 1 && cd.vs != want_vs)) continue;
       const UpdRawLayout rl = upd_raw_layout(cd.a_px, cd.vs, p.nb, pieces, 1, 8, 1);
@@ -1769,7 +1945,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     }
   }
   if (pl.has_cfg && pl.cfg.upd_splits > 0) splits = std::min(pl.cfg.upd_splits, p.stages_total);
-  if (DCONV_ENV("DCONV_UPD_SPLITS")) splits = std::max(1, std::min(std::atoi(DCONV_ENV("DCONV_UPD_SPLITS")), p.stages_total));
+  if (DCONV_ENV("DCONV_UPD_SPLITS")) splits = std::max(1, std::min(env_int("DCONV_UPD_SPLITS", 1), p.stages_total));
   p.splits = splits;
   // fp32-accurate: bound the accumulation chain per TMEM accumulator (the tensor
   // core truncates each fp32 accumulate; a 1-split cfg2 chain of 6272 k-steps drifted
@@ -1815,7 +1991,30 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   L.ws_in = L.split_in ? align256(static_cast<size_t>(pieces) * act_elems(in) * 2) : 0;
   L.ws_do = L.split_do ? align256(static_cast<size_t>(pieces) * act_elems(dout) * 2) : 0;
   L.ws_partial = align256(static_cast<size_t>(splits) * p.n_taps * p.c_pad * p.k_pad * sizeof(float));
+  if (!L.raw) {
+    p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !DCONV_ENV("DCONV_UPD_NO_SW32")) ? 1 : 0;
+    // cp.async loader warps in place of the TMA box loads: opt-in experiment only
+    // (DCONV_UPD_LSU=1). Measured 2-5x SLOWER than the TMA boxes on every ResNet-50
+    // layer (per-chunk address arithmetic on six warps, and the loaders share the
+    // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
+    // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
+    p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && DCONV_ENV("DCONV_UPD_LSU")) ? 1 : 0;
+  }
   if (!encode_maps) return L;
+  encode_upd_maps(L, pl, in, dout, in_pieces, do_pieces);
+  return L;
+}
+
+// operand tensor maps of a resolved weight-update launch (and the cp.async
+// loader pointers of developer-mode lsu plans)
+void encode_upd_maps(UpdLaunch& L, const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_act_t& dout,
+                     const void* in_pieces, const void* do_pieces) {
+  UpdParams& p = L.p;
+  const dconv_spec_t& s = pl.spec;
+  const int pieces = pl.pieces;
+  const int st = s.stride;
+  const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
+  const bool linear = p.linear != 0;
   // operand maps over bf16 piece tensors (piece-major planes)
   auto act_map = [&](const dconv_act_t& a, const void* data, int chans_blocks, bool is_in) {
     const int hp = a.h + 2 * a.halo_h, wp = a.w + 2 * a.halo_w;
@@ -1888,15 +2087,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   if (L.raw) {
     L.map_in = raw_map(in, true);
     L.map_do = raw_map(dout, false);
-    return L;
+    return;
   }
-  p.sw32 = (pieces == 1 && !L.split_in && !L.split_do && !p.half && !DCONV_ENV("DCONV_UPD_NO_SW32")) ? 1 : 0;
-  // cp.async loader warps in place of the TMA box loads: opt-in experiment only
-  // (DCONV_UPD_LSU=1). Measured 2-5x SLOWER than the TMA boxes on every ResNet-50
-  // layer (per-chunk address arithmetic on six warps, and the loaders share the
-  // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
-  // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
-  p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && DCONV_ENV("DCONV_UPD_LSU")) ? 1 : 0;
   if (p.lsu) {
     const int ihp = in.h + 2 * in.halo_h, iwp = in.w + 2 * in.halo_w;
     const int dhp = dout.h + 2 * dout.halo_h, dwp = dout.w + 2 * dout.halo_w;
@@ -1913,7 +2105,47 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   }
   L.map_in = act_map(in, in_pieces, cb, true);
   L.map_do = act_map(dout, do_pieces, kb, false);
-  return L;
+}
+
+}  // namespace
+
+struct UpdEntry {
+  UpdLaunch L;  // maps encoded for the pointers below
+  const void* in_ptr = nullptr;
+  const void* do_ptr = nullptr;
+  bool maps = false;
+  std::string desc;
+};
+
+namespace {
+
+std::string json_upd(const UpdLaunch& L, int pieces) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf),
+                "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
+                "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
+                "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d,\"a_in_tmem\":%d,\"drain\":%d,"
+                "\"drain_bufs\":%d}",
+                L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
+                L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, pieces, L.passes,
+                L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0, L.p.drain, L.p.drain_bufs);
+  return buf;
+}
+
+// the weight-update plan's resolved launch for (in, grad_out) geometry (caller holds pl->mu)
+UpdEntry& upd_entry(dconv_upd_plan* pl, const dconv_act_t& in, const dconv_act_t& dout) {
+  const GeoKey key = geo_key(in, dout);
+  auto it = pl->cache.find(key);
+  if (it != pl->cache.end()) {
+    if (!g_dev_mode) return *it->second;
+    delete it->second;
+    pl->cache.erase(it);
+  }
+  auto* e = new UpdEntry();
+  e->L = plan_upd(*pl, in, dout, false, nullptr, nullptr, nullptr);
+  e->desc = json_upd(e->L, pl->pieces);
+  pl->cache[key] = e;
+  return *e;
 }
 
 void launch_split(const dconv_act_t& a, void* dst, int pieces, cudaStream_t cs) {
@@ -1951,7 +2183,11 @@ int dconv_upd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
   return st;
 }
 
-void dconv_upd_plan_destroy(dconv_upd_plan_t plan) { delete plan; }
+void dconv_upd_plan_destroy(dconv_upd_plan_t plan) {
+  if (!plan) return;
+  for (auto& kv : plan->cache) delete kv.second;
+  delete plan;
+}
 
 static dconv_act_t default_act(const dconv_spec_t& s, bool grad, int dtype) {
   dconv_act_t a;
@@ -1973,9 +2209,8 @@ int dconv_upd_splits(dconv_upd_plan_t plan) {
   int v = -1;
   guarded([&] {
     const int dt = plan->pieces == 3 ? DCONV_F32 : DCONV_BF16;
-    v = plan_upd(*plan, default_act(plan->spec, false, dt), default_act(plan->spec, true, dt), false, nullptr,
-                 nullptr, nullptr)
-            .p.splits;
+    std::lock_guard<std::mutex> lk(plan->mu);
+    v = upd_entry(plan, default_act(plan->spec, false, dt), default_act(plan->spec, true, dt)).L.p.splits;
   });
   return v;
 }
@@ -1983,8 +2218,8 @@ int dconv_upd_splits(dconv_upd_plan_t plan) {
 int dconv_upd_plan_describe(dconv_upd_plan_t plan, char* buf, size_t len) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
-    copy_out(plan->last_desc.empty() ? std::string("{\"tile\":\"chosen at first execute\"}") : plan->last_desc, buf,
-             len);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    copy_out(plan->last_desc ? *plan->last_desc : std::string("{\"tile\":\"chosen at first execute\"}"), buf, len);
   });
 }
 
@@ -1992,7 +2227,8 @@ size_t dconv_upd_workspace_bytes(dconv_upd_plan_t plan, const dconv_act_t* in, c
   if (!plan || !in || !grad_out) return 0;
   size_t v = 0;
   guarded([&] {
-    const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    const UpdLaunch& L = upd_entry(plan, *in, *grad_out).L;
     v = L.ws_in + L.ws_do + L.ws_partial;
   });
   return v;
@@ -2002,7 +2238,8 @@ int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv
   if (!plan || !in || !grad_out) return 0;
   int v = 0;
   guarded([&] {
-    const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    const UpdLaunch& L = upd_entry(plan, *in, *grad_out).L;
     v = 1 + L.passes + (L.split_in ? 1 : 0) + (L.split_do ? 1 : 0);
   });
   return v;
@@ -2027,26 +2264,38 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     if (grad_w->k != s.K || grad_w->c != s.C || grad_w->r != s.R || grad_w->s != s.S || grad_w->vlen != s.vlen)
       fail(DCONV_ERR_SHAPE_MISMATCH, "weight_update: grad_w does not match the layer spec");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-    UpdLaunch L0 = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
     char* ws = reinterpret_cast<char*>(workspace);
-    void* in_pc = L0.split_in ? ws : in->data;
-    void* do_pc = L0.split_do ? ws + L0.ws_in : grad_out->data;
-    float* partial = reinterpret_cast<float*>(ws + L0.ws_in + L0.ws_do);
-    if (L0.split_in) launch_split(*in, in_pc, plan->pieces, cs);
-    if (L0.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
-    UpdLaunch L = plan_upd(*plan, *in, *grad_out, true, in_pc, do_pc, partial);
+    UpdLaunch L;
+    void* in_pc = nullptr;
+    void* do_pc = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      UpdEntry& e = upd_entry(plan, *in, *grad_out);
+      in_pc = e.L.split_in ? ws : in->data;
+      do_pc = e.L.split_do ? ws + e.L.ws_in : grad_out->data;
+      if (!e.maps || e.in_ptr != in_pc || e.do_ptr != do_pc) {
+        encode_upd_maps(e.L, *plan, *in, *grad_out, in_pc, do_pc);
+        e.in_ptr = in_pc;
+        e.do_ptr = do_pc;
+        e.maps = true;
+      }
+      L = e.L;
+      plan->last_desc = &e.desc;
+    }
+    float* partial = reinterpret_cast<float*>(ws + L.ws_in + L.ws_do);
+    L.p.partial = partial;
     L.p.dbg_mode = g_fwd_dbg_mode;
+    if (L.split_in) launch_split(*in, in_pc, plan->pieces, cs);
+    if (L.split_do) launch_split(*grad_out, do_pc, plan->pieces, cs);
     bool opened = false;  // profiling bracket opens right before the first conv kernel
     auto go = [&](auto kern, int a_base, int acc) {
-      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
-                 "smem attribute");
+      ensure_smem(kern, L.smem);
       if (!opened) prof_begin(2, cs), opened = true;
       kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages, a_base, acc);
       cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
     };
     auto go_raw = [&](auto kern) {
-      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.smem)),
-                 "smem attribute");
+      ensure_smem(kern, L.smem);
       if (!opened) prof_begin(2, cs), opened = true;
       kern<<<L.grid, (L.tsa ? kUpdTsWarps : kUpdRawWarps) * 32, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.raw_stages,
                                                                              L.pc_stages);
@@ -2079,6 +2328,8 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
     const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
     {
+      // programmatic dependent launch: the reduce waits (griddepcontrol.wait) for the
+      // update kernel that precedes it on this stream, before it reads the partials
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr.val.programmaticStreamSerializationAllowed = g_prof ? 0 : 1;
@@ -2098,15 +2349,6 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
                  "upd_reduce launch");
     }
     cuda_check(cudaGetLastError(), "upd_reduce launch");
-    char buf[512];
-    std::snprintf(buf, sizeof(buf),
-                  "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
-                  "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
-                  "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d,\"a_in_tmem\":%d}",
-                  L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
-                  L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, plan->pieces, L.passes,
-                  L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0);
-    plan->last_desc = buf;
   });
 }
 
@@ -2307,3 +2549,4 @@ int dconv_sgd(const dconv_wt_t* w, const dconv_wt_t* g, float lr, dconv_stream_t
 
 #include "host_step.cuh"
 #include "validate.cuh"
+#include "plan_io.cuh"

@@ -346,14 +346,15 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
-  long long* dbg = p.dbg ? p.dbg + static_cast<long long>(blockIdx.x) * 16 : nullptr;
+  long long* dbg = (kDevBuild && p.dbg) ? p.dbg + static_cast<long long>(blockIdx.x) * 16 : nullptr;
+  const int dbg_mode = kDevBuild ? p.dbg_mode : 0;  // ablation bits (developer builds)
   long long t_start = clock64();
   if (dbg && threadIdx.x == 0) {
     uint64_t gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     dbg[9] = static_cast<long long>(gt);
   }
-  long long c_a = 0, c_b = 0, c_c = 0, c_d = 0, c_e = 0, c_f = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
+  long long c_a = 0, c_b = 0;  // role-local counters (lane 0 / thread 0 of the role writes)
 
   // tile t -> (n, v0, ntile); output-channel tiles innermost so consecutive
   // CTAs share the activation tile through L2
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             mbar_wait_t(&pc_empty[s], rp.ph ^ 1u, dbg ? &c_a : nullptr);
             uint8_t* dst = smem + s * L.pc_slot;
             if (dbg && blockIdx.x == 0 && g < 256) dbg[gridDim.x * 16 + g * 8 + 6] = clock64() - t_start;
-            if (p.dbg_mode & 256) {  // ablation: no activation loads
+            if (dbg_mode & 256) {  // ablation: no activation loads
               mbar_arrive(&pc_full[s]);
               continue;
             }
@@ -485,9 +486,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             const int nt = min(p.w_taps, s_phase_ntaps[ph] - t0);
             const int s = wp.idx;
             mbar_wait(&w_empty[s], wp.ph ^ 1u);
-            if (p.dbg && blockIdx.x == 0 && g < 256) p.dbg[gridDim.x * 16 + g * 8 + 7] = clock64() - t_start;
+            if (dbg && blockIdx.x == 0 && g < 256) p.dbg[gridDim.x * 16 + g * 8 + 7] = clock64() - t_start;
             const uint32_t w_bytes = static_cast<uint32_t>(nt) * w_tap;
-            if (p.dbg_mode & 128) {  // ablation: no weight loads
+            if (dbg_mode & 128) {  // ablation: no weight loads
               mbar_arrive(&w_full[s]);
               continue;
             }
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               const uint64_t bk = bd0 + static_cast<uint64_t>((static_cast<uint32_t>(kk) * w_tap) >> 4);
               const uint32_t ak = a0 + static_cast<uint32_t>(kk) * kRingCols;
               const bool first = it == 0 && kk == 0;
-              if (p.dbg_mode & 8) continue;  // ablation: no MMAs
+              if (dbg_mode & 8) continue;  // ablation: no MMAs
               mma_bf16_ts(d_hi, ak, bk, idesc, first ? 0u : 1u);
               if (PIECES == 3) {
                 mma_bf16_ts(d_x, ak, bk + w_pc, idesc, (two_acc && first) ? 0u : 1u);
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
 #pragma unroll
             for (int i = 0; i < kFastTaps; ++i) sh[i] = i < nt ? kRow * static_cast<uint32_t>(s_tap_shift[tap0 + i]) : 0u;
             const uint32_t b_tap = w_tap >> 4;
-            const bool do_mma = !(p.dbg_mode & 8);  // ablation: no MMAs
+            const bool do_mma = !(dbg_mode & 8);  // ablation: no MMAs
             auto issue = [&](auto mb_c) {
               constexpr int MB = decltype(mb_c)::value;
               for (int kk = 0; kk < kc_eff; ++kk) {
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                   const uint32_t d_x = two_acc ? d_lo : d_hi;
                   const bool first = it == 0 && t0 == 0 && tp == 0 && kk == 0;
                   const uint64_t ad = a_base + a_off, bd = b_base + b_off;
-                  if (p.dbg_mode & 8) continue;  // ablation: no MMAs
+                  if (dbg_mode & 8) continue;  // ablation: no MMAs
                   mma_bf16(d_hi, ad, bd, idesc, first ? 0u : 1u);
                   if (PIECES == 3) {  // products (ia, ib) with ia + ib <= 2
                     mma_bf16(d_x, ad, bd + w_pc, idesc, (two_acc && first) ? 0u : 1u);
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     };
     bool done = false;
     if constexpr (!RAW_F32) {
-      if ((p.add != nullptr || p.mask != nullptr) && p.out_bf16 && !(p.dbg_mode & 512)) {  // dbg 512: no prefetch
+      if ((p.add != nullptr || p.mask != nullptr) && p.out_bf16 && !(dbg_mode & 512)) {  // dbg 512: no prefetch
         lean_fused_bf16(0);
         done = true;
       }
@@ -1034,7 +1035,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         tc_fence_after();
         const uint8_t* raw = smem + L.raw_off + rs * L.raw_slot;
         const int kc_eff = min(p.kc, p.cb_in - cbi * p.kc);
-        if (!(p.dbg_mode & 4))
+        if (!(dbg_mode & 4))
         for (int kk = 0; kk < kc_eff; ++kk) {
         const uint32_t px = base + static_cast<uint32_t>(kk) * kstride;
         float v[16];
@@ -1168,13 +1169,13 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         valid = valid && qq < p.Q;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
-        for (int g0 = 2 * (item - mb * n_pairs); g0 < ((p.dbg_mode & 64) ? g_lo : g_hi); g0 += 2 * n_pairs) {
+        for (int g0 = 2 * (item - mb * n_pairs); g0 < ((dbg_mode & 64) ? g_lo : g_hi); g0 += 2 * n_pairs) {
           // two 16-column TMEM loads in flight, one wait
           const int ng = min(2, g_hi - g0);
           uint32_t r[2][16], rl[2][16];
 #pragma unroll
           for (int k = 0; k < 2; ++k)
-            if (k < ng && !(p.dbg_mode & 2)) {
+            if (k < ng && !(dbg_mode & 2)) {
               tmem_ld16(d_base + static_cast<uint32_t>(mb * NT + (g0 + k) * 16), r[k]);
               if (two_acc) tmem_ld16(d_base + static_cast<uint32_t>((p.mb + mb) * NT + (g0 + k) * 16), rl[k]);
             }
@@ -1210,7 +1211,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
-            if (!(p.dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
+            if (!(dbg_mode & 1)) store16(obase + px_off, vals, p.out_bf16);
             if (p.out_fill) {
               // 1x1 / stride-2 backward: this lattice pixel (2y', 2x') owns the three
               // off-lattice neighbours, which are exactly zero (acceptance.cpp:106-117);

@@ -4,7 +4,15 @@
 #include <cuda.h>
 #include <stdint.h>
 
+// Developer build (tools/: role cycle counters and ablation bits). Product builds
+// compile every dbg / dbg_mode branch out of the kernels.
+#ifndef DCONV_DEV_BUILD
+#define DCONV_DEV_BUILD 0
+#endif
+
 namespace dconv_sm100 {
+
+constexpr bool kDevBuild = DCONV_DEV_BUILD != 0;
 
 constexpr int kMaxTaps = 64;
 constexpr int kMaxPhases = 4;

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
         for (int t = 0; t < n_acc; ++t) {
           const int shift = stacked ? 0 : s_tap_shift[tap0 + t];
           const uint32_t d_tmem = acc0 + static_cast<uint32_t>(t * acc_w);
-          for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
+          for (int ks = 0; ks < (((kDevBuild ? p.dbg_mode : 0) & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
             const bool first = p_first && ks == 0;
             const uint64_t ak = a0 + static_cast<uint32_t>(ks * 16 + shift);  // 16 B per pixel row
             const uint64_t bk = b0 + static_cast<uint32_t>(ks) * 16u;          // 256 B per k-step
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kUpdRawWarps * 32, 1)
       const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
       uint8_t* pcs = smem + R.pc_off + static_cast<uint32_t>(ps) * R.pc_slot;
 #pragma unroll
-      for (int u = 0; u < ((p.dbg_mode & 4) ? 0 : 6); ++u) {
+      for (int u = 0; u < (((kDevBuild ? p.dbg_mode : 0) & 4) ? 0 : 6); ++u) {
         const uint32_t piece_stride = piece_str[u];
         const uint8_t* src0 = raw + src_base[u];
         uint8_t* dst0 = pcs + dst_base[u];
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
         const uint64_t b_pc = b_piece >> 4;
         const uint32_t id3 = make_idesc(1, 0, 1, 128, 3u * NT), id2 = make_idesc(1, 0, 1, 128, 2u * NT),
                        id1 = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
-        for (int ks = 0; ks < ((p.dbg_mode & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
+        for (int ks = 0; ks < (((kDevBuild ? p.dbg_mode : 0) & 8) ? 0 : ksteps); ++ks) {  // dbg 8: ablation, no MMAs
           const bool first = p_first && ks == 0;
           const uint32_t ak = a_t + static_cast<uint32_t>(ks) * 8u;
           const uint64_t bk = b0 + static_cast<uint64_t>(ks) * 16u;  // 256 B per k-step
@@ -996,12 +996,12 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
       mbar_wait_backoff(&raw_full[rs], static_cast<uint32_t>(it / raw_stages) & 1u);
       tc_fence_after();
       const uint8_t* raw = smem + static_cast<uint32_t>(rs) * R.raw_slot;
-      if (!(p.dbg_mode & 4)) {
+      if (!((kDevBuild ? p.dbg_mode : 0) & 4)) {
         // A: this channel's values over the stage's pixels -> pieces, 2 pixels per column
         const uint32_t col0 = tmem_base + (q * 32u << 16) + acc_all + static_cast<uint32_t>(ps) * ring_slot;
         // 16-pixel units; the next unit's values are loaded before this unit's
         // tcgen05.st so shared-memory latency overlaps the split arithmetic
-        const int px_end = (p.dbg_mode & 64) ? 0 : p.vs;
+        const int px_end = ((kDevBuild ? p.dbg_mode : 0) & 64) ? 0 : p.vs;
         float xa[16];
         auto load_unit = [&](int px0) {
 #pragma unroll
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
         }
         // dO: chunk planes (8 k-channels) -> MN-major pieces in smem
         uint8_t* pcs = smem + R.pc_off + static_cast<uint32_t>(ps) * pc_slot;
-        for (int cp = static_cast<int>(q); cp < ((p.dbg_mode & 128) ? 0 : 2 * p.nb); cp += 4) {
+        for (int cp = static_cast<int>(q); cp < (((kDevBuild ? p.dbg_mode : 0) & 128) ? 0 : 2 * p.nb); cp += 4) {
           const uint32_t c0 = 2u * (cp & 1), rbase = static_cast<uint32_t>((cp >> 1) * p.vs);
           for (int px = lane; px < p.vs; px += 32) {
             const uint32_t off = sw64_row(rbase + px, c0);

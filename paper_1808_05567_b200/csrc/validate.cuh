@@ -81,6 +81,20 @@ void cover_launch(const FwdLaunch& L, std::vector<uint8_t>& cnt, VReport& r) {
   }
 }
 
+// the launch computes the problem it is attached to (a loaded or corrupted plan
+// is rejected before the coverage replay indexes anything)
+void check_problem(const FwdLaunch& L, int n_img, int P, int Q, int kb_out, int cb_red, VReport& r) {
+  const FwdParams& p = L.p;
+  r.fail_if(p.n_img != n_img || p.P != P || p.Q != Q || p.kb_out != kb_out || p.cb_in != cb_red,
+            "launch problem (images, output extents, channel blocks) differs from the tensors");
+  r.fail_if(p.mb < 1 || p.mb > 4 || p.nb < 1 || p.nb > 16 || p.wsub < p.Q || p.tiles_per_img < 0 || p.mimg < 0 ||
+                p.n_ntiles < 1 || p.n_ntiles * p.nb < kb_out || p.kc < 1 || p.kc > 4,
+            "tile shape outside the kernel's limits");
+  r.fail_if(p.n_phases < 1 || p.n_phases > kMaxPhases || p.n_taps < 1 || p.n_taps > kMaxTaps || p.w_taps < 1,
+            "tap tables outside the kernel's limits");
+  r.fail_if(L.grid.x < 1 || L.grid.y != 1 || L.grid.z != 1, "grid must be (ctas, 1, 1)");
+}
+
 // staging geometry of one launch
 void check_geometry(const FwdLaunch& L, int maxshift, VReport& r) {
   const FwdParams& p = L.p;
@@ -124,27 +138,25 @@ int dconv_fwd_plan_validate(dconv_fwd_plan_t plan, const dconv_act_t* in, const 
     if (in->n != s.N || in->c != s.C || in->h != s.H || in->w != s.W || out->n != s.N || out->c != s.K ||
         out->h != P || out->w != Q)
       fail(DCONV_ERR_SHAPE_MISMATCH, "validate: tensors do not match the layer spec");
-    ConvProblem pb;
-    pb.in = *in;
-    pb.cb_red = cdiv(s.C, 16);
-    pb.kb_out = cdiv(s.K, 16);
-    pb.P = P;
-    pb.Q = Q;
-    pb.R = s.R;
-    pb.S = s.S;
-    pb.stride = s.stride;
-    pb.row_off = -s.pad_h;
-    pb.col_off = -s.pad_w;
-    FwdLaunch L = plan_fwd_launch(pb, plan->taps, reinterpret_cast<void*>(256), plan->pieces,
-                                  plan->has_cfg ? &plan->cfg : nullptr);
+    // the launch the plan will execute for these tensors (cached, or loaded by
+    // dconv_plan_load: a reloaded plan is validated exactly as it will run)
+    FwdLaunch L;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      L = fwd_entry(plan, *in, *out).L.at(0);
+    }
+    struct {
+      int kb_out;
+    } pb{cdiv(s.K, 16)};
     VReport r;
     std::vector<uint8_t> cnt(static_cast<size_t>(s.N) * P * Q * pb.kb_out, 0);
     r.outputs = static_cast<long long>(cnt.size());
-    cover_launch(L, cnt, r);
+    check_problem(L, s.N, P, Q, pb.kb_out, cdiv(s.C, 16), r);
+    if (r.err.empty()) cover_launch(L, cnt, r);
     check_geometry(L, plan->taps.r2max * L.p.wsub + plan->taps.s2max, r);
     for (size_t i = 0; i < cnt.size() && r.err.empty(); ++i)
       r.fail_if(cnt[i] != 1, "output element " + std::to_string(i) + " written " + std::to_string(cnt[i]) + " times");
-    r.fail_if(dconv_fwd_workspace_bytes(plan) < prep_bytes(plan->pieces, pb.cb_red, L.p.n_taps, pb.kb_out),
+    r.fail_if(dconv_fwd_workspace_bytes(plan) < prep_bytes(plan->pieces, cdiv(s.C, 16), L.p.n_taps, pb.kb_out),
               "workspace smaller than the prepared weights");
     copy_out(vjson(r, ",\"plan\":" + json_tile(L)), report, len);
     if (!r.err.empty()) fail(DCONV_ERR_INVALID_DESCRIPTOR, "plan validation: " + r.err);
@@ -165,9 +177,13 @@ int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, 
     std::vector<uint8_t> cnt(static_cast<size_t>(s.N) * s.H * s.W * kb, 0);
     VReport r;
     r.outputs = static_cast<long long>(cnt.size());
-    int n_conv = 0;
-    for (auto& ph : plan->phases) n_conv += ph.zero ? 0 : 1;
-    const bool fill = s.stride == 2 && s.R == 1 && s.S == 1 && s.pad_h == 0 && s.pad_w == 0 && n_conv == 1;
+    const bool fill = bwd_fill(plan, false);
+    std::vector<FwdLaunch> Ls;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      Ls = bwd_entry(plan, *grad_out, *grad_in, false).L;
+    }
+    size_t conv_i = 0;
     std::string phases = "[";
     for (auto& ph : plan->phases) {
       const int ly = cdiv(s.H - ph.a, s.stride), lx = cdiv(s.W - ph.b, s.stride);
@@ -183,13 +199,16 @@ int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, 
         phases += std::string(phases.size() > 1 ? "," : "") + (fill ? "\"filled\"" : "\"zero\"");
         continue;
       }
-      ConvProblem pb = ph.pb;
-      pb.in = *grad_out;
-      FwdLaunch L = plan_fwd_launch(pb, ph.taps, reinterpret_cast<void*>(256), plan->pieces,
-                                    plan->has_cfg ? &plan->cfg : nullptr);
-      r.fail_if(L.p.P != ly || L.p.Q != lx, "phase output extent differs from its dI lattice");
-      std::vector<uint8_t> lat(static_cast<size_t>(s.N) * L.p.P * L.p.Q * L.p.kb_out, 0);
+      if (conv_i >= Ls.size()) {
+        r.fail_if(true, "plan has fewer phase launches than tap phases");
+        break;
+      }
+      const FwdLaunch& L = Ls[conv_i++];
       VReport pr;
+      check_problem(L, s.N, ly, lx, kb, cdiv(s.K, 16), pr);
+      r.fail_if(!pr.err.empty(), pr.err);
+      if (!r.err.empty()) break;
+      std::vector<uint8_t> lat(static_cast<size_t>(s.N) * L.p.P * L.p.Q * L.p.kb_out, 0);
       cover_launch(L, lat, pr);
       check_geometry(L, ph.taps.r2max * L.p.wsub + ph.taps.s2max, pr);
       r.fail_if(!pr.err.empty(), pr.err);
@@ -227,9 +246,22 @@ int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const 
     check_act(in, "validate input");
     check_act(grad_out, "validate grad_out");
     const dconv_spec_t& s = plan->spec;
-    const UpdLaunch L = plan_upd(*plan, *in, *grad_out, false, nullptr, nullptr, nullptr);
+    UpdLaunch L;
+    {
+      std::lock_guard<std::mutex> lk(plan->mu);
+      L = upd_entry(plan, *in, *grad_out).L;
+    }
     const UpdParams& p = L.p;
     VReport r;
+    r.fail_if(L.stages < 1 || L.stages > kMaxStages || L.raw_stages > kMaxStages || L.pc_stages > kMaxStages,
+              "ring depth outside 1..kMaxStages");
+    r.fail_if(p.n_tgroups < 1 || p.n_tgroups > kMaxTapGroups || p.n_taps != s.R * s.S || p.splits < 1 ||
+                  p.vs < 16 || p.vs % 16 != 0 || p.nb < 1 || p.nb > 16 || p.n_img != s.N ||
+                  p.stages_per_img < 1 || p.stages_total != p.n_img * p.stages_per_img,
+              "launch tables outside the kernel's limits");
+    r.fail_if(static_cast<int>(L.grid.z) != p.splits || static_cast<int>(L.grid.x) % p.n_tgroups != 0,
+              "grid does not match (c-tiles x tap groups, k-tiles, splits)");
+    if (!r.err.empty()) fail(DCONV_ERR_INVALID_DESCRIPTOR, "plan validation: " + r.err);
     // a CTA covers p.mc consecutive 128-channel c-tiles
     const int n_ctiles = static_cast<int>(L.grid.x) / p.n_tgroups * (p.mc > 1 ? p.mc : 1),
               n_ktiles = static_cast<int>(L.grid.y);

@@ -487,14 +487,19 @@ def test_update_tmem_and_smem_staging_agree(dconv, orc, shape, math, monkeypatch
     ref = orc.conv_update(s, x, g)
     ib = dconv.to_blocked_activation(dev(x), spec)
     gb = dconv.to_blocked_activation(dev(g), 16, 0, 0)
-    for env, flag in (("1", 1), ("0", 0)):
-        monkeypatch.setenv("DCONV_UPD_TSA", env)
-        up = dconv.UpdatePlan(spec, None, math)
-        dw = dconv.BlockedWeight(K, C_, 1, 1)
-        up.execute(ib, gb, dw)
-        torch.cuda.synchronize()
-        assert up.blocking["a_in_tmem"] == flag, up.blocking
-        gate(orc, ref, dconv.from_blocked_weight(dw).cpu().numpy(), math)
+    lib = dconv._lib.lib()
+    lib.dconv_set_dev_mode(1)  # the DCONV_* overrides are inert outside developer mode
+    try:
+        for env, flag in (("1", 1), ("0", 0)):
+            monkeypatch.setenv("DCONV_UPD_TSA", env)
+            up = dconv.UpdatePlan(spec, None, math)
+            dw = dconv.BlockedWeight(K, C_, 1, 1)
+            up.execute(ib, gb, dw)
+            torch.cuda.synchronize()
+            assert up.blocking["a_in_tmem"] == flag, up.blocking
+            gate(orc, ref, dconv.from_blocked_weight(dw).cpu().numpy(), math)
+    finally:
+        lib.dconv_set_dev_mode(0)
 
 
 # ------------------------------------------------------------------ bf16 storage (the executor's tensors)
