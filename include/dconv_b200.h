@@ -289,6 +289,72 @@ int dconv_host_step_run(dconv_host_step_t step, const dconv_act_t* x, const dcon
 /* kernels launched by the last run */
 int dconv_host_step_launches(dconv_host_step_t step);
 
+/* ---------------------------------------------------------------- layer-graph executor */
+/* run_chain (harness.cpp:311-358; ChainLayer harness.hpp:84-95) grown into the
+ * data-parallel training step of a conv DAG: forward (ReLU / residual add fused),
+ * backward-data (ReLU mask / branch sum fused), weight updates on a side stream,
+ * NCCL all-reduce of the fp32 weight gradients in buckets (backward order,
+ * overlapped with the backward of earlier layers; COPY_REDUCE over minibatch
+ * shards, propagation.cpp:357-375, promoted to GPUs), SGD; capturable into one
+ * CUDA graph per step at any world size. Tensors are blocked, halo 0, vlen 16. */
+typedef enum dconv_node_kind { DCONV_NODE_CONV = 0, DCONV_NODE_MAXPOOL = 1 /* 3x3, stride 2, pad 1 */ } dconv_node_kind_t;
+typedef struct dconv_graph_node {
+  int kind;
+  int src; /* input tensor id: 0 = the graph input, node i writes tensor i + 1 */
+  int add; /* conv: tensor id added before the ReLU (residual), -1 = none */
+  int C, K, R, S, stride, pad_h, pad_w;
+  int relu; /* conv: ReLU on the output */
+} dconv_graph_node_t;
+typedef struct dconv_graph_config {
+  float lr;             /* SGD learning rate */
+  int seed;             /* He-normal weights: splitmix64 seed * 1000 + conv index */
+  int64_t bucket_bytes; /* gradient all-reduce bucket size */
+  int world, rank;      /* data-parallel shard of the global minibatch */
+  void* nccl_comm;      /* ncclComm_t (dconv_nccl_comm_create) or NULL: no exchange (world 1, or the
+                           caller all-reduces dconv_graph_grads itself between backward and apply) */
+  int overlap_update;   /* 1: weight updates on a side stream, concurrent with backward-data */
+  int act_dtype;        /* activation storage (DCONV_BF16; DCONV_F32 for fp32-accurate math) */
+} dconv_graph_config_t;
+typedef struct dconv_graph* dconv_graph_t;
+void dconv_graph_config_default(dconv_graph_config_t* cfg);
+/* the chain checks of run_chain (harness.cpp:331-341): DCONV_ERR_CHAIN_SHAPE_MISMATCH */
+int dconv_graph_create(const dconv_graph_node_t* nodes, int n_nodes, int batch, int in_c, int in_h, int in_w,
+                       int math, const dconv_graph_config_t* cfg, dconv_graph_t* graph);
+void dconv_graph_destroy(dconv_graph_t graph);
+/* this step's images: NCHW fp32 on the device (packed into the input / the stem's layout) */
+int dconv_graph_load_input(dconv_graph_t graph, const float* nchw, dconv_stream_t stream);
+int dconv_graph_forward(dconv_graph_t graph, dconv_stream_t stream);
+/* dtop: gradient of the last tensor (its ReLU applied here); leaves dW in dconv_graph_grads,
+ * all-reduced when a communicator is set */
+int dconv_graph_backward(dconv_graph_t graph, const dconv_act_t* dtop, dconv_stream_t stream);
+/* waits for the exchange, averages over `world`, SGD on the flat master weights */
+int dconv_graph_apply(dconv_graph_t graph, dconv_stream_t stream);
+int dconv_graph_step(dconv_graph_t graph, const dconv_act_t* dtop, dconv_stream_t stream); /* all three */
+/* capture one step into a CUDA graph on `stream` (non-default), then replay it */
+int dconv_graph_capture(dconv_graph_t graph, const dconv_act_t* dtop, dconv_stream_t stream);
+int dconv_graph_replay(dconv_graph_t graph, dconv_stream_t stream);
+int dconv_graph_launches(dconv_graph_t graph); /* kernels of the last step (NCCL's excluded) */
+int dconv_graph_num_tensors(dconv_graph_t graph);
+int dconv_graph_num_convs(dconv_graph_t graph);
+int dconv_graph_buckets(dconv_graph_t graph);
+int dconv_graph_tensor(dconv_graph_t graph, int id, int grad, dconv_act_t* out);
+int dconv_graph_conv(dconv_graph_t graph, int conv, int* node, dconv_wt_t* w, dconv_wt_t* dw);
+/* flat fp32 buffers laid out in backward order: weight gradients / master weights */
+int dconv_graph_grads(dconv_graph_t graph, float** flat, size_t* n);
+int dconv_graph_weights(dconv_graph_t graph, float** flat, size_t* n);
+/* NCCL communicator helpers (libnccl.so.2 loaded at run time): the id (128 bytes) is
+ * made on one rank and broadcast by the caller */
+int dconv_nccl_unique_id(char* id, size_t len);
+int dconv_nccl_comm_create(const char* id, size_t len, int world, int rank, void** comm);
+int dconv_nccl_comm_destroy(void* comm);
+
+/* graph-executor element ops: g *= (act > 0); w *= scale (fp32) */
+int dconv_relu_mask(const dconv_act_t* grad, const dconv_act_t* act, dconv_stream_t stream);
+int dconv_scale_wt(const dconv_wt_t* w, float scale, dconv_stream_t stream);
+/* cap the SMs a persistent conv kernel occupies (0 = all): leaves room for
+ * collectives running concurrently; applies to launches resolved afterwards */
+int dconv_set_sm_budget(int sms);
+
 /* ---------------------------------------------------------------- developer mode */
 /* on != 0: the DCONV_* experiment variables of tools/ (tile / ring / split
  * overrides) take effect and plan caches are bypassed. Off by default: the

@@ -38,6 +38,18 @@ class Epilogue(C.Structure):
     _fields_ = [("add", C.c_void_p), ("mask", C.c_void_p), ("relu", C.c_int), ("flags", C.c_int)]
 
 
+class GraphNode(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("kind", "src", "add", "C", "K", "R", "S", "stride", "pad_h", "pad_w", "relu")]
+
+
+class GraphCfg(C.Structure):
+    _fields_ = [("lr", C.c_float), ("seed", C.c_int), ("bucket_bytes", C.c_int64), ("world", C.c_int),
+                ("rank", C.c_int), ("nccl_comm", C.c_void_p), ("overlap_update", C.c_int), ("act_dtype", C.c_int)]
+
+
+NODE_CONV, NODE_MAXPOOL = 0, 1
+
+
 class EngineCfg(C.Structure):
     _fields_ = [("min_accumulators", C.c_int), ("max_accumulators", C.c_int), ("cache_budget_bytes", C.c_int64),
                 ("prefetch_lookahead", C.c_int), ("prefetch_enabled", C.c_int), ("streaming_stores", C.c_int),
@@ -68,6 +80,12 @@ EXPORTS = [
     "dconv_host_step_chunk", "dconv_host_step_run", "dconv_host_step_launches", "dconv_fwd_plan_validate",
     "dconv_bwd_plan_validate", "dconv_upd_plan_validate", "dconv_set_dev_mode", "dconv_fwd_plan_save",
     "dconv_fwd_plan_load", "dconv_bwd_plan_save", "dconv_bwd_plan_load", "dconv_upd_plan_save", "dconv_upd_plan_load",
+    "dconv_graph_config_default", "dconv_graph_create", "dconv_graph_destroy", "dconv_graph_load_input",
+    "dconv_graph_forward", "dconv_graph_backward", "dconv_graph_apply", "dconv_graph_step", "dconv_graph_capture",
+    "dconv_graph_replay", "dconv_graph_launches", "dconv_graph_num_tensors", "dconv_graph_num_convs",
+    "dconv_graph_buckets", "dconv_graph_tensor", "dconv_graph_conv", "dconv_graph_grads", "dconv_graph_weights",
+    "dconv_nccl_unique_id", "dconv_nccl_comm_create", "dconv_nccl_comm_destroy", "dconv_relu_mask", "dconv_scale_wt",
+    "dconv_set_sm_budget",
 ]
 
 
@@ -141,6 +159,30 @@ def _bind(lib):
         "dconv_bwd_plan_load": (i, [C.c_char_p, sz, i, P(vp)]),
         "dconv_upd_plan_save": (i, [vp, C.c_char_p, sz, P(sz)]),
         "dconv_upd_plan_load": (i, [C.c_char_p, sz, i, P(vp)]),
+        "dconv_graph_config_default": (None, [P(GraphCfg)]),
+        "dconv_graph_create": (i, [P(GraphNode), i, i, i, i, i, i, P(GraphCfg), P(vp)]),
+        "dconv_graph_destroy": (None, [vp]),
+        "dconv_graph_load_input": (i, [vp, vp, vp]),
+        "dconv_graph_forward": (i, [vp, vp]),
+        "dconv_graph_backward": (i, [vp, P(Act), vp]),
+        "dconv_graph_apply": (i, [vp, vp]),
+        "dconv_graph_step": (i, [vp, P(Act), vp]),
+        "dconv_graph_capture": (i, [vp, P(Act), vp]),
+        "dconv_graph_replay": (i, [vp, vp]),
+        "dconv_graph_launches": (i, [vp]),
+        "dconv_graph_num_tensors": (i, [vp]),
+        "dconv_graph_num_convs": (i, [vp]),
+        "dconv_graph_buckets": (i, [vp]),
+        "dconv_graph_tensor": (i, [vp, i, i, P(Act)]),
+        "dconv_graph_conv": (i, [vp, i, P(i), P(Wt), P(Wt)]),
+        "dconv_graph_grads": (i, [vp, P(vp), P(sz)]),
+        "dconv_graph_weights": (i, [vp, P(vp), P(sz)]),
+        "dconv_nccl_unique_id": (i, [C.c_char_p, sz]),
+        "dconv_nccl_comm_create": (i, [C.c_char_p, sz, i, i, P(vp)]),
+        "dconv_nccl_comm_destroy": (i, [vp]),
+        "dconv_relu_mask": (i, [P(Act), P(Act), vp]),
+        "dconv_scale_wt": (i, [P(Wt), C.c_float, vp]),
+        "dconv_set_sm_budget": (i, [i]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -160,3 +202,51 @@ def lib():
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc sm_100a) first")
         _lib = _bind(C.CDLL(LIB_PATH))
     return _lib
+
+
+# ------------------------------------------------------------------ device views (DLPack)
+# Tensors owned by the library (the graph executor's activations, gradients and
+# flat weight buffers) are exposed to torch as aliasing views through a DLPack
+# capsule: no copy; the owner must outlive the view.
+
+
+class _DLDevice(C.Structure):
+    _fields_ = [("device_type", C.c_int32), ("device_id", C.c_int32)]
+
+
+class _DLDataType(C.Structure):
+    _fields_ = [("code", C.c_uint8), ("bits", C.c_uint8), ("lanes", C.c_uint16)]
+
+
+class _DLTensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("device", _DLDevice), ("ndim", C.c_int32), ("dtype", _DLDataType),
+                ("shape", C.POINTER(C.c_int64)), ("strides", C.POINTER(C.c_int64)), ("byte_offset", C.c_uint64)]
+
+
+class _DLManagedTensor(C.Structure):
+    pass
+
+
+_DLManagedTensor._fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", C.c_void_p),
+                             ("deleter", C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor)))]
+
+_KEEP = []  # ctypes storage referenced by live capsules
+
+
+def device_view(ptr: int, numel: int, dtype, device_index: int):
+    """A 1-D torch tensor aliasing `numel` elements of device memory at `ptr`."""
+    import torch
+
+    code, bits = {torch.float32: (2, 32), torch.bfloat16: (4, 16), torch.uint8: (1, 8)}[dtype]
+    shape = (C.c_int64 * 1)(numel)
+    mt = _DLManagedTensor()
+    mt.dl_tensor = _DLTensor(C.c_void_p(ptr), _DLDevice(2, device_index), 1, _DLDataType(code, bits, 1),
+                             C.cast(shape, C.POINTER(C.c_int64)), None, 0)
+    mt.manager_ctx = None
+    mt.deleter = C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor))()
+    _KEEP.append((shape, mt))
+    new = C.pythonapi.PyCapsule_New
+    new.restype = C.py_object
+    new.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+    cap = new(C.addressof(mt), b"dltensor", None)
+    return torch.utils.dlpack.from_dlpack(cap)

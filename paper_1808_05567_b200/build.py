@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "lib", "libdconv_b200.so")
-SOURCES = [os.path.join(CSRC, "dconv_capi.cu")]
+SOURCES = [os.path.join(CSRC, "dconv_capi.cu"), os.path.join(CSRC, "graph.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h"))] + [
     os.path.join(CSRC, "kernels", f) for f in os.listdir(os.path.join(CSRC, "kernels"))] + [
     os.path.join(ROOT, "include", "dconv_b200.h")]
@@ -36,7 +36,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", OUT + ".tmp"] + SOURCES
+    cmd = [nvcc()] + NVCC_FLAGS + ["-o", OUT + ".tmp"] + SOURCES + ["-ldl"]
+    if os.environ.get("DCONV_DEV_BUILD") == "1":  # tools/: kernel role counters and ablation bits
+        cmd.insert(1, "-DDCONV_DEV_BUILD=1")
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

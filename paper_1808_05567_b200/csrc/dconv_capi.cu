@@ -182,6 +182,10 @@ void prof_end(int which, cudaStream_t s) {
   g_slot[which].armed = true;
 }
 
+// SMs a persistent conv kernel may occupy: all of them, or dconv_set_sm_budget()'s
+// cap (leaves SMs free for concurrently running collectives, e.g. NCCL's kernels)
+int g_sm_budget = 0;
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -189,7 +193,7 @@ int sm_count() {
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
   }
-  return n;
+  return g_sm_budget > 0 ? std::min(n, g_sm_budget) : n;
 }
 
 constexpr int kSmemBudget = 227 * 1024 - 2048;  // dynamic smem per CTA (static barriers excluded)
@@ -772,7 +776,7 @@ using GeoKey = std::array<int, 16>;
 
 GeoKey geo_key(const dconv_act_t& a, const dconv_act_t& b, int extra = 0) {
   return {a.n, a.c, a.h, a.w, a.halo_h, a.halo_w, a.dtype, b.n, b.c, b.h, b.w, b.halo_h, b.halo_w, b.dtype,
-          extra, 0};
+          extra, g_sm_budget};
 }
 
 struct FwdEntry {
@@ -841,6 +845,8 @@ struct dconv_upd_plan {
 extern "C" {
 
 const char* dconv_last_error(void) { return g_err.c_str(); }
+// the executor (graph.cu) reports its own failures through dconv_last_error()
+void dconv_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
 
 const char* dconv_status_string(int s) {
   switch (s) {
@@ -2410,11 +2416,27 @@ int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argma
   });
 }
 
+}  // extern "C"
+
+namespace {
+// the 3x3 / stride 2 / pad 1 pool geometry between grad_out (pooled) and grad_in
+void check_pool_pair(const dconv_act_t* grad_out, const dconv_act_t* grad_in) {
+  check_act(grad_out, "maxpool grad_out");
+  check_act(grad_in, "maxpool grad_in");
+  const int P = (grad_in->h + 2 - 3) / 2 + 1, Q = (grad_in->w + 2 - 3) / 2 + 1;
+  if (grad_in->vlen != 16 || grad_out->vlen != 16 || grad_in->halo_h || grad_in->halo_w || grad_out->halo_h ||
+      grad_out->halo_w || grad_out->n != grad_in->n || grad_out->c != grad_in->c || grad_out->h != P ||
+      grad_out->w != Q || grad_out->dtype != grad_in->dtype)
+    fail(DCONV_ERR_SHAPE_MISMATCH, "maxpool backward: halo-0 vlen-16 tensors of one dtype, grad_out = (h+2-3)/2+1");
+}
+}  // namespace
+
+extern "C" {
+
 int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in,
                       const void* mask, dconv_stream_t stream) {
   return guarded([&] {
-    check_act(grad_out, "maxpool grad_out");
-    check_act(grad_in, "maxpool grad_in");
+    check_pool_pair(grad_out, grad_in);
     if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
     const int planes = grad_in->n * cdiv(grad_in->c, 16);
     const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w);
@@ -2510,8 +2532,7 @@ int dconv_s2d_wt(const dconv_wt_t* w, const dconv_wt_t* w2, int inverse, dconv_s
 int dconv_maxpool_bwd_pooled_mask(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in,
                                    const dconv_act_t* pooled, dconv_stream_t stream) {
   return guarded([&] {
-    check_act(grad_out, "maxpool grad_out");
-    check_act(grad_in, "maxpool grad_in");
+    check_pool_pair(grad_out, grad_in);
     check_act(pooled, "maxpool pooled mask");
     if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
     if (pooled->n != grad_out->n || pooled->c != grad_out->c || pooled->h != grad_out->h ||
@@ -2529,6 +2550,41 @@ int dconv_maxpool_bwd_pooled_mask(const dconv_act_t* grad_out, const void* argma
           (const __nv_bfloat16*)grad_out->data, (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data, nullptr,
           planes, grad_in->h, grad_in->w, grad_out->h, grad_out->w, (const __nv_bfloat16*)pooled->data);
     cuda_check(cudaGetLastError(), "maxpool_bwd");
+  });
+}
+
+int dconv_set_sm_budget(int sms) {
+  return guarded([&] {
+    if (sms < 0) fail(DCONV_ERR_INVALID_ARGUMENT, "sm budget must be >= 0 (0 = every SM)");
+    g_sm_budget = sms;
+  });
+}
+
+int dconv_relu_mask(const dconv_act_t* grad, const dconv_act_t* act, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(grad, "relu_mask grad");
+    check_act(act, "relu_mask act");
+    if (act_elems(*grad) != act_elems(*act) || grad->dtype != act->dtype || grad->n != act->n ||
+        grad->c != act->c || grad->h != act->h || grad->w != act->w)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "relu_mask: grad and activation must match");
+    const int64_t n = act_elems(*grad);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (grad->dtype == DCONV_F32)
+      relu_mask_kernel<float><<<grid1d(n), 256, 0, cs>>>((float*)grad->data, (const float*)act->data, n);
+    else
+      relu_mask_kernel<__nv_bfloat16><<<grid1d(n), 256, 0, cs>>>((__nv_bfloat16*)grad->data,
+                                                                 (const __nv_bfloat16*)act->data, n);
+    cuda_check(cudaGetLastError(), "relu_mask");
+  });
+}
+
+int dconv_scale_wt(const dconv_wt_t* w, float scale, dconv_stream_t stream) {
+  return guarded([&] {
+    check_wt(w, "scale weight");
+    if (w->dtype != DCONV_F32) fail(DCONV_ERR_UNSUPPORTED, "scale_wt: fp32 tensors");
+    const int64_t n = wt_elems(*w);
+    scale_kernel<<<grid1d(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>((float*)w->data, scale, n);
+    cuda_check(cudaGetLastError(), "scale_wt");
   });
 }
 

@@ -1090,7 +1090,9 @@ constexpr int kRedGroups = 8;  // max split groups per element (blockDim.y)
 __global__ void __launch_bounds__(256)
     upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C, int K,
                       int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
-  __shared__ float red[8192 + 256];  // [G][TX + 1], G * TX = 256
+  // [G][TX + 1] with G * TX = 256 and G in {1, 2, 8}: at most 8 x 33 = 264 floats, so the
+  // reduce CTAs never crowd out the ~220 KB conv CTAs they run beside
+  __shared__ float red[kRedGroups * 33];
   pdl_wait_primary();  // launched as a programmatic dependent of the UPD kernel
   const int G = blockDim.y, TX = blockDim.x;  // G split groups x TX consecutive elements
   const int kw = kb * 16, cw = cb * 16;

@@ -481,6 +481,10 @@ __global__ void s2d_wt_grad_kernel(const float* __restrict__ g2, float* __restri
 }
 
 // SGD on fp32 master weights: w -= lr * g (blocked layouts, identical shapes)
+__global__ void scale_kernel(float* __restrict__ w, float s, long long n) {
+  DCONV_GRID_STRIDE(i, n) w[i] *= s;
+}
+
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float lr, long long n) {
   DCONV_GRID_STRIDE(e, n) { w[e] -= lr * g[e]; }
 }

@@ -2,19 +2,21 @@
 
 The reference's `run_chain` (harness.cpp:311-358) runs a LINEAR chain of
 forward convs, each layer writing its output straight into the next layer's
-input surface. This executor is its training-time, multi-GPU generalisation:
-a DAG of convs (bottleneck blocks with identity / projection shortcuts and the
-stem max-pool) run forward, backward-data and weight-update on one B200 per
-process, with the fp32 weight gradients summed across ranks by NCCL all-reduce
-(the reference's COPY_REDUCE exchange promoted from threads to GPUs),
-bucketed and overlapped with the backward of earlier layers.
+input surface. Its training-time, multi-GPU generalisation is native code:
+`dconv_graph_*` in the C ABI (csrc/graph.cu) runs a DAG of convs (bottleneck
+blocks with identity / projection shortcuts and the stem max-pool) forward,
+backward-data and weight-update, with ReLU / residual add / ReLU mask /
+branch sums fused into the conv epilogues, weight updates on a side stream,
+the fp32 weight gradients all-reduced by NCCL in buckets (the reference's
+COPY_REDUCE exchange promoted from threads to GPUs) overlapped with the
+backward of earlier layers, SGD, and one CUDA graph per step at any world size.
 
-Everything elementwise is fused into the conv epilogues of the C ABI
-(`dconv_forward_ex` / `dconv_backward_data_ex`): ReLU and the residual add in
-the forward, the ReLU mask and the two-branch gradient sum in the backward.
-Activations are bf16 blocked tensors with halo 0 (padding is a TMA
-out-of-bounds fill), weights fp32 masters in the blocked layout (prepared to
-bf16 per pass), gradients fp32 for the weights.
+This module describes the graph (ResNet-50's 53 convs), and ConvStackExecutor
+is a thin handle over the native executor exposing its tensors as torch views.
+With a gloo process group (CPU tests, several ranks sharing one GPU) the
+gradient exchange runs in Python (torch.distributed) between the native
+backward and apply calls; with an NCCL group the native executor owns its
+own communicator (same ranks) and the exchange is inside the step / graph.
 """
 from __future__ import annotations
 
@@ -26,7 +28,7 @@ import torch
 
 from . import _lib
 from . import api as d
-from ._lib import Act, Epilogue, Wt
+from ._lib import Act, GraphCfg, GraphNode, Wt
 
 # ------------------------------------------------------------------ graph
 
@@ -104,7 +106,9 @@ def step_flops_per_image(nodes: Sequence, img: int = 224, skip_stem_bwd: bool = 
 
 
 class GradBucketer:
-    """Fixed-order bucketed all-reduce of a flat fp32 gradient buffer.
+    """Fixed-order bucketed all-reduce of a flat fp32 gradient buffer (the
+    exchange of ConvStackExecutor over a gloo group; the native executor,
+    csrc/graph.cu, cuts its NCCL buckets by the same rule on its own stream).
 
     Buckets are contiguous slices laid out in BACKWARD order (the first
     bucket is the last layers' gradients, ready first). `ready(i)` is called
@@ -165,252 +169,167 @@ class GradBucketer:
 
 # ------------------------------------------------------------------ executor
 
+_DT = {torch.float32: 0, torch.bfloat16: 1}
+
+
+def _nccl_comm(group, lib):
+    """A native NCCL communicator over the ranks of `group` (id made on rank 0)."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    idbuf = C.create_string_buffer(128)
+    if rank == 0:
+        d._check(lib.dconv_nccl_unique_id(idbuf, 128))
+    obj = [bytes(idbuf.raw)]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    comm = C.c_void_p()
+    d._check(lib.dconv_nccl_comm_create(obj[0], 128, world, rank, C.byref(comm)))
+    return comm
+
 
 class ConvStackExecutor:
+    """Handle over the native executor (dconv_graph_*). `nodes` use tensor names;
+    tensor 'x' is the input image."""
+
     def __init__(self, nodes: Sequence, batch: int, img: int = 224, math: d.Math = d.Math.BF16,
                  device: str = "cuda", group=None, lr: float = 1e-4, seed: int = 1, bucket_bytes: int = 8 << 20,
-                 act_dtype=torch.bfloat16, overlap_upd: bool = True):
-        self.nodes, self.N, self.img, self.math, self.dev = list(nodes), batch, img, d.Math(math), torch.device(device)
+                 act_dtype=torch.bfloat16, overlap_upd: bool = True, use_nccl: Optional[bool] = None):
+        self.nodes, self.N, self.img, self.math = list(nodes), batch, img, d.Math(math)
+        self.dev = torch.device(device)
+        if self.dev.type == "cuda" and self.dev.index is None:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
         self.group, self.lr, self.adt = group, lr, act_dtype
         self.lib = _lib.lib()
         self.shapes = tensor_shapes(self.nodes, img)
         self.convs = [nd for nd in self.nodes if isinstance(nd, ConvNode)]
-        relu_out = {nd.out for nd in self.nodes if isinstance(nd, ConvNode) and nd.relu}
-        relu_out |= {nd.out for nd in self.nodes if isinstance(nd, PoolNode) and nd.src in relu_out}
-        self.relu_out = relu_out
-        # activations and their gradients (halo 0 blocked, bf16)
+        ids = {"x": 0}
+        for i, nd in enumerate(self.nodes):
+            ids[nd.out] = i + 1
+        self.ids = ids
+        arr = (GraphNode * len(self.nodes))()
+        for i, nd in enumerate(self.nodes):
+            if isinstance(nd, PoolNode):
+                arr[i] = GraphNode(_lib.NODE_MAXPOOL, ids[nd.src], -1, 0, 0, 0, 0, 0, 0, 0, 0)
+            else:
+                arr[i] = GraphNode(_lib.NODE_CONV, ids[nd.src], ids[nd.add] if nd.add else -1, nd.C, nd.K, nd.R,
+                                   nd.S, nd.stride, nd.pad, nd.pad, int(nd.relu))
+        cfg = GraphCfg()
+        self.lib.dconv_graph_config_default(C.byref(cfg))
+        cfg.lr, cfg.seed, cfg.bucket_bytes = lr, seed, bucket_bytes
+        cfg.overlap_update, cfg.act_dtype = int(overlap_upd), _DT[act_dtype]
+        self._comm = None
+        self._py_exchange = False
+        if group is not None:
+            import torch.distributed as dist
+
+            cfg.world, cfg.rank = dist.get_world_size(group), dist.get_rank(group)
+            if use_nccl is None:
+                use_nccl = dist.get_backend(group) == "nccl"
+            if use_nccl:
+                self._comm = _nccl_comm(group, self.lib)
+                cfg.nccl_comm = self._comm
+            else:
+                self._py_exchange = cfg.world > 1
+        self._bucket_bytes = bucket_bytes
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.dev):
+            d._check(self.lib.dconv_graph_create(arr, len(self.nodes), batch, 3, img, img, int(self.math),
+                                                 C.byref(cfg), C.byref(self._h)))
+        self._views()
+
+    def _views(self):
+        lib, di = self.lib, self.dev.index
         self.act: Dict[str, d.BlockedActivation] = {}
         self.grad: Dict[str, d.BlockedActivation] = {}
-        for name, (c, h, w) in self.shapes.items():
-            self.act[name] = d.BlockedActivation(batch, c, h, w, 16, 0, 0, act_dtype, self.dev)
-            if name != "x":
-                self.grad[name] = d.BlockedActivation(batch, c, h, w, 16, 0, 0, act_dtype, self.dev)
-        # a projection's output only feeds a residual add: its dL/dz is the block's dz
-        for nd in self.convs:
-            if nd.add is not None and nd.add in {c.out for c in self.convs if not c.relu}:
-                self.grad[nd.add] = self.grad[nd.out]
-        pools = [nd for nd in self.nodes if isinstance(nd, PoolNode)]
-        self.argmax = {nd.name: torch.empty(self.act[nd.out].data.numel(), dtype=torch.uint8, device=self.dev)
-                       for nd in pools}
-        # weights: fp32 masters (He-normal, seeded host generator), flat fp32 gradient buffer in backward order
+        for name, i in self.ids.items():
+            for grad, dst in ((0, self.act), (1, self.grad)):
+                if grad and i == 0:
+                    continue
+                a = Act()
+                d._check(lib.dconv_graph_tensor(self._h, i, grad, C.byref(a)))
+                numel = a.n * -(-a.c // 16) * a.h * a.w * 16
+                dst[name] = d.BlockedActivation(a.n, a.c, a.h, a.w, 16, 0, 0, self.adt, self.dev,
+                                                data=_lib.device_view(a.data, numel, self.adt, di))
         self.w: Dict[str, d.BlockedWeight] = {}
-        self.specs: Dict[str, d.ConvLayerSpec] = {}
-        sizes = []
-        for nd in self.convs:
-            c, h, w = self.shapes[nd.src]
-            spec = d.ConvLayerSpec(batch, nd.C, nd.K, h, w, nd.R, nd.S, nd.stride, nd.pad, nd.pad, 16)
-            spec.validate()
-            self.specs[nd.name] = spec
-            host = torch.empty(nd.K, nd.C, nd.R, nd.S, dtype=torch.float32)
-            std = float((2.0 / (nd.C * nd.R * nd.S)) ** 0.5)
-            self.lib.dconv_fill_he_normal_host(seed * 1000 + len(sizes), std, host.data_ptr(), host.numel())
-            self.w[nd.name] = d.to_blocked_weight(host.to(self.dev), spec)
-            sizes.append(self.w[nd.name].data.numel())
-        order = list(reversed(range(len(self.convs))))  # gradients become final in reverse order
-        self.flat = torch.zeros(sum(sizes), dtype=torch.float32, device=self.dev)
-        self.slices: List[slice] = [slice(0, 0)] * len(self.convs)
-        off = 0
-        for i in order:
-            self.slices[i] = slice(off, off + sizes[i])
-            off += sizes[i]
-        self.dw = {nd.name: d.BlockedWeight(nd.K, nd.C, nd.R, nd.S, 16, torch.float32, self.dev,
-                                            data=self.flat[self.slices[i]])
-                   for i, nd in enumerate(self.convs)}
-        # master weights in one flat buffer laid out like the gradients: SGD is ONE launch
-        self.wflat = torch.empty_like(self.flat)
-        for i, nd in enumerate(self.convs):
-            self.wflat[self.slices[i]].copy_(self.w[nd.name].data.reshape(-1))
-            self.w[nd.name] = d.BlockedWeight(nd.K, nd.C, nd.R, nd.S, 16, torch.float32, self.dev,
-                                              data=self.wflat[self.slices[i]])
-        n256 = self.flat.numel() // 256  # every blocked weight is a whole number of 16x16 lane blocks
-        self._wflat_view = d.BlockedWeight(16, 16, 1, n256, 16, torch.float32, self.dev, data=self.wflat)
-        self._gflat_view = d.BlockedWeight(16, 16, 1, n256, 16, torch.float32, self.dev, data=self.flat)
-        self.bucketer = GradBucketer(self.flat, [self.slices[i] for i in order], bucket_bytes, group)
-        self._bucket_index = {i: k for k, i in enumerate(order)}
-        # narrow stride-2 input convs (the 7x7/s2 stem, C=3) run as a stride-1 conv over a
-        # space-to-depth copy of their input: 4x4 taps over 12 of 16 lanes instead of
-        # 49 taps over 3 of 16 (the MMA K dimension is a 16-lane channel block)
-        self.s2d: Dict[str, dict] = {}
-        for nd in self.convs:
-            c, h, w = self.shapes[nd.src]
-            if nd.stride == 2 and nd.C * 4 <= 16 and nd.R > 1 and nd.S > 1:
-                _, P, Q = self.shapes[nd.out]
-                r2, s2 = (nd.R + 1) // 2, (nd.S + 1) // 2
-                hs, wsz = P + r2 - 1, Q + s2 - 1
-                spec2 = d.ConvLayerSpec(batch, 4 * nd.C, nd.K, hs, wsz, r2, s2, 1, 0, 0, 16)
-                spec2.validate()
-                self.s2d[nd.name] = {
-                    "spec": spec2,
-                    "x": d.BlockedActivation(batch, 4 * nd.C, hs, wsz, 16, 0, 0, act_dtype, self.dev),
-                    "w": d.BlockedWeight(nd.K, 4 * nd.C, r2, s2, 16, torch.float32, self.dev),
-                    "dw": d.BlockedWeight(nd.K, 4 * nd.C, r2, s2, 16, torch.float32, self.dev),
-                }
-        # plans
-        self.input_s2d = False  # set by load_input_nchw: the stem's s2d input is packed directly
-        self.pspec = {n: (self.s2d[n]["spec"] if n in self.s2d else s) for n, s in self.specs.items()}
-        self.fplan = {n: d.ExecutionPlan(s, None, None, self.math, 0, 0) for n, s in self.pspec.items()}
-        self.bplan = {n: d.BackwardContext(s, None, 1, None, self.math) for n, s in self.specs.items()
-                      if self._needs_bwd(n)}
-        self.uplan = {n: d.UpdatePlan(s, None, self.math) for n, s in self.pspec.items()}
-        self.comm_stream = torch.cuda.Stream(self.dev) if group is not None else None
-        self._ev = {i: torch.cuda.Event() for i in range(len(self.convs))}
-        # weight updates (+ their split reductions) run on a side stream, concurrent with the
-        # backward-data chain: each kernel's last-wave tail is filled by the other's CTAs and
-        # the small reduction kernels leave the critical path. A layer's update is forked
-        # once its output gradient is final; SGD joins.
-        self.upd_stream = torch.cuda.Stream(self.dev) if (self.dev.type == "cuda" and overlap_upd) else None
-        self._ev_gready = {i: torch.cuda.Event() for i in range(len(self.convs))}
+        self.dw: Dict[str, d.BlockedWeight] = {}
+        for ci, nd in enumerate(self.convs):
+            w, g, node = Wt(), Wt(), C.c_int()
+            d._check(lib.dconv_graph_conv(self._h, ci, C.byref(node), C.byref(w), C.byref(g)))
+            for src, dst in ((w, self.w), (g, self.dw)):
+                numel = -(-src.k // 16) * -(-src.c // 16) * src.r * src.s * 256
+                dst[nd.name] = d.BlockedWeight(src.k, src.c, src.r, src.s, 16, torch.float32, self.dev,
+                                               data=_lib.device_view(src.data, numel, torch.float32, di))
+        for attr, fn in (("flat", lib.dconv_graph_grads), ("wflat", lib.dconv_graph_weights)):
+            p, n = C.c_void_p(), C.c_size_t()
+            d._check(fn(self._h, C.byref(p), C.byref(n)))
+            setattr(self, attr, _lib.device_view(p.value, n.value, torch.float32, di))
+        # the gloo path exchanges the same flat buffer in fixed backward-order buckets
+        order = sorted(self.convs, key=lambda nd: self.dw[nd.name].data.data_ptr())
+        base = self.flat.data_ptr()
+        slices = []
+        for nd in order:
+            off = (self.dw[nd.name].data.data_ptr() - base) // 4
+            slices.append(slice(off, off + self.dw[nd.name].data.numel()))
+        self.bucketer = GradBucketer(self.flat, slices, self._bucket_bytes, self.group if self._py_exchange else None)
+        self.specs = {nd.name: d.ConvLayerSpec(self.N, nd.C, nd.K, *self.shapes[nd.src][1:], nd.R, nd.S, nd.stride,
+                                               nd.pad, nd.pad, 16) for nd in self.convs}
 
-    def _needs_bwd(self, name):
-        nd = next(n for n in self.convs if n.name == name)
-        return nd.src != "x"  # the stem's backward-data (image gradient) is skipped
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        try:
+            if h is not None and h.value:
+                self.lib.dconv_graph_destroy(h)
+                self._h = None
+            if getattr(self, "_comm", None) is not None:
+                self.lib.dconv_nccl_comm_destroy(self._comm)
+                self._comm = None
+        except Exception:  # interpreter shutdown
+            pass
 
     # -------------------------------------------------------------- passes
     def _stream(self):
-        return torch.cuda.current_stream().cuda_stream
-
-    def _ep(self, add=None, mask=None, relu=False):
-        return Epilogue(add.data.data_ptr() if add is not None else None,
-                        mask.data.data_ptr() if mask is not None else None, 1 if relu else 0)
-
-    def forward(self):
-        for nd in self.nodes:
-            if isinstance(nd, PoolNode):
-                _check(self.lib.dconv_maxpool_fwd(C.byref(self.act[nd.src].to_c()), C.byref(self.act[nd.out].to_c()),
-                                                  self.argmax[nd.name].data_ptr(), self._stream()))
-                continue
-            self.conv_forward(nd)
-
-    def conv_forward(self, nd: ConvNode):
-        plan = self.fplan[nd.name]
-        ep = self._ep(add=self.act[nd.add] if nd.add else None, relu=nd.relu)
-        ws = plan._ws.get(self.lib.dconv_fwd_workspace_bytes(plan._h), self.dev)
-        src, wt = self.act[nd.src], self.w[nd.name]
-        if nd.name in self.s2d:
-            sd = self.s2d[nd.name]
-            if not (nd.src == "x" and self.input_s2d):  # load_input_nchw packed it already
-                _check(self.lib.dconv_s2d_act(C.byref(src.to_c()), C.byref(sd["x"].to_c()), nd.pad, self._stream()))
-            _check(self.lib.dconv_s2d_wt(C.byref(wt.to_c()), C.byref(sd["w"].to_c()), 0, self._stream()))
-            src, wt = sd["x"], sd["w"]
-        _check(self.lib.dconv_forward_ex(plan._h, C.byref(src.to_c()), C.byref(wt.to_c()),
-                                         C.byref(self.act[nd.out].to_c()), C.byref(ep), ws, self._stream()))
+        return torch.cuda.current_stream(self.dev).cuda_stream
 
     def load_input_nchw(self, nchw: torch.Tensor):
-        """Pack this step's images (N, 3, H, W fp32 on the device) into the executor's
-        input: straight into the stem's space-to-depth layout when the stem runs that
-        way (one pass, no full-resolution 16-lane copy), else the blocked tensor 'x'.
-        Steps after this skip the stem's own space-to-depth."""
-        stem = next((nd for nd in self.convs if nd.src == "x"), None)
-        if stem is not None and stem.name in self.s2d:
-            n, c, h, w = nchw.shape
-            _check(self.lib.dconv_pack_s2d(nchw.data_ptr(), n, c, h, w, C.byref(self.s2d[stem.name]["x"].to_c()),
-                                           stem.pad, self._stream()))
-            self.input_s2d = True
-        else:
-            _check(self.lib.dconv_pack_act(nchw.data_ptr(), 0, C.byref(self.act["x"].to_c()), self._stream()))
+        """This step's images (N, 3, H, W fp32 on the device), packed straight into
+        the stem's space-to-depth layout (one pass)."""
+        d._check(self.lib.dconv_graph_load_input(self._h, nchw.data_ptr(), self._stream()))
 
-    def conv_update(self, nd: ConvNode):
-        up = self.uplan[nd.name]
-        src, dw = self.act[nd.src], self.dw[nd.name]
-        if nd.name in self.s2d:  # s2d copy of the input was made by the forward of this step
-            src, dw = self.s2d[nd.name]["x"], self.s2d[nd.name]["dw"]
-        a, g = src.to_c(), self.grad[nd.out].to_c()
-        ws = up._ws.get(self.lib.dconv_upd_workspace_bytes(up._h, C.byref(a), C.byref(g)), self.dev)
-        _check(self.lib.dconv_weight_update(up._h, C.byref(a), C.byref(g), C.byref(dw.to_c()), 0, ws,
-                                            self._stream()))
-        if nd.name in self.s2d:
-            _check(self.lib.dconv_s2d_wt(C.byref(self.dw[nd.name].to_c()), C.byref(dw.to_c()), 1, self._stream()))
+    def forward(self):
+        d._check(self.lib.dconv_graph_forward(self._h, self._stream()))
 
     def backward(self, dtop: d.BlockedActivation):
-        """Gradient buffers hold dL/dz (already through the ReLU of their tensor)."""
-        top = self.nodes[-1].out
-        mask = self.act[top] if top in self.relu_out else None
-        self.grad[top].data.copy_(dtop.data)
-        if mask is not None:
-            self.grad[top].data.mul_((mask.data > 0).to(self.grad[top].data.dtype))
-        self.bucketer.begin()
-        written = set()
-        for idx in reversed(range(len(self.nodes))):
-            nd = self.nodes[idx]
-            if isinstance(nd, PoolNode):
-                if nd.src in self.relu_out:  # ReLU mask of the pooled input, read off the pooled output
-                    _check(self.lib.dconv_maxpool_bwd_pooled_mask(
-                        C.byref(self.grad[nd.out].to_c()), self.argmax[nd.name].data_ptr(),
-                        C.byref(self.grad[nd.src].to_c()), C.byref(self.act[nd.out].to_c()), self._stream()))
-                else:
-                    _check(self.lib.dconv_maxpool_bwd(C.byref(self.grad[nd.out].to_c()),
-                                                      self.argmax[nd.name].data_ptr(),
-                                                      C.byref(self.grad[nd.src].to_c()), None, self._stream()))
-                written.add(nd.src)
-                continue
-            ci = self.convs.index(nd)
-            g_out = self.grad[nd.out]  # = dL/dz of this conv (its epilogue's pre-activation), final here
-            if self.upd_stream is not None:
-                self._ev_gready[ci].record()
-                self.upd_stream.wait_event(self._ev_gready[ci])
-                with torch.cuda.stream(self.upd_stream):
-                    self.conv_update(nd)  # weight gradient
-                    if self.group is not None:
-                        self._ev[ci].record()
-                        self.comm_stream.wait_event(self._ev[ci])
-            else:
-                self.conv_update(nd)
-                if self.group is not None:
-                    self._ev[ci].record()
-                    self.comm_stream.wait_event(self._ev[ci])
-            self.bucketer.ready(self._bucket_index[ci], self.comm_stream)
-            # residual branch: a projection shares this dz (aliased buffer); an identity
-            # shortcut's contribution is folded into the input-gradient epilogue below
-            if nd.src == "x":
-                continue
-            # data gradient of the conv input, through the ReLU of that tensor, summing branches
-            gi = self.grad[nd.src]
-            mask = self.act[nd.src] if nd.src in self.relu_out else None
-            add = None
-            if nd.src in written:
-                add = gi  # second contribution: accumulate in place
-            else:
-                ident = [c for c in self.convs if c.add == nd.src]  # identity shortcut consumer of src
-                if ident:
-                    add = self.grad[ident[0].out]
-            bp = self.bplan[nd.name]
-            ws = bp._ws.get(self.lib.dconv_bwd_workspace_bytes(bp._h), self.dev)
-            ep = self._ep(add=add, mask=mask)
-            _check(self.lib.dconv_backward_data_ex(bp._h, C.byref(self.w[nd.name].to_c()), C.byref(g_out.to_c()),
-                                                   C.byref(gi.to_c()), C.byref(ep), ws, self._stream()))
-            written.add(nd.src)
-        if self.upd_stream is not None:
-            torch.cuda.current_stream().wait_stream(self.upd_stream)  # join: every dW final
+        """Leaves the (all-reduced) weight gradients in `flat` / `dw`."""
+        d._check(self.lib.dconv_graph_backward(self._h, C.byref(dtop.to_c()), self._stream()))
+        if self._py_exchange:  # host-side (gloo) exchange, bucket by bucket in backward order
+            self.bucketer.begin()
+            for k in range(len(self.bucketer.slices)):
+                self.bucketer.ready(k)
+            self.bucketer.finish()
 
     def sgd(self):
-        self.bucketer.finish()
-        if self.group is not None:
-            import torch.distributed as dist
-
-            self.flat.div_(dist.get_world_size(self.group))
-        _check(self.lib.dconv_sgd(C.byref(self._wflat_view.to_c()), C.byref(self._gflat_view.to_c()), self.lr,
-                                  self._stream()))
+        d._check(self.lib.dconv_graph_apply(self._h, self._stream()))
 
     def step(self, dtop: d.BlockedActivation):
-        self.forward()
-        self.backward(dtop)
-        self.sgd()
+        if self._py_exchange:
+            self.forward()
+            self.backward(dtop)
+            self.sgd()
+        else:
+            d._check(self.lib.dconv_graph_step(self._h, C.byref(dtop.to_c()), self._stream()))
+
+    def capture(self, dtop: d.BlockedActivation):
+        """Capture one step (exchange included) into a CUDA graph on the current stream."""
+        if self._py_exchange:
+            raise d.Unsupported("capture: the gloo exchange runs on the host")
+        d._check(self.lib.dconv_graph_capture(self._h, C.byref(dtop.to_c()), self._stream()))
+
+    def replay(self):
+        d._check(self.lib.dconv_graph_replay(self._h, self._stream()))
 
     def launches_per_step(self) -> int:
-        n = 0
-        for nd in self.nodes:
-            if isinstance(nd, PoolNode):
-                n += 2
-                continue
-            n += self.fplan[nd.name].launches()
-            src = self.s2d[nd.name]["x"] if nd.name in self.s2d else self.act[nd.src]
-            n += self.uplan[nd.name].launches(src, self.grad[nd.out])
-            if nd.name in self.s2d:
-                n += 3  # input / filter space-to-depth, gradient back
-            if nd.name in self.bplan:
-                n += self.bplan[nd.name].launches()
-        return n + 1  # one SGD launch over the flat weights
+        """kernels launched by the last step (ours; NCCL's excluded)."""
+        return self.lib.dconv_graph_launches(self._h)
 
-
-def _check(st):
-    d._check(st)
+    def buckets(self) -> int:
+        return self.lib.dconv_graph_buckets(self._h)
