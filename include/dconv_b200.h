@@ -334,6 +334,11 @@ int dconv_graph_step(dconv_graph_t graph, const dconv_act_t* dtop, dconv_stream_
 int dconv_graph_capture(dconv_graph_t graph, const dconv_act_t* dtop, dconv_stream_t stream);
 int dconv_graph_replay(dconv_graph_t graph, dconv_stream_t stream);
 int dconv_graph_launches(dconv_graph_t graph); /* kernels of the last step (NCCL's excluded) */
+/* per-layer device time (LayerReport analog, harness.hpp:36-60): runs one step, then
+ * times each conv's forward, backward-data and weight update alone on `stream`
+ * (best of 2 x `reps` back-to-back calls); ms[3*conv + {0,1,2}]. Overwrites the
+ * step's tensors. */
+int dconv_graph_profile(dconv_graph_t graph, const dconv_act_t* dtop, int reps, float* ms, dconv_stream_t stream);
 int dconv_graph_num_tensors(dconv_graph_t graph);
 int dconv_graph_num_convs(dconv_graph_t graph);
 int dconv_graph_buckets(dconv_graph_t graph);

@@ -212,18 +212,51 @@ def apply_op_canonical(out, kind, bias=None):
 
 
 # ------------------------------------------------------------- the reference itself
-_ref = None
+# Two builds of the unmodified reference core (oracle/Makefile):
+#   _ref/libdconv_ref.so        -O3 -march=x86-64-v3 -ffp-contract=off: bitwise pins;
+#   _ref/libdconv_ref_native.so the reference's own Release flags (-O3 -march=native,
+#                               default FP contraction): the timed CPU baseline.
+_ref = {}
+_NATIVE_FLAGS = ("avx512f", "avx512bw", "avx512vl", "avx512dq", "avx512_fp16", "amx_tile")
 
 
-def ref_available() -> bool:
-    return os.path.exists(os.path.join(_HERE, "_ref", "libdconv_ref.so"))
+def _host_flags():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
 
 
-def ref():
-    """The reference core (oracle/_ref/libdconv_ref.so), or None."""
-    global _ref
-    if _ref is None:
-        path = os.path.join(_HERE, "_ref", "libdconv_ref.so")
+def ref_available(native: bool = False) -> bool:
+    return os.path.exists(_ref_path(native))
+
+
+def _ref_path(native: bool) -> str:
+    return os.path.join(_HERE, "_ref", "libdconv_ref_native.so" if native else "libdconv_ref.so")
+
+
+def native_usable() -> bool:
+    """the -march=native (sapphirerapids) build runs on this host"""
+    return ref_available(True) and all(f in _host_flags() for f in _NATIVE_FLAGS)
+
+
+def ref_build_info(native: bool) -> str:
+    p = os.path.join(_HERE, "_ref", "COMPILER_NATIVE" if native else "COMPILER")
+    try:
+        with open(p) as f:
+            return " ".join(f.read().split())
+    except OSError:
+        return "unknown"
+
+
+def ref(native: bool = False):
+    """The reference core (oracle/_ref/libdconv_ref[_native].so), or None."""
+    if native not in _ref:
+        path = _ref_path(native)
         if not os.path.exists(path):
             return None
         r = C.CDLL(path)
@@ -239,17 +272,17 @@ def ref():
         r.ref_transform_weight_stride1.argtypes = [_F32P] + [C.c_int] * 5 + [_F32P]
         r.ref_direct_pass.argtypes = [ip, C.c_int, C.c_int, C.c_int, _F32P, _F32P, _F32P,
                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
-        _ref = r
-    return _ref
+        _ref[native] = r
+    return _ref[native]
 
 
 def spec_array(s: Spec):
     return (C.c_int * 11)(s.N, s.C, s.K, s.H, s.W, s.R, s.S, s.stride, s.pad_h, s.pad_w, s.vlen)
 
 
-def ref_direct_pass(s: Spec, pass_: int, threads: int, iters: int, a, b):
+def ref_direct_pass(s: Spec, pass_: int, threads: int, iters: int, a, b, native: bool = False):
     """Time the reference direct engine (pass 0 F / 1 B / 2 U). Returns (out, best_ms, avg_ms)."""
-    r = ref()
+    r = ref(native)
     P, Q = output_shape(s)
     shape = [(s.N, s.K, P, Q), (s.N, s.C, s.H, s.W), (s.K, s.C, s.R, s.S)][pass_]
     out = np.empty(shape, np.float32)

@@ -85,7 +85,7 @@ EXPORTS = [
     "dconv_graph_replay", "dconv_graph_launches", "dconv_graph_num_tensors", "dconv_graph_num_convs",
     "dconv_graph_buckets", "dconv_graph_tensor", "dconv_graph_conv", "dconv_graph_grads", "dconv_graph_weights",
     "dconv_nccl_unique_id", "dconv_nccl_comm_create", "dconv_nccl_comm_destroy", "dconv_relu_mask", "dconv_scale_wt",
-    "dconv_set_sm_budget",
+    "dconv_set_sm_budget", "dconv_graph_profile",
 ]
 
 
@@ -170,6 +170,7 @@ def _bind(lib):
         "dconv_graph_capture": (i, [vp, P(Act), vp]),
         "dconv_graph_replay": (i, [vp, vp]),
         "dconv_graph_launches": (i, [vp]),
+        "dconv_graph_profile": (i, [vp, P(Act), i, P(C.c_float), vp]),
         "dconv_graph_num_tensors": (i, [vp]),
         "dconv_graph_num_convs": (i, [vp]),
         "dconv_graph_buckets": (i, [vp]),

@@ -159,6 +159,7 @@ struct dconv_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;  // kernels of the last step (ours, NCCL excluded)
+  bool profiling = false;  // dconv_graph_profile: one rank alone, no collectives
   std::vector<void*> allocs;
 };
 
@@ -438,7 +439,7 @@ void backward(dconv_graph* g, const dconv_act_t* dtop, cudaStream_t s) {
   }
   std::vector<int> left(g->buckets.size());
   for (size_t b = 0; b < g->buckets.size(); ++b) left[b] = g->buckets[b].n_convs;
-  const bool comm = g->cfg.nccl_comm != nullptr;
+  const bool comm = g->cfg.nccl_comm != nullptr && !g->profiling;
   std::vector<char> written(g->t.size(), 0);
   for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
     const dconv_graph_node_t& nd = g->nodes[i];
@@ -665,6 +666,68 @@ int dconv_graph_replay(dconv_graph_t g, dconv_stream_t stream) {
   return gguard([&] {
     if (!g || !g->exec) gfail(DCONV_ERR_INVALID_ARGUMENT, "graph_replay: no captured step");
     cuck(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)), "graph launch");
+  });
+}
+
+int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, float* ms, dconv_stream_t stream) {
+  return gguard([&] {
+    if (!g || !dtop || !ms || reps < 1) gfail(DCONV_ERR_INVALID_ARGUMENT, "graph_profile: bad arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    dconv_stream_t st = stream;
+    // one whole step first: every tensor holds this step's values (and every plan is resolved)
+    g->profiling = true;
+    struct Reset {
+      dconv_graph* g;
+      ~Reset() { g->profiling = false; }
+    } reset{g};
+    forward(g, s);
+    backward(g, dtop, s);
+    cuck(cudaStreamSynchronize(s), "profile sync");
+    cudaEvent_t e0, e1;
+    cuck(cudaEventCreate(&e0), "event");
+    cuck(cudaEventCreate(&e1), "event");
+    auto timed = [&](auto&& fn) -> float {
+      fn();  // warm
+      float best = 1e30f;
+      for (int trial = 0; trial < 2; ++trial) {
+        cuck(cudaEventRecord(e0, s), "event");
+        for (int r = 0; r < reps; ++r) fn();
+        cuck(cudaEventRecord(e1, s), "event");
+        cuck(cudaEventSynchronize(e1), "event sync");
+        float t = 0;
+        cuck(cudaEventElapsedTime(&t, e0, e1), "elapsed");
+        best = std::min(best, t / reps);
+      }
+      return best;
+    };
+    for (size_t ci = 0; ci < g->convs.size(); ++ci) {
+      Conv& cv = g->convs[ci];
+      const dconv_graph_node_t& nd = g->nodes[cv.node];
+      const dconv_act_t src = act_of(g, nd.src, false), out = act_of(g, cv.node + 1, false);
+      dconv_act_t x = src;
+      dconv_wt_t w = conv_w(g, cv, false);
+      if (cv.s2d) {
+        x.data = cv.s2d_x;
+        x.c = cv.pspec.C;
+        x.h = cv.pspec.H;
+        x.w = cv.pspec.W;
+        w = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
+      }
+      const dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
+      ms[3 * ci + 0] = timed([&] { ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, g->ws_main, st), "profile fwd"); });
+      ms[3 * ci + 1] = 0.0f;
+      if (cv.bp) {
+        const dconv_act_t go = act_of(g, cv.node + 1, true), gi = act_of(g, nd.src, true);
+        const void* mask = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
+        const dconv_epilogue_t eb = epi(nullptr, mask, 0);  // (the branch sum's extra read is not timed)
+        const dconv_wt_t wf = conv_w(g, cv, false);
+        ms[3 * ci + 1] =
+            timed([&] { ck(dconv_backward_data_ex(cv.bp, &wf, &go, &gi, &eb, g->ws_main, st), "profile bwd"); });
+      }
+      ms[3 * ci + 2] = timed([&] { update(g, cv, s); });
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 

@@ -327,6 +327,12 @@ class ConvStackExecutor:
     def replay(self):
         d._check(self.lib.dconv_graph_replay(self._h, self._stream()))
 
+    def profile(self, dtop: d.BlockedActivation, reps: int = 3) -> Dict[str, Dict[str, float]]:
+        """per-conv device ms of each pass timed alone (dconv_graph_profile); clobbers tensors"""
+        ms = (C.c_float * (3 * len(self.convs)))()
+        d._check(self.lib.dconv_graph_profile(self._h, C.byref(dtop.to_c()), reps, ms, self._stream()))
+        return {nd.name: {"F": ms[3 * i], "B": ms[3 * i + 1], "U": ms[3 * i + 2]} for i, nd in enumerate(self.convs)}
+
     def launches_per_step(self) -> int:
         """kernels launched by the last step (ours; NCCL's excluded)."""
         return self.lib.dconv_graph_launches(self._h)
