@@ -126,3 +126,21 @@ def test_header_compiles_as_c():
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
                         tmp], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/core/include"), reason="needs the reference headers")
+def test_cpp_shim_compiles_against_reference_headers():
+    """include/dconv_b200.hpp (the header-compatible C++ shim, reference signatures
+    over the C ABI) compiles and links against the reference's own headers and core
+    (oracle/Makefile `shim`; tests/shim/shim_check.cpp runs it on the GPU)."""
+    oracle = os.path.join(ROOT, "oracle")
+    binary = os.path.join(oracle, "_ref", "shim_check")
+    if os.path.exists(binary):
+        os.remove(binary)
+    r = subprocess.run(["make", "-s", "shim"], cwd=oracle, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "warning" not in (r.stdout + r.stderr).lower(), r.stderr
+    nm = subprocess.run(["nm", "-C", "-u", binary], capture_output=True, text=True).stdout
+    for sym in ("dconv_forward", "dconv_backward_data", "dconv_weight_update", "dconv::make_forward_plan",
+                "dconv::weight_update"):
+        assert sym in nm, sym  # both engines are called: the C ABI and the reference's own

@@ -238,3 +238,18 @@ def test_execute_host_cost_after_first_call(dconv, orc):
     torch.cuda.synchronize()
     print(f"forward execute host cost: first call {first * 1e6:.1f} us, then {per * 1e6:.1f} us/call (2 launches)")
     assert per < 40e-6, per
+
+
+def test_cpp_shim_runs_both_engines(dconv):
+    """include/dconv_b200.hpp: the reference's own calls (forward / backward / weight_update,
+    same signatures, reference host tensors) on the B200 vs the reference engine and its
+    naive oracle (tests/shim/shim_check.cpp, built against the reference by `make shim`)."""
+    import os
+    import subprocess
+
+    binary = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "shim_check")
+    if not os.path.exists(binary):
+        pytest.skip("shim_check not built (needs /root/reference at build time)")
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0 and "SHIM CHECK OK" in r.stdout, r.stdout + r.stderr
