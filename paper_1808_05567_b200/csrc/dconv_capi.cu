@@ -233,7 +233,7 @@ Taps phase_taps(int R, int S, int st) {
       for (int r = a; r < R; r += st)
         for (int s = b; s < S; s += st) list.emplace_back(r, s);
       if (list.empty()) continue;
-      if (t.n_phases >= kMaxPhases) fail(DCONV_ERR_UNSUPPORTED, "more than 4 stride phases (stride > 2)");
+      if (t.n_phases >= kMaxPhases) fail(DCONV_ERR_UNSUPPORTED, "more than 16 stride phases (stride > 4)");
       const int ph = t.n_phases++;
       t.phase_row[ph] = a;
       t.phase_col[ph] = b;
@@ -249,7 +249,7 @@ Taps phase_taps(int R, int S, int st) {
         t.s2max = std::max(t.s2max, rs.second / st);
       }
     }
-  if (static_cast<int>(t.r.size()) > kMaxTaps) fail(DCONV_ERR_UNSUPPORTED, "more than 64 filter taps");
+  if (static_cast<int>(t.r.size()) > kMaxTaps) fail(DCONV_ERR_UNSUPPORTED, "more than 128 filter taps");
   return t;
 }
 
@@ -311,7 +311,10 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.split_acc = (pieces == 3 && red_len > 1024) ? 1 : 0;
   const int n_acc = (pieces == 3 && p.split_acc) ? 2 : 1;
   // linear mode: the halo'd physical plane is the virtual grid
-  const bool linear = st == 1 && -pb.row_off == in.halo_h && -pb.col_off == in.halo_w;
+  // (and every shifted tap stays inside the halo'd plane: a stride phase of the
+  // backward route can have more output rows / columns than its input supplies)
+  const bool linear = st == 1 && -pb.row_off == in.halo_h && -pb.col_off == in.halo_w &&
+                      pb.P + taps.r2max <= in.h + 2 * in.halo_h && pb.Q + taps.s2max <= in.w + 2 * in.halo_w;
   p.linear = linear ? 1 : 0;
   // multi-image tiles: 1x1 stride-1 on halo-free planes of <= 128 pixels
   const int hw = in.h * in.w;
@@ -767,6 +770,66 @@ void copy_out(const std::string& s, char* buf, size_t len) {
 
 }  // namespace
 
+namespace {
+// ------------------------------------------------------------------ vlen != 16
+// The tensor-core passes run on 16-lane channel blocks. A plan for another vlen
+// (the reference runs vlen 4, 5, 8 ..., test_propagation.cpp:64-76) keeps a
+// vlen-16 twin; each execute re-blocks its operands into workspace copies
+// (device kernels, bitwise data moves), runs the twin and re-blocks the result
+// back into the caller's vlen-v tensor (halo and tail lanes zeroed).
+dconv_spec_t spec16(const dconv_spec_t& s) {
+  dconv_spec_t t = s;
+  t.vlen = 16;
+  return t;
+}
+dconv_act_t act_as16(const dconv_act_t& a, void* data, int hh, int hw) {
+  dconv_act_t t = a;
+  t.data = data;
+  t.vlen = 16;
+  t.halo_h = hh;
+  t.halo_w = hw;
+  return t;
+}
+dconv_wt_t wt_as16(const dconv_wt_t& w, void* data, int dtype) {
+  dconv_wt_t t = w;
+  t.data = data;
+  t.vlen = 16;
+  t.dtype = dtype;
+  return t;
+}
+size_t act_bytes(const dconv_act_t& a) { return align256(static_cast<size_t>(act_elems(a)) * (a.dtype == DCONV_BF16 ? 2 : 4)); }
+size_t wt_bytes(const dconv_wt_t& w) { return align256(static_cast<size_t>(wt_elems(w)) * (w.dtype == DCONV_BF16 ? 2 : 4)); }
+
+void launch_reblock_act(const dconv_act_t& src, const dconv_act_t& dst, int accumulate, cudaStream_t cs) {
+  if (src.dtype != dst.dtype) fail(DCONV_ERR_INVALID_ARGUMENT, "reblock: dtypes differ");
+  const int g = grid1d(act_elems(dst));
+  if (src.dtype == DCONV_F32)
+    reblock_act_kernel<float><<<g, 256, 0, cs>>>((const float*)src.data, (float*)dst.data, src.n, src.c, src.h, src.w,
+                                                 src.vlen, src.halo_h, src.halo_w, dst.vlen, dst.halo_h, dst.halo_w,
+                                                 accumulate);
+  else
+    reblock_act_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)src.data, (__nv_bfloat16*)dst.data,
+                                                         src.n, src.c, src.h, src.w, src.vlen, src.halo_h, src.halo_w,
+                                                         dst.vlen, dst.halo_h, dst.halo_w, accumulate);
+  cuda_check(cudaGetLastError(), "reblock_act");
+}
+void launch_reblock_wt(const dconv_wt_t& src, const dconv_wt_t& dst, int accumulate, cudaStream_t cs) {
+  if (src.dtype != dst.dtype) fail(DCONV_ERR_INVALID_ARGUMENT, "reblock: dtypes differ");
+  const int g = grid1d(wt_elems(dst));
+  if (src.dtype == DCONV_F32)
+    reblock_wt_kernel<float><<<g, 256, 0, cs>>>((const float*)src.data, (float*)dst.data, src.k, src.c, src.r, src.s,
+                                                src.vlen, dst.vlen, accumulate);
+  else
+    reblock_wt_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)src.data, (__nv_bfloat16*)dst.data,
+                                                        src.k, src.c, src.r, src.s, src.vlen, dst.vlen, accumulate);
+  cuda_check(cudaGetLastError(), "reblock_wt");
+}
+void reblock_epilogue_check(const dconv_epilogue_t* ep) {
+  if (ep && (ep->add || ep->mask || ep->flags))
+    fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: fused graph epilogues need 16-lane tensors");
+}
+}  // namespace
+
 // ====================================================================== plans
 // Resolved launches are cached per tensor geometry (the reference builds its
 // ExecutionPlan once per layer, propagation.cpp:42-54): the tile search, the
@@ -800,6 +863,7 @@ struct dconv_fwd_plan {
   std::mutex mu;
   std::map<GeoKey, FwdEntry> cache;
   const std::string* last_desc = nullptr;
+  dconv_fwd_plan* inner = nullptr;  // vlen != 16: the vlen-16 twin the execute re-blocks around
 };
 
 struct BwdPhase {
@@ -823,6 +887,7 @@ struct dconv_bwd_plan {
   std::mutex mu;
   std::map<GeoKey, FwdEntry> cache;  // key: (grad_out, grad_in, accumulate)
   const std::string* last_desc = nullptr;
+  dconv_bwd_plan* inner = nullptr;  // vlen != 16: the vlen-16 twin
 };
 
 struct UpdEntry;
@@ -836,6 +901,7 @@ struct dconv_upd_plan {
   std::mutex mu;
   std::map<GeoKey, UpdEntry*> cache;
   const std::string* last_desc = nullptr;
+  dconv_upd_plan* inner = nullptr;  // vlen != 16: the vlen-16 twin
   // modelled bf16 variant choice (k-tile width, stacking, c-tiles per CTA) per operand
   // geometry: computed once, not on every execute (the search evaluates ~10 plans)
   mutable std::mutex sel_mu;
@@ -1167,12 +1233,20 @@ int dconv_fwd_plan_create(const dconv_spec_t* spec, const dconv_fusion_t* fusion
   const int st = guarded([&] {
     if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
     validate_spec(*spec);
-    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
     if (out_halo_h < 0 || out_halo_w < 0) fail(DCONV_ERR_INVALID_LAYER_SPEC, "output halo must be >= 0");
     pl = new dconv_fwd_plan();
     pl->spec = *spec;
     pl->math = math;
     pl->pieces = math_pieces(math);
+    if (spec->vlen != 16) {  // the tensor-core passes run on 16-lane blocks: re-block around a twin
+      const dconv_spec_t s16 = spec16(*spec);
+      const int rc = dconv_fwd_plan_create(&s16, fusion, cfg, math, out_halo_h, out_halo_w, &pl->inner);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      pl->out_halo_h = out_halo_h;
+      pl->out_halo_w = out_halo_w;
+      *plan = pl;
+      return;
+    }
     pl->fuse_kind = fusion ? fusion->kind : DCONV_FUSE_NONE;
     pl->out_halo_h = out_halo_h;
     pl->out_halo_w = out_halo_w;
@@ -1203,6 +1277,7 @@ int dconv_fwd_plan_create(const dconv_spec_t* spec, const dconv_fusion_t* fusion
   if (st != DCONV_OK && pl) {
     if (pl->bias_dev) cudaFree(pl->bias_dev);
     if (pl->tapmap_dev) cudaFree(pl->tapmap_dev);
+    if (pl->inner) dconv_fwd_plan_destroy(pl->inner);
     delete pl;
   }
   return st;
@@ -1210,6 +1285,7 @@ int dconv_fwd_plan_create(const dconv_spec_t* spec, const dconv_fusion_t* fusion
 
 void dconv_fwd_plan_destroy(dconv_fwd_plan_t plan) {
   if (!plan) return;
+  if (plan->inner) dconv_fwd_plan_destroy(plan->inner);
   if (plan->bias_dev) cudaFree(plan->bias_dev);
   if (plan->tapmap_dev) cudaFree(plan->tapmap_dev);
   delete plan;
@@ -1217,11 +1293,19 @@ void dconv_fwd_plan_destroy(dconv_fwd_plan_t plan) {
 
 size_t dconv_fwd_workspace_bytes(dconv_fwd_plan_t plan) {
   if (!plan) return 0;
+  if (plan->inner) {  // twin's workspace + 16-lane copies of input (halo = pad), weights, output
+    const dconv_spec_t& s = plan->spec;
+    const dconv_act_t in{nullptr, s.N, s.C, s.H, s.W, 16, s.pad_h, s.pad_w, DCONV_F32};
+    const dconv_act_t out{nullptr, s.N, s.K, out_P(s), out_Q(s), 16, plan->out_halo_h, plan->out_halo_w, DCONV_F32};
+    const dconv_wt_t w{nullptr, s.K, s.C, s.R, s.S, 16, DCONV_F32};
+    return dconv_fwd_workspace_bytes(plan->inner) + act_bytes(in) + wt_bytes(w) + act_bytes(out);
+  }
   const dconv_spec_t& s = plan->spec;
   return align256(prep_bytes(plan->pieces, cdiv(s.C, 16), s.R * s.S, cdiv(s.K, 16)));
 }
 
 int dconv_fwd_plan_describe(dconv_fwd_plan_t plan, char* buf, size_t len) {
+  if (plan && plan->inner) return dconv_fwd_plan_describe(plan->inner, buf, len);
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -1229,7 +1313,7 @@ int dconv_fwd_plan_describe(dconv_fwd_plan_t plan, char* buf, size_t len) {
   });
 }
 
-int dconv_fwd_launches(dconv_fwd_plan_t plan) { return plan ? 2 : 0; }
+int dconv_fwd_launches(dconv_fwd_plan_t plan) { return plan ? (plan->inner ? 5 : 2) : 0; }
 
 int dconv_forward(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_wt_t* wt, const dconv_act_t* out,
                   void* workspace, dconv_stream_t stream) {
@@ -1299,6 +1383,21 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
     if (out->halo_h != plan->out_halo_h || out->halo_w != plan->out_halo_w)
       fail(DCONV_ERR_PLAN_TENSOR_MISMATCH, "forward: output halo differs from the plan's output surface");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (plan->inner) {  // vlen != 16: re-block around the 16-lane twin
+      reblock_epilogue_check(ep);
+      if (in->dtype != out->dtype || wt->dtype != in->dtype)
+        fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: input, weights and output share one dtype");
+      char* w8 = reinterpret_cast<char*>(workspace) + dconv_fwd_workspace_bytes(plan->inner);
+      const dconv_act_t in16 = act_as16(*in, w8, s.pad_h, s.pad_w);
+      const dconv_wt_t w16 = wt_as16(*wt, w8 + act_bytes(in16), wt->dtype);
+      const dconv_act_t out16 = act_as16(*out, w8 + act_bytes(in16) + wt_bytes(w16), out->halo_h, out->halo_w);
+      launch_reblock_act(*in, in16, 0, cs);
+      launch_reblock_wt(*wt, w16, 0, cs);
+      const int rc = dconv_forward_ex(plan->inner, &in16, &w16, &out16, nullptr, workspace, stream);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      launch_reblock_act(out16, *out, 0, cs);
+      return;
+    }
     const int cb = cdiv(s.C, 16);
     FwdLaunch L;
     {
@@ -1354,12 +1453,18 @@ int dconv_bwd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
   const int st = guarded([&] {
     if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
     validate_spec(*spec);
-    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
     pl = new dconv_bwd_plan();
     pl->spec = *spec;
     pl->math = math;
     pl->pieces = math_pieces(math);
     pl->route = choose_route(*spec);
+    if (spec->vlen != 16) {
+      const dconv_spec_t s16 = spec16(*spec);
+      const int rc = dconv_bwd_plan_create(&s16, cfg, math, &pl->inner);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      *plan = pl;
+      return;
+    }
     pl->has_cfg = cfg != nullptr;
     if (cfg) pl->cfg = *cfg;
     const dconv_spec_t& s = *spec;
@@ -1416,6 +1521,7 @@ int dconv_bwd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
   });
   if (st != DCONV_OK && pl) {
     if (pl->tapmap_dev) cudaFree(pl->tapmap_dev);
+    if (pl->inner) dconv_bwd_plan_destroy(pl->inner);
     delete pl;
   }
   return st;
@@ -1423,13 +1529,24 @@ int dconv_bwd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
 
 void dconv_bwd_plan_destroy(dconv_bwd_plan_t plan) {
   if (!plan) return;
+  if (plan->inner) dconv_bwd_plan_destroy(plan->inner);
   if (plan->tapmap_dev) cudaFree(plan->tapmap_dev);
   delete plan;
 }
 
 int dconv_bwd_route(dconv_bwd_plan_t plan) { return plan ? plan->route : -1; }
-size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan) { return plan ? std::max<size_t>(plan->ws_bytes, 256) : 0; }
+size_t dconv_bwd_workspace_bytes(dconv_bwd_plan_t plan) {
+  if (plan && plan->inner) {  // twin's workspace + 16-lane dO (halo 0), weights, dI (halo 0)
+    const dconv_spec_t& s = plan->spec;
+    const dconv_act_t go{nullptr, s.N, s.K, out_P(s), out_Q(s), 16, 0, 0, DCONV_F32};
+    const dconv_act_t gi{nullptr, s.N, s.C, s.H, s.W, 16, 0, 0, DCONV_F32};
+    const dconv_wt_t w{nullptr, s.K, s.C, s.R, s.S, 16, DCONV_F32};
+    return dconv_bwd_workspace_bytes(plan->inner) + act_bytes(go) + wt_bytes(w) + act_bytes(gi);
+  }
+  return plan ? std::max<size_t>(align256(plan->ws_bytes), 256) : 0;
+}
 int dconv_bwd_plan_describe(dconv_bwd_plan_t plan, char* buf, size_t len) {
+  if (plan && plan->inner) return dconv_bwd_plan_describe(plan->inner, buf, len);
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -1443,6 +1560,7 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
 
 int dconv_bwd_launches(dconv_bwd_plan_t plan) {
   if (!plan) return 0;
+  if (plan->inner) return dconv_bwd_launches(plan->inner) + 3;
   int n = 0;
   for (auto& ph : plan->phases) n += ph.zero ? 1 : 2;
   return n;
@@ -1527,6 +1645,21 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
     if (grad_in->n != s.N || grad_in->c != s.C || grad_in->h != s.H || grad_in->w != s.W || grad_in->vlen != s.vlen)
       fail(DCONV_ERR_SHAPE_MISMATCH, "backward: grad_in does not match the layer spec");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (plan->inner) {  // vlen != 16: re-block around the 16-lane twin
+      reblock_epilogue_check(ep);
+      if (grad_out->dtype != grad_in->dtype || wt->dtype != grad_out->dtype)
+        fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: grad_out, weights and grad_in share one dtype");
+      char* w8 = reinterpret_cast<char*>(workspace) + dconv_bwd_workspace_bytes(plan->inner);
+      const dconv_act_t go16 = act_as16(*grad_out, w8, 0, 0);
+      const dconv_wt_t w16 = wt_as16(*wt, w8 + act_bytes(go16), wt->dtype);
+      const dconv_act_t gi16 = act_as16(*grad_in, w8 + act_bytes(go16) + wt_bytes(w16), 0, 0);
+      launch_reblock_act(*grad_out, go16, 0, cs);
+      launch_reblock_wt(*wt, w16, 0, cs);
+      const int rc = dconv_backward_data_ex(plan->inner, &w16, &go16, &gi16, nullptr, workspace, stream);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      launch_reblock_act(gi16, *grad_in, 0, cs);
+      return;
+    }
     const int kb = cdiv(s.K, 16), cb = cdiv(s.C, 16);
     const int hp = s.H + 2 * grad_in->halo_h, wp = s.W + 2 * grad_in->halo_w;
     const bool accumulate = ep && ep->add && ep->add == grad_in->data;
@@ -2175,9 +2308,17 @@ int dconv_upd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
   const int st = guarded([&] {
     if (!spec || !plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null argument");
     validate_spec(*spec);
-    if (spec->vlen != 16) fail(DCONV_ERR_UNSUPPORTED, "sm_100a kernels use vlen 16 channel blocks");
     pl = new dconv_upd_plan();
     pl->spec = *spec;
+    if (spec->vlen != 16) {
+      const dconv_spec_t s16 = spec16(*spec);
+      const int rc = dconv_upd_plan_create(&s16, cfg, math, &pl->inner);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      pl->math = math;
+      pl->pieces = math_pieces(math);
+      *plan = pl;
+      return;
+    }
     pl->math = math;
     pl->pieces = math_pieces(math);
     pl->has_cfg = cfg != nullptr;
@@ -2185,12 +2326,16 @@ int dconv_upd_plan_create(const dconv_spec_t* spec, const dconv_engine_config_t*
     pl->taps = phase_taps(spec->R, spec->S, spec->stride);
     *plan = pl;
   });
-  if (st != DCONV_OK && pl) delete pl;
+  if (st != DCONV_OK && pl) {
+    if (pl->inner) dconv_upd_plan_destroy(pl->inner);
+    delete pl;
+  }
   return st;
 }
 
 void dconv_upd_plan_destroy(dconv_upd_plan_t plan) {
   if (!plan) return;
+  if (plan->inner) dconv_upd_plan_destroy(plan->inner);
   for (auto& kv : plan->cache) delete kv.second;
   delete plan;
 }
@@ -2212,6 +2357,7 @@ static dconv_act_t default_act(const dconv_spec_t& s, bool grad, int dtype) {
 
 int dconv_upd_splits(dconv_upd_plan_t plan) {
   if (!plan) return -1;
+  if (plan->inner) return dconv_upd_splits(plan->inner);
   int v = -1;
   guarded([&] {
     const int dt = plan->pieces == 3 ? DCONV_F32 : DCONV_BF16;
@@ -2222,6 +2368,7 @@ int dconv_upd_splits(dconv_upd_plan_t plan) {
 }
 
 int dconv_upd_plan_describe(dconv_upd_plan_t plan, char* buf, size_t len) {
+  if (plan && plan->inner) return dconv_upd_plan_describe(plan->inner, buf, len);
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -2231,6 +2378,14 @@ int dconv_upd_plan_describe(dconv_upd_plan_t plan, char* buf, size_t len) {
 
 size_t dconv_upd_workspace_bytes(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out) {
   if (!plan || !in || !grad_out) return 0;
+  if (plan->inner) {  // twin's workspace + 16-lane input (halo = pad), dO (halo 0), dW
+    const dconv_spec_t& s = plan->spec;
+    const dconv_act_t in16 = act_as16(*in, reinterpret_cast<void*>(256), s.pad_h, s.pad_w);
+    const dconv_act_t go16 = act_as16(*grad_out, reinterpret_cast<void*>(256), 0, 0);
+    const dconv_wt_t w{nullptr, s.K, s.C, s.R, s.S, 16, DCONV_F32};
+    return align256(dconv_upd_workspace_bytes(plan->inner, &in16, &go16)) + act_bytes(in16) + act_bytes(go16) +
+           wt_bytes(w);
+  }
   size_t v = 0;
   guarded([&] {
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -2242,6 +2397,11 @@ size_t dconv_upd_workspace_bytes(dconv_upd_plan_t plan, const dconv_act_t* in, c
 
 int dconv_upd_launches(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out) {
   if (!plan || !in || !grad_out) return 0;
+  if (plan->inner) {
+    const dconv_act_t in16 = act_as16(*in, in->data, plan->spec.pad_h, plan->spec.pad_w);
+    const dconv_act_t go16 = act_as16(*grad_out, grad_out->data, 0, 0);
+    return dconv_upd_launches(plan->inner, &in16, &go16) + 3;
+  }
   int v = 0;
   guarded([&] {
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -2270,6 +2430,21 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     if (grad_w->k != s.K || grad_w->c != s.C || grad_w->r != s.R || grad_w->s != s.S || grad_w->vlen != s.vlen)
       fail(DCONV_ERR_SHAPE_MISMATCH, "weight_update: grad_w does not match the layer spec");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (plan->inner) {  // vlen != 16: re-block around the 16-lane twin
+      if (in->dtype != grad_out->dtype) fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: input and grad_out share one dtype");
+      const dconv_act_t in16p = act_as16(*in, reinterpret_cast<void*>(256), s.pad_h, s.pad_w);
+      const dconv_act_t go16p = act_as16(*grad_out, reinterpret_cast<void*>(256), 0, 0);
+      char* w8 = reinterpret_cast<char*>(workspace) + align256(dconv_upd_workspace_bytes(plan->inner, &in16p, &go16p));
+      const dconv_act_t in16 = act_as16(*in, w8, s.pad_h, s.pad_w);
+      const dconv_act_t go16 = act_as16(*grad_out, w8 + act_bytes(in16), 0, 0);
+      const dconv_wt_t dw16 = wt_as16(*grad_w, w8 + act_bytes(in16) + act_bytes(go16), grad_w->dtype);
+      launch_reblock_act(*in, in16, 0, cs);
+      launch_reblock_act(*grad_out, go16, 0, cs);
+      const int rc = dconv_weight_update(plan->inner, &in16, &go16, &dw16, 0, workspace, stream);
+      if (rc != DCONV_OK) fail(rc, g_err);
+      launch_reblock_wt(dw16, *grad_w, accumulate ? 1 : 0, cs);
+      return;
+    }
     char* ws = reinterpret_cast<char*>(workspace);
     UpdLaunch L;
     void* in_pc = nullptr;

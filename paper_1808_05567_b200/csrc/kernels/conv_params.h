@@ -14,9 +14,9 @@ namespace dconv_sm100 {
 
 constexpr bool kDevBuild = DCONV_DEV_BUILD != 0;
 
-constexpr int kMaxTaps = 64;
-constexpr int kMaxPhases = 4;
-constexpr int kMaxTapGroups = 64;
+constexpr int kMaxTaps = 128;     // filter taps (R * S <= 128: up to 11 x 11)
+constexpr int kMaxPhases = 16;    // stride phases (stride <= 4)
+constexpr int kMaxTapGroups = 128;
 
 // Implicit-GEMM forward over the "virtual row" grid: output pixel (p, q) of
 // image n is virtual position v = p * wsub + q; tap t of phase ph reads the

@@ -111,6 +111,64 @@ __global__ void unpack_wt_kernel(const S* __restrict__ src, D* __restrict__ dst,
   }
 }
 
+// blocked(vs, halo shh/shw) -> blocked(vd, halo dhh/dhw), same channels / extents:
+// the internal re-blocking of vlen != 16 tensors for the 16-lane tensor-core passes.
+// Destination halo and tail lanes are written as zeros; accumulate adds into dst
+// (interior lanes) instead of overwriting.
+template <typename T>
+__global__ void reblock_act_kernel(const T* __restrict__ src, T* __restrict__ dst, int n, int c, int h, int w, int vs,
+                                   int shh, int shw, int vd, int dhh, int dhw, int accumulate) {
+  const int cbs = (c + vs - 1) / vs, cbd = (c + vd - 1) / vd;
+  const int shp = h + 2 * shh, swp = w + 2 * shw, dhp = h + 2 * dhh, dwp = w + 2 * dhw;
+  const long long total = static_cast<long long>(n) * cbd * dhp * dwp * vd;
+  DCONV_GRID_STRIDE(e, total) {
+    const int lane = static_cast<int>(e % vd);
+    long long r = e / vd;
+    const int x = static_cast<int>(r % dwp) - dhw;
+    r /= dwp;
+    const int y = static_cast<int>(r % dhp) - dhh;
+    r /= dhp;
+    const int b = static_cast<int>(r % cbd);
+    const int img = static_cast<int>(r / cbd);
+    const int ch = b * vd + lane;
+    const bool live = ch < c && y >= 0 && y < h && x >= 0 && x < w;
+    float val = 0.0f;
+    if (live)
+      val = to_f<T>(src[((((static_cast<long long>(img) * cbs + ch / vs) * shp + y + shh) * swp) + x + shw) * vs +
+                        ch % vs]);
+    if (accumulate && live) val += to_f<T>(dst[e]);
+    dst[e] = from_f<T>(val);
+  }
+}
+
+// [kb][cb][r][s][c][k] at vs -> at vd (tail lanes zero); accumulate adds into dst
+template <typename T>
+__global__ void reblock_wt_kernel(const T* __restrict__ src, T* __restrict__ dst, int k, int c, int r, int s, int vs,
+                                  int vd, int accumulate) {
+  const int kbs = (k + vs - 1) / vs, cbs = (c + vs - 1) / vs, kbd = (k + vd - 1) / vd, cbd = (c + vd - 1) / vd;
+  (void)kbs;
+  const long long total = static_cast<long long>(kbd) * cbd * r * s * vd * vd;
+  DCONV_GRID_STRIDE(e, total) {
+    const int kl = static_cast<int>(e % vd);
+    const int cl = static_cast<int>((e / vd) % vd);
+    long long q = e / (static_cast<long long>(vd) * vd);
+    const int fs = static_cast<int>(q % s);
+    q /= s;
+    const int fr = static_cast<int>(q % r);
+    q /= r;
+    const int cbi = static_cast<int>(q % cbd);
+    const int kbi = static_cast<int>(q / cbd);
+    const int ko = kbi * vd + kl, ci = cbi * vd + cl;
+    const bool live = ko < k && ci < c;
+    float val = 0.0f;
+    if (live)
+      val = to_f<T>(src[((((static_cast<long long>(ko / vs) * cbs + ci / vs) * r + fr) * s + fs) * vs + ci % vs) * vs +
+                        ko % vs]);
+    if (accumulate && live) val += to_f<T>(dst[e]);
+    dst[e] = from_f<T>(val);
+  }
+}
+
 // dual weights: out (k<->c roles swapped) [cb'=k_b... ] as transform_weight_stride1
 template <typename T>
 __global__ void dual_wt_kernel(const T* __restrict__ src, T* __restrict__ dst, int k, int c, int r, int s, int v) {

@@ -293,6 +293,7 @@ int dconv_set_dev_mode(int on) {
 int dconv_fwd_plan_save(dconv_fwd_plan_t plan, char* buf, size_t len, size_t* needed) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    if (plan->inner) fail(DCONV_ERR_UNSUPPORTED, "plan save: vlen != 16 plans re-block around a vlen-16 twin");
     std::ostringstream os;
     save_header(os, "fwd", plan->spec, plan->math, plan->has_cfg, plan->cfg);
     put(os, "out_halo", {plan->out_halo_h, plan->out_halo_w});
@@ -365,6 +366,7 @@ int dconv_fwd_plan_load(const char* text, size_t len, int validate, dconv_fwd_pl
 int dconv_bwd_plan_save(dconv_bwd_plan_t plan, char* buf, size_t len, size_t* needed) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    if (plan->inner) fail(DCONV_ERR_UNSUPPORTED, "plan save: vlen != 16 plans re-block around a vlen-16 twin");
     std::ostringstream os;
     save_header(os, "bwd", plan->spec, plan->math, plan->has_cfg, plan->cfg);
     std::lock_guard<std::mutex> lk(plan->mu);
@@ -428,6 +430,7 @@ int dconv_bwd_plan_load(const char* text, size_t len, int validate, dconv_bwd_pl
 int dconv_upd_plan_save(dconv_upd_plan_t plan, char* buf, size_t len, size_t* needed) {
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
+    if (plan->inner) fail(DCONV_ERR_UNSUPPORTED, "plan save: vlen != 16 plans re-block around a vlen-16 twin");
     std::ostringstream os;
     save_header(os, "upd", plan->spec, plan->math, plan->has_cfg, plan->cfg);
     std::lock_guard<std::mutex> lk(plan->mu);

@@ -129,6 +129,11 @@ extern "C" {
 
 int dconv_fwd_plan_validate(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_act_t* out, char* report,
                             size_t len) {
+  if (plan && plan->inner && in && out) {  // vlen != 16: the twin's launch on the re-blocked tensors
+    const dconv_act_t a = act_as16(*in, in->data, plan->spec.pad_h, plan->spec.pad_w);
+    const dconv_act_t b = act_as16(*out, out->data, out->halo_h, out->halo_w);
+    return dconv_fwd_plan_validate(plan->inner, &a, &b, report, len);
+  }
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     check_act(in, "validate input");
@@ -165,6 +170,11 @@ int dconv_fwd_plan_validate(dconv_fwd_plan_t plan, const dconv_act_t* in, const 
 
 int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, const dconv_act_t* grad_in,
                             char* report, size_t len) {
+  if (plan && plan->inner && grad_out && grad_in) {
+    const dconv_act_t a = act_as16(*grad_out, grad_out->data, 0, 0);
+    const dconv_act_t b = act_as16(*grad_in, grad_in->data, 0, 0);
+    return dconv_bwd_plan_validate(plan->inner, &a, &b, report, len);
+  }
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     check_act(grad_out, "validate grad_out");
@@ -241,6 +251,11 @@ int dconv_bwd_plan_validate(dconv_bwd_plan_t plan, const dconv_act_t* grad_out, 
 
 int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const dconv_act_t* grad_out,
                             char* report, size_t len) {
+  if (plan && plan->inner && in && grad_out) {
+    const dconv_act_t a = act_as16(*in, in->data, plan->spec.pad_h, plan->spec.pad_w);
+    const dconv_act_t b = act_as16(*grad_out, grad_out->data, 0, 0);
+    return dconv_upd_plan_validate(plan->inner, &a, &b, report, len);
+  }
   return guarded([&] {
     if (!plan) fail(DCONV_ERR_INVALID_ARGUMENT, "null plan");
     check_act(in, "validate input");
