@@ -503,11 +503,17 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // when all the stages' weights fit, each gets its own slot, loaded once per CTA
           // (the stem, the 56x56 3x3 and 1x1 layers re-streamed them for every tile)
           w_all = false;
-          if (nb >= kb_total && taps.n_phases == 1 && wt == taps.taps_box && !DCONV_ENV("DCONV_NO_WALL")) {
+          // ... also with several output-channel tiles when every CTA keeps ONE of them for
+          // the whole launch (persistent striding by a multiple of the n-tile count): the
+          // 1x1 layers with K > 256 then stream only activations, not the weights per tile
+          const int n_nt_tiles = cdiv(kb_total, nb);
+          const int m_tiles_e = mimg_ok ? cdiv(in.n, std::max(1, (128 * mb) / hw)) : in.n * cdiv(pb.P * p.wsub, 128 * mb);
+          const bool fixed_nt = nb >= kb_total || std::min(m_tiles_e * n_nt_tiles, sm_count()) % n_nt_tiles == 0;
+          if (fixed_nt && taps.n_phases == 1 && wt == taps.taps_box && !DCONV_ENV("DCONV_NO_WALL")) {
             const int kst = cdiv(pb.cb_red, kc);
             const FwdSmem lk = fwd_smem_layout(apx * kc, wt * kc, nb, pieces, raw_f32, 1, 1);
             const int w_bytes = kst * static_cast<int>(lk.w_slot);
-            const int pcs2 = kst <= kMaxStages && w_bytes <= 112 * 1024
+            const int pcs2 = kst <= kMaxStages && w_bytes <= env_int("DCONV_WALL_KB", 160) * 1024
                                  ? std::min<int>(kMaxStages, (kFwdBudget - stg_res - w_bytes) / static_cast<int>(lk.pc_slot))
                                  : 0;
             if (pcs2 >= 2) {
@@ -638,6 +644,7 @@ void finalize_fwd(FwdLaunch& L) {
   p.tma_store = 0;
   if (p.mimg == 0 && p.out_halo_h == 0 && p.out_halo_w == 0 && p.out_scale == 1 && p.out_y0 == 0 &&
       p.out_x0 == 0 && p.out_hp == p.P && p.out_wp == p.Q && p.wsub == p.Q && !(p.dbg_mode & 1) &&
+      !DCONV_ENV("DCONV_NO_TMA_STORE") &&
       L.smem + staging <= static_cast<size_t>(kSmemBudget)) {
     p.tma_store = 1;
     L.smem_launch = L.smem + staging;
@@ -1416,6 +1423,8 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
       plan->last_desc = &e.desc;
     }
     FwdParams& p = L.p;
+    p.dbg = g_fwd_dbg;  // developer builds: role counters / ablation bits (set per call)
+    p.dbg_mode = g_fwd_dbg_mode;
     p.wprep = workspace;
     p.out = out->data;
     p.bias = (plan->fuse_kind == DCONV_FUSE_BIAS_ADD || plan->fuse_kind == DCONV_FUSE_BIAS_RELU) ? plan->bias_dev
@@ -1706,6 +1715,8 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
       FwdLaunch& L = Ls[conv_i];
       void* wprep = reinterpret_cast<char*>(workspace) + ph.ws_off;
       FwdParams& p = L.p;
+      p.dbg = g_fwd_dbg;
+      p.dbg_mode = g_fwd_dbg_mode;
       p.wprep = wprep;
       if (prep)
         launch_weight_prep(*wt, p.n_taps, plan->tapmap_dev + tap_off, wprep, kb, p.nb, p.n_ntiles, 1, plan->pieces,

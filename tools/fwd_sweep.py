@@ -12,6 +12,7 @@ from paper_1808_05567_b200 import _lib  # noqa: E402
 
 lib = _lib.lib()
 lib.dconv_profile(1)
+lib.dconv_set_dev_mode(1)  # DCONV_* overrides act only in developer mode
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 N = int(os.environ.get("N", "256"))
 LAYERS = [(64, 64, 56, 3), (128, 128, 28, 3), (256, 256, 14, 3), (512, 512, 7, 3)]
