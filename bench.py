@@ -373,7 +373,22 @@ def measure_cfg2(torch, d, dev, steps, warmup, math_f32=True):
         for k, idx in (("F", 0), ("B", 1), ("U", 2)):
             kern[k].append(lib.dconv_profile_last_ms(idx))
     lib.dconv_profile(0)
+    # layout kernels on the same tensor (to_/from_blocked_activation, blocked.hpp:133-178):
+    # NCHW fp32 <-> NCHW16c fp32, bytes = read + write
+    import ctypes as C
+
+    x_nchw = torch.empty(spec.N, spec.C, spec.H, spec.W, dtype=torch.float32, device=dev).uniform_(-1, 1)
+    blk = d.BlockedActivation(spec.N, spec.C, spec.H, spec.W, 16, 0, 0, torch.float32, dev)
+    st = stream.cuda_stream
+    t_pack = _timed(torch, lambda: lib.dconv_pack_act(x_nchw.data_ptr(), 0, C.byref(blk.to_c()), st), reps=10)
+    t_unpack = _timed(torch, lambda: lib.dconv_unpack_act(C.byref(blk.to_c()), x_nchw.data_ptr(), 0, st), reps=10)
+    layout_bytes = 2 * x_nchw.numel() * 4
     hbm, _, _, src = measured_peaks()
+    layout = {"tensor": f"NCHW fp32 [{spec.N},{spec.C},{spec.H},{spec.W}] <-> NCHW16c", "bytes": layout_bytes,
+              "pack_gbs": round(layout_bytes / (t_pack * 1e-3) / 1e9, 1),
+              "unpack_gbs": round(layout_bytes / (t_unpack * 1e-3) / 1e9, 1),
+              "pack_frac": round(layout_bytes / (t_pack * 1e-3) / 1e9 / hbm, 3),
+              "unpack_frac": round(layout_bytes / (t_unpack * 1e-3) / 1e9 / hbm, 3)}
     byts = alg_bytes(w)
     avg = {k: sum(v) / len(v) for k, v in kern.items()}
     dom = max(avg, key=avg.get)
@@ -393,6 +408,7 @@ def measure_cfg2(torch, d, dev, steps, warmup, math_f32=True):
                      "peak_source": src},
         "l2": "flushed between timed steps (256 MiB write + read-back, untimed)",
         "launches_per_step": fplan.launches() + bctx.launches() + uplan.launches(ib, gb),
+        "layout_kernels": layout,
     }
     return res, (fplan, bctx, uplan, spec, ib, wb, gb, out, gi, dw)
 

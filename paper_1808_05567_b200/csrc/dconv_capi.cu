@@ -1001,8 +1001,25 @@ int dconv_pack_act(const void* nchw, int src_dtype, const dconv_act_t* dst, dcon
     check_dtype(src_dtype);
     if (!nchw) fail(DCONV_ERR_INVALID_ARGUMENT, "pack_act: null source");
     const dconv_act_t& d = *dst;
-    const int g = grid1d(act_elems(d));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (d.vlen == 16) {  // thread per pixel, vector lane rows
+      const int g16 = grid1d(act_elems(d) / 16);
+      if (src_dtype == DCONV_F32 && d.dtype == DCONV_F32)
+        pack_act16_kernel<float, float><<<g16, 256, 0, s>>>((const float*)nchw, (float*)d.data, d.n, d.c, d.h, d.w,
+                                                            d.halo_h, d.halo_w);
+      else if (src_dtype == DCONV_F32)
+        pack_act16_kernel<float, __nv_bfloat16><<<g16, 256, 0, s>>>((const float*)nchw, (__nv_bfloat16*)d.data, d.n,
+                                                                    d.c, d.h, d.w, d.halo_h, d.halo_w);
+      else if (d.dtype == DCONV_F32)
+        pack_act16_kernel<__nv_bfloat16, float><<<g16, 256, 0, s>>>((const __nv_bfloat16*)nchw, (float*)d.data, d.n,
+                                                                    d.c, d.h, d.w, d.halo_h, d.halo_w);
+      else
+        pack_act16_kernel<__nv_bfloat16, __nv_bfloat16><<<g16, 256, 0, s>>>(
+            (const __nv_bfloat16*)nchw, (__nv_bfloat16*)d.data, d.n, d.c, d.h, d.w, d.halo_h, d.halo_w);
+      cuda_check(cudaGetLastError(), "pack_act");
+      return;
+    }
+    const int g = grid1d(act_elems(d));
     if (src_dtype == DCONV_F32 && d.dtype == DCONV_F32)
       pack_act_kernel<float, float><<<g, 256, 0, s>>>((const float*)nchw, (float*)d.data, d.n, d.c, d.h, d.w, d.vlen,
                                                       d.halo_h, d.halo_w);
@@ -1025,8 +1042,25 @@ int dconv_unpack_act(const dconv_act_t* src, void* nchw, int dst_dtype, dconv_st
     check_dtype(dst_dtype);
     if (!nchw) fail(DCONV_ERR_INVALID_ARGUMENT, "unpack_act: null destination");
     const dconv_act_t& a = *src;
-    const int g = grid1d(static_cast<int64_t>(a.n) * a.c * a.h * a.w);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (a.vlen == 16) {  // thread per pixel, vector lane rows
+      const int g16 = grid1d(static_cast<int64_t>(a.n) * cdiv(a.c, 16) * a.h * a.w);
+      if (a.dtype == DCONV_F32 && dst_dtype == DCONV_F32)
+        unpack_act16_kernel<float, float><<<g16, 256, 0, s>>>((const float*)a.data, (float*)nchw, a.n, a.c, a.h, a.w,
+                                                              a.halo_h, a.halo_w);
+      else if (a.dtype == DCONV_F32)
+        unpack_act16_kernel<float, __nv_bfloat16><<<g16, 256, 0, s>>>((const float*)a.data, (__nv_bfloat16*)nchw, a.n,
+                                                                      a.c, a.h, a.w, a.halo_h, a.halo_w);
+      else if (dst_dtype == DCONV_F32)
+        unpack_act16_kernel<__nv_bfloat16, float><<<g16, 256, 0, s>>>((const __nv_bfloat16*)a.data, (float*)nchw, a.n,
+                                                                      a.c, a.h, a.w, a.halo_h, a.halo_w);
+      else
+        unpack_act16_kernel<__nv_bfloat16, __nv_bfloat16><<<g16, 256, 0, s>>>(
+            (const __nv_bfloat16*)a.data, (__nv_bfloat16*)nchw, a.n, a.c, a.h, a.w, a.halo_h, a.halo_w);
+      cuda_check(cudaGetLastError(), "unpack_act");
+      return;
+    }
+    const int g = grid1d(static_cast<int64_t>(a.n) * a.c * a.h * a.w);
     if (a.dtype == DCONV_F32 && dst_dtype == DCONV_F32)
       unpack_act_kernel<float, float><<<g, 256, 0, s>>>((const float*)a.data, (float*)nchw, a.n, a.c, a.h, a.w, a.vlen,
                                                         a.halo_h, a.halo_w);

@@ -54,6 +54,102 @@ __global__ void pack_act_kernel(const S* __restrict__ src, D* __restrict__ dst, 
   }
 }
 
+// 16 consecutive lanes of one blocked pixel
+template <typename T>
+struct Lanes16;
+template <>
+struct Lanes16<float> {
+  static __device__ __forceinline__ void store(float* dst, const float (&v)[16]) {
+    float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+  static __device__ __forceinline__ void load(const float* src, float (&v)[16]) {
+    const float4* s = reinterpret_cast<const float4*>(src);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 t = s[i];
+      v[4 * i] = t.x, v[4 * i + 1] = t.y, v[4 * i + 2] = t.z, v[4 * i + 3] = t.w;
+    }
+  }
+};
+template <>
+struct Lanes16<__nv_bfloat16> {
+  static __device__ __forceinline__ void store(__nv_bfloat16* dst, const float (&v)[16]) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  static __device__ __forceinline__ void load(const __nv_bfloat16* src, float (&v)[16]) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    const uint4 a = s[0], b = s[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+
+// vlen 16: one thread per destination PIXEL (all 16 lanes). The 16 channel reads
+// are coalesced across the warp (consecutive x), the 64 / 32 B lane row is written
+// with 16 B vector stores (a warp writes one contiguous 2 / 1 KB run); halo pixels
+// and tail lanes are written as zeros. Bitwise equal to pack_act_kernel.
+template <typename S, typename D>
+__global__ void __launch_bounds__(256) pack_act16_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int c,
+                                                         int h, int w, int hh, int hw) {
+  const int cb = (c + 15) / 16, hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long total = static_cast<long long>(n) * cb * hp * wp;
+  const long long plane = static_cast<long long>(h) * w;
+  DCONV_GRID_STRIDE(e, total) {
+    long long r = e;
+    const int x = static_cast<int>(r % wp) - hw;
+    r /= wp;
+    const int y = static_cast<int>(r % hp) - hh;
+    r /= hp;
+    const int b = static_cast<int>(r % cb);
+    const int img = static_cast<int>(r / cb);
+    float v[16];
+    const bool in = y >= 0 && y < h && x >= 0 && x < w;
+    const S* sp = src + ((static_cast<long long>(img) * c + b * 16) * h + (in ? y : 0)) * w + (in ? x : 0);
+#pragma unroll
+    for (int l = 0; l < 16; ++l) v[l] = (in && b * 16 + l < c) ? to_f<S>(sp[l * plane]) : 0.0f;
+    Lanes16<D>::store(dst + e * 16, v);
+  }
+}
+
+// vlen 16: one thread per interior pixel: 16 B vector loads of the lane row, 16
+// channel writes coalesced across the warp
+template <typename S, typename D>
+__global__ void __launch_bounds__(256) unpack_act16_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int c,
+                                                           int h, int w, int hh, int hw) {
+  const int cb = (c + 15) / 16, hp = h + 2 * hh, wp = w + 2 * hw;
+  const long long total = static_cast<long long>(n) * cb * h * w;
+  const long long plane = static_cast<long long>(h) * w;
+  DCONV_GRID_STRIDE(e, total) {
+    long long r = e;
+    const int x = static_cast<int>(r % w);
+    r /= w;
+    const int y = static_cast<int>(r % h);
+    r /= h;
+    const int b = static_cast<int>(r % cb);
+    const int img = static_cast<int>(r / cb);
+    float v[16];
+    Lanes16<S>::load(src + ((((static_cast<long long>(img) * cb + b) * hp + y + hh) * wp) + x + hw) * 16, v);
+    D* dp = dst + ((static_cast<long long>(img) * c + b * 16) * h + y) * w + x;
+#pragma unroll
+    for (int l = 0; l < 16; ++l)
+      if (b * 16 + l < c) dp[l * plane] = from_f<D>(v[l]);
+  }
+}
+
 // blocked (S) -> NCHW (D), interior only
 template <typename S, typename D>
 __global__ void unpack_act_kernel(const S* __restrict__ src, D* __restrict__ dst, int n, int c, int h, int w, int v,
