@@ -450,6 +450,34 @@ def measure_cfg5(torch, d, dev):
             "roof_frac_of_sum": round(tot_roof / tot_ms, 3), "peaks": "bf16 burst TF/s and HBM GB/s (MEASURED_PEAKS)"}
 
 
+def fused_operand_bytes(e, n):
+    """extra compulsory bytes of each conv's fused graph epilogue (bf16): the forward's
+    residual add reads the shortcut tensor; the backward-data's ReLU mask reads the
+    input activation and its branch sum reads the other branch's gradient."""
+    from paper_1808_05567_b200 import executor as ex
+
+    convs = [nd for nd in e.nodes if isinstance(nd, ex.ConvNode)]
+    ident = {nd.add for nd in convs if nd.add is not None}
+    n_conv_consumers = {}
+    for nd in convs:
+        n_conv_consumers[nd.src] = n_conv_consumers.get(nd.src, 0) + 1
+    out = {}
+    for nd in convs:
+        c, h, w = e.shapes[nd.src]
+        k, p, q = e.shapes[nd.out]
+        f = 2 * n * k * p * q if nd.add else 0
+        b = 0
+        # strided 1x1 backward-data touches only its stride lattice of dI with the mask / sum
+        pix = p * q if (nd.R == 1 and nd.S == 1 and nd.stride > 1) else h * w
+        if nd.src != "x":
+            if nd.src in e.relu_out:
+                b += 2 * n * c * pix  # mask
+            if nd.src in ident or n_conv_consumers.get(nd.src, 0) > 1:
+                b += 2 * n * c * pix  # branch-gradient sum
+        out[nd.name] = {"F": f, "B": b, "U": 0}
+    return out
+
+
 def stack_layer_roofline(e, prof, n):
     """the dominant (layer shape, pass) group of the step: largest total device time"""
     from paper_1808_05567_b200 import executor as ex
@@ -457,11 +485,14 @@ def stack_layer_roofline(e, prof, n):
     hbm, peak, _, src = measured_peaks()
     groups = {}
     step_roof = 0.0
+    fused = fused_operand_bytes(e, n)
     for nd in e.convs:
         c, h, w = e.shapes[nd.src]
         wl = dict(N=n, C=nd.C, K=nd.K, H=h, W=w, R=nd.R, S=nd.S, stride=nd.stride, pad_h=nd.pad, pad_w=nd.pad)
         fl = pass_flops(wl)
         byts = alg_bytes(wl, 2, 2)
+        for k in byts:  # the executor's fused epilogue operands are compulsory traffic of that kernel
+            byts[k] += fused[nd.name][k]
         for k in ("F", "B", "U"):
             ms = prof[nd.name][k]
             if ms <= 0:

@@ -686,6 +686,31 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
     cudaEvent_t e0, e1;
     cuck(cudaEventCreate(&e0), "event");
     cuck(cudaEventCreate(&e1), "event");
+    // each conv's backward epilogue exactly as backward() forms it (mask, branch sum)
+    std::vector<const void*> b_add(g->convs.size(), nullptr), b_mask(g->convs.size(), nullptr);
+    {
+      std::vector<char> written(g->t.size(), 0);
+      for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
+        const dconv_graph_node_t& nd = g->nodes[i];
+        if (nd.kind == DCONV_NODE_MAXPOOL) {
+          written[nd.src] = 1;
+          continue;
+        }
+        const int ci = g->conv_of_node[i];
+        if (nd.src == 0) continue;
+        b_mask[ci] = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
+        if (written[nd.src]) {
+          b_add[ci] = g->t[nd.src].grad;
+        } else {
+          for (size_t j = 0; j < g->nodes.size(); ++j)
+            if (g->nodes[j].kind == DCONV_NODE_CONV && g->nodes[j].add == nd.src) {
+              b_add[ci] = g->t[j + 1].grad;
+              break;
+            }
+        }
+        written[nd.src] = 1;
+      }
+    }
     auto timed = [&](auto&& fn) -> float {
       fn();  // warm
       float best = 1e30f;
@@ -718,8 +743,7 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
       ms[3 * ci + 1] = 0.0f;
       if (cv.bp) {
         const dconv_act_t go = act_of(g, cv.node + 1, true), gi = act_of(g, nd.src, true);
-        const void* mask = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
-        const dconv_epilogue_t eb = epi(nullptr, mask, 0);  // (the branch sum's extra read is not timed)
+        const dconv_epilogue_t eb = epi(b_add[ci], b_mask[ci], 0);
         const dconv_wt_t wf = conv_w(g, cv, false);
         ms[3 * ci + 1] =
             timed([&] { ck(dconv_backward_data_ex(cv.bp, &wf, &go, &gi, &eb, g->ws_main, st), "profile bwd"); });

@@ -202,6 +202,9 @@ class ConvStackExecutor:
         self.lib = _lib.lib()
         self.shapes = tensor_shapes(self.nodes, img)
         self.convs = [nd for nd in self.nodes if isinstance(nd, ConvNode)]
+        relu_out = {nd.out for nd in self.convs if nd.relu}
+        relu_out |= {nd.out for nd in self.nodes if isinstance(nd, PoolNode) and nd.src in relu_out}
+        self.relu_out = relu_out  # tensors produced by a ReLU (their gradients carry its mask)
         ids = {"x": 0}
         for i, nd in enumerate(self.nodes):
             ids[nd.out] = i + 1

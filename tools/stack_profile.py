@@ -20,6 +20,7 @@ x = torch.empty(N, 3, 224, 224, device="cuda").uniform_(-1, 1)
 e.load_input_nchw(x)
 prof = e.profile(dtop)
 hbm, peak, _, _ = bench.measured_peaks()
+fused = bench.fused_operand_bytes(e, N)
 tot = {"F": 0.0, "B": 0.0, "U": 0.0}
 troof = {"F": 0.0, "B": 0.0, "U": 0.0}
 print(f"{'layer':7s} {'C':>5s} {'K':>5s} {'H':>4s} R s  " + "  ".join(f"{p}_ms  roof  frac" for p in "FBU"))
@@ -28,6 +29,7 @@ for nd in e.convs:
     wl = dict(N=N, C=nd.C, K=nd.K, H=hh, W=ww, R=nd.R, S=nd.S, stride=nd.stride, pad_h=nd.pad, pad_w=nd.pad)
     fl = bench.pass_flops(wl)
     byts = bench.alg_bytes(wl, 2, 2)
+    byts = {k: v + fused[nd.name][k] for k, v in byts.items()}
     cols = []
     for p in "FBU":
         ms = prof[nd.name][p]
