@@ -497,7 +497,7 @@ def stack_layer_roofline(e, prof, n):
             ms = prof[nd.name][k]
             if ms <= 0:
                 continue
-            key = (nd.C, nd.K, h, w, nd.R, nd.S, nd.stride, k)
+            key = (nd.C, nd.K, h, w, nd.R, nd.S, nd.stride, k, byts[k])  # same shape AND same fused operands
             gdat = groups.setdefault(key, {"ms": 0.0, "count": 0, "flops": fl, "bytes": byts[k],
                                            "layers": []})
             gdat["ms"] += ms
@@ -505,7 +505,7 @@ def stack_layer_roofline(e, prof, n):
             gdat["layers"].append(nd.name)
             step_roof += roof_ms(fl, byts[k], peak, hbm)
     key, g = max(groups.items(), key=lambda kv: kv[1]["ms"])
-    C_, K, H, W, R, S, st, pss = key
+    C_, K, H, W, R, S, st, pss, _ = key
     avg = g["ms"] / g["count"]
     ai = g["flops"] / g["bytes"]
     ridge = peak * 1e12 / (hbm * 1e9)
@@ -519,6 +519,7 @@ def stack_layer_roofline(e, prof, n):
         achieved, unit, pk, bound = g["bytes"] / (avg * 1e-3) / 1e9, "GB/s", hbm, "hbm"
     total = sum(v["F"] + v["B"] + v["U"] for v in prof.values())
     return {"bound": bound, "kernel": kern, "layer": f"{C_}->{K} {R}x{S}/s{st} @{H}x{W} {pss}",
+            "layers": g["layers"],
             "instances": g["count"], "achieved": round(achieved, 1), "peak": pk, "unit": unit,
             "frac": round(achieved / pk, 4), "traffic": traffic, "traffic_key": tkey, "traffic_source": tsrc,
             "alg_flops_per_launch": g["flops"], "alg_bytes_per_launch": g["bytes"], "kernel_ms": round(avg, 4),
