@@ -34,6 +34,10 @@
 #include "conv_params.h"
 #include "sm100_ptx.cuh"
 
+#ifndef DCONV_FWD_WARPS_P
+#define DCONV_FWD_WARPS_P 12  // fp32 smem-staged plans: 8 role warps + 4 converters (12 warps: 168 regs, no spill)
+#endif
+
 namespace dconv_sm100 {
 
 constexpr int kFwdThreads = 256;
@@ -201,12 +205,12 @@ struct RingPos {
 };
 
 // w0 activation producer, w1 MMA, w2 weight producer, w3 idle, w4-7 epilogue
-// (one warp per TMEM lane quarter), w8-13 converters in two groups of three that
+// (one warp per TMEM lane quarter), w8-11 converters in two groups of two that
 // take alternate pipeline stages
-constexpr int kFwdWarps = 14;
+constexpr int kFwdWarps = DCONV_FWD_WARPS_P;
 constexpr int kFwdThreadsP = kFwdWarps * 32;
 constexpr int kEpiWarp0 = 4, kEpiWarps = 4;
-constexpr int kCvtWarp0 = 8, kCvtWarps = 6;
+constexpr int kCvtWarp0 = 8, kCvtWarps = DCONV_FWD_WARPS_P - 8;
 
 // Persistent implicit-GEMM forward: grid = #SMs, CTA c handles tiles c, c+G, ...
 // (tile = (image, virtual-row block) x output-channel tile). Two TMEM
