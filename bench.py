@@ -551,8 +551,10 @@ def run_stack(args):
     global_batch = args.global_batch
     n = global_batch // world
     nodes = ex.resnet50_conv_stack(224)
-    e = ex.ConvStackExecutor(nodes, n, 224, d.Math.BF16, "cuda", group=pg, lr=1e-6)
     lib = _lib.lib()
+    if args.sm_budget:  # leave SMs for NCCL's kernels (persistent conv grids use the rest)
+        d.api._check(lib.dconv_set_sm_budget(args.sm_budget))
+    e = ex.ConvStackExecutor(nodes, n, 224, d.Math.BF16, "cuda", group=pg, lr=1e-6)
     # seeded synthetic images (this rank's shard) and top gradient
     x_h = torch.empty(n, 3, 224, 224, dtype=torch.float32)
     lib.dconv_fill_uniform_host(1000 * rank, -1.0, 1.0, x_h.data_ptr(), x_h.numel())
@@ -699,7 +701,7 @@ def run_stack(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded splitmix64 images 3x224x224 and top gradient; He-normal weights)",
             "config": stack_config(world),
-            "details": {"per_gpu_batch": n, "cuda_graph": graph, "math": "bf16 operands, fp32 accumulate; fp32 "
+            "details": {"per_gpu_batch": n, "cuda_graph": graph, "sm_budget": args.sm_budget or None, "math": "bf16 operands, fp32 accumulate; fp32 "
                         "master weights / gradients", "l2": "not flushed: the step's working set (activations "
                         "and gradients, GBs) is far larger than the 126 MB L2",
                         "exchange": "NCCL all-reduce of fp32 dW in backward-order buckets inside the step"
@@ -866,18 +868,184 @@ def run_layer(args):
     return 0
 
 
+# ---------------------------------------------------------------------- cfg5 (--workload cfg5)
+
+
+def cfg5_config(world):
+    return {"workload": "inception_v3_layer_mix (BASELINE configs[4]): 10 layers F+B+U, bf16, dW all-reduce",
+            "global_batch": 128, "parallelism": f"dp{world}"}
+
+
+def run_cfg5(args):
+    """BASELINE configs[4] as a data-parallel step: every layer of the Inception-v3 mix
+    forward, then backward-data || weight update, at 128 / world images per rank; the
+    fp32 dW of all layers live in one flat buffer, all-reduced with NCCL at the end of
+    the step (the COPY_REDUCE exchange); the step is one CUDA graph."""
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as orc
+
+        threads = os.cpu_count() or 1
+        builds = _ref_builds()
+        n_img, tot = 2, 0.0
+        for (C_, K, H, W, R, S, st, ph, pw) in CFG5:
+            sp = orc.spec(n_img, C_, K, H, W, R, S, st, ph, pw, 16)
+            P, Q = orc.output_shape(sp)
+            x = orc.uniform(0, (n_img, C_, H, W))
+            wt = orc.he_normal(1, (K, C_, R, S), C_ * R * S)
+            g = orc.uniform(2, (n_img, K, P, Q))
+            for pss, (a, b) in enumerate(((x, wt), (g, wt), (x, g))):
+                tot += _ref_pass_best(orc, sp, pss, threads, 3, a, b, builds, {})[0]
+        value = n_img / tot
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "images/s",
+                          "n_gpus": world, "steps": 1, "warmup": 1, "ms_per_step": round(128 / value * 1e3, 1),
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                          "data": "synthetic (seeded splitmix64)", "config": cfg5_config(world),
+                          "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads,
+                                           "kind": "reference", "sample": "2 images through the 10 layers, F+B+U, "
+                                           "best of 3 per pass, faster build per pass"},
+                          "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+    import torch
+
+    import paper_1808_05567_b200 as d
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    n = 128 // world
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    side = torch.cuda.Stream(dev)
+    layers, sizes = [], []
+    gen = torch.Generator(device="cpu").manual_seed(7 + rank)
+    for (C_, K, H, W, R, S, st, ph, pw) in CFG5:
+        spec = d.make_layer_spec(n, C_, K, H, W, R, S, st, ph, pw, 16)
+        P, Q = d.derive_output_shape(spec)
+        ib = d.to_blocked_activation((torch.rand(n, C_, H, W, generator=gen) * 2 - 1).to(dev), 16, 0, 0,
+                                     dtype=torch.bfloat16)
+        wb = d.to_blocked_weight((torch.randn(K, C_, R, S, generator=gen) * (2.0 / (C_ * R * S)) ** 0.5).to(dev), spec)
+        gb = d.to_blocked_activation((torch.rand(n, K, P, Q, generator=gen) * 2 - 1).to(dev), 16, 0, 0,
+                                     dtype=torch.bfloat16)
+        layers.append(dict(spec=spec, ib=ib, wb=wb, gb=gb,
+                           out=d.BlockedActivation(n, K, P, Q, 16, 0, 0, torch.bfloat16, dev),
+                           gi=d.BlockedActivation(n, C_, H, W, 16, 0, 0, torch.bfloat16, dev),
+                           fp=d.make_forward_plan(spec, 1, None, None, d.Math.BF16),
+                           bp=d.prepare_backward(spec, wb, 1, None, d.Math.BF16),
+                           up=d.UpdatePlan(spec, None, d.Math.BF16)))
+        sizes.append(wb.data.numel())
+    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
+    off = 0
+    for L, sz in zip(layers, sizes):
+        L["dw"] = d.BlockedWeight(L["spec"].K, L["spec"].C, L["spec"].R, L["spec"].S, 16, torch.float32, dev,
+                                  data=flat[off:off + sz])
+        off += sz
+    ev = [torch.cuda.Event() for _ in layers]
+
+    def step():
+        for i, L in enumerate(layers):
+            L["fp"].execute(L["ib"], L["wb"], L["out"])
+            ev[i].record(stream)
+            side.wait_event(ev[i])
+            with torch.cuda.stream(side):
+                L["up"].execute(L["ib"], L["gb"], L["dw"])
+            L["bp"].execute(L["wb"], L["gb"], L["gi"])
+        stream.wait_stream(side)
+        if pg is not None:
+            pg.all_reduce(flat)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+    launches = sum(L["fp"].launches() + L["bp"].launches() + L["up"].launches(L["ib"], L["gb"]) for L in layers)
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if pg is not None:
+        pg.all_reduce(ms, op=pg.ReduceOp.MAX)
+    ms = float(ms.item())
+    # end to end: every layer's input activations and output gradients copied H2D
+    # (pinned) each step, the flat dW read back
+    host_in = [(L["ib"].data.cpu().pin_memory(), L["gb"].data.cpu().pin_memory()) for L in layers]
+    dw_host = torch.empty_like(flat, device="cpu").pin_memory()
+    h2d = sum(a.numel() * 2 + b.numel() * 2 for a, b in host_in)
+
+    def e2e_step():
+        for L, (a, b) in zip(layers, host_in):
+            L["ib"].data.copy_(a, non_blocking=True)
+            L["gb"].data.copy_(b, non_blocking=True)
+        run()
+        dw_host.copy_(flat, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if pg is not None:
+        pg.all_reduce(e2e, op=pg.ReduceOp.MAX)
+    e2e = float(e2e.item())
+    hbm, peak, _, src = measured_peaks()
+    fl = sum(3 * pass_flops(dict(N=128, C=c, K=k, H=h, W=w, R=r, S=s_, stride=st, pad_h=ph, pad_w=pw))
+             for (c, k, h, w, r, s_, st, ph, pw) in CFG5)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(128 / (ms * 1e-3), 1), "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform / He-normal)",
+            "config": cfg5_config(world),
+            "details": {"per_gpu_batch": n, "cuda_graph": graph is not None, "step_tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+                        "step_frac_of_burst_bf16": round(fl / (ms * 1e-3) / 1e12 / peak, 4),
+                        "l2": "not flushed (the step's 10 layers move ~1.3 GB)"},
+            "e2e": {"value": round(128 / (e2e * 1e-3), 1), "unit": "images/s", "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": flat.numel() * 4 * world, "ms_per_step": round(e2e, 4)},
+            "gpu_launches": launches * args.steps, "clocks": sampler.report()}), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "layer"])
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "layer", "cfg5"])
     ap.add_argument("--global-batch", type=int, default=256)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the captured CUDA graph")
     ap.add_argument("--no-layers", action="store_true", help="skip the per-layer / cfg2 / cfg5 sub-objects")
     ap.add_argument("--chunk", type=int, default=8, help="images per host-step chunk (layer e2e); 0 = N/4")
+    ap.add_argument("--sm-budget", type=int, default=0, help="cap the persistent conv kernels at this many SMs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -885,6 +1053,8 @@ def main():
         return relaunch(args)
     if args.workload == "layer":
         return run_layer(args)
+    if args.workload == "cfg5":
+        return run_cfg5(args)
     return run_stack(args)
 
 
