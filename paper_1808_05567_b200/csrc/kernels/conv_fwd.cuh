@@ -20,8 +20,8 @@
 // Weights are pre-laid-out bf16 pieces (layout.cuh weight_prep_kernel), one
 // TMA box per piece per stage.
 //
-// Warp roles (448 threads): w0 activation TMA producer, w1 MMA issuer (+TMEM
-// owner), w2 weight producer (fp32 path), w4..w7 epilogue, w8..w13 converters
+// Warp roles (384 threads): w0 activation TMA producer, w1 MMA issuer (+TMEM
+// owner), w2 weight producer (fp32 path), w4..w7 epilogue, w8..w11 converters
 // (fp32 activations only). Persistent over tiles with double-buffered TMEM.
 //
 // Numerics: pieces = 1 is bf16 x bf16 -> fp32 (TMEM). pieces = 3 splits every
