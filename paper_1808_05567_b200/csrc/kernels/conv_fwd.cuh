@@ -551,8 +551,13 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       const uint32_t a_lo0 = static_cast<uint32_t>(make_smem_desc_sw32(smem0));
       const uint32_t b_lo0 = static_cast<uint32_t>(make_smem_desc(smem0 + L.w_off, 128, 256));
       const uint32_t pc_u = L.pc_slot >> 4, w_u = L.w_slot >> 4, b_tap = w_tap >> 4;
-      auto run = [&](auto mb_c) {
-        constexpr int MB = decltype(mb_c)::value;
+      // KC / NTAPS > 0: compile-time channel blocks per stage and taps (every MMA of a full
+      // stage is straight-line code whose operands are kernel parameters plus the stage's
+      // slot bases). Measured (tools/probe_bisect.cu): the runtime-trip-count loop issued a
+      // 128x128x16 MMA every ~144 cycles, the unrolled one every ~80 (floor 64), the rest
+      // being the stage's barrier waits; partial stages (kc_eff < KC) take the runtime loop.
+      auto run = [&](auto mb_c, auto kc_c, auto nt_c) {
+        constexpr int MB = decltype(mb_c)::value, KC = decltype(kc_c)::value, NTAPS = decltype(nt_c)::value;
         uint32_t tl = 0, g = 0;
         RingPos pcp, wpp;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
@@ -567,24 +572,41 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           const uint32_t d_base = tmem_base + acc * acc_cols;
           for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages), ++g) {
             long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
-            mbar_wait(&pc_full[pcp.idx], pcp.ph);
+            const bool no_wait = kDevBuild && (dbg_mode & 2048);  // ablation: MMAs do not wait for operands
+            if (!no_wait) mbar_wait(&pc_full[pcp.idx], pcp.ph);
             if (trace) trace[0] = clock64() - t_start;
-            if (!p.w_all || tl == 0) mbar_wait(&w_full[wpp.idx], wpp.ph);
+            if ((!p.w_all || tl == 0) && !no_wait) mbar_wait(&w_full[wpp.idx], wpp.ph);
             if (trace) trace[1] = clock64() - t_start;
             tc_fence_after();
             const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
-            for (int kk = 0; kk < kc_eff; ++kk) {
-              const uint32_t ak = a_lo0 + static_cast<uint32_t>(pcp.idx) * pc_u +
-                                  2u * static_cast<uint32_t>(kk * p.a_px) + v_off2;
-              const uint32_t bk = b_lo0 + static_cast<uint32_t>(wpp.idx) * w_u + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
-              const bool first_k = it == 0 && kk == 0;
+            const uint32_t a_st = a_lo0 + static_cast<uint32_t>(pcp.idx) * pc_u + v_off2;
+            const uint32_t b_st = b_lo0 + static_cast<uint32_t>(wpp.idx) * w_u;
+            if (KC > 0 && kc_eff == KC) {
+              const uint32_t acc0 = it == 0 ? 0u : 1u;
 #pragma unroll
-              for (int tp = 0; tp < kFastTaps; ++tp) {
-                if (tp >= nt) break;
+              for (int kk = 0; kk < (KC > 0 ? KC : 1); ++kk) {
+                const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
+                const uint32_t bk = b_st + static_cast<uint32_t>(kk * NTAPS) * b_tap;
 #pragma unroll
-                for (int mb = 0; mb < MB; ++mb)
-                  mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
-                              bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
+                for (int tp = 0; tp < NTAPS; ++tp)
+#pragma unroll
+                  for (int mb = 0; mb < MB; ++mb)
+                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                                bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (kk == 0 && tp == 0) ? acc0 : 1u);
+              }
+            } else {
+              for (int kk = 0; kk < kc_eff; ++kk) {
+                const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
+                const uint32_t bk = b_st + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
+                const bool first_k = it == 0 && kk == 0;
+#pragma unroll
+                for (int tp = 0; tp < kFastTaps; ++tp) {
+                  if (tp >= nt) break;
+#pragma unroll
+                  for (int mb = 0; mb < MB; ++mb)
+                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                                bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
+                }
               }
             }
             if (trace) trace[3] = clock64() - t_start;
@@ -595,12 +617,37 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           mma_commit(&acc_full[acc]);
         }
       };
-      if (p.mb == 1)
-        run(std::integral_constant<int, 1>{});
-      else if (p.mb == 2)
-        run(std::integral_constant<int, 2>{});
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I4 = std::integral_constant<int, 4>;
+      using I9 = std::integral_constant<int, 9>;
+      using I16 = std::integral_constant<int, 16>;
+      // the ResNet-50 / Inception shapes: 1x1 (four channel blocks per stage), 3x3 and 4x4
+      // (one block per stage); anything else runs the runtime-trip-count loop
+      auto by_mb = [&](auto kc_c, auto nt_c) {
+        if (p.mb == 1)
+          run(I1{}, kc_c, nt_c);
+        else if (p.mb == 2)
+          run(I2{}, kc_c, nt_c);
+        else
+          run(I4{}, kc_c, nt_c);
+      };
+      using I8 = std::integral_constant<int, 8>;
+      if (nt == 1 && p.kc == 8)
+        by_mb(I8{}, I1{});
+      else if (nt == 1 && p.kc == 4)
+        by_mb(I4{}, I1{});
+      else if (nt == 9 && p.kc == 2)
+        by_mb(I2{}, I9{});
+      else if (nt == 1 && p.kc == 2)
+        by_mb(I2{}, I1{});
+      else if (nt == 9 && p.kc == 1)
+        by_mb(I1{}, I9{});
+      else if (nt == 16 && p.kc == 1)
+        by_mb(I1{}, I16{});
       else
-        run(std::integral_constant<int, 4>{});
+        by_mb(I0{}, I1{});
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -769,6 +816,22 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     if (dbg && lane == 0) {
       dbg[4] = c_a;
       dbg[5] = c_b;
+    }
+  } else if (kDevBuild && !RAW_F32 && !TS && (dbg_mode & 1024) && warp >= kEpiWarp0) {
+    // ablation (developer builds): the epilogue does no work, it only hands the
+    // accumulators back (warps 4..7 arrive for every epilogue group)
+    if (warp < kEpiWarp0 + 4) {
+      uint32_t tl = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+        const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+        const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+        mbar_wait(&acc_full[acc], apar);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          for (int g = 0; g < n_epi_groups; ++g) mbar_arrive(&acc_empty[acc]);
+      }
     }
   } else if (p.tma_store && ((warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) ||
                              (epi2 && warp >= kCvtWarp0 && warp < kEpiWarp0 + 4 * n_epi_groups) ||

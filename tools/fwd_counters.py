@@ -13,15 +13,22 @@ lib = _lib.lib()
 lib.dconv_debug_counters.argtypes = [C.c_void_p]
 lib.dconv_debug_mode(int(os.environ.get("DBG_MODE", "0")))
 math = d.Math.BF16 if (len(sys.argv) > 1 and sys.argv[1] == "bf16") else d.Math.F32
-spec = d.make_layer_spec(32, 256, 64, 56, 56, 1, 1, 1, 0, 0, 16)
-x = torch.rand(32, 256, 56, 56, device="cuda") * 2 - 1
-w = torch.randn(64, 256, 1, 1, device="cuda") * 0.088
-g = torch.rand(32, 64, 56, 56, device="cuda") * 2 - 1
+Nn, Cc, Kk, Hh, Rr = (int(v) for v in os.environ.get("LAYER", "32,256,64,56,1").split(","))
+pad = (Rr - 1) // 2
+spec = d.make_layer_spec(Nn, Cc, Kk, Hh, Hh, Rr, Rr, 1, pad, pad, 16)
+x = torch.rand(Nn, Cc, Hh, Hh, device="cuda") * 2 - 1
+w = torch.randn(Kk, Cc, Rr, Rr, device="cuda") * 0.088
+g = torch.rand(Nn, Kk, Hh, Hh, device="cuda") * 2 - 1
 ib, wb, gb = d.to_blocked_activation(x, spec), d.to_blocked_weight(w, spec), d.to_blocked_activation(g, 16, 0, 0)
+if math == d.Math.BF16:
+    ib = d.BlockedActivation(Nn, Cc, Hh, Hh, 16, 0, 0, torch.bfloat16)
+    ib.data.uniform_(-1, 1)
+    gb = d.BlockedActivation(Nn, Kk, Hh, Hh, 16, 0, 0, torch.bfloat16)
+    gb.data.uniform_(-1, 1)
 fp = d.make_forward_plan(spec, 1, None, None, math)
 bc = d.prepare_backward(spec, wb, 1, None, math)
-out = d.BlockedActivation(32, 64, 56, 56, 16, 0, 0)
-gi = d.BlockedActivation(32, 256, 56, 56, 16, 0, 0)
+out = d.BlockedActivation(Nn, Kk, Hh, Hh, 16, 0, 0, *( [torch.bfloat16] if math == d.Math.BF16 else []))
+gi = d.BlockedActivation(Nn, Cc, Hh, Hh, 16, 0, 0, *( [torch.bfloat16] if math == d.Math.BF16 else []))
 buf = torch.zeros(148 * 16 + 8 * 256 + 2 * 148 + 5 * 148, dtype=torch.int64, device="cuda")
 names = ["prod_wait", "cvt_wait_raw", "cvt_wait_slot", "cvt_busy", "mma_wait_ops", "mma_wait_acc", "epi_wait",
          "epi_busy", "total"]

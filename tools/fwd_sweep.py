@@ -70,6 +70,11 @@ for (C, K, H, R) in LAYERS:
                 out.append(f"U {t:7.1f} us {fl / t / 1e6:6.0f} TF")
             if "u" in PASSES and os.environ.get("SHOWU"):
                 print("   upd plan", up.blocking)
+            if os.environ.get("FULL"):
+                if "f" in PASSES:
+                    print("   fwd plan", fp.blocking)
+                if "b" in PASSES:
+                    print("   bwd plan", bc.blocking)
             blk = fp.blocking if "f" in PASSES else {}
             print(f"C{C} K{K} H{H} R{R} [{sw or 'default'}] " + " | ".join(out) +
                   f"  wst={blk.get('w_stages')} pcst={blk.get('pc_stages')} mb={blk.get('mb')} nb={blk.get('nb')}",

@@ -1,0 +1,171 @@
+// Bisect probe: the same 1x1-conv MMA stage (mb 2, kc 4, 2-slot ring of operand bases)
+// issued from kernels that differ in ONE structural detail each, to find what
+// halves the tcgen05 issue rate in the conv kernels' MMA warp.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o probe_bisect probe_bisect.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "../paper_1808_05567_b200/csrc/kernels/sm100_ptx.cuh"
+
+using namespace dconv_sm100;
+
+struct P {
+  int N, iters, ring;
+};
+
+// V: 0 baseline (thread 0 of warp 0 issues, others at bar.sync)
+//    1 lane 0 issues inside `if (warp == 0) { if (lane == 0) ... __syncwarp(); }`
+//    2 baseline + runtime never-taken mbarrier wait / commit per stage (p.ring == 0)
+//    3 baseline + the stage loop bound read from the parameter struct each stage
+//    4 baseline with the stage's descriptors built from runtime parameters
+template <int V>
+__global__ void __launch_bounds__(256, 1) kern(P p, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar, full[2], empty[2];
+  __shared__ uint32_t tbase_sh;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0x3f803f80u, 0);
+  if (warp == 0) tmem_alloc(&tbase_sh, 512);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tbase_sh;
+  const uint32_t s0 = smem_u32(smem);
+  const uint32_t a0 = s0, b0 = s0 + 65536;
+  const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(p.N));
+  const uint32_t ahi = static_cast<uint32_t>(make_smem_desc_sw32(a0) >> 32);
+  const uint32_t bhi = static_cast<uint32_t>(make_smem_desc(b0, 128, 256) >> 32);
+  auto body = [&]() {
+    const long long t0 = clock64();
+    for (int it = 0; it < (V == 3 ? p.iters : 8192); it += 8) {
+      const uint32_t slot = static_cast<uint32_t>(it >> 3) & 1u;
+      if (V == 2 && p.ring) mbar_wait(&full[slot], 0);
+      const uint32_t a_st = static_cast<uint32_t>(make_smem_desc_sw32(a0 + slot * 32768u));
+      const uint32_t b_st = static_cast<uint32_t>(make_smem_desc(b0 + slot * 16384u, 128, 256));
+      const uint32_t a_px2 = V == 4 ? 2u * static_cast<uint32_t>(p.iters >> 5) : 512u;  // 256 rows
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        mma_bf16_lo(tbase + static_cast<uint32_t>(i & 1) * 128u,
+                    a_st + static_cast<uint32_t>(i >> 1) * a_px2 + static_cast<uint32_t>(i & 1) * 256u, ahi,
+                    b_st + static_cast<uint32_t>(i >> 1) * 256u, bhi, idesc, 1u);
+      if (V == 2 && p.ring) mma_commit(&empty[slot]);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    return clock64() - t0;
+  };
+  // V5 / V6: the conv_fwd fast path's per-stage shape: wait operand + weight barriers (already
+  // complete: parity 1 of a fresh barrier), kc x nt x mb MMAs, two commits. V5 runtime trip
+  // counts (the production loop), V6 compile-time (KC 4, NT 1, MB 2).
+  auto body_conv = [&]() {
+    __shared__ int s_tap[16];
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 16; ++i) s_tap[i] = i;
+    const int kc = p.ring ? 1 : 4, nt = p.ring ? 9 : 1, a_px = 256;
+    uint32_t sh[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sh[i] = i < nt ? 2u * static_cast<uint32_t>(s_tap[i]) : 0u;
+    const uint32_t a_lo0 = static_cast<uint32_t>(make_smem_desc_sw32(a0));
+    const uint32_t b_lo0 = static_cast<uint32_t>(make_smem_desc(b0, 128, 256));
+    const uint32_t w_tap = (static_cast<uint32_t>(p.N) / 8u) * 256u, b_tap = w_tap >> 4;
+    const long long t0 = clock64();
+    int slot = 0;
+    for (int it = 0; it < 8192 / (kc * nt * 2); ++it) {
+      if (V != 7) {
+        mbar_wait(&full[slot], 1);
+        if (V != 9) mbar_wait(&full[slot ^ 1], 1);
+        tc_fence_after();
+      }
+      const uint32_t ak0 = a_lo0 + static_cast<uint32_t>(slot) * 2048u;
+      const uint32_t bk0 = b_lo0 + static_cast<uint32_t>(slot) * 1024u;
+      if (V == 5) {
+        for (int kk = 0; kk < kc; ++kk) {
+          const uint32_t ak = ak0 + 2u * static_cast<uint32_t>(kk * a_px);
+          const uint32_t bk = bk0 + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
+          const bool first_k = it == 0 && kk == 0;
+#pragma unroll
+          for (int tp = 0; tp < 16; ++tp) {
+            if (tp >= nt) break;
+#pragma unroll
+            for (int mb = 0; mb < 2; ++mb)
+              mma_bf16_lo(tbase + static_cast<uint32_t>(mb * p.N), ak + sh[tp] + 256u * mb, ahi,
+                          bk + static_cast<uint32_t>(tp) * b_tap, bhi, idesc, (first_k && tp == 0) ? 0u : 1u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ak = ak0 + 2u * static_cast<uint32_t>(kk * a_px);
+          const uint32_t bk = bk0 + static_cast<uint32_t>(kk) * b_tap;
+#pragma unroll
+          for (int mb = 0; mb < 2; ++mb)
+            mma_bf16_lo(tbase + static_cast<uint32_t>(mb * p.N), ak + 256u * mb, ahi, bk, bhi, idesc,
+                        (it == 0 && kk == 0) ? 0u : 1u);
+        }
+      }
+      if (V != 8) {
+        mma_commit(&empty[slot]);
+        if (V != 9) mma_commit(&empty[slot ^ 1]);
+      }
+      slot ^= 1;
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    return clock64() - t0;
+  };
+  long long t = 0;
+  if (V >= 5) {
+    if (warp == 0) {
+      if (lane == 0) t = body_conv();
+      __syncwarp();
+    }
+  } else if (V == 1) {
+    if (warp == 0) {
+      if (lane == 0) t = body();
+      __syncwarp();
+    }
+  } else if (warp == 0 && threadIdx.x == 0) {
+    t = body();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+template <int V>
+void run(int threads, int N, long long* d, int ring = 0) {
+  cudaFuncSetAttribute(kern<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  P p{N, 8192, ring};
+  kern<V><<<148, threads, 160 * 1024>>>(p, d);
+  cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+  printf("variant %d threads %d N %d ring %d: %.1f cyc/MMA\n", V, threads, N, ring, static_cast<double>(mx) / 8192);
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 148 * sizeof(long long));
+  for (int N : {128}) {
+    run<6>(128, N, d);
+    run<7>(128, N, d);
+    run<8>(128, N, d);
+    run<9>(128, N, d);
+  }
+  return 0;
+}
