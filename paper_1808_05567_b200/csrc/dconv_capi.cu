@@ -452,7 +452,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
           int kcx = (taps.r.size() == 1) ? std::min(env_int("DCONV_FWD_KC", 4), pb.cb_red)
-                                         : std::min(env_int("DCONV_FWD_KC", 1), pb.cb_red);
+                                         : std::min(env_int("DCONV_FWD_KC", 2), pb.cb_red);
           // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
           const int stg_res = (taps.r.size() == 1 || DCONV_ENV("DCONV_STG_RES")) ? 3 * 16384 : 0;
           pcs = 0;
@@ -2184,6 +2184,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     // MMA warp's schedulers), although a bare cp.async stream reaches ~45-60 B/clk/SM
     // (tools/probe_cpasync.cu) against the TMA's ~27 B/clk/SM for 32 B rows.
     p.lsu = (p.sw32 && p.mc == 1 && L.stages > kUpdLsuDepth && DCONV_ENV("DCONV_UPD_LSU")) ? 1 : 0;
+    // linear plans over planes of 4k pixels, 32-pixel stages: 128 B rows (see UpdParams::sw32)
+    if (p.sw32 && !p.lsu && p.linear && p.stack == 1 && p.vs % 32 == 0 && (in.h * in.w) % 4 == 0 &&
+        (dout.h * dout.w) % 4 == 0 && !DCONV_ENV("DCONV_UPD_NO_SW128"))
+      p.sw32 = 2;
   }
   if (!encode_maps) return L;
   encode_upd_maps(L, pl, in, dout, in_pieces, do_pieces);
@@ -2206,6 +2210,14 @@ void encode_upd_maps(UpdLaunch& L, const dconv_upd_plan& pl, const dconv_act_t& 
     const uint64_t planes = static_cast<uint64_t>(is_in ? pieces : pieces) * a.n * chans_blocks;
     if (p.sw32) {  // bf16 tensors in place: 32 B pixel rows, SWIZZLE_32B (MN-major SW32 operands)
       const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_32B;
+      if (linear && p.sw32 == 2) {  // 128 B rows of four pixels, SWIZZLE_128B
+        const uint64_t dims[3] = {64, static_cast<uint64_t>(a.h) * a.w / 4, planes};
+        const uint64_t strides[2] = {128, static_cast<uint64_t>(a.h) * a.w * 32};
+        const uint32_t box[3] = {64, static_cast<uint32_t>(p.vs / 4),
+                                 static_cast<uint32_t>(is_in ? p.cb_eff * p.mc : p.nb)};
+        return encode(1, 3, data, dims, strides, box, nullptr, is_in ? "upd input linear sw128" : "upd dO linear sw128",
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+      }
       if (linear) {
         const uint64_t dims[3] = {16, static_cast<uint64_t>(a.h) * a.w, planes};
         const uint64_t strides[2] = {32, static_cast<uint64_t>(a.h) * a.w * 32};

@@ -640,6 +640,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         by_mb(I4{}, I1{});
       else if (nt == 9 && p.kc == 2)
         by_mb(I2{}, I9{});
+      else if (nt == 3 && p.kc == 2)
+        by_mb(I2{}, std::integral_constant<int, 3>{});
+      else if (nt == 7 && p.kc == 2)
+        by_mb(I2{}, std::integral_constant<int, 7>{});
+      else if (nt == 7 && p.kc == 1)
+        by_mb(I1{}, std::integral_constant<int, 7>{});
       else if (nt == 1 && p.kc == 2)
         by_mb(I2{}, I1{});
       else if (nt == 9 && p.kc == 1)

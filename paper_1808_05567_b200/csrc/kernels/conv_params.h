@@ -111,7 +111,14 @@ struct UpdParams {
   int stack;               // 1 = shared-tile mode (taps via descriptor shifts)
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
-  int sw32;                // bf16 operands staged as SWIZZLE_32B 32 B pixel rows (MN-major SW32 descriptors)
+  // bf16 operands read through MN-major SWIZZLE_32B descriptors. 1: staged as SWIZZLE_32B
+  // 32 B pixel rows; 2 (linear single-tap plans, planes of 4k pixels): staged as
+  // SWIZZLE_128B 128 B rows of four pixels -- the TMA unit moves ~1 box row per clock
+  // whatever its width, so this stages 2.5x the bytes per clock. Read back through the
+  // SW32 descriptors the rows come out with their halves intact and the pixels of each
+  // 32-pixel group permuted (q -> q ^ ((q >> 3) & 3)); both operands of the K = pixel
+  // reduction carry the same permutation, so every MMA sums the same products.
+  int sw32;
   int mc;                  // single-tap sw32 plans: 128-channel c-tiles per CTA (2: the dO tile is staged once for both)
   // lsu = 1: the operand rows are staged by cp.async from loader warps (the TMA
   // unit moves 32 B rows at ~27 B/clk/SM; 16 B cp.async from six warps ~2x that)

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                             p.in_row0 + p.phase_row[tph] + p.stride * (band * p.rows_ps + p.tap_r2[tp]), pa);
               }
             } else if (p.linear) {
-              tma_load_3d(a_dst, &map_in, &full_bar[s], 0, band * p.vs, pa);
+              tma_load_3d(a_dst, &map_in, &full_bar[s], 0, p.sw32 == 2 ? band * (p.vs / 4) : band * p.vs, pa);
             } else {
               tma_load_4d(a_dst, &map_in, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
                           p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], pa);
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint8_t* b_dst = st + L.b_off + pc * L.b_piece;
           if (p.sw32) {
             if (p.linear)
-              tma_load_3d(b_dst, &map_do, &full_bar[s], 0, band * p.vs, pb);
+              tma_load_3d(b_dst, &map_do, &full_bar[s], 0, p.sw32 == 2 ? band * (p.vs / 4) : band * p.vs, pb);
             else
               tma_load_4d(b_dst, &map_do, &full_bar[s], 0, 0, band * p.rows_ps, pb);
           } else if (p.linear)
@@ -301,23 +301,62 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t a_hi = static_cast<uint32_t>(a_d >> 32), b_hi = static_cast<uint32_t>(b_d >> 32);
       const uint32_t a_lo0 = static_cast<uint32_t>(a_d), b_lo0 = static_cast<uint32_t>(b_d);
       const uint32_t slot_u = L.bytes >> 4;
-      RingPos rp;
-      for (int it = 0; it < iters; ++it, rp.adv(n_stages)) {
-        mbar_wait(&full_bar[rp.idx], rp.ph);
-        tc_fence_after();
-        const uint32_t a_s = a_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
-        const uint32_t b_s = b_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
-        for (int ks = 0; ks < ksteps; ++ks) {
+      // KS / NACC > 0: compile-time k-steps per stage and accumulators (straight-line MMAs
+      // whose operands are the stage's slot bases plus launch constants; see the forward
+      // issuer in conv_fwd.cuh), 0: runtime trip counts
+      auto run = [&](auto ks_c, auto na_c) {
+        constexpr int KS = decltype(ks_c)::value, NACC = decltype(na_c)::value;
+        RingPos rp;
+        for (int it = 0; it < iters; ++it, rp.adv(n_stages)) {
+          mbar_wait(&full_bar[rp.idx], rp.ph);
+          tc_fence_after();
+          const uint32_t a_s = a_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
+          const uint32_t b_s = b_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
+          if (KS > 0) {
+            const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
-          for (int t = 0; t < kFastTaps; ++t) {
-            if (t >= n_acc) break;
-            mma_bf16_lo(tmem_base + static_cast<uint32_t>(t * NT), a_s + 32u * ks + sh[t], a_hi, b_s + 32u * ks, b_hi,
-                        idesc, (it > 0 || ks > 0) ? 1u : 0u);
+            for (int ks = 0; ks < (KS > 0 ? KS : 1); ++ks)
+#pragma unroll
+              for (int t = 0; t < NACC; ++t)
+                mma_bf16_lo(tmem_base + static_cast<uint32_t>(t * NT), a_s + 32u * ks + sh[t], a_hi, b_s + 32u * ks,
+                            b_hi, idesc, ks > 0 ? 1u : acc0);
+          } else {
+            for (int ks = 0; ks < ksteps; ++ks) {
+#pragma unroll
+              for (int t = 0; t < kFastTaps; ++t) {
+                if (t >= n_acc) break;
+                mma_bf16_lo(tmem_base + static_cast<uint32_t>(t * NT), a_s + 32u * ks + sh[t], a_hi, b_s + 32u * ks,
+                            b_hi, idesc, (it > 0 || ks > 0) ? 1u : 0u);
+              }
+            }
           }
+          mma_commit(&empty_bar[rp.idx]);
         }
-        mma_commit(&empty_bar[rp.idx]);
-      }
-      if (iters > 0) mma_commit(&acc_full[0]);
+        if (iters > 0) mma_commit(&acc_full[0]);
+      };
+      using I0 = std::integral_constant<int, 0>;
+      auto by_acc = [&](auto ks_c) {
+        if (n_acc == 1)
+          run(ks_c, std::integral_constant<int, 1>{});
+        else if (n_acc == 2)
+          run(ks_c, std::integral_constant<int, 2>{});
+        else if (n_acc == 3)
+          run(ks_c, std::integral_constant<int, 3>{});
+        else if (n_acc == 4)
+          run(ks_c, std::integral_constant<int, 4>{});
+        else
+          run(I0{}, std::integral_constant<int, 1>{});
+      };
+      if (ksteps == 2)
+        by_acc(std::integral_constant<int, 2>{});
+      else if (ksteps == 4)
+        by_acc(std::integral_constant<int, 4>{});
+      else if (ksteps == 8)
+        by_acc(std::integral_constant<int, 8>{});
+      else if (ksteps == 9)
+        by_acc(std::integral_constant<int, 9>{});
+      else
+        run(I0{}, std::integral_constant<int, 1>{});
     }
     __syncwarp();
   } else if (warp == 1) {
