@@ -540,7 +540,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     // the next there are only the commits and the two barrier waits (the tensor
     // pipe's queue is short: issue blocks at the tensor rate, and whatever the
     // issuing thread does between stages is a bubble in the pipe).
-    if (lane == 0) {
+    {  // the whole warp runs the loop (warp-uniform values); one elected lane issues each stage
       const uint32_t idesc = make_idesc(1, 0, 1, 128, static_cast<uint32_t>(NT));
       const int nt = p.n_taps;
       uint32_t sh[kFastTaps];
@@ -558,30 +558,39 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       // being the stage's barrier waits; partial stages (kc_eff < KC) take the runtime loop.
       auto run = [&](auto mb_c, auto kc_c, auto nt_c) {
         constexpr int MB = decltype(mb_c)::value, KC = decltype(kc_c)::value, NTAPS = decltype(nt_c)::value;
+        // full stages first (compile-time MMA sequence), then the partial one (runtime loop)
+        const int k_full = (KC > 0 && p.n_phases == 1) ? p.cb_in / p.kc : 0;
         uint32_t tl = 0, g = 0;
-        RingPos pcp, wpp;
+        int pci = 0, wi = 0;
+        uint32_t pph = 0, wph = 0;
+        // linear and multi-image tiles start their A slot at the tile's first pixel: the
+        // MMA side needs no tile coordinates (no divisions between tiles)
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
-          int n, v0, ntile;
-          tile_coords(t, n, v0, ntile);
-          const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
-          const uint32_t v_off2 = 2u * static_cast<uint32_t>(v0 - a_px0);
+          uint32_t v_off2 = 0;
+          if (!p.linear && p.mimg == 0) {
+            int n, v0, ntile;
+            tile_coords(t, n, v0, ntile);
+            v_off2 = 2u * static_cast<uint32_t>(v0 - (v0 / p.wsub) * p.wsub);
+          }
           const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
           const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
           mbar_wait(&acc_empty[acc], apar ^ 1u);
           tc_fence_after();
           const uint32_t d_base = tmem_base + acc * acc_cols;
-          for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages), ++g) {
-            long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
+          const bool wait_w = !p.w_all || tl == 0;
+          for (int it = 0; it < k_iters; ++it, ++g) {
+            long long* trace =
+                (kDevBuild && dbg && blockIdx.x == 0 && g < 256 && lane == 0) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
             const bool no_wait = kDevBuild && (dbg_mode & 2048);  // ablation: MMAs do not wait for operands
-            if (!no_wait) mbar_wait(&pc_full[pcp.idx], pcp.ph);
+            if (!no_wait) mbar_wait(&pc_full[pci], pph);
             if (trace) trace[0] = clock64() - t_start;
-            if ((!p.w_all || tl == 0) && !no_wait) mbar_wait(&w_full[wpp.idx], wpp.ph);
+            if (wait_w && !no_wait) mbar_wait(&w_full[wi], wph);
             if (trace) trace[1] = clock64() - t_start;
             tc_fence_after();
-            const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
-            const uint32_t a_st = a_lo0 + static_cast<uint32_t>(pcp.idx) * pc_u + v_off2;
-            const uint32_t b_st = b_lo0 + static_cast<uint32_t>(wpp.idx) * w_u;
-            if (KC > 0 && kc_eff == KC) {
+            const uint32_t a_st = a_lo0 + static_cast<uint32_t>(pci) * pc_u + v_off2;
+            const uint32_t b_st = b_lo0 + static_cast<uint32_t>(wi) * w_u;
+            if (elect_one()) {
+            if (it < k_full) {
               const uint32_t acc0 = it == 0 ? 0u : 1u;
 #pragma unroll
               for (int kk = 0; kk < (KC > 0 ? KC : 1); ++kk) {
@@ -595,6 +604,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                                 bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (kk == 0 && tp == 0) ? acc0 : 1u);
               }
             } else {
+              const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
               for (int kk = 0; kk < kc_eff; ++kk) {
                 const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
                 const uint32_t bk = b_st + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
@@ -610,11 +620,20 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               }
             }
             if (trace) trace[3] = clock64() - t_start;
-            if (!p.w_all) mma_commit(&w_empty[wpp.idx]);
-            mma_commit(&pc_empty[pcp.idx]);
+            if (!p.w_all) mma_commit(&w_empty[wi]);
+            mma_commit(&pc_empty[pci]);
             if (trace) trace[2] = clock64() - t_start;
+            }
+            __syncwarp();
+            // ring positions, branch-free
+            const bool pw = ++pci == pc_stages, ww = ++wi == w_stages;
+            pci = pw ? 0 : pci;
+            pph ^= pw ? 1u : 0u;
+            wi = ww ? 0 : wi;
+            wph ^= ww ? 1u : 0u;
           }
-          mma_commit(&acc_full[acc]);
+          if (elect_one()) mma_commit(&acc_full[acc]);
+          __syncwarp();
         }
       };
       using I0 = std::integral_constant<int, 0>;
