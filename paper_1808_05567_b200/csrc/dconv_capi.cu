@@ -452,7 +452,8 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // single-tap bf16 problems carry kc channel blocks per stage (amortises the
           // per-stage barrier / commit cost over kc x mb MMAs)
           int kcx = (taps.r.size() == 1) ? std::min(env_int("DCONV_FWD_KC", 4), pb.cb_red)
-                                         : std::min(env_int("DCONV_FWD_KC", 2), pb.cb_red);
+                                         : (linear && apx > 256) ? 1  // one TMA box per block: <= 256 rows
+                                                                 : std::min(env_int("DCONV_FWD_KC", 2), pb.cb_red);
           // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
           const int stg_res = (taps.r.size() == 1 || DCONV_ENV("DCONV_STG_RES")) ? 3 * 16384 : 0;
           pcs = 0;

@@ -115,7 +115,10 @@ void check_geometry(const FwdLaunch& L, int maxshift, VReport& r) {
   const int acc_cols = ((L.pieces == 3 && p.split_acc) ? 2 : 1) * p.mb * 16 * p.nb;
   const int ring = L.ts ? L.stages * L.pieces * 8 * p.kc : 0;
   r.fail_if(p.acc_bufs * acc_cols + ring > 512, "TMEM columns > 512");
-  r.fail_if(p.kc < 1 || (p.kc > 1 && p.n_taps != 1), "multi-block stages need a single-tap problem");
+  // multi-block stages: any single-tap plan; multi-tap plans only with bf16 activations
+  // (one box of kc planes lands straight in the MMA layout)
+  r.fail_if(p.kc < 1 || (p.kc > 1 && p.n_taps != 1 && (L.raw_f32 || L.ts)),
+            "multi-block multi-tap stages need bf16 activations");
 }
 
 std::string vjson(const VReport& r, const std::string& extra) {
