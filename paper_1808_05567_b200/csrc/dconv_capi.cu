@@ -400,14 +400,30 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     }
     if (!found) L.ts = false;
   }
+  // small grids (bf16 plans of small batches: e.g. 14x14 layers at 32 images): the
+  // persistent kernel's time is one CTA's serial K loop, so when the widest tiles
+  // leave SMs idle the N tile narrows (down to 64 channels) and 256-row tiles are
+  // skipped until the tiles fill the grid
+  auto est_tiles = [&](int mb, int n_nt) {
+    const int m_t = mimg_ok ? cdiv(in.n, std::max(1, (128 * mb) / hw)) : in.n * cdiv(pb.P * p.wsub, 128 * mb);
+    return m_t * n_nt;
+  };
+  // (measured: narrower N tiles do not pay -- the N = 128 MMAs are issue-bound -- so only
+  // developer mode enables it: DCONV_SHAPE_GRID=1)
+  const bool shape_grid = !raw_f32 && !want_nb && !want_mb && DCONV_ENV("DCONV_SHAPE_GRID");
+  int n_nt0 = cdiv(kb_total, 16);
+  if (shape_grid)
+    while (est_tiles(1, n_nt0) < sm_count() && cdiv(kb_total, n_nt0 + 1) >= 4 && cdiv(kb_total, n_nt0 + 1) < cdiv(kb_total, n_nt0))
+      ++n_nt0;
   for (int tier = 0; tier < 6 && !found; ++tier) {
     const int want_pc = tier < 2 ? 3 : tier < 4 ? 2 : 1;
     const int want_bufs = (tier % 2 == 0) ? 2 : 1;
-    for (int n_nt = cdiv(kb_total, 16); !found; ++n_nt) {
+    for (int n_nt = n_nt0; !found; ++n_nt) {
       const int nb = want_nb ? want_nb : cdiv(kb_total, n_nt);
       for (int mb : {4, 2, 1}) {
         if (want_mb && mb != want_mb) continue;
         if (mb == 4 && !want_mb) continue;  // 512-row tiles: explicit override only (DCONV_FWD_MB / tile_mb)
+        if (shape_grid && mb == 2 && est_tiles(2, n_nt) < sm_count() && !mimg_ok) continue;
         // accumulators: (pieces == 3 ? 2 : 1) x mb x 16nb columns, double-buffered when they fit
         const int acc_cols = n_acc * mb * 16 * nb;
         if (acc_cols > 512) continue;
@@ -453,6 +469,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           // per-stage barrier / commit cost over kc x mb MMAs)
           int kcx = (taps.r.size() == 1) ? std::min(env_int("DCONV_FWD_KC", 4), pb.cb_red)
                                          : (linear && apx > 256) ? 1  // one TMA box per block: <= 256 rows
+                                         : (pb.cb_red % 2 != 0)  ? 1  // whole stages only (the multi-tap issuer)
                                                                  : std::min(env_int("DCONV_FWD_KC", 2), pb.cb_red);
           // multi-tap outputs are never dense (wsub > Q): no TMA-store staging to reserve
           const int stg_res = (taps.r.size() == 1 || DCONV_ENV("DCONV_STG_RES")) ? 3 * 16384 : 0;

@@ -556,8 +556,83 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       // slot bases). Measured (tools/probe_bisect.cu): the runtime-trip-count loop issued a
       // 128x128x16 MMA every ~144 cycles, the unrolled one every ~80 (floor 64), the rest
       // being the stage's barrier waits; partial stages (kc_eff < KC) take the runtime loop.
+      // single-tap stages (lane 0 only): the round-1 loop shape. The lean multi-tap loop
+      // below measured 10 % SLOWER on the epilogue-bound fused 1x1 layers (residual add,
+      // ReLU mask), so the two stay separate
+      auto run1 = [&](auto mb_c, auto kc_c, auto nt_c) {
+        constexpr int MB = decltype(mb_c)::value, KC = decltype(kc_c)::value, NTAPS = decltype(nt_c)::value;
+        uint32_t tl = 0, g = 0;
+        RingPos pcp, wpp;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+          int n, v0, ntile;
+          tile_coords(t, n, v0, ntile);
+          const int a_px0 = p.linear ? v0 : (v0 / p.wsub) * p.wsub;
+          const uint32_t v_off2 = 2u * static_cast<uint32_t>(v0 - a_px0);
+          const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
+          const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
+          mbar_wait(&acc_empty[acc], apar ^ 1u);
+          tc_fence_after();
+          const uint32_t d_base = tmem_base + acc * acc_cols;
+          for (int it = 0; it < k_iters; ++it, pcp.adv(pc_stages), wpp.adv(w_stages), ++g) {
+            long long* trace = (dbg && blockIdx.x == 0 && g < 256) ? dbg + gridDim.x * 16 + g * 8 : nullptr;
+            const bool no_wait = kDevBuild && (dbg_mode & 2048);  // ablation: MMAs do not wait for operands
+            if (!no_wait) mbar_wait(&pc_full[pcp.idx], pcp.ph);
+            if (trace) trace[0] = clock64() - t_start;
+            if ((!p.w_all || tl == 0) && !no_wait) mbar_wait(&w_full[wpp.idx], wpp.ph);
+            if (trace) trace[1] = clock64() - t_start;
+            tc_fence_after();
+            const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
+            const uint32_t a_st = a_lo0 + static_cast<uint32_t>(pcp.idx) * pc_u + v_off2;
+            const uint32_t b_st = b_lo0 + static_cast<uint32_t>(wpp.idx) * w_u;
+            if (KC > 0 && kc_eff == KC) {
+              const uint32_t acc0 = it == 0 ? 0u : 1u;
+#pragma unroll
+              for (int kk = 0; kk < (KC > 0 ? KC : 1); ++kk) {
+                const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
+                const uint32_t bk = b_st + static_cast<uint32_t>(kk * NTAPS) * b_tap;
+#pragma unroll
+                for (int tp = 0; tp < NTAPS; ++tp)
+#pragma unroll
+                  for (int mb = 0; mb < MB; ++mb)
+                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                                bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (kk == 0 && tp == 0) ? acc0 : 1u);
+              }
+            } else {
+              for (int kk = 0; kk < kc_eff; ++kk) {
+                const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
+                const uint32_t bk = b_st + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
+                const bool first_k = it == 0 && kk == 0;
+#pragma unroll
+                for (int tp = 0; tp < kFastTaps; ++tp) {
+                  if (tp >= nt) break;
+#pragma unroll
+                  for (int mb = 0; mb < MB; ++mb)
+                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                                bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
+                }
+              }
+            }
+            if (trace) trace[3] = clock64() - t_start;
+            if (!p.w_all) mma_commit(&w_empty[wpp.idx]);
+            mma_commit(&pc_empty[pcp.idx]);
+            if (trace) trace[2] = clock64() - t_start;
+          }
+          mma_commit(&acc_full[acc]);
+        }
+      };
       auto run = [&](auto mb_c, auto kc_c, auto nt_c) {
         constexpr int MB = decltype(mb_c)::value, KC = decltype(kc_c)::value, NTAPS = decltype(nt_c)::value;
+        // multi-tap stages (9+ MMAs each): the whole warp runs the loop and one elected lane
+        // issues (warp-uniform descriptor arithmetic, measured 7-13 % on the 3x3 layers);
+        // single-tap stages: lane 0 alone (the other lanes do not compete for issue slots with
+        // the epilogue warps on this SM sub-partition, measured 5-10 % on fused epilogues)
+        constexpr bool kWarp = NTAPS > 1;
+        if (!kWarp) {
+          if (lane == 0) run1(mb_c, kc_c, nt_c);
+          return;
+        }
+        const unsigned wmask = kWarp ? 0xffffffffu : 1u;
+        auto issuer = [&]() { return kWarp ? elect_one() : true; };
         // full stages first (compile-time MMA sequence), then the partial one (runtime loop)
         const int k_full = (KC > 0 && p.n_phases == 1) ? p.cb_in / p.kc : 0;
         uint32_t tl = 0, g = 0;
@@ -589,7 +664,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             tc_fence_after();
             const uint32_t a_st = a_lo0 + static_cast<uint32_t>(pci) * pc_u + v_off2;
             const uint32_t b_st = b_lo0 + static_cast<uint32_t>(wi) * w_u;
-            if (elect_one()) {
+            if (issuer()) {
             if (it < k_full) {
               const uint32_t acc0 = it == 0 ? 0u : 1u;
 #pragma unroll
@@ -600,10 +675,11 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                 for (int tp = 0; tp < NTAPS; ++tp)
 #pragma unroll
                   for (int mb = 0; mb < MB; ++mb)
-                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
+                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT),
+                                ak + 2u * static_cast<uint32_t>(p.tap_shift[tp]) + 256u * mb, a_hi,
                                 bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (kk == 0 && tp == 0) ? acc0 : 1u);
               }
-            } else {
+            } else if constexpr (!kWarp) {  // (multi-tap plans carry whole stages: host-checked)
               const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
               for (int kk = 0; kk < kc_eff; ++kk) {
                 const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
@@ -624,7 +700,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             mma_commit(&pc_empty[pci]);
             if (trace) trace[2] = clock64() - t_start;
             }
-            __syncwarp();
+            __syncwarp(wmask);
             // ring positions, branch-free
             const bool pw = ++pci == pc_stages, ww = ++wi == w_stages;
             pci = pw ? 0 : pci;
@@ -632,8 +708,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             wi = ww ? 0 : wi;
             wph ^= ww ? 1u : 0u;
           }
-          if (elect_one()) mma_commit(&acc_full[acc]);
-          __syncwarp();
+          if (issuer()) mma_commit(&acc_full[acc]);
+          __syncwarp(wmask);
         }
       };
       using I0 = std::integral_constant<int, 0>;
@@ -652,19 +728,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         else
           run(I4{}, kc_c, nt_c);
       };
-      using I8 = std::integral_constant<int, 8>;
-      if (nt == 1 && p.kc == 8)
-        by_mb(I8{}, I1{});
-      else if (nt == 1 && p.kc == 4)
+      if (nt == 1 && p.kc == 4)
         by_mb(I4{}, I1{});
       else if (nt == 9 && p.kc == 2)
         by_mb(I2{}, I9{});
-      else if (nt == 3 && p.kc == 2)
-        by_mb(I2{}, std::integral_constant<int, 3>{});
-      else if (nt == 7 && p.kc == 2)
-        by_mb(I2{}, std::integral_constant<int, 7>{});
-      else if (nt == 7 && p.kc == 1)
-        by_mb(I1{}, std::integral_constant<int, 7>{});
       else if (nt == 1 && p.kc == 2)
         by_mb(I2{}, I1{});
       else if (nt == 9 && p.kc == 1)
