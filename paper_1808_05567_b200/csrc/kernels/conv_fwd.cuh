@@ -1332,6 +1332,24 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           // two 16-column TMEM loads in flight, one wait
           const int ng = min(2, g_hi - g0);
           uint32_t r[2][16], rl[2][16];
+          // a bf16 residual OR ReLU-mask operand (one of them: the register budget) of both
+          // blocks is fetched before the TMEM loads: its HBM latency overlaps them
+          const void* pre_src = (p.add != nullptr) != (p.mask != nullptr) ? (p.add ? p.add : p.mask) : nullptr;
+          const bool pre_on = !RAW_F32 && p.out_bf16 && pre_src != nullptr;  // (bf16 kernels only: registers)
+          uint4 pre[2][2];
+          if (pre_on) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int kb = ntile * p.nb + g0 + k;
+              const bool live = k < ng && valid && kb < p.kb_out;
+              const long long off =
+                  (((static_cast<long long>(nn) * p.out_cb + kb) * p.out_hp + y) * p.out_wp + x) * 32LL;
+              const uint4 z = make_uint4(0, 0, 0, 0);
+              const uint8_t* src = reinterpret_cast<const uint8_t*>(pre_src) + off;
+              pre[k][0] = live ? *reinterpret_cast<const uint4*>(src) : z;
+              pre[k][1] = live ? *reinterpret_cast<const uint4*>(src + 16) : z;
+            }
+          }
 #pragma unroll
           for (int k = 0; k < 2; ++k)
             if (k < ng && !(dbg_mode & 2)) {
@@ -1356,7 +1374,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             const long long px_off = ((plane * p.out_hp + y) * p.out_wp + x) * 16LL * esz;
             if (p.add != nullptr) {  // residual add / gradient sum
               float a[16];
-              load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
+              if (pre_on)
+                load16(&pre[k][0], 1, a);
+              else
+                load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += a[e];
             }
@@ -1366,7 +1387,10 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             }
             if (p.mask != nullptr) {  // ReLU backward: gradient through the forward activation
               float m[16];
-              load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
+              if (pre_on)
+                load16(&pre[k][0], 1, m);
+              else
+                load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
