@@ -2690,17 +2690,16 @@ int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dco
     check_pool_pair(grad_out, grad_in);
     if (!argmax) fail(DCONV_ERR_INVALID_ARGUMENT, "maxpool: null argmax");
     const int planes = grad_in->n * cdiv(grad_in->c, 16);
-    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w);
+    const int g = grid1d(static_cast<int64_t>(planes) * ((grad_in->h + 1) / 2) * ((grad_in->w + 1) / 2));
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (grad_in->dtype == DCONV_F32)
-      maxpool_bwd_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
-                                                   (float*)grad_in->data, (const float*)mask, planes, grad_in->h,
-                                                   grad_in->w, grad_out->h, grad_out->w);
+      maxpool_bwd_quad_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
+                                                        (float*)grad_in->data, (const float*)mask, planes,
+                                                        grad_in->h, grad_in->w, grad_out->h, grad_out->w, nullptr);
     else
-      maxpool_bwd_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)grad_out->data,
-                                                           (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data,
-                                                           (const __nv_bfloat16*)mask, planes, grad_in->h,
-                                                           grad_in->w, grad_out->h, grad_out->w);
+      maxpool_bwd_quad_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>(
+          (const __nv_bfloat16*)grad_out->data, (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data,
+          (const __nv_bfloat16*)mask, planes, grad_in->h, grad_in->w, grad_out->h, grad_out->w, nullptr);
     cuda_check(cudaGetLastError(), "maxpool_bwd");
   });
 }
@@ -2790,14 +2789,15 @@ int dconv_maxpool_bwd_pooled_mask(const dconv_act_t* grad_out, const void* argma
         pooled->w != grad_out->w || pooled->dtype != grad_out->dtype)
       fail(DCONV_ERR_SHAPE_MISMATCH, "maxpool: pooled mask must match grad_out");
     const int planes = grad_in->n * cdiv(grad_in->c, 16);
-    const int g = grid1d(static_cast<int64_t>(planes) * grad_in->h * grad_in->w);
+    const int g = grid1d(static_cast<int64_t>(planes) * ((grad_in->h + 1) / 2) * ((grad_in->w + 1) / 2));
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (grad_in->dtype == DCONV_F32)
-      maxpool_bwd_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
-                                                   (float*)grad_in->data, nullptr, planes, grad_in->h, grad_in->w,
-                                                   grad_out->h, grad_out->w, (const float*)pooled->data);
+      maxpool_bwd_quad_kernel<float><<<g, 256, 0, cs>>>((const float*)grad_out->data, (const uint8_t*)argmax,
+                                                        (float*)grad_in->data, nullptr, planes, grad_in->h,
+                                                        grad_in->w, grad_out->h, grad_out->w,
+                                                        (const float*)pooled->data);
     else
-      maxpool_bwd_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>(
+      maxpool_bwd_quad_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>(
           (const __nv_bfloat16*)grad_out->data, (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data, nullptr,
           planes, grad_in->h, grad_in->w, grad_out->h, grad_out->w, (const __nv_bfloat16*)pooled->data);
     cuda_check(cudaGetLastError(), "maxpool_bwd");

@@ -535,6 +535,81 @@ __global__ void maxpool_bwd_kernel(const T* __restrict__ gout, const uint8_t* __
   }
 }
 
+// Quad form of the same backward: one thread per 2x2 input quad (2y.., 2x..), whose
+// four pixels are covered by exactly the windows (y | y+1, x | x+1). Each window's
+// argmax codes, gradient and pooled mask are read once for the quad instead of once
+// per covered pixel; every pixel sums its windows in the same (y, x) ascending order
+// as maxpool_bwd_kernel, so the result is bitwise identical.
+template <typename T>
+__global__ void maxpool_bwd_quad_kernel(const T* __restrict__ gout, const uint8_t* __restrict__ arg,
+                                        T* __restrict__ gin, const T* __restrict__ mask, int planes, int h, int w,
+                                        int p, int q, const T* __restrict__ pmask) {
+  const int qh = (h + 1) / 2, qw = (w + 1) / 2;
+  const long long total = static_cast<long long>(planes) * qh * qw;
+  DCONV_GRID_STRIDE(e, total) {
+    const int x = static_cast<int>(e % qw);
+    const long long r = e / qw;
+    const int y = static_cast<int>(r % qh);
+    const long long plane = r / qh;
+    float acc[4][16];  // pixels (2y, 2x), (2y, 2x+1), (2y+1, 2x), (2y+1, 2x+1)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int l = 0; l < 16; ++l) acc[i][l] = 0.0f;
+#pragma unroll
+    for (int wy = 0; wy < 2; ++wy)
+#pragma unroll
+      for (int wx = 0; wx < 2; ++wx) {
+        const int oy = y + wy, ox = x + wx;
+        if (oy >= p || ox >= q) continue;
+        const long long o = (plane * p + oy) * q + ox;
+        const uint4 a4 = reinterpret_cast<const uint4*>(arg)[o];
+        const uint32_t aw[4] = {a4.x, a4.y, a4.z, a4.w};
+        float g[16];
+        ld16f(gout + o * 16, g);
+        if (pmask != nullptr) {
+          float pm[16];
+          ld16f(pmask + o * 16, pm);
+#pragma unroll
+          for (int l = 0; l < 16; ++l)
+            if (!(pm[l] > 0.0f)) g[l] = 0.0f;
+        }
+        // quad pixel (py, px) sits at (dy, dx) = (2(y - oy) + 1 + py, 2(x - ox) + 1 + px) of this window
+#pragma unroll
+        for (int py = 0; py < 2; ++py)
+#pragma unroll
+          for (int px = 0; px < 2; ++px) {
+            const int dy = 2 * (y - oy) + 1 + py, dx = 2 * (x - ox) + 1 + px;
+            if (dy < 0 || dx < 0) continue;  // window (y+1, .) / (., x+1) covers only the odd row / column
+            const uint32_t code = static_cast<uint32_t>(dy * 3 + dx);
+#pragma unroll
+            for (int l = 0; l < 16; ++l)
+              if (((aw[l / 4] >> (8 * (l % 4))) & 0xFFu) == code) acc[py * 2 + px][l] += g[l];
+          }
+      }
+#pragma unroll
+    for (int py = 0; py < 2; ++py)
+#pragma unroll
+      for (int px = 0; px < 2; ++px) {
+        const int iy = 2 * y + py, ix = 2 * x + px;
+        if (iy >= h || ix >= w) continue;
+        const long long pe = (plane * h + iy) * w + ix;
+        float* a = acc[py * 2 + px];
+        if (mask != nullptr) {
+          float m[16];
+          ld16f(mask + pe * 16, m);
+#pragma unroll
+          for (int l = 0; l < 16; ++l)
+            if (!(m[l] > 0.0f)) a[l] = 0.0f;
+        }
+        float v[16];
+#pragma unroll
+        for (int l = 0; l < 16; ++l) v[l] = a[l];
+        st16f(gin + pe * 16, v);
+      }
+  }
+}
+
 // Space-to-depth of a narrow (C <= 4), halo-0, one-block input for a stride-2
 // conv: xs[n][i][j][(dy*2+dx)*C + c] = x[n][c][2i+dy-pad][2j+dx-pad] (zero
 // outside; lanes >= 4C zero). A stride-2 RxS conv over x equals a stride-1
