@@ -1921,6 +1921,28 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   const int NT = 16 * p.nb;
   const int n_ktiles = cdiv(kb, p.nb);
   const int n_ctiles = cdiv(cb, 8);
+  // cross-stacking (stride-1 bf16 stacked plans, see UpdParams::xs): xs dO copies shifted
+  // by 0..xs-1 columns along N, A slots = the input tile at rows 0..R-1 x columns
+  // 0, xs, 2xs.. Chosen by staged planes per stage over all tap groups (the TMA row
+  // rate bounds these plans): the 64-channel 3x3 takes xs = 3 (36 planes for 9 taps
+  // instead of 60), the space-to-depth stem xs = 2 (16 instead of 24)
+  int xs = 1;
+  if (stacked && bf16_ops && !p.half && st == 1 && taps.n_phases == 1 && pieces == 1 &&
+      static_cast<int>(taps.r.size()) == s.R * s.S && !DCONV_ENV("DCONV_UPD_NO_SW32") && !DCONV_ENV("DCONV_UPD_NO_XS")) {
+    long long best_planes = 0;
+    for (int x = 1; x <= 4; ++x) {
+      if (s.S % x != 0 || x * NT > 256) continue;
+      const int slots = s.R * (s.S / x);
+      if (x > 1 && slots > kMaxXsSlots) continue;
+      const int groups = cdiv(slots, p.stack);
+      const long long planes = static_cast<long long>(slots) * cb + static_cast<long long>(groups) * x * p.nb;
+      if (x == 1 || planes < best_planes) {
+        best_planes = planes;
+        xs = x;
+      }
+    }
+  }
+  const int nb_b = p.nb * xs;  // dO planes staged per stage
   // c-tiles per CTA (see the selector above); only the bf16 SW32 single-tap kernel path
   const int mc = (force_mc == 2 && bf16_ops && !stacked && taps.r.size() == 1 && cb % 16 == 0 && !p.half &&
                   !DCONV_ENV("DCONV_UPD_NO_SW32")) ? 2 : 1;
@@ -1940,7 +1962,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     if (linear && vs > 256) return;
     for (int passes : {1, 3}) {
       if (passes == 3 && pieces == 1) continue;
-      const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, p.nb, pieces, pieces, mc)
+      const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, nb_b, pieces, pieces, mc)
                                        : upd_stage_layout(a_px, vs, p.nb, 1, 3);
       const int stg = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
       if (stg >= 2) cands.push_back({wsub, rows_ps, in_rows, vs, a_px, stg, passes, lay});
@@ -1970,19 +1992,22 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   // modelled cycles of one candidate over the whole launch (bf16 in-place plans)
   auto cand_cycles = [&](const Cand& cd) -> double {
     const int tgv = std::max(1, std::min(512 / NT, taps.taps_box));
-    std::vector<int> groups;  // taps per CTA accumulator group
-    if (stacked) {
+    std::vector<int> groups;  // taps (cross-stacked: A slots) per CTA accumulator group
+    if (xs > 1) {
+      const int slots = s.R * (s.S / xs);
+      for (int t0 = 0; t0 < slots; t0 += p.stack) groups.push_back(std::min(p.stack, slots - t0));
+    } else if (stacked) {
       for (int t0 = 0; t0 < static_cast<int>(taps.r.size()); t0 += p.stack)
         groups.push_back(std::min(p.stack, static_cast<int>(taps.r.size()) - t0));
     } else {
       for (int ph = 0; ph < taps.n_phases; ++ph)
         for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += tgv) groups.push_back(std::min(tgv, taps.phase_ntaps[ph] - t0));
     }
-    const double b_bytes = 2.0 * p.nb * cd.lay.b_plane;
+    const double b_bytes = 2.0 * nb_b * cd.lay.b_plane;
     const double spi = linear ? cdiv(P * Q, cd.vs) : cdiv(P, cd.rows_ps);
     // cycles per 128 x NT x 16 MMA: tensor time NT/2, or the shared-memory reads of its
     // operands (4 KB of A + NT x 32 B of B at ~128 B/clk) when those are longer (NT < 128)
-    const double mma_unit = std::max(NT / 2.0, (4096.0 + 32.0 * NT) / 128.0);
+    const double mma_unit = std::max(xs * NT / 2.0, (4096.0 + 32.0 * xs * NT) / 128.0);
     double cyc = 0;
     for (int g : groups) {
       const double a_bytes = stacked ? static_cast<double>(g) * (p.half ? 1 : 2 * p.cb_eff) * cd.lay.a_plane
@@ -2094,7 +2119,25 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     p.tap_s2[t] = taps.s2[t];
   }
   p.n_tgroups = 0;
-  if (stacked) {
+  if (xs > 1) {
+    // cross-stacked: A slots (r, 0 / xs / 2xs ..) in groups of `stack`; N holds xs dO copies
+    p.xs = xs;
+    p.xs_S = s.S;
+    p.tg = xs;
+    int n_slots = 0;
+    for (int r = 0; r < s.R; ++r)
+      for (int sa = 0; sa < s.S; sa += xs) {
+        p.xs_slot_r[n_slots] = r;
+        p.xs_slot_s[n_slots] = sa;
+        ++n_slots;
+      }
+    for (int t0 = 0; t0 < n_slots; t0 += p.stack) {
+      p.tg_phase[p.n_tgroups] = 0;
+      p.tg_tap0[p.n_tgroups] = t0;
+      p.tg_ntaps[p.n_tgroups] = std::min(p.stack, n_slots - t0);
+      ++p.n_tgroups;
+    }
+  } else if (stacked) {
     // one accumulator per CTA holding `stack` consecutive (phase-sorted) taps
     p.tg = 1;
     for (int t0 = 0; t0 < static_cast<int>(taps.r.size()); t0 += p.stack) {

@@ -16,6 +16,7 @@ constexpr bool kDevBuild = DCONV_DEV_BUILD != 0;
 
 constexpr int kMaxTaps = 128;     // filter taps (R * S <= 128: up to 11 x 11)
 constexpr int kMaxPhases = 16;    // stride phases (stride <= 4)
+constexpr int kMaxXsSlots = 32;   // cross-stacked UPD: A slots (row / column shifted input tiles)
 constexpr int kMaxTapGroups = 128;
 
 // Implicit-GEMM forward over the "virtual row" grid: output pixel (p, q) of
@@ -109,6 +110,13 @@ struct UpdParams {
   // tap stacking (layers with < 8 input channel blocks): the 128 MMA rows hold
   // `stack` taps x cb_eff channel blocks, each slot staged by its own shifted box
   int stack;               // 1 = shared-tile mode (taps via descriptor shifts)
+  // cross-stacking (xs >= 2; stride-1 bf16 stacked plans): the N dimension also holds
+  // xs copies of the dO tile, copy j shifted by j columns (TMA box at column -j, zero
+  // fill), and A slot i is the input tile shifted by (xs_slot_r[i], xs_slot_s[i]):
+  // accumulator block (i, j) is the weight gradient of tap (r_i, s_i + j). The A
+  // slots of a tap group are xs_slot[tg_tap0 ..] (their columns are multiples of xs)
+  int xs, xs_S;            // B copies (0 / 1: off), filter width (tap = r * xs_S + s)
+  int xs_slot_r[kMaxXsSlots], xs_slot_s[kMaxXsSlots];
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)
   // bf16 operands read through MN-major SWIZZLE_32B descriptors. 1: staged as SWIZZLE_32B

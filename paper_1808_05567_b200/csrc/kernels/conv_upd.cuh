@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int mc = p.mc > 1 ? p.mc : 1;
   // accumulation periods (fp32-accurate long chains, see AccPeriods); the bf16 paths keep drain = 0
   const AccPeriods per_acc{(PA == 1 && PB == 1) ? 0 : p.drain, p.drain_bufs > 1 ? 2 : 1};
-  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb, PA, PB, mc);
+  const int xsn = p.xs > 1 ? p.xs : 1;  // dO copies along N (cross-stacked plans)
+  const UpdStage L = upd_stage_layout(p.a_px, p.vs, p.nb * xsn, PA, PB, mc);
   const uint32_t smem0 = smem_u32(smem);
 
   // CTA coordinates: x = c-tile * n_tgroups + tap group, y = k-tile, z = split
@@ -236,7 +237,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8 * mc;
           uint8_t* a_dst = st + pc * L.a_piece;
           if (p.sw32) {  // 32 B pixel rows: {16, px[, rows], planes} boxes
-            if (p.stack > 1) {
+            if (p.xs > 1) {  // cross-stacked: slot j = the input tile shifted by (r_j, s_j)
+              for (int j = 0; j < ntaps; ++j)
+                tma_load_4d(a_dst + j * 2 * p.cb_eff * L.a_plane, &map_in, &full_bar[s], 0,
+                            p.in_col0 + p.xs_slot_s[tap0 + j], p.in_row0 + band * p.rows_ps + p.xs_slot_r[tap0 + j],
+                            pa);
+            } else if (p.stack > 1) {
               for (int j = 0; j < ntaps; ++j) {
                 const int tp = tap0 + j, tph = p.tap_ph[tp];
                 tma_load_4d(a_dst + j * 2 * p.cb_eff * L.a_plane, &map_in, &full_bar[s], 0,
@@ -271,7 +277,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if (p.linear)
               tma_load_3d(b_dst, &map_do, &full_bar[s], 0, p.sw32 == 2 ? band * (p.vs / 4) : band * p.vs, pb);
             else
-              tma_load_4d(b_dst, &map_do, &full_bar[s], 0, 0, band * p.rows_ps, pb);
+              for (int j = 0; j < xsn; ++j)  // copy j shifted right by j columns (zero fill at the left edge)
+                tma_load_4d(b_dst + j * p.nb * 2 * L.b_plane, &map_do, &full_bar[s], 0, -j, band * p.rows_ps, pb);
           } else if (p.linear)
             tma_load_4d(b_dst, &map_do, &full_bar[s], 0, band * p.vs, 0, pb);
           else
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // shifts and descriptor words hoisted out of the stage loop; between stages
     // only the commit and the full-barrier wait (see conv_fwd_kernel)
     if (lane == 0) {
-      const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
+      const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT * xsn));  // (cross-stacked: xs dO copies)
       const int ksteps = p.vs / 16;
       // accumulators: one per tap of the group, or (single-tap, mc > 1) one per c-tile,
       // whose A rows are the next 8 channel-block planes (a_piece / mc bytes on)
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT));
+    const uint32_t idesc = make_idesc(1, 1, 1, 128, static_cast<uint32_t>(NT * xsn));
     const int ksteps = p.vs / 16;
     for (int it = 0; it < iters; ++it) {
       const int s = it % n_stages;
@@ -418,15 +425,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       const uint32_t acc_col0 = static_cast<uint32_t>(per_acc.buf(jd)) * buf_cols;
       const bool add_old = accumulate || jd > 0;
-    const int n_acc = p.stack > 1 ? 1 : (mc > 1 ? mc : ntaps);
+    const int n_acc = p.stack > 1 ? xsn : (mc > 1 ? mc : ntaps);
     for (int t = 0; t < n_acc; ++t) {
       const int c_glob = (ctile * mc + (mc > 1 ? t : 0)) * 128 + qrow + lane;
-      // stacked: TMEM row = (slot j, channel c) of tap tap0 + j
+      // stacked: TMEM row = (slot j, channel c) of tap tap0 + j; cross-stacked: column
+      // block t of slot j is tap (r_j, s_j + t)
       const int rows_slot = p.half ? 8 : 16 * p.cb_eff;
       const int slot = p.stack > 1 ? (qrow + lane) / rows_slot : 0;
       const int c_row = p.stack > 1 ? (qrow + lane) % rows_slot : c_glob;
       const bool row_ok = p.stack > 1 ? slot < ntaps : true;
-      const int rs = p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : (mc > 1 ? 0 : t))];
+      const int sl = tap0 + (row_ok ? slot : 0);
+      if (p.xs > 1 && p.xs_slot_s[sl] + t >= p.xs_S) continue;  // (no such tap: S not a multiple of xs)
+      const int rs = p.xs > 1 ? p.xs_slot_r[sl] * p.xs_S + p.xs_slot_s[sl] + t
+                              : p.tap_src[tap0 + (p.stack > 1 ? (row_ok ? slot : 0) : (mc > 1 ? 0 : t))];
       float* dst_row =
           p.partial + ((static_cast<long long>(split) * p.n_taps + rs) * p.c_pad + c_row) * p.k_pad + ktile * NT;
       for (int g = 0; g < p.nb; ++g) {

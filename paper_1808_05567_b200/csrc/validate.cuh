@@ -291,11 +291,22 @@ int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const 
       for (int g = sp * per; g < std::min(p.stages_total, (sp + 1) * per); ++g) ++st[g];
     for (int g = 0; g < p.stages_total; ++g)
       r.fail_if(st[g] != 1, "stage " + std::to_string(g) + " reduced " + std::to_string(st[g]) + " times");
-    // tap groups partition the taps
+    // tap groups partition the taps (cross-stacked: every (A slot, dO copy) pair is one tap)
     std::vector<uint8_t> tp(static_cast<size_t>(p.n_taps), 0);
-    for (int g = 0; g < p.n_tgroups; ++g)
-      for (int t = p.tg_tap0[g]; t < p.tg_tap0[g] + p.tg_ntaps[g]; ++t)
-        if (t >= 0 && t < p.n_taps) ++tp[t];
+    r.fail_if(p.xs > 1 && (p.xs > 4 || p.xs_S != s.S || s.stride != 1 || p.stack < 2 || p.tg != p.xs),
+              "cross-stacked plan outside the kernel's limits");
+    for (int g = 0; g < p.n_tgroups && r.err.empty(); ++g)
+      for (int t = p.tg_tap0[g]; t < p.tg_tap0[g] + p.tg_ntaps[g]; ++t) {
+        if (p.xs > 1) {
+          if (t < 0 || t >= kMaxXsSlots) continue;
+          for (int j = 0; j < p.xs; ++j) {
+            const int tr = p.xs_slot_r[t], tc = p.xs_slot_s[t] + j;
+            if (tr >= 0 && tr < s.R && tc >= 0 && tc < s.S) ++tp[tr * s.S + tc];
+          }
+        } else if (t >= 0 && t < p.n_taps) {
+          ++tp[t];
+        }
+      }
     for (int t = 0; t < p.n_taps; ++t) r.fail_if(tp[t] != 1, "tap " + std::to_string(t) + " not covered once");
     // stages cover every output pixel of every image; channel tiles cover C and K
     const int P = out_P(s), Q = out_Q(s);
