@@ -1955,9 +1955,10 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   struct Cand {
     int wsub, rows_ps, in_rows, vs, a_px, stages, passes;
     UpdStage lay;
+    int pimg;  // packed images per stage (UpdParams::pimg), 0 = row bands
   };
   std::vector<Cand> cands;
-  auto add = [&](int wsub, int rows_ps, int in_rows, int vs, int a_px) {
+  auto add = [&](int wsub, int rows_ps, int in_rows, int vs, int a_px, int pimg = 0) {
     if (!linear && (wsub * st > 256 || in_rows * st > 256 || rows_ps > 256)) return;
     if (linear && vs > 256) return;
     for (int passes : {1, 3}) {
@@ -1965,7 +1966,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       const UpdStage lay = passes == 1 ? upd_stage_layout(a_px, vs, nb_b, pieces, pieces, mc)
                                        : upd_stage_layout(a_px, vs, p.nb, 1, 3);
       const int stg = std::min<int>(kMaxStages, kSmemBudget / static_cast<int>(lay.bytes));
-      if (stg >= 2) cands.push_back({wsub, rows_ps, in_rows, vs, a_px, stg, passes, lay});
+      if (stg >= 2) cands.push_back({wsub, rows_ps, in_rows, vs, a_px, stg, passes, lay, pimg});
     }
   };
   if (linear) {
@@ -1987,6 +1988,18 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       const int in_rows = stacked ? rows_ps : rows_ps + maxshift_rows + (s2max > 0 ? 1 : 0);
       add(wsub, rows_ps, in_rows, rows_ps * wsub, in_rows * wsub);
     }
+    // packed images (UpdParams::pimg): small stride-1 planes with symmetric padding
+    if (bf16_ops && !stacked && xs == 1 && st == 1 && taps.n_phases == 1 && in.halo_h == 0 && in.halo_w == 0 &&
+        dout.halo_h == 0 && dout.halo_w == 0 && s.H <= 16 && s.R - 1 - s.pad_h <= s.pad_h &&
+        s.S - 1 - s.pad_w <= s.pad_w && P == s.H && Q == s.W && ((s.H + s.pad_h) * (s.W + 2 * s.pad_w)) % 8 == 0 &&
+        !DCONV_ENV("DCONV_UPD_NO_PIMG")) {
+      const int wsub = s.W + 2 * s.pad_w, rows = s.H + s.pad_h, pitch = rows * wsub;
+      for (int k : {1, 2, 4}) {
+        if ((k * pitch) % 16 != 0 || k * pitch > 256) continue;
+        add(wsub, rows, rows, k * pitch, (k + 1) * pitch, k);
+        break;
+      }
+    }
   }
   const Cand* best = nullptr;
   // modelled cycles of one candidate over the whole launch (bf16 in-place plans)
@@ -2004,7 +2017,7 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
         for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += tgv) groups.push_back(std::min(tgv, taps.phase_ntaps[ph] - t0));
     }
     const double b_bytes = 2.0 * nb_b * cd.lay.b_plane;
-    const double spi = linear ? cdiv(P * Q, cd.vs) : cdiv(P, cd.rows_ps);
+    const double spi = linear ? cdiv(P * Q, cd.vs) : cd.pimg > 0 ? 1.0 / cd.pimg : cdiv(P, cd.rows_ps);
     // cycles per 128 x NT x 16 MMA: tensor time NT/2, or the shared-memory reads of its
     // operands (4 KB of A + NT x 32 B of B at ~128 B/clk) when those are longer (NT < 128)
     const double mma_unit = std::max(xs * NT / 2.0, (4096.0 + 32.0 * xs * NT) / 128.0);
@@ -2104,6 +2117,12 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
   if (stages < 2) fail(DCONV_ERR_PLAN_INFEASIBLE, "weight-update stage does not fit shared memory");
   if (pl.has_cfg && pl.cfg.stages > 0) stages = std::min(stages, pl.cfg.stages);
   p.stages_total = s.N * p.stages_per_img;
+  if (best->pimg > 0) {  // a stage = pimg whole images (the last group may run past N: zero fill)
+    p.pimg = best->pimg;
+    p.img_pitch = best->rows_ps * best->wsub;
+    p.stages_per_img = 1;
+    p.stages_total = cdiv(s.N, p.pimg);
+  }
   for (size_t t = 0; t < taps.r.size(); ++t) {
     p.tap_shift[t] = taps.r2[t] * p.wsub + taps.s2[t];
     p.tap_src[t] = taps.r[t] * s.S + taps.s[t];
@@ -2288,6 +2307,17 @@ void encode_upd_maps(UpdLaunch& L, const dconv_upd_plan& pl, const dconv_act_t& 
                       swz);
       }
       const char* base = reinterpret_cast<const char*>(data) + (static_cast<uint64_t>(a.halo_h) * wp + a.halo_w) * 32;
+      if (p.pimg > 0) {  // packed images: dims {16, w, h, images, channel blocks}, images inside the planes
+        const uint64_t cbs = static_cast<uint64_t>(chans_blocks);
+        const uint64_t dims5[5] = {16, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h),
+                                   static_cast<uint64_t>(a.n), cbs};
+        const uint64_t plane_b = static_cast<uint64_t>(wp) * hp * 32;
+        const uint64_t strides5[4] = {32, static_cast<uint64_t>(wp) * 32, plane_b * cbs, plane_b};
+        const uint32_t box5[5] = {16, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.rows_ps),
+                                  static_cast<uint32_t>(is_in ? p.pimg + 1 : p.pimg),
+                                  static_cast<uint32_t>(is_in ? p.cb_eff * p.mc : p.nb)};
+        return encode(1, 5, base, dims5, strides5, box5, nullptr, is_in ? "upd input packed" : "upd dO packed", swz);
+      }
       const uint64_t dims[4] = {16, static_cast<uint64_t>(a.w), static_cast<uint64_t>(a.h), planes};
       const uint64_t strides3[3] = {32, static_cast<uint64_t>(wp) * 32, static_cast<uint64_t>(wp) * hp * 32};
       if (is_in) {

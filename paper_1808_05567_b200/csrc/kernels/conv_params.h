@@ -116,6 +116,13 @@ struct UpdParams {
   // accumulator block (i, j) is the weight gradient of tap (r_i, s_i + j). The A
   // slots of a tap group are xs_slot[tg_tap0 ..] (their columns are multiples of xs)
   int xs, xs_S;            // B copies (0 / 1: off), filter width (tap = r * xs_S + s)
+  // packed image planes (pimg >= 1; stride-1 bf16 rows plans of small images): a stage
+  // holds pimg whole images along K at a pitch of img_pitch pixels ((H + pad) rows of
+  // wsub): each image's bottom padding is the next image's top padding (zero fill), so
+  // the 7x7 3x3 update spends 98 of 144 K rows on real pixels instead of 49 of 144.
+  // One 5-D box per operand (images inside the channel-block planes); the A box
+  // carries pimg + 1 images so that the last image's bottom padding is zero too.
+  int pimg, img_pitch;
   int xs_slot_r[kMaxXsSlots], xs_slot_s[kMaxXsSlots];
   int cb_eff;
   int half;                // stacked with C <= 8: a tap slot is one 8-channel chunk (16 taps per 128 rows)

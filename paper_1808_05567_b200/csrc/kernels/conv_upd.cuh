@@ -251,6 +251,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               }
             } else if (p.linear) {
               tma_load_3d(a_dst, &map_in, &full_bar[s], 0, p.sw32 == 2 ? band * (p.vs / 4) : band * p.vs, pa);
+            } else if (p.pimg > 0) {  // packed images: {16, wsub, H + pad, pimg + 1, planes}
+              tma_load_5d(a_dst, &map_in, &full_bar[s], 0, p.in_col0, p.in_row0, n * p.pimg, ctile * 8 * mc);
             } else {
               tma_load_4d(a_dst, &map_in, &full_bar[s], 0, p.in_col0 + p.phase_col[ph],
                           p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], pa);
@@ -276,6 +278,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (p.sw32) {
             if (p.linear)
               tma_load_3d(b_dst, &map_do, &full_bar[s], 0, p.sw32 == 2 ? band * (p.vs / 4) : band * p.vs, pb);
+            else if (p.pimg > 0)
+              tma_load_5d(b_dst, &map_do, &full_bar[s], 0, 0, 0, n * p.pimg, ktile * p.nb);
             else
               for (int j = 0; j < xsn; ++j)  // copy j shifted right by j columns (zero fill at the left edge)
                 tma_load_4d(b_dst + j * p.nb * 2 * L.b_plane, &map_do, &full_bar[s], 0, -j, band * p.rows_ps, pb);

@@ -23,6 +23,8 @@
 
 namespace {
 
+inline int P_chk(const dconv_spec_t& s) { return out_P(s); }
+
 struct VReport {
   std::string err;
   long long outputs = 0, writes = 0, tiles = 0;
@@ -275,7 +277,9 @@ int dconv_upd_plan_validate(dconv_upd_plan_t plan, const dconv_act_t* in, const 
               "ring depth outside 1..kMaxStages");
     r.fail_if(p.n_tgroups < 1 || p.n_tgroups > kMaxTapGroups || p.n_taps != s.R * s.S || p.splits < 1 ||
                   p.vs < 16 || p.vs % 16 != 0 || p.nb < 1 || p.nb > 16 || p.n_img != s.N ||
-                  p.stages_per_img < 1 || p.stages_total != p.n_img * p.stages_per_img,
+                  p.stages_per_img < 1 ||
+                  p.stages_total != (p.pimg > 0 ? (p.n_img + p.pimg - 1) / p.pimg : p.n_img * p.stages_per_img) ||
+                  (p.pimg > 0 && (p.stages_per_img != 1 || p.vs < p.pimg * p.img_pitch || p.img_pitch < P_chk(s) * p.wsub)),
               "launch tables outside the kernel's limits");
     r.fail_if(static_cast<int>(L.grid.z) != p.splits || static_cast<int>(L.grid.x) % p.n_tgroups != 0,
               "grid does not match (c-tiles x tap groups, k-tiles, splits)");
