@@ -321,6 +321,16 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   const bool mimg_ok = linear && pb.R == 1 && pb.S == 1 && in.halo_h == 0 && in.halo_w == 0 && hw <= 128 &&
                        (cfg == nullptr || cfg->tile_mb == 0 || cfg->tile_mb == 2);
   p.wsub = linear ? wp : pb.Q + taps.s2max;
+  // packed multi-tap tiles (FwdParams::img_pitch): small stride-1 same-padded images of a
+  // bf16 rows plan, three 7x7 images per 256-row tile (57 % of the MMA rows real
+  // pixels instead of 38 % for one image per 128-row tile)
+  const int pk_pitch = (in.h + (-pb.row_off)) * (pb.Q + taps.s2max);
+  const bool pk_ok = !raw_f32 && !linear && st == 1 && taps.n_phases == 1 && in.halo_h == 0 && in.halo_w == 0 &&
+                     pb.P == in.h && pb.Q == in.w && pb.row_off <= 0 && pb.col_off <= 0 &&
+                     pb.R - 1 + pb.row_off <= -pb.row_off && pb.S - 1 + pb.col_off <= -pb.col_off &&
+                     -pb.col_off * 2 == taps.s2max && pk_pitch % 8 == 0 && 2 * pk_pitch <= 256 &&
+                     in.h - pb.row_off <= 256 && pb.Q + taps.s2max <= 256 && !(cfg && cfg->tile_mb) &&
+                     !DCONV_ENV("DCONV_FWD_NO_PK");
   p.in_row0 = pb.row_off;
   p.in_col0 = pb.col_off;
   for (size_t t = 0; t < taps.r.size(); ++t) p.tap_shift[t] = taps.r2[t] * p.wsub + taps.s2[t];
@@ -411,6 +421,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   // (measured: narrower N tiles do not pay -- the N = 128 MMAs are issue-bound -- so only
   // developer mode enables it: DCONV_SHAPE_GRID=1)
   const bool shape_grid = !raw_f32 && !want_nb && !want_mb && DCONV_ENV("DCONV_SHAPE_GRID");
+  const bool pk = pk_ok && !want_mb;  // (an explicit m-tile override keeps row tiles)
   int n_nt0 = cdiv(kb_total, 16);
   if (shape_grid)
     while (est_tiles(1, n_nt0) < sm_count() && cdiv(kb_total, n_nt0 + 1) >= 4 && cdiv(kb_total, n_nt0 + 1) < cdiv(kb_total, n_nt0))
@@ -430,9 +441,14 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
         const int bufs = 2 * acc_cols <= 512 ? 2 : 1;
         if (bufs == 1 && mb > 1 && !want_mb) continue;
         if (bufs < want_bufs) continue;
+        if (pk && mb == 1 && nb > 8) continue;  // packed tiles first: 256 rows x (N <= 128, two buffers)
         const int Lpx = 128 * mb;
         int apx, lb = 0;
-        if (mimg_ok) {
+        if (pk && mb == 2) {  // (pki + 1) images per chunk plane; reads reach Lpx + maxshift rows
+          const int pki = Lpx / pk_pitch;
+          apx = (pki + 1) * pk_pitch;
+          if (apx < Lpx + maxshift) continue;  // the box must cover every row the MMA reads
+        } else if (mimg_ok) {
           if (mb != 2) continue;
           apx = Lpx;
         } else if (linear) {
@@ -576,7 +592,12 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   p.lin_boxes = lin_boxes;
   p.tiles_per_img = cdiv(pb.P * p.wsub, 128 * tile.mb);
   p.mimg = 0;
-  if (mimg_ok && (tile.mb == 2 || L.ts)) {
+  p.img_pitch = 0;
+  if (pk && tile.mb == 2) {
+    p.mimg = (128 * tile.mb) / pk_pitch;
+    p.img_pitch = pk_pitch;
+    p.a_load_px = (p.mimg + 1) * pk_pitch;
+  } else if (mimg_ok && (tile.mb == 2 || L.ts)) {
     p.mimg = (128 * tile.mb) / hw;
     p.a_load_px = p.mimg * hw;
   }
@@ -607,7 +628,15 @@ void encode_fwd_act_map(FwdLaunch& L, const dconv_act_t& in) {
   const uint64_t planes = static_cast<uint64_t>(in.n) * p.in_cb;
   const uint64_t pix = raw_f32 ? 64 : 32;
   const CUtensorMapSwizzle swz = raw_f32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  if (p.mimg > 0) {
+  if (p.img_pitch > 0) {  // packed multi-tap: {16, w, h, images, channel blocks}, images inside the planes
+    const uint64_t plane_b = static_cast<uint64_t>(wp) * hp * pix;
+    const uint64_t dims[5] = {16, static_cast<uint64_t>(in.w), static_cast<uint64_t>(in.h),
+                              static_cast<uint64_t>(in.n), static_cast<uint64_t>(p.in_cb)};
+    const uint64_t strides[4] = {pix, pix * wp, plane_b * p.in_cb, plane_b};
+    const uint32_t box[5] = {16, static_cast<uint32_t>(p.wsub), static_cast<uint32_t>(p.img_pitch / p.wsub),
+                             static_cast<uint32_t>(p.mimg + 1), static_cast<uint32_t>(kc)};
+    L.map_a = encode(!raw_f32, 5, in.data, dims, strides, box, nullptr, "activation packed images", swz);
+  } else if (p.mimg > 0) {
     const uint64_t dims[4] = {16, static_cast<uint64_t>(hw), static_cast<uint64_t>(p.in_cb),
                               static_cast<uint64_t>(in.n)};
     const uint64_t strides[3] = {pix, pix * hw, pix * hw * p.in_cb};

@@ -419,7 +419,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             }
             mbar_arrive_expect_tx(&pc_full[s], a_bytes);
             // bf16 pixels as SWIZZLE_32B rows: the MMA reads them in place
-            if (p.mimg > 0) {
+            if (p.img_pitch > 0) {  // packed images: one box {16, wsub, H + pad, mimg + 1, kc}
+              tma_load_5d(dst, &map_a, &pc_full[s], 0, p.in_col0, p.in_row0, n, cb * p.kc);
+            } else if (p.mimg > 0) {
               for (int kk = 0; kk < p.kc; ++kk)  // box {16, hw, 1, mimg} per block: rows contiguous per block
                 tma_load_4d(dst + kk * p.a_px * 32, &map_a, &pc_full[s], 0, 0, cb * p.kc + kk, n);
             } else if (p.linear) {
@@ -1315,17 +1317,18 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         int v = v0 + mb * 128 + qrow + lane;
         int nn = n;
         bool valid;
-        if (p.mimg > 0) {  // row -> (image, pixel) of the multi-image tile
-          const int img = v / v_end;
+        if (p.mimg > 0) {  // row -> (image, pixel) of the multi-image tile (packed: at img_pitch)
+          const int pitch = p.img_pitch > 0 ? p.img_pitch : v_end;
+          const int img = v / pitch;
           nn = n + img;
-          v -= img * v_end;
+          v -= img * pitch;
           valid = img < p.mimg && nn < p.n_img;
         } else {
           valid = v < v_end;
         }
         const int pp = v / p.wsub;
         const int qq = v - pp * p.wsub;
-        valid = valid && qq < p.Q;
+        valid = valid && qq < p.Q && pp < p.P;
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
         for (int g0 = 2 * (item - mb * n_pairs); g0 < ((dbg_mode & 64) ? g_lo : g_hi); g0 += 2 * n_pairs) {

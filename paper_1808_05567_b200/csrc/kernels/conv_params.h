@@ -38,6 +38,11 @@ struct FwdParams {
   // A staging: smem chunk planes hold a_px pixels starting at virtual pixel a_px0
   int linear;          // 1: virtual index == physical pixel index of the halo'd plane
   int mimg;            // >0: multi-image tiles (1x1 stride 1, small planes): mimg whole images per tile
+  // > 0 (with mimg): packed multi-tap tiles (stride-1 bf16 rows plans of small images):
+  // mimg whole images along M at this pitch ((H + pad) rows of wsub), each image's
+  // bottom padding the next one's top padding; one 5-D activation box of mimg + 1
+  // images (images inside the channel-block planes) so the last image's is zero too
+  int img_pitch;
   int a_px;            // pixels per chunk plane per stage
   int a_load_px;       // pixels the activation TMA writes per stage
   int lin_boxes;       // linear mode: 128-pixel boxes per chunk plane

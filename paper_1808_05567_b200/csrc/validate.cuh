@@ -62,15 +62,16 @@ void cover_launch(const FwdLaunch& L, std::vector<uint8_t>& cnt, VReport& r) {
       int v = v0 + row, nn = n;
       bool valid;
       if (p.mimg > 0) {
-        const int img = v / v_end;
+        const int pitch = p.img_pitch > 0 ? p.img_pitch : v_end;
+        const int img = v / pitch;
         nn = n + img;
-        v -= img * v_end;
+        v -= img * pitch;
         valid = img < p.mimg && nn < p.n_img;
       } else {
         valid = v < v_end;
       }
       const int pp = v / p.wsub, qq = v - (v / p.wsub) * p.wsub;
-      valid = valid && qq < p.Q;
+      valid = valid && qq < p.Q && pp < p.P;
       if (!valid) continue;
       for (int g = 0; g < p.nb; ++g) {
         const int kb = ntile * p.nb + g;
@@ -101,7 +102,11 @@ void check_problem(const FwdLaunch& L, int n_img, int P, int Q, int kb_out, int 
 void check_geometry(const FwdLaunch& L, int maxshift, VReport& r) {
   const FwdParams& p = L.p;
   const int M = 128 * p.mb;
-  if (p.mimg > 0) {
+  if (p.img_pitch > 0) {
+    r.fail_if(p.mimg < 1 || p.mimg * p.img_pitch > M || p.img_pitch % p.wsub != 0 ||
+                  (p.mimg + 1) * p.img_pitch < M + maxshift || p.a_load_px > p.a_px,
+              "packed tile: images / staged rows do not cover the rows the MMA reads");
+  } else if (p.mimg > 0) {
     r.fail_if(p.a_load_px > p.a_px, "multi-image tile loads more pixels than its slot holds");
   } else if (p.linear) {
     // rows v_off .. v_off + M - 1 shifted by up to maxshift must be staged

@@ -1,4 +1,5 @@
-"""GPU parity of the bf16 weight-update staging modes added in round 2, each pinned
+"""GPU parity of the bf16 staging modes added in round 2 (weight update, and the packed
+multi-tap forward / backward-data tiles), each pinned
 to the plan it is meant to run (plan describe) and checked against the oracle on
 the same bf16-rounded operands (tolerance 2e-2, BASELINE north_star):
 
@@ -62,3 +63,37 @@ def test_bf16_update_modes(dconv, orc, case):
     assert torch.equal(dw.data, dw2.data)
     # the plan validator accepts the launch (tap coverage, stage coverage, limits)
     assert up.validate(ib, gb)["ok"]
+
+
+@pytest.mark.parametrize("N", [4, 5])
+def test_packed_image_forward_backward(dconv, orc, N):
+    """Packed multi-tap tiles (FwdParams::img_pitch): three 7x7 images per 256-row tile,
+    forward and the dual backward-data, batch not a multiple of three (a tile's last
+    images past the batch), against the oracle on the same bf16-rounded operands."""
+    C_, K, H = 128, 256, 7
+    s = orc.spec(N, C_, K, H, H, 3, 3, 1, 1, 1, 16)
+    spec = dconv.make_layer_spec(N, C_, K, H, H, 3, 3, 1, 1, 1, 16)
+    rnd = lambda a: torch.from_numpy(a).bfloat16().float().numpy()  # noqa: E731
+    x = rnd(orc.uniform(31, (N, C_, H, H)))
+    w = rnd(orc.he_normal(32, (K, C_, 3, 3), C_ * 9))
+    g = rnd(orc.uniform(33, (N, K, H, H)))
+    bf = torch.bfloat16
+    ib = dconv.to_blocked_activation(dev(x), 16, 0, 0, dtype=bf)
+    gb = dconv.to_blocked_activation(dev(g), 16, 0, 0, dtype=bf)
+    wb = dconv.to_blocked_weight(dev(w), spec)
+    M = dconv.Math.BF16
+    fp = dconv.make_forward_plan(spec, 1, None, None, M)
+    y = dconv.BlockedActivation(N, K, H, H, 16, 0, 0, bf)
+    fp.execute(ib, wb, y)
+    torch.cuda.synchronize()
+    assert fp.blocking["mimg"] == 3 and fp.blocking["mode"] == "rows", fp.blocking
+    n = orc.error_norms(orc.conv_forward(s, x, w), dconv.from_blocked_activation(y, dtype=torch.float32).cpu().numpy())
+    assert n["max_over_rms"] <= 2e-2, n
+    assert fp.validate(ib, y)["ok"]
+    bc = dconv.prepare_backward(spec, wb, 1, None, M)
+    dx = dconv.BlockedActivation(N, C_, H, H, 16, 0, 0, bf)
+    bc.execute(wb, gb, dx)
+    torch.cuda.synchronize()
+    assert bc.blocking["phases"][0]["mimg"] == 3, bc.blocking
+    n = orc.error_norms(orc.conv_backward(s, g, w), dconv.from_blocked_activation(dx, dtype=torch.float32).cpu().numpy())
+    assert n["max_over_rms"] <= 2e-2, n
