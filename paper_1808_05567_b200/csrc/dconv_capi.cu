@@ -1999,7 +1999,9 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     }
   };
   if (linear) {
-    for (int vs : {256, 128, 64, 32, 16}) add(Q, 0, 0, vs, vs);
+    const int want_vs = env_int("DCONV_UPD_VS", 0);  // developer mode: force the stage band
+    for (int vs : {256, 128, 64, 32, 16})
+      if (!want_vs || vs == want_vs) add(Q, 0, 0, vs, vs);
   } else {
     const int wmin = Q + s2max;
     const int w16 = (wmin + 15) / 16 * 16;

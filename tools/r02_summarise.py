@@ -22,7 +22,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 # bench.py traffic keys of the captured launches
 TRAFFIC = {"r02_ncu_l1_3x3_U": "r50_64_64_56_3x3s1_U", "r02_ncu_l1_3x3_F": "r50_64_64_56_3x3s1_F",
            "r02_ncu_l3_3x3_F": "r50_256_256_14_3x3s1_F", "r02_ncu_l3_1x1_F": "r50_1024_256_14_1x1s1_F",
-           "r02_ncu_l3_1x1_U": "r50_256_1024_14_1x1s1_U", "r02_ncu_cfg2_U": "cfg2_U"}
+           "r02_ncu_l3_1x1_U": "r50_256_1024_14_1x1s1_U", "r02_ncu_cfg2_U": "cfg2_U",
+           "r02_ncu_l1_1x1_res_F": "r50_64_256_56_1x1s1_F", "r02_ncu_l4_3x3_U": "r50_512_512_7_3x3s1_U",
+           "r02_ncu_l4_3x3_F": "r50_512_512_7_3x3s1_F"}
 
 
 def raw(rep):
@@ -88,7 +90,13 @@ def launches(path, out, note):
 
 
 def main(src):
+    # merged into the committed summaries (a capture set may cover only some kernels)
     summary, traffic = {}, {}
+    try:
+        summary = json.load(open(os.path.join(OUT, "r02_ncu_full.json")))["captures"]
+        traffic = json.load(open(os.path.join(OUT, "r02_ncu_traffic.json")))
+    except (OSError, ValueError, KeyError):
+        pass
     for rep in sorted(glob.glob(os.path.join(src, "r02_ncu_*.ncu-rep"))):
         name = os.path.basename(rep)[:-len(".ncu-rep")]
         ks = raw(rep)
