@@ -1033,11 +1033,18 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     // AHEAD into registers (the first step of a tile before its accumulator wait),
     // so their HBM latency overlaps the previous step instead of stalling every
     // step (these epilogues move ~3x the bytes of their mainloop)
-    auto lean_fused_bf16 = [&](auto) {  // generic: instantiated only for the bf16-activation kernels
+    // NOPS = fused operands (1: residual add OR ReLU mask, 2: both); DEPTH = steps the
+    // operand loads run ahead of their use (the fused 1x1 layers are bound by these
+    // loads: the forward's residual add runs two steps -- 4 KB per warp -- ahead)
+    auto lean_fused_bf16 = [&](auto nops_c, auto depth_c) {  // instantiated only for the bf16-activation kernels
+      constexpr int NOPS = decltype(nops_c)::value, DEPTH = decltype(depth_c)::value;
+      constexpr int NB = 4 * NOPS;  // uint4 per step: (op) x (2 blocks) x (2 halves)
       uint32_t n_st = 0, tl = 0;
       const uint8_t* addp = reinterpret_cast<const uint8_t*>(p.add);
       const uint8_t* maskp = reinterpret_cast<const uint8_t*>(p.mask);
-      auto fetch = [&](int n, int v0, int ntile, int s, int ng, uint4 (&b)[8]) {
+      // operand slots: [0, 4) the first operand (add if present, else mask), [4, 8) the mask when both
+      const uint8_t* op0 = addp ? addp : maskp;
+      auto fetch = [&](int n, int v0, int ntile, int s, int ng, uint4 (&b)[NB]) {
         const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - (s / ng) * ng);
         const int kb0 = ntile * p.nb + g0;
         const bool pair = g0 + 1 < p.nb;
@@ -1048,10 +1055,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           const bool live = v < v_end && kb < p.kb_out && (j == 0 || pair);
           const long long off = ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 32LL;
           const uint4 z = make_uint4(0, 0, 0, 0);
-          b[2 * j] = (addp && live) ? *reinterpret_cast<const uint4*>(addp + off) : z;
-          b[2 * j + 1] = (addp && live) ? *reinterpret_cast<const uint4*>(addp + off + 16) : z;
-          b[4 + 2 * j] = (maskp && live) ? *reinterpret_cast<const uint4*>(maskp + off) : z;
-          b[4 + 2 * j + 1] = (maskp && live) ? *reinterpret_cast<const uint4*>(maskp + off + 16) : z;
+          b[2 * j] = live ? *reinterpret_cast<const uint4*>(op0 + off) : z;
+          b[2 * j + 1] = live ? *reinterpret_cast<const uint4*>(op0 + off + 16) : z;
+          if constexpr (NOPS == 2) {
+            b[4 + 2 * j] = live ? *reinterpret_cast<const uint4*>(maskp + off) : z;
+            b[4 + 2 * j + 1] = live ? *reinterpret_cast<const uint4*>(maskp + off + 16) : z;
+          }
         }
       };
       auto unpack = [](const uint4& a, const uint4& b, float (&f)[16]) {
@@ -1068,15 +1077,17 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         int ng = 0;  // this group's block pairs in the tile
         for (int g0 = 2 * eg; g0 < p.nb && ntile * p.nb + g0 < p.kb_out; g0 += 2 * n_eg) ++ng;
         const int total = p.mb * ng;
-        uint4 cur[8], nxt[8];
-        if (total > 0) fetch(n, v0, ntile, 0, ng, cur);
+        uint4 buf[DEPTH + 1][NB];  // buf[0] = this step's operands, buf[d] = step + d's
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d)
+          if (d < total) fetch(n, v0, ntile, d, ng, buf[d]);
         const uint32_t acc = p.acc_bufs == 2 ? (tl & 1u) : 0u;
         const uint32_t apar = p.acc_bufs == 2 ? ((tl >> 1) & 1u) : (tl & 1u);
         mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
         tc_fence_after();
         const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
         for (int s = 0; s < total; ++s) {
-          if (s + 1 < total) fetch(n, v0, ntile, s + 1, ng, nxt);
+          if (s + DEPTH < total) fetch(n, v0, ntile, s + DEPTH, ng, buf[DEPTH]);
           const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - mb * ng);
           const int kb0 = ntile * p.nb + g0;
           const bool pair = g0 + 1 < p.nb;
@@ -1104,7 +1115,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             }
             if (addp) {
               float a[16];
-              unpack(cur[2 * j], cur[2 * j + 1], a);
+              unpack(buf[0][2 * j], buf[0][2 * j + 1], a);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] += a[e];
             }
@@ -1114,7 +1125,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
             }
             if (maskp) {
               float m[16];
-              unpack(cur[4 + 2 * j], cur[4 + 2 * j + 1], m);
+              constexpr int mo = NOPS == 2 ? 4 : 0;
+              unpack(buf[0][mo + 2 * j], buf[0][mo + 2 * j + 1], m);
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
@@ -1132,7 +1144,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           }
           ++n_st;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+          for (int d = 0; d < DEPTH; ++d)
+#pragma unroll
+            for (int i = 0; i < NB; ++i) buf[d][i] = buf[d + 1][i];
         }
         tc_fence_before();
         __syncwarp();
@@ -1142,7 +1156,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     bool done = false;
     if constexpr (!RAW_F32) {
       if ((p.add != nullptr || p.mask != nullptr) && p.out_bf16 && !(dbg_mode & 512)) {  // dbg 512: no prefetch
-        lean_fused_bf16(0);
+        if (p.add != nullptr && p.mask != nullptr)
+          lean_fused_bf16(std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
+        else if (p.add != nullptr)  // residual add (forward): measured +5 % with two steps ahead
+          lean_fused_bf16(std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{});
+        else  // ReLU mask alone (backward-data): one step ahead measured faster
+          lean_fused_bf16(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
         done = true;
       }
     }
