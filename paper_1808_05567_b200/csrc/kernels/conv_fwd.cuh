@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         int nn = n;
         bool valid;
         if (p.mimg > 0) {  // row -> (image, pixel) of the multi-image tile (packed: at img_pitch)
-          const int pitch = p.img_pitch > 0 ? p.img_pitch : v_end;
+          const int pitch = (!RAW_F32 && p.img_pitch > 0) ? p.img_pitch : v_end;  // (packed: bf16 plans only)
           const int img = v / pitch;
           nn = n + img;
           v -= img * pitch;
@@ -1347,7 +1347,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         }
         const int pp = v / p.wsub;
         const int qq = v - pp * p.wsub;
-        valid = valid && qq < p.Q && pp < p.P;
+        valid = valid && qq < p.Q && (RAW_F32 || pp < p.P);  // (packed tiles' padding rows: bf16 plans)
         const int y = p.out_y0 + pp * p.out_scale;
         const int x = p.out_x0 + qq * p.out_scale;
         for (int g0 = 2 * (item - mb * n_pairs); g0 < ((dbg_mode & 64) ? g_lo : g_hi); g0 += 2 * n_pairs) {
