@@ -204,6 +204,12 @@ int dconv_maxpool_fwd(const dconv_act_t* in, const dconv_act_t* out, void* argma
 /* mask (nullable, grad_in's geometry): ReLU backward of the pooled activation */
 int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dconv_act_t* grad_in, const void* mask,
                       dconv_stream_t stream);
+/* stride-2 lattice of a halo-0 blocked tensor (inverse = 0: sub[n][c][y][x] =
+ * in[n][c][2y][2x]) and back (inverse = 1: in = the lattice values of sub, exact
+ * zeros elsewhere): a stride-2 1x1 conv is a stride-1 1x1 conv over the lattice,
+ * and its backward-data the lattice scatter of that conv's (the reference runs it
+ * as DUALITY_1x1, propagation.cpp:35-40, 277-355); sub = ((h+1)/2, (w+1)/2) */
+int dconv_subsample2(const dconv_act_t* in, const dconv_act_t* sub, int inverse, dconv_stream_t stream);
 /* space-to-depth for a stride-2 conv on a narrow input (the 7x7/s2/p3 stem):
  * xs[n][i][j][(dy*2+dx)*C+c] = x[n][c][2i+dy-pad][2j+dx-pad], C <= 4 -> 4C
  * channels; the conv becomes stride 1 with a ceil(R/2) x ceil(S/2) filter */

@@ -968,6 +968,8 @@ extern "C" {
 const char* dconv_last_error(void) { return g_err.c_str(); }
 // the executor (graph.cu) reports its own failures through dconv_last_error()
 void dconv_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+// the DCONV_* developer overrides for graph.cu (null outside developer mode)
+const char* dconv_internal_dev_env(const char* name) { return dev_env(name); }
 
 const char* dconv_status_string(int s) {
   switch (s) {
@@ -2805,6 +2807,39 @@ int dconv_maxpool_bwd(const dconv_act_t* grad_out, const void* argmax, const dco
           (const __nv_bfloat16*)grad_out->data, (const uint8_t*)argmax, (__nv_bfloat16*)grad_in->data,
           (const __nv_bfloat16*)mask, planes, grad_in->h, grad_in->w, grad_out->h, grad_out->w, nullptr);
     cuda_check(cudaGetLastError(), "maxpool_bwd");
+  });
+}
+
+int dconv_subsample2(const dconv_act_t* in, const dconv_act_t* sub, int inverse, dconv_stream_t stream) {
+  return guarded([&] {
+    check_act(in, "subsample full-size tensor");
+    check_act(sub, "subsample lattice tensor");
+    if (in->vlen != 16 || sub->vlen != 16 || in->halo_h || in->halo_w || sub->halo_h || sub->halo_w ||
+        sub->n != in->n || sub->c != in->c || sub->h != (in->h + 1) / 2 || sub->w != (in->w + 1) / 2 ||
+        sub->dtype != in->dtype)
+      fail(DCONV_ERR_SHAPE_MISMATCH, "subsample2: halo-0 vlen-16 tensors of one dtype, lattice = ((h+1)/2, (w+1)/2)");
+    const long long planes = static_cast<long long>(in->n) * cdiv(in->c, 16);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t work = planes * (inverse ? static_cast<int64_t>(in->h) * in->w : static_cast<int64_t>(sub->h) * sub->w);
+    const int g = grid1d(work);
+    if (in->dtype == DCONV_F32) {
+      if (inverse)
+        unsubsample2_kernel<float><<<g, 256, 0, cs>>>((const float*)sub->data, (float*)in->data, planes, in->h, in->w,
+                                                      sub->h, sub->w);
+      else
+        subsample2_kernel<float><<<g, 256, 0, cs>>>((const float*)in->data, (float*)sub->data, planes, in->h, in->w,
+                                                    sub->h, sub->w);
+    } else {
+      if (inverse)
+        unsubsample2_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)sub->data,
+                                                              (__nv_bfloat16*)in->data, planes, in->h, in->w, sub->h,
+                                                              sub->w);
+      else
+        subsample2_kernel<__nv_bfloat16><<<g, 256, 0, cs>>>((const __nv_bfloat16*)in->data,
+                                                            (__nv_bfloat16*)sub->data, planes, in->h, in->w, sub->h,
+                                                            sub->w);
+    }
+    cuda_check(cudaGetLastError(), "subsample2");
   });
 }
 

@@ -38,6 +38,7 @@
 #include "../../include/dconv_b200.h"
 
 extern "C" void dconv_internal_set_error(const char* msg);  // dconv_capi.cu
+extern "C" const char* dconv_internal_dev_env(const char* name);  // dconv_capi.cu (developer mode only)
 
 namespace {
 
@@ -113,12 +114,20 @@ struct Tensor {
   void* grad = nullptr;  // dL/dz (through this tensor's ReLU), may alias another tensor's
   bool relu = false;     // produced by a ReLU (a conv with relu, or a pool of such)
   bool owns_grad = true;
+  // stride-2 lattice copy (every consumer a stride-2 1x1 conv: the ResNet v1
+  // downsampling blocks' input): the consumers run as stride-1 1x1 convs over it
+  // (dense planes: linear / multi-image / SWIZZLE_128B plans instead of strided
+  // row gathers), their data gradients sum into sub_grad, scattered back once
+  int sub_consumers = 0, sh = 0, sw = 0;
+  void* sub_act = nullptr;
+  void* sub_grad = nullptr;
 };
 
 struct Conv {
   int node;  // index into nodes
-  dconv_spec_t spec, pspec;  // layer, and as executed (space-to-depth stem)
+  dconv_spec_t spec, pspec;  // layer, and as executed (space-to-depth stem, stride-2 1x1 over the lattice)
   bool s2d = false;
+  bool sub = false;  // a stride-2 1x1 conv run at stride 1 over its input's lattice copy
   dconv_fwd_plan_t fp = nullptr;
   dconv_bwd_plan_t bp = nullptr;
   dconv_upd_plan_t up = nullptr;
@@ -212,6 +221,26 @@ dconv_wt_t conv_w(const dconv_graph* g, const Conv& cv, bool grad) {
   return wt_view((grad ? g->gflat : g->wflat) + cv.w_off, s.K, s.C, s.R, s.S);
 }
 
+// a conv's input (grad: its data gradient) as executed: the space-to-depth copy, the
+// stride-2 lattice copy, or the tensor itself
+dconv_act_t conv_in(const dconv_graph* g, const Conv& cv, bool grad) {
+  const int src = g->nodes[cv.node].src;
+  dconv_act_t a = act_of(g, src, grad);
+  if (cv.s2d && !grad) {
+    a.data = cv.s2d_x;
+    a.c = cv.pspec.C;
+    a.h = cv.pspec.H;
+    a.w = cv.pspec.W;
+  }
+  if (cv.sub) {
+    const Tensor& x = g->t[src];
+    a.data = grad ? x.sub_grad : x.sub_act;
+    a.h = x.sh;
+    a.w = x.sw;
+  }
+  return a;
+}
+
 void build(dconv_graph* g, int in_c, int in_h, int in_w) {
   const int n_t = static_cast<int>(g->nodes.size()) + 1;  // tensor 0 = input, node i writes tensor i + 1
   g->t.assign(n_t, Tensor{});
@@ -260,10 +289,43 @@ void build(dconv_graph* g, int in_c, int in_h, int in_w) {
     g->conv_of_node[i] = static_cast<int>(g->convs.size());
     g->convs.push_back(cv);
   }
+  // stride-2 1x1 consumers over a lattice copy (Tensor::sub_*): every consumer of the
+  // tensor such a conv, the tensor no residual operand, not the image
+  for (int id = 1; id < n_t; ++id) {
+    int strided = 0, other = 0;
+    for (size_t i = 0; i < g->nodes.size(); ++i) {
+      const dconv_graph_node_t& nd = g->nodes[i];
+      if (nd.add == id) ++other;
+      if (nd.src != id) continue;
+      const int ci = g->conv_of_node[i];
+      if (nd.kind == DCONV_NODE_CONV && ci >= 0 && !g->convs[ci].s2d && nd.stride == 2 && nd.R == 1 && nd.S == 1 &&
+          nd.pad_h == 0 && nd.pad_w == 0)
+        ++strided;
+      else
+        ++other;
+    }
+    if (strided == 0 || other > 0 || dconv_internal_dev_env("DCONV_GRAPH_NO_LATTICE")) continue;
+    Tensor& x = g->t[id];
+    x.sub_consumers = strided;
+    x.sh = (x.h + 1) / 2;
+    x.sw = (x.w + 1) / 2;
+    for (size_t i = 0; i < g->nodes.size(); ++i)
+      if (g->nodes[i].src == id) {
+        Conv& cv = g->convs[g->conv_of_node[i]];
+        const dconv_graph_node_t& nd = g->nodes[i];
+        ck(dconv_make_spec(g->N, nd.C, nd.K, x.sh, x.sw, 1, 1, 1, 0, 0, 16, &cv.pspec), "lattice spec");
+        cv.sub = true;
+      }
+  }
   // tensors and gradients; a projection's output only feeds a residual add, so its
   // dL/dz is the block output's (aliased buffer)
   for (int id = 0; id < n_t; ++id) {
     g->t[id].act = dalloc(g, act_bytes(g, g->t[id]));
+    if (g->t[id].sub_consumers > 0) {
+      const size_t sb = static_cast<size_t>(g->N) * cdiv(g->t[id].c, 16) * g->t[id].sh * g->t[id].sw * 16 * esz(g->dtype);
+      g->t[id].sub_act = dalloc(g, sb);
+      g->t[id].sub_grad = dalloc(g, sb);
+    }
   }
   for (size_t i = 0; i < g->nodes.size(); ++i) {
     const dconv_graph_node_t& nd = g->nodes[i];
@@ -328,7 +390,7 @@ void build(dconv_graph* g, int in_c, int in_h, int in_w) {
   for (Conv& cv : g->convs) {
     const dconv_graph_node_t& nd = g->nodes[cv.node];
     ck(dconv_fwd_plan_create(&cv.pspec, nullptr, nullptr, g->math, 0, 0, &cv.fp), "graph forward plan");
-    if (nd.src != 0) ck(dconv_bwd_plan_create(&cv.spec, nullptr, g->math, &cv.bp), "graph backward plan");
+    if (nd.src != 0) ck(dconv_bwd_plan_create(cv.sub ? &cv.pspec : &cv.spec, nullptr, g->math, &cv.bp), "graph backward plan");
     ck(dconv_upd_plan_create(&cv.pspec, nullptr, g->math, &cv.up), "graph update plan");
     g->ws_main_bytes = std::max(g->ws_main_bytes, dconv_fwd_workspace_bytes(cv.fp));
     if (cv.bp) g->ws_main_bytes = std::max(g->ws_main_bytes, dconv_bwd_workspace_bytes(cv.bp));
@@ -342,13 +404,7 @@ void build(dconv_graph* g, int in_c, int in_h, int in_w) {
     cuck(cudaEventCreateWithFlags(&cv.ev_dw, cudaEventDisableTiming), "event");
   }
   for (Conv& cv : g->convs) {
-    dconv_act_t in = act_of(g, g->nodes[cv.node].src, false), gout = act_of(g, cv.node + 1, true);
-    if (cv.s2d) {
-      in.data = cv.s2d_x;
-      in.c = cv.pspec.C;
-      in.h = cv.pspec.H;
-      in.w = cv.pspec.W;
-    }
+    const dconv_act_t in = conv_in(g, cv, false), gout = act_of(g, cv.node + 1, true);
     g->ws_upd_bytes = std::max(g->ws_upd_bytes, dconv_upd_workspace_bytes(cv.up, &in, &gout));
   }
   g->ws_main = dalloc(g, g->ws_main_bytes);
@@ -371,6 +427,7 @@ dconv_epilogue_t epi(const void* add, const void* mask, int relu) {
 
 void forward(dconv_graph* g, cudaStream_t s) {
   dconv_stream_t st = reinterpret_cast<dconv_stream_t>(s);
+  std::vector<char> subbed(g->t.size(), 0);
   for (size_t i = 0; i < g->nodes.size(); ++i) {
     const dconv_graph_node_t& nd = g->nodes[i];
     const dconv_act_t src = act_of(g, nd.src, false), out = act_of(g, static_cast<int>(i) + 1, false);
@@ -399,6 +456,14 @@ void forward(dconv_graph* g, cudaStream_t s) {
       x = xs;
       w = w2;
     }
+    if (cv.sub) {  // the first strided consumer makes the lattice copy
+      x = conv_in(g, cv, false);
+      if (!subbed[nd.src]) {
+        ck(dconv_subsample2(&src, &x, 0, st), "graph lattice copy");
+        g->launches += 1;
+        subbed[nd.src] = 1;
+      }
+    }
     ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, g->ws_main, st), "graph forward");
     g->launches += dconv_fwd_launches(cv.fp);
   }
@@ -406,15 +471,10 @@ void forward(dconv_graph* g, cudaStream_t s) {
 
 void update(dconv_graph* g, Conv& cv, cudaStream_t s) {
   dconv_stream_t st = reinterpret_cast<dconv_stream_t>(s);
-  const dconv_graph_node_t& nd = g->nodes[cv.node];
-  dconv_act_t in = act_of(g, nd.src, false);
+  const dconv_act_t in = conv_in(g, cv, false);  // (s2d / lattice copies: made by this step's forward)
   const dconv_act_t gout = act_of(g, cv.node + 1, true);
   dconv_wt_t dw = conv_w(g, cv, true);
-  if (cv.s2d) {  // the s2d copy of the input was made by this step's forward
-    in.data = cv.s2d_x;
-    in.c = cv.pspec.C;
-    in.h = cv.pspec.H;
-    in.w = cv.pspec.W;
+  if (cv.s2d) {
     const dconv_wt_t dw2 = wt_view(cv.s2d_dw, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
     ck(dconv_weight_update(cv.up, &in, &gout, &dw2, 0, g->ws_upd, st), "graph update");
     ck(dconv_s2d_wt(&dw, &dw2, 1, st), "graph s2d gradient");
@@ -441,6 +501,7 @@ void backward(dconv_graph* g, const dconv_act_t* dtop, cudaStream_t s) {
   for (size_t b = 0; b < g->buckets.size(); ++b) left[b] = g->buckets[b].n_convs;
   const bool comm = g->cfg.nccl_comm != nullptr && !g->profiling;
   std::vector<char> written(g->t.size(), 0);
+  std::vector<int> sub_done(g->t.size(), 0);
   for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
     const dconv_graph_node_t& nd = g->nodes[i];
     if (nd.kind == DCONV_NODE_MAXPOOL) {
@@ -473,6 +534,24 @@ void backward(dconv_graph* g, const dconv_act_t* dtop, cudaStream_t s) {
           "ncclAllReduce");
     }
     if (nd.src == 0) continue;  // the image gradient is not needed
+    if (cv.sub) {
+      // lattice consumers: stride-1 backward-data into the lattice gradient (the
+      // consumers' sum and the ReLU mask -- the lattice copy -- fused), scattered back
+      // to the full-size gradient (zeros off the lattice) after the last consumer
+      const dconv_act_t go = act_of(g, i + 1, true), gi = conv_in(g, cv, true);
+      Tensor& x = g->t[nd.src];
+      const dconv_epilogue_t e = epi(sub_done[nd.src] > 0 ? x.sub_grad : nullptr, x.relu ? x.sub_act : nullptr, 0);
+      const dconv_wt_t w = conv_w(g, cv, false);
+      ck(dconv_backward_data_ex(cv.bp, &w, &go, &gi, &e, g->ws_main, st), "graph backward");
+      g->launches += dconv_bwd_launches(cv.bp);
+      if (++sub_done[nd.src] == x.sub_consumers) {
+        const dconv_act_t full = act_of(g, nd.src, true);
+        ck(dconv_subsample2(&full, &gi, 1, st), "graph lattice scatter");
+        g->launches += 1;
+        written[nd.src] = 1;
+      }
+      continue;
+    }
     // data gradient of the conv input, through the ReLU of that tensor, summing branches
     const dconv_act_t go = act_of(g, i + 1, true), gi = act_of(g, nd.src, true);
     const void* mask = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
@@ -690,6 +769,7 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
     std::vector<const void*> b_add(g->convs.size(), nullptr), b_mask(g->convs.size(), nullptr);
     {
       std::vector<char> written(g->t.size(), 0);
+      std::vector<int> sub_done(g->t.size(), 0);
       for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
         const dconv_graph_node_t& nd = g->nodes[i];
         if (nd.kind == DCONV_NODE_MAXPOOL) {
@@ -698,6 +778,13 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
         }
         const int ci = g->conv_of_node[i];
         if (nd.src == 0) continue;
+        if (g->convs[ci].sub) {
+          const Tensor& x = g->t[nd.src];
+          b_mask[ci] = x.relu ? x.sub_act : nullptr;
+          b_add[ci] = sub_done[nd.src]++ > 0 ? x.sub_grad : nullptr;
+          if (sub_done[nd.src] == x.sub_consumers) written[nd.src] = 1;
+          continue;
+        }
         b_mask[ci] = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
         if (written[nd.src]) {
           b_add[ci] = g->t[nd.src].grad;
@@ -728,21 +815,15 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
     for (size_t ci = 0; ci < g->convs.size(); ++ci) {
       Conv& cv = g->convs[ci];
       const dconv_graph_node_t& nd = g->nodes[cv.node];
-      const dconv_act_t src = act_of(g, nd.src, false), out = act_of(g, cv.node + 1, false);
-      dconv_act_t x = src;
+      const dconv_act_t out = act_of(g, cv.node + 1, false);
+      const dconv_act_t x = conv_in(g, cv, false);
       dconv_wt_t w = conv_w(g, cv, false);
-      if (cv.s2d) {
-        x.data = cv.s2d_x;
-        x.c = cv.pspec.C;
-        x.h = cv.pspec.H;
-        x.w = cv.pspec.W;
-        w = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
-      }
+      if (cv.s2d) w = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
       const dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
       ms[3 * ci + 0] = timed([&] { ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, g->ws_main, st), "profile fwd"); });
       ms[3 * ci + 1] = 0.0f;
       if (cv.bp) {
-        const dconv_act_t go = act_of(g, cv.node + 1, true), gi = act_of(g, nd.src, true);
+        const dconv_act_t go = act_of(g, cv.node + 1, true), gi = conv_in(g, cv, true);
         const dconv_epilogue_t eb = epi(b_add[ci], b_mask[ci], 0);
         const dconv_wt_t wf = conv_w(g, cv, false);
         ms[3 * ci + 1] =

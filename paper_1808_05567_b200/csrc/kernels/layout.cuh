@@ -610,6 +610,48 @@ __global__ void maxpool_bwd_quad_kernel(const T* __restrict__ gout, const uint8_
   }
 }
 
+// Stride-2 lattice of a halo-0 blocked tensor as its own dense tensor (the input of
+// a stride-2 1x1 conv: the conv becomes stride 1 over it) and back: the full-size
+// tensor with the lattice values and exact zeros elsewhere (a stride-2 1x1
+// backward-data's result). One thread per destination pixel, 16-byte moves.
+template <typename T>
+__global__ void subsample2_kernel(const T* __restrict__ in, T* __restrict__ out, long long planes, int h, int w,
+                                  int p, int q) {
+  constexpr int kV = static_cast<int>(16 * sizeof(T) / 16);  // uint4 per pixel
+  const long long total = planes * p * q;
+  DCONV_GRID_STRIDE(e, total) {
+    const int x = static_cast<int>(e % q);
+    const long long r = e / q;
+    const int y = static_cast<int>(r % p);
+    const long long plane = r / p;
+    const uint4* src = reinterpret_cast<const uint4*>(in + ((plane * h + 2 * y) * w + 2 * x) * 16);
+    uint4* dst = reinterpret_cast<uint4*>(out + e * 16);
+#pragma unroll
+    for (int k = 0; k < kV; ++k) dst[k] = src[k];
+  }
+}
+template <typename T>
+__global__ void unsubsample2_kernel(const T* __restrict__ in, T* __restrict__ out, long long planes, int h, int w,
+                                    int p, int q) {
+  constexpr int kV = static_cast<int>(16 * sizeof(T) / 16);
+  const long long total = planes * h * w;
+  DCONV_GRID_STRIDE(e, total) {
+    const int ix = static_cast<int>(e % w);
+    const long long r = e / w;
+    const int iy = static_cast<int>(r % h);
+    const long long plane = r / h;
+    uint4* dst = reinterpret_cast<uint4*>(out + e * 16);
+    if (((ix | iy) & 1) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(in + ((plane * p + iy / 2) * q + ix / 2) * 16);
+#pragma unroll
+      for (int k = 0; k < kV; ++k) dst[k] = src[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < kV; ++k) dst[k] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
 // Space-to-depth of a narrow (C <= 4), halo-0, one-block input for a stride-2
 // conv: xs[n][i][j][(dy*2+dx)*C + c] = x[n][c][2i+dy-pad][2j+dx-pad] (zero
 // outside; lanes >= 4C zero). A stride-2 RxS conv over x equals a stride-1
