@@ -2011,8 +2011,13 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     while (g > 1 && wmin % g != 0) g >>= 1;
     const int base_rows = 16 / g;  // rows so that rows * wmin % 16 == 0
     std::vector<std::pair<int, int>> geo;
-    if (w16 * 4 <= wmin * 5)  // 16-aligned pitch wastes <= 25%: 1-row bands allowed
+    if (w16 * 4 <= wmin * 5) {  // 16-aligned pitch wastes <= 25%: 1-row bands allowed
       for (int rows : {4, 2, 1}) geo.emplace_back(w16, rows);
+      // taller bands stage fewer halo rows per output row (the TMA row rate bounds
+      // these plans): half and whole small planes
+      for (int rows : {(P + 1) / 2, P})
+        if (rows > 4 && rows <= 16) geo.emplace_back(w16, rows);
+    }
     for (int m : {4, 2, 1}) geo.emplace_back(wmin, base_rows * m);
     for (int rows : {2, 1}) geo.emplace_back(w16, rows);
     for (auto& gr : geo) {
@@ -2441,15 +2446,16 @@ struct UpdEntry {
 namespace {
 
 std::string json_upd(const UpdLaunch& L, int pieces) {
-  char buf[512];
+  char buf[640];
   std::snprintf(buf, sizeof(buf),
                 "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
                 "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
                 "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d,\"a_in_tmem\":%d,\"drain\":%d,"
-                "\"drain_bufs\":%d}",
+                "\"drain_bufs\":%d,\"sw32\":%d,\"xs\":%d,\"pimg\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
                 L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, pieces, L.passes,
-                L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0, L.p.drain, L.p.drain_bufs);
+                L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0, L.p.drain, L.p.drain_bufs,
+                L.p.sw32, L.p.xs, L.p.pimg);
   return buf;
 }
 

@@ -21,9 +21,10 @@ struct P {
 //    3 baseline + the stage loop bound read from the parameter struct each stage
 //    4 baseline with the stage's descriptors built from runtime parameters
 template <int V>
-__global__ void __launch_bounds__(256, 1) kern(P p, long long* out) {
+__global__ void __launch_bounds__(512, 1) kern(P p, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar, full[2], empty[2];
+  __shared__ __align__(8) uint64_t bar, full[2], empty[2], never;
+  __shared__ volatile int done_flag;
   __shared__ uint32_t tbase_sh;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
@@ -31,6 +32,8 @@ __global__ void __launch_bounds__(256, 1) kern(P p, long long* out) {
   if (warp == 0) tmem_alloc(&tbase_sh, 512);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&never, 1);
+    done_flag = 0;
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -125,8 +128,88 @@ __global__ void __launch_bounds__(256, 1) kern(P p, long long* out) {
     mbar_wait(&bar, 0);
     return clock64() - t0;
   };
+  // V10: the whole MMA warp runs the stage loop (converged: every loop value is warp-uniform),
+  // all lanes wait the barriers, one elected lane issues the stage's MMAs and commits
+  auto body_warp = [&]() {
+    const uint32_t a_lo0 = static_cast<uint32_t>(make_smem_desc_sw32(a0));
+    const uint32_t b_lo0 = static_cast<uint32_t>(make_smem_desc(b0, 128, 256));
+    const uint32_t b_tap = (static_cast<uint32_t>(p.N) / 8u) * 256u >> 4;
+    const long long t0 = clock64();
+    int slot = 0;
+    for (int it = 0; it < 8192 / 8; ++it) {
+      mbar_wait(&full[slot], 1);
+      mbar_wait(&full[slot ^ 1], 1);
+      tc_fence_after();
+      const uint32_t ak0 = a_lo0 + static_cast<uint32_t>(slot) * 2048u;
+      const uint32_t bk0 = b_lo0 + static_cast<uint32_t>(slot) * 1024u;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ak = ak0 + 2u * static_cast<uint32_t>(kk * 256);
+          const uint32_t bk = bk0 + static_cast<uint32_t>(kk) * b_tap;
+#pragma unroll
+          for (int mb = 0; mb < 2; ++mb)
+            mma_bf16_lo(tbase + static_cast<uint32_t>(mb * p.N), ak + 256u * mb, ahi, bk, bhi, idesc,
+                        (it == 0 && kk == 0) ? 0u : 1u);
+        }
+        mma_commit(&empty[slot]);
+        mma_commit(&empty[slot ^ 1]);
+      }
+      __syncwarp();
+      slot ^= 1;
+    }
+    if (elect_one()) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    return clock64() - t0;
+  };
+  auto body_w1 = [&]() {
+    const uint32_t a_lo0 = static_cast<uint32_t>(make_smem_desc_sw32(a0));
+    const uint32_t b_lo0 = static_cast<uint32_t>(make_smem_desc(b0, 128, 256));
+    const uint32_t b_tap = (static_cast<uint32_t>(p.N) / 8u) * 256u >> 4;
+    const long long t0 = clock64();
+    int slot = 0;
+    for (int it = 0; it < 8192 / 4; ++it) {
+      mbar_wait(&full[slot], 1);
+      tc_fence_after();
+      const uint32_t ak0 = a_lo0 + static_cast<uint32_t>(slot) * 2048u;
+      const uint32_t bk0 = b_lo0;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_lo(tbase, ak0 + 2u * static_cast<uint32_t>(kk * 128), ahi, bk0 + static_cast<uint32_t>(kk) * b_tap,
+                      bhi, idesc, (it == 0 && kk == 0) ? 0u : 1u);
+        mma_commit(&empty[slot]);
+      }
+      __syncwarp();
+      slot ^= 1;
+    }
+    if (elect_one()) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    return clock64() - t0;
+  };
   long long t = 0;
-  if (V >= 5) {
+  if (V == 11 || V == 12 || V == 13 || V == 14) {
+    if (warp == 0) {
+      t = body_w1();
+      if (lane == 0) {
+        done_flag = 1;
+        mbar_arrive(&never);
+      }
+    } else if (warp >= 4 && V == 12) {  // waiters spinning on try_wait
+      mbar_wait(&never, 0);
+    } else if (warp >= 4 && V == 13) {  // waiters with back-off
+      mbar_wait_backoff(&never, 0);
+    } else if (warp >= 4 && V == 14) {  // ALU-busy warps (an epilogue's math)
+      float x = threadIdx.x;
+      while (!done_flag)
+        for (int i = 0; i < 64; ++i) x = x * 1.0001f + 0.5f;
+      if (x == 1.2345f) out[0] = 1;
+    }
+  } else if (V == 10) {
+    if (warp == 0) t = body_warp();
+  } else if (V >= 5) {
     if (warp == 0) {
       if (lane == 0) t = body_conv();
       __syncwarp();
@@ -141,7 +224,7 @@ __global__ void __launch_bounds__(256, 1) kern(P p, long long* out) {
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) out[blockIdx.x] = t;
+  if (threadIdx.x == 0) out[blockIdx.x] = t;  // (V10: lane 0's clock)
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
@@ -161,11 +244,11 @@ void run(int threads, int N, long long* d, int ring = 0) {
 int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  for (int N : {128}) {
-    run<6>(128, N, d);
-    run<7>(128, N, d);
-    run<8>(128, N, d);
-    run<9>(128, N, d);
+  for (int N : {256, 128}) {
+    run<11>(512, N, d);
+    run<12>(512, N, d);
+    run<13>(512, N, d);
+    run<14>(512, N, d);
   }
   return 0;
 }
