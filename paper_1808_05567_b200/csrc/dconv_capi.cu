@@ -777,13 +777,14 @@ void launch_fwd(const FwdLaunch& L, cudaStream_t stream, bool pdl, int prof_slot
 void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int nb,
                         int n_ntiles, int dual, int pieces, int nt_major, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(cb_in) * n_ntiles * n_taps * 2 * nb * 128;
+  if (total >= (int64_t{1} << 31)) fail(DCONV_ERR_UNSUPPORTED, "weight prep: more than 2^31 prepared weights");
   const int kbs = cdiv(w.k, 16), cbs = cdiv(w.c, 16);
   if (w.dtype == DCONV_F32)
-    weight_prep_kernel<float><<<grid1d(total), 256, 0, stream>>>(
+    weight_prep_kernel<float><<<grid1d(total / 8), 256, 0, stream>>>(
         reinterpret_cast<const float*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
         tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major);
   else
-    weight_prep_kernel<__nv_bfloat16><<<grid1d(total), 256, 0, stream>>>(
+    weight_prep_kernel<__nv_bfloat16><<<grid1d(total / 8), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
         tapmap_dev, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major);
   cuda_check(cudaGetLastError(), "weight_prep launch");
@@ -2695,7 +2696,7 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     }
     prof_end(2, cs);
     const int cb = cdiv(s.C, 16), kb = cdiv(s.K, 16);
-    const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 256;
+    const int64_t total = static_cast<int64_t>(kb) * cb * s.R * s.S * 64;  // k quads
     {
       // programmatic dependent launch: the reduce waits (griddepcontrol.wait) for the
       // update kernel that precedes it on this stream, before it reads the partials
@@ -2705,8 +2706,8 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
       cudaLaunchConfig_t lc = {};
       // split groups per element: enough memory-level parallelism for many splits,
       // all 256 threads on distinct elements when there are few
-      const int G = L.p.splits >= 32 ? kRedGroups : L.p.splits >= 8 ? 2 : 1;
-      const int TX = 256 / G;
+      const int G = L.p.splits >= 24 ? kRedGroups : L.p.splits >= 8 ? 2 : 1;
+      const int TX = G == 1 ? 256 : 64;  // (the group sums are exchanged through [G][64] float4)
       lc.gridDim = dim3(static_cast<unsigned>(cdiv64(total, TX)), 1, 1);
       lc.blockDim = dim3(TX, G, 1);
       lc.stream = cs;

@@ -232,8 +232,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t a_bytes = p.stack > 1 ? static_cast<uint32_t>(ntaps * (p.half ? 1 : 2 * p.cb_eff)) * L.a_plane
                                  : p.sw32     ? static_cast<uint32_t>(2 * p.cb_eff * mc) * L.a_plane
                                               : L.a_piece;
-        mbar_arrive_expect_tx(&full_bar[s], PA * a_bytes + PB * L.b_piece);
-        for (int pc = 0; pc < PA; ++pc) {
+        // dev ablation bits: 256 no operand loads, 512 no input loads, 1024 no dO loads
+        const int dbl = kDevBuild ? p.dbg_mode : 0;
+        if (dbl & 256) {
+          mbar_arrive(&full_bar[s]);
+          continue;
+        }
+        mbar_arrive_expect_tx(&full_bar[s], ((dbl & 512) ? 0u : PA * a_bytes) + ((dbl & 1024) ? 0u : PB * L.b_piece));
+        for (int pc = 0; pc < ((dbl & 512) ? 0 : PA); ++pc) {
           const int pa = (a_base + pc) * in_planes + n * p.in_cb + ctile * 8 * mc;
           uint8_t* a_dst = st + pc * L.a_piece;
           if (p.sw32) {  // 32 B pixel rows: {16, px[, rows], planes} boxes
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                         p.in_row0 + p.stride * band * p.rows_ps + p.phase_row[ph], 0, pa);
           }
         }
-        for (int pc = 0; pc < PB; ++pc) {
+        for (int pc = 0; pc < ((dbl & 1024) ? 0 : PB); ++pc) {
           const int pb = pc * do_planes + n * p.do_cb + ktile * p.nb;
           uint8_t* b_dst = st + L.b_off + pc * L.b_piece;
           if (p.sw32) {
@@ -323,7 +329,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc_fence_after();
           const uint32_t a_s = a_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
           const uint32_t b_s = b_lo0 + static_cast<uint32_t>(rp.idx) * slot_u;
-          if (KS > 0) {
+          if (kDevBuild && (p.dbg_mode & 8)) {  // dev ablation: no MMAs
+          } else if (KS > 0) {
             const uint32_t acc0 = it > 0 ? 1u : 0u;
 #pragma unroll
             for (int ks = 0; ks < (KS > 0 ? KS : 1); ++ks)
@@ -429,7 +436,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       const uint32_t acc_col0 = static_cast<uint32_t>(per_acc.buf(jd)) * buf_cols;
       const bool add_old = accumulate || jd > 0;
-    const int n_acc = p.stack > 1 ? xsn : (mc > 1 ? mc : ntaps);
+    // dev ablation bits: 4096 no epilogue, 2048 no partial stores
+    const int n_acc = ((kDevBuild ? p.dbg_mode : 0) & 4096) ? 0 : p.stack > 1 ? xsn : (mc > 1 ? mc : ntaps);
     for (int t = 0; t < n_acc; ++t) {
       const int c_glob = (ctile * mc + (mc > 1 ? t : 0)) * 128 + qrow + lane;
       // stacked: TMEM row = (slot j, channel c) of tap tap0 + j; cross-stacked: column
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t r[16];
         tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + acc_col0 + static_cast<uint32_t>(t * NT + g * 16), r);
         tmem_ld_wait();
-        if (!row_ok) continue;
+        if (!row_ok || ((kDevBuild ? p.dbg_mode : 0) & 2048)) continue;
         float4* d = reinterpret_cast<float4*>(dst_row + g * 16);
         const bool live = iters > 0;
 #pragma unroll
@@ -1136,68 +1144,96 @@ __global__ void __launch_bounds__(kUpdTsWarps * 32, 1)
 
 // Fixed-order reduction of the split partials into the blocked dW
 // [k_b][c_b][r][s][c][k] (tail lanes written as exact zeros).
-// reduce_weight_copies analog (propagation.cpp:357-375). Block = 32 partial
-// elements (coalesced along k) x kRedGroups split groups: group y sums splits
-// y, y + G, y + 2G, ... in increasing order, then the G group sums are added in
-// group order — the same fixed order on every run, so dW is bitwise reproducible.
-constexpr int kRedGroups = 8;  // max split groups per element (blockDim.y)
+// reduce_weight_copies analog (propagation.cpp:357-375). A thread owns four
+// consecutive k of one (tap, c) partial row (16 B loads, coalesced along k; one
+// 16 B / 8 B store into the dW block) and 32-bit index math; blockDim.y = G split
+// groups: group y sums splits y, y + G, y + 2G, ... in increasing order, then the
+// G group sums are added in group order -- the same fixed order on every run, so
+// dW is bitwise reproducible.
+constexpr int kRedGroups = 4;  // max split groups per element (blockDim.y)
 __global__ void __launch_bounds__(256)
     upd_reduce_kernel(const float* __restrict__ partial, int splits, int n_taps, int c_pad, int k_pad, int C, int K,
                       int cb, int kb, void* __restrict__ dw, int dw_bf16, int accumulate) {
-  // [G][TX + 1] with G * TX = 256 and G in {1, 2, 8}: at most 8 x 33 = 264 floats, so the
-  // reduce CTAs never crowd out the ~220 KB conv CTAs they run beside
-  __shared__ float red[kRedGroups * 33];
+  __shared__ float4 red[kRedGroups * 64];
   pdl_wait_primary();  // launched as a programmatic dependent of the UPD kernel
-  const int G = blockDim.y, TX = blockDim.x;  // G split groups x TX consecutive elements
-  const int kw = kb * 16, cw = cb * 16;
-  const long long total = static_cast<long long>(n_taps) * cw * kw;
-  const long long f = static_cast<long long>(blockIdx.x) * TX + threadIdx.x;
+  const int G = blockDim.y, TX = blockDim.x;
+  const int kq = kb * 4, cw = cb * 16;  // k quads per row, c rows per tap
+  const int total = n_taps * cw * kq;
+  const int f = blockIdx.x * TX + threadIdx.x;
   const int y = threadIdx.y;
   const bool in_range = f < total;
-  const int k = in_range ? static_cast<int>(f % kw) : 0;
-  const int c = in_range ? static_cast<int>((f / kw) % cw) : 0;
-  const int rs = in_range ? static_cast<int>(f / (static_cast<long long>(kw) * cw)) : 0;
+  const int k = in_range ? (f % kq) * 4 : 0;
+  const int rc = in_range ? f / kq : 0;
+  const int c = rc % cw, rs = rc / cw;
   const bool live = in_range && c < C && k < K;
   const long long split_stride = static_cast<long long>(n_taps) * c_pad * k_pad;
-  float sum = 0.0f;
+  float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live) {
-    const float* src = partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k;
-    // up to 12 independent loads in flight per thread before the (fixed-order) adds:
-    // the partials were just written by the update kernel, so this is L2 latency bound
+    const float4* src = reinterpret_cast<const float4*>(partial + (static_cast<long long>(rs) * c_pad + c) * k_pad + k);
+    const long long st4 = split_stride / 4;
+    // up to 8 independent 16 B loads in flight per thread before the (fixed-order) adds
     int sp = y;
-    for (; sp + 11 * G < splits; sp += 12 * G) {
-      float v[12];
+    for (; sp + 7 * G < splits; sp += 8 * G) {
+      float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 12; ++u) v[u] = __ldg(src + (sp + u * G) * split_stride);
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sp + u * G) * st4);
 #pragma unroll
-      for (int u = 0; u < 12; ++u) sum += v[u];
+      for (int u = 0; u < 8; ++u) {
+        sum.x += v[u].x;
+        sum.y += v[u].y;
+        sum.z += v[u].z;
+        sum.w += v[u].w;
+      }
     }
-    {
-      float v[12];
-#pragma unroll
-      for (int u = 0; u < 12; ++u) v[u] = (sp + u * G < splits) ? __ldg(src + (sp + u * G) * split_stride) : 0.0f;
-#pragma unroll
-      for (int u = 0; u < 12; ++u)
-        if (sp + u * G < splits) sum += v[u];
+    for (; sp < splits; sp += G) {
+      const float4 v = __ldg(src + sp * st4);
+      sum.x += v.x;
+      sum.y += v.y;
+      sum.z += v.z;
+      sum.w += v.w;
     }
   }
   if (G > 1) {
-    red[y * (TX + 1) + threadIdx.x] = sum;
+    red[y * 64 + threadIdx.x] = sum;
     __syncthreads();
     if (y != 0) return;
     sum = red[threadIdx.x];
-    for (int g = 1; g < G; ++g) sum += red[g * (TX + 1) + threadIdx.x];
+    for (int g = 1; g < G; ++g) {
+      const float4 v = red[g * 64 + threadIdx.x];
+      sum.x += v.x;
+      sum.y += v.y;
+      sum.z += v.z;
+      sum.w += v.w;
+    }
   }
   if (!in_range) return;
-  const float tot = live ? sum : 0.0f;
+  const bool cl_ok = c < C;
+  float t[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (!(cl_ok && k + j < K)) t[j] = 0.0f;
   const int kbi = k / 16, kl = k % 16, cbi = c / 16, cl = c % 16;
   const long long e = ((static_cast<long long>(kbi) * cb + cbi) * n_taps + rs) * 256 + cl * 16 + kl;
   if (dw_bf16) {
     __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dw) + e;
-    *d = __float2bfloat16_rn(accumulate ? tot + __bfloat162float(*d) : tot);
+    uint2 old = make_uint2(0u, 0u);
+    if (accumulate) old = *reinterpret_cast<const uint2*>(d);
+    const __nv_bfloat16* o = reinterpret_cast<const __nv_bfloat16*>(&old);
+    __align__(8) __nv_bfloat16 h[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __float2bfloat16_rn(accumulate ? t[j] + __bfloat162float(o[j]) : t[j]);
+    *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(h);
   } else {
-    float* d = reinterpret_cast<float*>(dw) + e;
-    *d = accumulate ? *d + tot : tot;
+    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(dw) + e);
+    float4 v = make_float4(t[0], t[1], t[2], t[3]);
+    if (accumulate) {
+      const float4 o = *d;
+      v.x = o.x + v.x;
+      v.y = o.y + v.y;
+      v.z = o.z + v.z;
+      v.w = o.w + v.w;
+    }
+    *d = v;
   }
 }
 

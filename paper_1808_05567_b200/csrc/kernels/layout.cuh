@@ -327,38 +327,50 @@ __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __r
   // the conv kernel launched after this one (programmatic dependent launch) may
   // start its prologue and activation loads now; it waits before reading weights
   pdl_launch_dependents();
-  const long long per_piece = static_cast<long long>(cb_in) * n_ntiles * n_taps * (2 * nb) * 128;
-  DCONV_GRID_STRIDE(e, per_piece) {
-    const int kk = static_cast<int>(e % 8);
-    const int ci = static_cast<int>((e / 8) % 16);
-    long long q = e / 128;
-    const int ng = static_cast<int>(q % (2 * nb));
+  // one thread per 8 output lanes (kk = 0..7: one 16 B store per piece), 32-bit
+  // indices (host-checked: a piece has < 2^31 elements)
+  const int per_piece = cb_in * n_ntiles * n_taps * (2 * nb) * 128;
+  const int n8 = per_piece / 8;
+  for (int e8 = blockIdx.x * blockDim.x + threadIdx.x; e8 < n8; e8 += gridDim.x * blockDim.x) {
+    const int ci = e8 % 16;
+    int q = e8 / 16;
+    const int ng = q % (2 * nb);
     q /= (2 * nb);
-    const int t = static_cast<int>(q % n_taps);
+    const int t = q % n_taps;
     q /= n_taps;
     // nt_major: [piece][n_tile][c_b][tap][2nb][16][8] -- one n-tile's channel blocks are
     // contiguous, so a streamed stage's kc blocks (all taps) are ONE bulk copy. Otherwise
     // [piece][c_b][n_tile][tap][..] (the fp32-activation plans keep the original layout)
-    const int cbi = nt_major ? static_cast<int>(q % cb_in) : static_cast<int>(q / n_ntiles);
-    const int nt = nt_major ? static_cast<int>(q / cb_in) : static_cast<int>(q % n_ntiles);
-    const int ob = nt * nb + ng / 2, ol = (ng % 2) * 8 + kk;  // out block / lane
-    const int ib = cbi, il = ci;                    // in block / lane
+    const int cbi = nt_major ? q % cb_in : q / n_ntiles;
+    const int nt = nt_major ? q / cb_in : q % n_ntiles;
+    const int ob = nt * nb + ng / 2, ol0 = (ng % 2) * 8;  // out block / first lane
     const int rs = tapmap[t];
-    float val = 0.0f;
-    if (rs >= 0) {
-      // blocked src [kb][cb][rs][c lane][k lane]
-      const int kb = dual ? ib : ob, cb = dual ? ob : ib;
-      const int cl = dual ? ol : il, kl = dual ? il : ol;
-      if (kb < kb_src && cb < cb_src)
-        val = to_f<S>(src[(((static_cast<long long>(kb) * cb_src + cb) * rs_src + rs) * 16 + cl) * 16 + kl]);
+    float val[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) val[kk] = 0.0f;
+    // blocked src [kb][cb][rs][c lane][k lane]
+    const int kb = dual ? cbi : ob, cb = dual ? ob : cbi;
+    if (rs >= 0 && kb < kb_src && cb < cb_src) {
+      const S* row = src + ((static_cast<long long>(kb) * cb_src + cb) * rs_src + rs) * 256;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)  // forward: 8 consecutive k lanes; backward-data: 8 c lanes (stride 16)
+        val[kk] = to_f<S>(dual ? row[(ol0 + kk) * 16 + ci] : row[ci * 16 + ol0 + kk]);
     }
-    const __nv_bfloat16 h = __float2bfloat16_rn(val);
-    dst[e] = h;
+    __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) h[kk] = __float2bfloat16_rn(val[kk]);
+    uint4* d = reinterpret_cast<uint4*>(dst) + e8;
+    *d = *reinterpret_cast<const uint4*>(h);
     if (pieces == 3) {
-      const float r1 = val - __bfloat162float(h);
-      const __nv_bfloat16 m = __float2bfloat16_rn(r1);
-      dst[e + per_piece] = m;
-      dst[e + 2 * per_piece] = __float2bfloat16_rn(r1 - __bfloat162float(m));
+      __align__(16) __nv_bfloat16 m[8], l[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const float r1 = val[kk] - __bfloat162float(h[kk]);
+        m[kk] = __float2bfloat16_rn(r1);
+        l[kk] = __float2bfloat16_rn(r1 - __bfloat162float(m[kk]));
+      }
+      d[n8] = *reinterpret_cast<const uint4*>(m);
+      d[2 * n8] = *reinterpret_cast<const uint4*>(l);
     }
   }
 }

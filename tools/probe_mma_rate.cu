@@ -7,6 +7,7 @@
 //   layout 2: A K-major SWIZZLE_128B, B K-major SWIZZLE_128B (plain GEMM tiles)
 //   layout 3: A in TMEM, B as 0
 //   layout 4: A K-major SWIZZLE_128B, B K-major no-swizzle
+//   layout 8: A and B MN-major SWIZZLE_32B (weight update: channels x pixels, LBO = block plane)
 // shift = 1: the A start address moves by a pixel row per MMA (3x3 tap pattern)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o probe_mma_rate probe_mma_rate.cu
 #include <cuda.h>
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(128, 1) probe(int N, int iters, int shift, lon
   const uint32_t tbase = tbase_sh;
   const uint32_t s0 = smem_u32(smem);
   const uint32_t a0 = s0, b0 = s0 + 64 * 1024;
-  const uint32_t idesc = make_idesc(1, 0, LAYOUT == 2 ? 0 : 1, 128, static_cast<uint32_t>(N));  // conv weights: MN-major
+  const uint32_t idesc = make_idesc(1, LAYOUT == 8 ? 1 : 0, LAYOUT == 2 ? 0 : 1, 128, static_cast<uint32_t>(N));  // conv weights: MN-major
   long long t = 0;
   if (warp == 0 && threadIdx.x == 0) {
     uint32_t alo[8], blo[8];
@@ -77,6 +78,10 @@ __global__ void __launch_bounds__(128, 1) probe(int N, int iters, int shift, lon
       } else if (LAYOUT == 5) {  // conv 1x1 stage, mb = 2, kc = 4: A (kk, mb) blocks, B per kk, D per mb
         ad = make_smem_desc_sw32(a0 + static_cast<uint32_t>(i >> 1) * 8192u + static_cast<uint32_t>(i & 1) * 4096u);
         bd = make_smem_desc(b0 + static_cast<uint32_t>(i >> 1) * 4096u, 128, 256);
+      } else if (LAYOUT == 8) {  // A: 8 planes of 160 px x 32 B; B: N/16 planes of 112 px x 32 B
+        ad = make_smem_desc_mn_sw32(a0 + (static_cast<uint32_t>(i & 3) * 16u + (shift ? static_cast<uint32_t>(i >> 2) * 17u : 0u)) * 32u,
+                                    160 * 32);
+        bd = make_smem_desc_mn_sw32(b0 + static_cast<uint32_t>(i & 3) * 16u * 32u, 112 * 32);
       } else if (LAYOUT == 4) {
         ad = desc_sw128(a0 + sh * 128u + (i & 3) * 32u);
         bd = make_smem_desc(b0 + (i & 3) * 4096u, 128, 256);
@@ -136,11 +141,12 @@ int main(int argc, char** argv) {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
   const char* names[] = {"A sw32 / B nosw", "A nosw16 / B nosw", "A sw128 / B sw128", "A tmem / B nosw",
-                         "A sw128 / B nosw", "conv 1x1 mb2 kc4", "1x1 ring", "1x1 ring acc0"};
-  for (int layout = 5; layout < 8; ++layout)
+                         "A sw128 / B nosw", "conv 1x1 mb2 kc4", "1x1 ring", "1x1 ring acc0", "upd A/B mn sw32"};
+  const int l0 = argc > 2 ? atoi(argv[2]) : 5, l1 = argc > 3 ? atoi(argv[3]) : 8;
+  for (int layout = l0; layout <= l1; ++layout)
     for (int shift = 0; shift < 2; ++shift) {
       if (layout == 3 && shift) continue;
-      for (int N : {64, 128}) {
+      for (int N : {64, 128, 256}) {
         for (int grid : {1, 148}) {
           if (layout == 0) run<0>(N, iters, shift, grid, d);
           if (layout == 1) run<1>(N, iters, shift, grid, d);
@@ -150,6 +156,7 @@ int main(int argc, char** argv) {
           if (layout == 5) run<5>(N, iters, shift, grid, d);
           if (layout == 6) run<6>(N, iters, shift, grid, d);
           if (layout == 7) run<7>(N, iters, shift, grid, d);
+          if (layout == 8) run<8>(N, iters, shift, grid, d);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) {
             printf("error %s\n", cudaGetErrorString(e));
