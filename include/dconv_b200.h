@@ -197,6 +197,16 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
                            const dconv_act_t* grad_in, const dconv_epilogue_t* ep, void* workspace,
                            dconv_stream_t stream);
 
+/* Batched weight preparation (executor extension; no reference counterpart): between
+ * dconv_prep_batch_begin() and dconv_prep_batch_end(stream), dconv_forward_ex /
+ * dconv_backward_data_ex calls with DCONV_EP_PREP_ONLY made by the calling thread
+ * record their weight preparation instead of launching it; _end launches every recorded
+ * preparation as ONE kernel on `stream` (its job table is a kernel parameter, so the
+ * launch is graph-capturable). The convs then run with DCONV_EP_WEIGHTS_READY on the
+ * same workspaces -- one launch per step instead of one per conv. */
+int dconv_prep_batch_begin(void);
+int dconv_prep_batch_end(dconv_stream_t stream);
+
 /* ---------------------------------------------------------------- graph-executor ops */
 /* 3x3 / stride 2 / pad 1 max pool (ResNet stem) on halo-0 blocked tensors;
  * argmax: n*c_b*P*Q*16 bytes, consumed by the backward (gather, no atomics) */

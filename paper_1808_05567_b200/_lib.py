@@ -85,7 +85,7 @@ EXPORTS = [
     "dconv_graph_replay", "dconv_graph_launches", "dconv_graph_num_tensors", "dconv_graph_num_convs",
     "dconv_graph_buckets", "dconv_graph_tensor", "dconv_graph_conv", "dconv_graph_grads", "dconv_graph_weights",
     "dconv_nccl_unique_id", "dconv_nccl_comm_create", "dconv_nccl_comm_destroy", "dconv_relu_mask", "dconv_scale_wt",
-    "dconv_set_sm_budget", "dconv_graph_profile", "dconv_subsample2",
+    "dconv_set_sm_budget", "dconv_graph_profile", "dconv_subsample2", "dconv_prep_batch_begin", "dconv_prep_batch_end",
 ]
 
 
@@ -142,6 +142,8 @@ def _bind(lib):
         "dconv_maxpool_bwd_pooled_mask": (i, [P(Act), vp, P(Act), P(Act), vp]),
         "dconv_s2d_act": (i, [P(Act), P(Act), i, vp]),
         "dconv_subsample2": (i, [P(Act), P(Act), i, vp]),
+        "dconv_prep_batch_begin": (i, []),
+        "dconv_prep_batch_end": (i, [vp]),
         "dconv_s2d_wt": (i, [P(Wt), P(Wt), i, vp]),
         "dconv_pack_s2d": (i, [vp, i, i, i, i, P(Act), i, vp]),
         "dconv_host_step_create": (i, [P(Spec), i, i, P(vp)]),

@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <array>
+#include <memory>
 
 #include "../../include/dconv_b200.h"
 #include "kernels/conv_fwd.cuh"
@@ -772,6 +773,9 @@ void launch_fwd(const FwdLaunch& L, cudaStream_t stream, bool pdl, int prof_slot
   cuda_check(cudaGetLastError(), "conv_fwd_kernel launch");
 }
 
+// dconv_prep_batch_begin .. _end: this thread's weight preps are recorded, not launched
+thread_local std::vector<PrepJob>* g_prep_rec = nullptr;
+
 // weight prep: src blocked weights -> bf16 pieces in the phase-sorted tap order
 // (tapmap_dev is uploaded once at plan creation so execute calls are graph-capturable)
 void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, void* dst, int cb_in, int nb,
@@ -779,6 +783,27 @@ void launch_weight_prep(const dconv_wt_t& w, int n_taps, const int* tapmap_dev, 
   const int64_t total = static_cast<int64_t>(cb_in) * n_ntiles * n_taps * 2 * nb * 128;
   if (total >= (int64_t{1} << 31)) fail(DCONV_ERR_UNSUPPORTED, "weight prep: more than 2^31 prepared weights");
   const int kbs = cdiv(w.k, 16), cbs = cdiv(w.c, 16);
+  if (g_prep_rec) {
+    PrepJob j;
+    j.src = w.data;
+    j.dst = dst;
+    j.tapmap = tapmap_dev;
+    j.src_bf16 = w.dtype == DCONV_F32 ? 0 : 1;
+    j.kb_src = kbs;
+    j.cb_src = cbs;
+    j.rs_src = w.r * w.s;
+    j.n_taps = n_taps;
+    j.cb_in = cb_in;
+    j.nb = nb;
+    j.n_ntiles = n_ntiles;
+    j.dual = dual;
+    j.pieces = pieces;
+    j.nt_major = nt_major;
+    j.n8 = static_cast<int>(total / 8);
+    j.off8 = 0;
+    g_prep_rec->push_back(j);
+    return;
+  }
   if (w.dtype == DCONV_F32)
     weight_prep_kernel<float><<<grid1d(total / 8), 256, 0, stream>>>(
         reinterpret_cast<const float*>(w.data), reinterpret_cast<__nv_bfloat16*>(dst), kbs, cbs, w.r * w.s,
@@ -971,6 +996,36 @@ const char* dconv_last_error(void) { return g_err.c_str(); }
 void dconv_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
 // the DCONV_* developer overrides for graph.cu (null outside developer mode)
 const char* dconv_internal_dev_env(const char* name) { return dev_env(name); }
+
+int dconv_prep_batch_begin(void) {
+  return guarded([&] {
+    if (g_prep_rec) fail(DCONV_ERR_INVALID_ARGUMENT, "prep_batch_begin: a batch is already open on this thread");
+    g_prep_rec = new std::vector<PrepJob>();
+  });
+}
+
+int dconv_prep_batch_end(dconv_stream_t stream) {
+  std::unique_ptr<std::vector<PrepJob>> jobs(g_prep_rec);
+  g_prep_rec = nullptr;
+  return guarded([&] {
+    if (!jobs) fail(DCONV_ERR_INVALID_ARGUMENT, "prep_batch_end: no open batch on this thread");
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    for (size_t j0 = 0; j0 < jobs->size(); j0 += kPrepBatchMax) {
+      PrepBatch b;
+      b.n_jobs = static_cast<int>(std::min<size_t>(kPrepBatchMax, jobs->size() - j0));
+      int64_t off = 0;
+      for (int j = 0; j < b.n_jobs; ++j) {
+        b.job[j] = (*jobs)[j0 + j];
+        b.job[j].off8 = static_cast<int>(off);
+        off += b.job[j].n8;
+      }
+      if (off >= (int64_t{1} << 31)) fail(DCONV_ERR_UNSUPPORTED, "prep_batch_end: more than 2^31 prepared groups");
+      b.total8 = static_cast<int>(off);
+      weight_prep_batch_kernel<<<grid1d(off), 256, 0, cs>>>(b);
+      cuda_check(cudaGetLastError(), "weight_prep_batch launch");
+    }
+  });
+}
 
 const char* dconv_status_string(int s) {
   switch (s) {
@@ -1476,6 +1531,8 @@ int dconv_forward_ex(dconv_fwd_plan_t plan, const dconv_act_t* in, const dconv_w
       fail(DCONV_ERR_PLAN_TENSOR_MISMATCH, "forward: output halo differs from the plan's output surface");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (plan->inner) {  // vlen != 16: re-block around the 16-lane twin
+      if (ep && (ep->flags & (DCONV_EP_PREP_ONLY | DCONV_EP_WEIGHTS_READY)))
+        fail(DCONV_ERR_UNSUPPORTED, "weight preparation flags need vlen 16 tensors");
       reblock_epilogue_check(ep);
       if (in->dtype != out->dtype || wt->dtype != in->dtype)
         fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: input, weights and output share one dtype");
@@ -1652,6 +1709,15 @@ int dconv_backward_data(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dconv
   return dconv_backward_data_ex(plan, wt, grad_out, grad_in, nullptr, workspace, stream);
 }
 
+// weight preparations one backward-data execute launches (graph executor accounting)
+int dconv_internal_bwd_prep_launches(dconv_bwd_plan_t plan) {
+  if (!plan) return 0;
+  if (plan->inner) return dconv_internal_bwd_prep_launches(plan->inner);
+  int n = 0;
+  for (auto& ph : plan->phases) n += ph.zero ? 0 : 1;
+  return n;
+}
+
 int dconv_bwd_launches(dconv_bwd_plan_t plan) {
   if (!plan) return 0;
   if (plan->inner) return dconv_bwd_launches(plan->inner) + 3;
@@ -1740,6 +1806,8 @@ int dconv_backward_data_ex(dconv_bwd_plan_t plan, const dconv_wt_t* wt, const dc
       fail(DCONV_ERR_SHAPE_MISMATCH, "backward: grad_in does not match the layer spec");
     cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
     if (plan->inner) {  // vlen != 16: re-block around the 16-lane twin
+      if (ep && (ep->flags & (DCONV_EP_PREP_ONLY | DCONV_EP_WEIGHTS_READY)))
+        fail(DCONV_ERR_UNSUPPORTED, "weight preparation flags need vlen 16 tensors");
       reblock_epilogue_check(ep);
       if (grad_out->dtype != grad_in->dtype || wt->dtype != grad_out->dtype)
         fail(DCONV_ERR_UNSUPPORTED, "vlen != 16: grad_out, weights and grad_in share one dtype");

@@ -39,6 +39,7 @@
 
 extern "C" void dconv_internal_set_error(const char* msg);  // dconv_capi.cu
 extern "C" const char* dconv_internal_dev_env(const char* name);  // dconv_capi.cu (developer mode only)
+extern "C" int dconv_internal_bwd_prep_launches(dconv_bwd_plan_t plan);  // dconv_capi.cu: weight preps per execute
 
 namespace {
 
@@ -137,6 +138,14 @@ struct Conv {
   float* s2d_dw = nullptr;
   int bucket = -1;
   cudaEvent_t ev_gready = nullptr, ev_dw = nullptr;
+  // prepared weights: every step's forward prepares all forward and backward-data
+  // weights in one batched launch (dconv_prep_batch_*) into these per-conv workspaces
+  void* ws_f = nullptr;
+  void* ws_b = nullptr;
+  // the backward-data epilogue operands (fixed by the graph; computed once at build):
+  // the other branch's gradient to add (or this gradient itself, accumulating), the mask
+  const void* b_add = nullptr;
+  const void* b_mask = nullptr;
 };
 
 struct Bucket {
@@ -409,6 +418,45 @@ void build(dconv_graph* g, int in_c, int in_h, int in_w) {
   }
   g->ws_main = dalloc(g, g->ws_main_bytes);
   g->ws_upd = dalloc(g, g->ws_upd_bytes);
+  for (Conv& cv : g->convs) {
+    cv.ws_f = dalloc(g, dconv_fwd_workspace_bytes(cv.fp));
+    if (cv.bp) cv.ws_b = dalloc(g, dconv_bwd_workspace_bytes(cv.bp));
+  }
+  // backward-data epilogue operands, in the backward walk's order: a tensor's first
+  // data-gradient contribution adds the identity-shortcut consumer's gradient (if any),
+  // later ones accumulate in place; lattice consumers sum into the lattice gradient
+  {
+    std::vector<char> written(g->t.size(), 0);
+    std::vector<int> sub_done(g->t.size(), 0);
+    for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
+      const dconv_graph_node_t& nd = g->nodes[i];
+      if (nd.kind == DCONV_NODE_MAXPOOL) {
+        written[nd.src] = 1;
+        continue;
+      }
+      Conv& cv = g->convs[g->conv_of_node[i]];
+      if (nd.src == 0) continue;
+      Tensor& x = g->t[nd.src];
+      if (cv.sub) {
+        cv.b_add = sub_done[nd.src] > 0 ? x.sub_grad : nullptr;
+        cv.b_mask = x.relu ? x.sub_act : nullptr;
+        if (++sub_done[nd.src] == x.sub_consumers) written[nd.src] = 1;
+        continue;
+      }
+      cv.b_mask = x.relu ? x.act : nullptr;
+      cv.b_add = nullptr;
+      if (written[nd.src]) {
+        cv.b_add = x.grad;  // second contribution: accumulate in place
+      } else {
+        for (size_t j = 0; j < g->nodes.size(); ++j)  // identity-shortcut consumer of src
+          if (g->nodes[j].kind == DCONV_NODE_CONV && g->nodes[j].add == nd.src) {
+            cv.b_add = g->t[j + 1].grad;
+            break;
+          }
+      }
+      written[nd.src] = 1;
+    }
+  }
   cuck(cudaStreamCreateWithFlags(&g->s_upd, cudaStreamNonBlocking), "stream");
   cuck(cudaStreamCreateWithFlags(&g->s_comm, cudaStreamNonBlocking), "stream");
   cuck(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "event");
@@ -425,9 +473,52 @@ dconv_epilogue_t epi(const void* add, const void* mask, int relu) {
   return e;
 }
 
+// the data-gradient tensor a conv's backward-data writes (lattice consumers: the lattice gradient)
+dconv_act_t bwd_out(const dconv_graph* g, const Conv& cv) {
+  return cv.sub ? conv_in(g, cv, true) : act_of(g, g->nodes[cv.node].src, true);
+}
+
+// every conv's forward and backward-data weights, prepared in one batched launch
+void prepare_weights(dconv_graph* g, cudaStream_t s) {
+  dconv_stream_t st = reinterpret_cast<dconv_stream_t>(s);
+  for (Conv& cv : g->convs)
+    if (cv.s2d) {  // the space-to-depth stem's weights are transformed first
+      const dconv_wt_t w = conv_w(g, cv, false);
+      const dconv_wt_t w2 = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
+      ck(dconv_s2d_wt(&w, &w2, 0, st), "graph s2d weights");
+      g->launches += 1;
+    }
+  ck(dconv_prep_batch_begin(), "graph weight prep");
+  int jobs = 0;
+  const int rc = gguard([&] {
+    for (Conv& cv : g->convs) {
+      const dconv_graph_node_t& nd = g->nodes[cv.node];
+      dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
+      e.flags = DCONV_EP_PREP_ONLY;
+      const dconv_act_t x = conv_in(g, cv, false), out = act_of(g, cv.node + 1, false);
+      const dconv_wt_t w = cv.s2d ? wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S)
+                                  : conv_w(g, cv, false);
+      ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, cv.ws_f, st), "graph forward weight prep");
+      jobs += 1;
+      if (!cv.bp) continue;
+      dconv_epilogue_t eb = epi(cv.b_add, cv.b_mask, 0);
+      eb.flags = DCONV_EP_PREP_ONLY;
+      const dconv_act_t go = act_of(g, cv.node + 1, true), gi = bwd_out(g, cv);
+      const dconv_wt_t wb = conv_w(g, cv, false);
+      ck(dconv_backward_data_ex(cv.bp, &wb, &go, &gi, &eb, cv.ws_b, st), "graph backward weight prep");
+      jobs += dconv_internal_bwd_prep_launches(cv.bp);
+    }
+  });
+  const int rc_end = dconv_prep_batch_end(st);  // (closes the batch even after an error)
+  if (rc != DCONV_OK) gfail(rc, dconv_last_error());
+  ck(rc_end, "graph weight prep launch");
+  g->launches += (jobs + 127) / 128;
+}
+
 void forward(dconv_graph* g, cudaStream_t s) {
   dconv_stream_t st = reinterpret_cast<dconv_stream_t>(s);
   std::vector<char> subbed(g->t.size(), 0);
+  prepare_weights(g, s);
   for (size_t i = 0; i < g->nodes.size(); ++i) {
     const dconv_graph_node_t& nd = g->nodes[i];
     const dconv_act_t src = act_of(g, nd.src, false), out = act_of(g, static_cast<int>(i) + 1, false);
@@ -437,7 +528,8 @@ void forward(dconv_graph* g, cudaStream_t s) {
       continue;
     }
     Conv& cv = g->convs[g->conv_of_node[i]];
-    const dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
+    dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
+    e.flags = DCONV_EP_WEIGHTS_READY;  // prepare_weights
     dconv_act_t x = src;
     dconv_wt_t w = conv_w(g, cv, false);
     if (cv.s2d) {
@@ -450,11 +542,8 @@ void forward(dconv_graph* g, cudaStream_t s) {
         ck(dconv_s2d_act(&src, &xs, nd.pad_h, st), "graph s2d input");
         g->launches += 1;
       }
-      const dconv_wt_t w2 = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
-      ck(dconv_s2d_wt(&w, &w2, 0, st), "graph s2d weights");
-      g->launches += 1;
       x = xs;
-      w = w2;
+      w = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
     }
     if (cv.sub) {  // the first strided consumer makes the lattice copy
       x = conv_in(g, cv, false);
@@ -464,8 +553,8 @@ void forward(dconv_graph* g, cudaStream_t s) {
         subbed[nd.src] = 1;
       }
     }
-    ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, g->ws_main, st), "graph forward");
-    g->launches += dconv_fwd_launches(cv.fp);
+    ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, cv.ws_f, st), "graph forward");
+    g->launches += dconv_fwd_launches(cv.fp) - 1;  // (weights prepared)
   }
 }
 
@@ -538,12 +627,13 @@ void backward(dconv_graph* g, const dconv_act_t* dtop, cudaStream_t s) {
       // lattice consumers: stride-1 backward-data into the lattice gradient (the
       // consumers' sum and the ReLU mask -- the lattice copy -- fused), scattered back
       // to the full-size gradient (zeros off the lattice) after the last consumer
-      const dconv_act_t go = act_of(g, i + 1, true), gi = conv_in(g, cv, true);
+      const dconv_act_t go = act_of(g, i + 1, true), gi = bwd_out(g, cv);
       Tensor& x = g->t[nd.src];
-      const dconv_epilogue_t e = epi(sub_done[nd.src] > 0 ? x.sub_grad : nullptr, x.relu ? x.sub_act : nullptr, 0);
+      dconv_epilogue_t e = epi(cv.b_add, cv.b_mask, 0);
+      e.flags = DCONV_EP_WEIGHTS_READY;  // prepare_weights
       const dconv_wt_t w = conv_w(g, cv, false);
-      ck(dconv_backward_data_ex(cv.bp, &w, &go, &gi, &e, g->ws_main, st), "graph backward");
-      g->launches += dconv_bwd_launches(cv.bp);
+      ck(dconv_backward_data_ex(cv.bp, &w, &go, &gi, &e, cv.ws_b, st), "graph backward");
+      g->launches += dconv_bwd_launches(cv.bp) - dconv_internal_bwd_prep_launches(cv.bp);
       if (++sub_done[nd.src] == x.sub_consumers) {
         const dconv_act_t full = act_of(g, nd.src, true);
         ck(dconv_subsample2(&full, &gi, 1, st), "graph lattice scatter");
@@ -553,22 +643,13 @@ void backward(dconv_graph* g, const dconv_act_t* dtop, cudaStream_t s) {
       continue;
     }
     // data gradient of the conv input, through the ReLU of that tensor, summing branches
-    const dconv_act_t go = act_of(g, i + 1, true), gi = act_of(g, nd.src, true);
-    const void* mask = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
-    const void* add = nullptr;
-    if (written[nd.src]) {
-      add = gi.data;  // second contribution: accumulate in place
-    } else {
-      for (size_t j = 0; j < g->nodes.size(); ++j)  // identity-shortcut consumer of src
-        if (g->nodes[j].kind == DCONV_NODE_CONV && g->nodes[j].add == nd.src) {
-          add = g->t[j + 1].grad;
-          break;
-        }
-    }
-    const dconv_epilogue_t e = epi(add, mask, 0);
+    // (epilogue operands: Conv::b_add / b_mask, fixed at build)
+    const dconv_act_t go = act_of(g, i + 1, true), gi = bwd_out(g, cv);
+    dconv_epilogue_t e = epi(cv.b_add, cv.b_mask, 0);
+    e.flags = DCONV_EP_WEIGHTS_READY;  // prepare_weights
     const dconv_wt_t w = conv_w(g, cv, false);
-    ck(dconv_backward_data_ex(cv.bp, &w, &go, &gi, &e, g->ws_main, st), "graph backward");
-    g->launches += dconv_bwd_launches(cv.bp);
+    ck(dconv_backward_data_ex(cv.bp, &w, &go, &gi, &e, cv.ws_b, st), "graph backward");
+    g->launches += dconv_bwd_launches(cv.bp) - dconv_internal_bwd_prep_launches(cv.bp);
     written[nd.src] = 1;
   }
   if (g->s_upd) {  // join: every dW final
@@ -765,39 +846,6 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
     cudaEvent_t e0, e1;
     cuck(cudaEventCreate(&e0), "event");
     cuck(cudaEventCreate(&e1), "event");
-    // each conv's backward epilogue exactly as backward() forms it (mask, branch sum)
-    std::vector<const void*> b_add(g->convs.size(), nullptr), b_mask(g->convs.size(), nullptr);
-    {
-      std::vector<char> written(g->t.size(), 0);
-      std::vector<int> sub_done(g->t.size(), 0);
-      for (int i = static_cast<int>(g->nodes.size()) - 1; i >= 0; --i) {
-        const dconv_graph_node_t& nd = g->nodes[i];
-        if (nd.kind == DCONV_NODE_MAXPOOL) {
-          written[nd.src] = 1;
-          continue;
-        }
-        const int ci = g->conv_of_node[i];
-        if (nd.src == 0) continue;
-        if (g->convs[ci].sub) {
-          const Tensor& x = g->t[nd.src];
-          b_mask[ci] = x.relu ? x.sub_act : nullptr;
-          b_add[ci] = sub_done[nd.src]++ > 0 ? x.sub_grad : nullptr;
-          if (sub_done[nd.src] == x.sub_consumers) written[nd.src] = 1;
-          continue;
-        }
-        b_mask[ci] = g->t[nd.src].relu ? g->t[nd.src].act : nullptr;
-        if (written[nd.src]) {
-          b_add[ci] = g->t[nd.src].grad;
-        } else {
-          for (size_t j = 0; j < g->nodes.size(); ++j)
-            if (g->nodes[j].kind == DCONV_NODE_CONV && g->nodes[j].add == nd.src) {
-              b_add[ci] = g->t[j + 1].grad;
-              break;
-            }
-        }
-        written[nd.src] = 1;
-      }
-    }
     auto timed = [&](auto&& fn) -> float {
       fn();  // warm
       float best = 1e30f;
@@ -819,15 +867,18 @@ int dconv_graph_profile(dconv_graph_t g, const dconv_act_t* dtop, int reps, floa
       const dconv_act_t x = conv_in(g, cv, false);
       dconv_wt_t w = conv_w(g, cv, false);
       if (cv.s2d) w = wt_view(cv.s2d_w, cv.pspec.K, cv.pspec.C, cv.pspec.R, cv.pspec.S);
-      const dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
-      ms[3 * ci + 0] = timed([&] { ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, g->ws_main, st), "profile fwd"); });
+      // as the step runs them: weights prepared (by the forward above), fused epilogues
+      dconv_epilogue_t e = epi(nd.add >= 0 ? g->t[nd.add].act : nullptr, nullptr, nd.relu);
+      e.flags = DCONV_EP_WEIGHTS_READY;
+      ms[3 * ci + 0] = timed([&] { ck(dconv_forward_ex(cv.fp, &x, &w, &out, &e, cv.ws_f, st), "profile fwd"); });
       ms[3 * ci + 1] = 0.0f;
       if (cv.bp) {
-        const dconv_act_t go = act_of(g, cv.node + 1, true), gi = conv_in(g, cv, true);
-        const dconv_epilogue_t eb = epi(b_add[ci], b_mask[ci], 0);
+        const dconv_act_t go = act_of(g, cv.node + 1, true), gi = bwd_out(g, cv);
+        dconv_epilogue_t eb = epi(cv.b_add, cv.b_mask, 0);
+        eb.flags = DCONV_EP_WEIGHTS_READY;
         const dconv_wt_t wf = conv_w(g, cv, false);
         ms[3 * ci + 1] =
-            timed([&] { ck(dconv_backward_data_ex(cv.bp, &wf, &go, &gi, &eb, g->ws_main, st), "profile bwd"); });
+            timed([&] { ck(dconv_backward_data_ex(cv.bp, &wf, &go, &gi, &eb, cv.ws_b, st), "profile bwd"); });
       }
       ms[3 * ci + 2] = timed([&] { update(g, cv, s); });
     }

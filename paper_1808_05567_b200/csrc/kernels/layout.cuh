@@ -320,6 +320,56 @@ __global__ void rehalo_kernel(const T* __restrict__ src, T* __restrict__ dst, in
 // tapmap[t] = source tap r*S+s (or -1 for an all-zero tap).
 // dual = 0: out = k, in = c (forward). dual = 1: out = c, in = k (backward-data).
 // pieces = 3 stores the exact hi/mid/lo bf16 split of each fp32 weight.
+// one thread's share of a weight prep: the 8 output lanes (kk = 0..7, one 16 B store
+// per piece) of prepared element group e8, 32-bit indices (host-checked: a piece has
+// < 2^31 elements)
+template <typename S>
+__device__ __forceinline__ void weight_prep8(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
+                                             int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps,
+                                             int cb_in, int nb, int n_ntiles, int dual, int pieces, int nt_major,
+                                             int n8, int e8) {
+  const int ci = e8 % 16;
+  int q = e8 / 16;
+  const int ng = q % (2 * nb);
+  q /= (2 * nb);
+  const int t = q % n_taps;
+  q /= n_taps;
+  // nt_major: [piece][n_tile][c_b][tap][2nb][16][8] -- one n-tile's channel blocks are
+  // contiguous, so a streamed stage's kc blocks (all taps) are ONE bulk copy. Otherwise
+  // [piece][c_b][n_tile][tap][..] (the fp32-activation plans keep the original layout)
+  const int cbi = nt_major ? q % cb_in : q / n_ntiles;
+  const int nt = nt_major ? q / cb_in : q % n_ntiles;
+  const int ob = nt * nb + ng / 2, ol0 = (ng % 2) * 8;  // out block / first lane
+  const int rs = tapmap[t];
+  float val[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) val[kk] = 0.0f;
+  // blocked src [kb][cb][rs][c lane][k lane]
+  const int kb = dual ? cbi : ob, cb = dual ? ob : cbi;
+  if (rs >= 0 && kb < kb_src && cb < cb_src) {
+    const S* row = src + ((static_cast<long long>(kb) * cb_src + cb) * rs_src + rs) * 256;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)  // forward: 8 consecutive k lanes; backward-data: 8 c lanes (stride 16)
+      val[kk] = to_f<S>(dual ? row[(ol0 + kk) * 16 + ci] : row[ci * 16 + ol0 + kk]);
+  }
+  __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) h[kk] = __float2bfloat16_rn(val[kk]);
+  uint4* d = reinterpret_cast<uint4*>(dst) + e8;
+  *d = *reinterpret_cast<const uint4*>(h);
+  if (pieces == 3) {
+    __align__(16) __nv_bfloat16 m[8], l[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const float r1 = val[kk] - __bfloat162float(h[kk]);
+      m[kk] = __float2bfloat16_rn(r1);
+      l[kk] = __float2bfloat16_rn(r1 - __bfloat162float(m[kk]));
+    }
+    d[n8] = *reinterpret_cast<const uint4*>(m);
+    d[2 * n8] = *reinterpret_cast<const uint4*>(l);
+  }
+}
+
 template <typename S>
 __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __restrict__ dst, int kb_src,
                                    int cb_src, int rs_src, const int* __restrict__ tapmap, int n_taps, int cb_in,
@@ -327,51 +377,43 @@ __global__ void weight_prep_kernel(const S* __restrict__ src, __nv_bfloat16* __r
   // the conv kernel launched after this one (programmatic dependent launch) may
   // start its prologue and activation loads now; it waits before reading weights
   pdl_launch_dependents();
-  // one thread per 8 output lanes (kk = 0..7: one 16 B store per piece), 32-bit
-  // indices (host-checked: a piece has < 2^31 elements)
-  const int per_piece = cb_in * n_ntiles * n_taps * (2 * nb) * 128;
-  const int n8 = per_piece / 8;
-  for (int e8 = blockIdx.x * blockDim.x + threadIdx.x; e8 < n8; e8 += gridDim.x * blockDim.x) {
-    const int ci = e8 % 16;
-    int q = e8 / 16;
-    const int ng = q % (2 * nb);
-    q /= (2 * nb);
-    const int t = q % n_taps;
-    q /= n_taps;
-    // nt_major: [piece][n_tile][c_b][tap][2nb][16][8] -- one n-tile's channel blocks are
-    // contiguous, so a streamed stage's kc blocks (all taps) are ONE bulk copy. Otherwise
-    // [piece][c_b][n_tile][tap][..] (the fp32-activation plans keep the original layout)
-    const int cbi = nt_major ? q % cb_in : q / n_ntiles;
-    const int nt = nt_major ? q / cb_in : q % n_ntiles;
-    const int ob = nt * nb + ng / 2, ol0 = (ng % 2) * 8;  // out block / first lane
-    const int rs = tapmap[t];
-    float val[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) val[kk] = 0.0f;
-    // blocked src [kb][cb][rs][c lane][k lane]
-    const int kb = dual ? cbi : ob, cb = dual ? ob : cbi;
-    if (rs >= 0 && kb < kb_src && cb < cb_src) {
-      const S* row = src + ((static_cast<long long>(kb) * cb_src + cb) * rs_src + rs) * 256;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)  // forward: 8 consecutive k lanes; backward-data: 8 c lanes (stride 16)
-        val[kk] = to_f<S>(dual ? row[(ol0 + kk) * 16 + ci] : row[ci * 16 + ol0 + kk]);
+  const int n8 = cb_in * n_ntiles * n_taps * (2 * nb) * 16;
+  for (int e8 = blockIdx.x * blockDim.x + threadIdx.x; e8 < n8; e8 += gridDim.x * blockDim.x)
+    weight_prep8(src, dst, kb_src, cb_src, rs_src, tapmap, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major, n8,
+                 e8);
+}
+
+// Batched weight prep (dconv_prep_batch_*): many convs' preparations in one launch.
+// The job table travels as a kernel parameter (graph-capturable, no device table);
+// job j owns the element groups [off8, off8 + n8) of the launch.
+struct PrepJob {
+  const void* src;
+  void* dst;
+  const int* tapmap;
+  int src_bf16, kb_src, cb_src, rs_src, n_taps, cb_in, nb, n_ntiles, dual, pieces, nt_major, n8, off8;
+};
+constexpr int kPrepBatchMax = 128;  // ~10 KB of kernel parameters (CUDA >= 12.1: up to 32 KB)
+struct PrepBatch {
+  int n_jobs, total8;
+  PrepJob job[kPrepBatchMax];
+};
+
+__global__ void __launch_bounds__(256) weight_prep_batch_kernel(const __grid_constant__ PrepBatch b) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < b.total8; g += gridDim.x * blockDim.x) {
+    int lo = 0, hi = b.n_jobs - 1;  // last job with off8 <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (b.job[mid].off8 <= g) lo = mid;
+      else hi = mid - 1;
     }
-    __align__(16) __nv_bfloat16 h[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) h[kk] = __float2bfloat16_rn(val[kk]);
-    uint4* d = reinterpret_cast<uint4*>(dst) + e8;
-    *d = *reinterpret_cast<const uint4*>(h);
-    if (pieces == 3) {
-      __align__(16) __nv_bfloat16 m[8], l[8];
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const float r1 = val[kk] - __bfloat162float(h[kk]);
-        m[kk] = __float2bfloat16_rn(r1);
-        l[kk] = __float2bfloat16_rn(r1 - __bfloat162float(m[kk]));
-      }
-      d[n8] = *reinterpret_cast<const uint4*>(m);
-      d[2 * n8] = *reinterpret_cast<const uint4*>(l);
-    }
+    const PrepJob& j = b.job[lo];
+    const int e8 = g - j.off8;
+    if (j.src_bf16)
+      weight_prep8(static_cast<const __nv_bfloat16*>(j.src), static_cast<__nv_bfloat16*>(j.dst), j.kb_src, j.cb_src,
+                   j.rs_src, j.tapmap, j.n_taps, j.cb_in, j.nb, j.n_ntiles, j.dual, j.pieces, j.nt_major, j.n8, e8);
+    else
+      weight_prep8(static_cast<const float*>(j.src), static_cast<__nv_bfloat16*>(j.dst), j.kb_src, j.cb_src, j.rs_src,
+                   j.tapmap, j.n_taps, j.cb_in, j.nb, j.n_ntiles, j.dual, j.pieces, j.nt_major, j.n8, e8);
   }
 }
 
