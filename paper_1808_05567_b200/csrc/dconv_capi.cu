@@ -1909,6 +1909,8 @@ struct UpdLaunch {
   UpdParams p;
   int passes;  // 1, or 3 (one A piece per pass)
   CUtensorMap map_in, map_do;
+  CUtensorMap map_part;  // partials [split][tap][c_pad] rows x k_pad fp32 (UpdParams::epi_tma)
+  const void* part_ptr = nullptr;  // the partial buffer map_part was encoded for
   dim3 grid;
   int stages;
   size_t smem;
@@ -2376,6 +2378,13 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
         (dout.h * dout.w) % 4 == 0 && !DCONV_ENV("DCONV_UPD_NO_SW128"))
       p.sw32 = 2;
   }
+  // partials through TMA stores: bf16 single-period plans whose epilogue warps each own
+  // 32 consecutive partial rows of one tap (staging: 16 KB of the idle operand ring)
+  p.epi_tma = (!L.raw && !L.tsa && pieces == 1 && p.sw32 && !p.lsu && p.drain == 0 &&
+               (p.stack == 1 || (!p.half && (16 * p.cb_eff) % 32 == 0)) && L.smem >= 16384 &&
+               !DCONV_ENV("DCONV_UPD_NO_EPI_TMA"))
+                  ? 1
+                  : 0;
   if (!encode_maps) return L;
   encode_upd_maps(L, pl, in, dout, in_pieces, do_pieces);
   return L;
@@ -2520,11 +2529,11 @@ std::string json_upd(const UpdLaunch& L, int pieces) {
                 "{\"mode\":\"%s\",\"wsub\":%d,\"rows_ps\":%d,\"vs\":%d,\"a_px\":%d,\"nb\":%d,\"tap_groups\":%d,"
                 "\"tg\":%d,\"splits\":%d,\"stages\":%d,\"smem\":%zu,\"grid\":[%u,%u,%u],\"pieces\":%d,\"passes\":%d,"
                 "\"smem_convert\":%d,\"raw_stages\":%d,\"pc_stages\":%d,\"cat\":%d,\"a_in_tmem\":%d,\"drain\":%d,"
-                "\"drain_bufs\":%d,\"sw32\":%d,\"xs\":%d,\"pimg\":%d}",
+                "\"drain_bufs\":%d,\"sw32\":%d,\"xs\":%d,\"pimg\":%d,\"epi_tma\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.rows_ps, L.p.vs, L.p.a_px, L.p.nb, L.p.n_tgroups,
                 L.p.tg, L.p.splits, L.stages, L.smem, L.grid.x, L.grid.y, L.grid.z, pieces, L.passes,
                 L.raw ? 1 : 0, L.raw_stages, L.pc_stages, L.cat ? 1 : 0, L.tsa ? 1 : 0, L.p.drain, L.p.drain_bufs,
-                L.p.sw32, L.p.xs, L.p.pimg);
+                L.p.sw32, L.p.xs, L.p.pimg, L.p.epi_tma);
   return buf;
 }
 
@@ -2717,6 +2726,16 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
         e.do_ptr = do_pc;
         e.maps = true;
       }
+      const void* part = ws + e.L.ws_in + e.L.ws_do;
+      if (e.L.p.epi_tma && e.L.part_ptr != part) {  // partial rows x k_pad fp32, 32 x 16 boxes
+        const UpdParams& q = e.L.p;
+        const uint64_t dims[2] = {static_cast<uint64_t>(q.k_pad),
+                                  static_cast<uint64_t>(q.splits) * q.n_taps * q.c_pad};
+        const uint64_t strides[1] = {static_cast<uint64_t>(q.k_pad) * 4};
+        const uint32_t box[2] = {16, 32};
+        e.L.map_part = encode(0, 2, part, dims, strides, box, nullptr, "upd partials", CU_TENSOR_MAP_SWIZZLE_64B);
+        e.L.part_ptr = part;
+      }
       L = e.L;
       plan->last_desc = &e.desc;
     }
@@ -2729,7 +2748,7 @@ int dconv_weight_update(dconv_upd_plan_t plan, const dconv_act_t* in, const dcon
     auto go = [&](auto kern, int a_base, int acc) {
       ensure_smem(kern, L.smem);
       if (!opened) prof_begin(2, cs), opened = true;
-      kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.p, L.stages, a_base, acc);
+      kern<<<L.grid, kFwdThreads, L.smem, cs>>>(L.map_in, L.map_do, L.map_part, L.p, L.stages, a_base, acc);
       cuda_check(cudaGetLastError(), "conv_upd_kernel launch");
     };
     auto go_raw = [&](auto kern) {

@@ -161,6 +161,11 @@ struct UpdParams {
   // waits on the drain. drain = 0: one period (no drains).
   int drain;
   int drain_bufs;
+  // 1: the partials leave through TMA stores (bf16 single-period plans whose warps own
+  // 32 consecutive partial rows): each epilogue warp stages 32 rows x 16 columns in
+  // shared memory (the idle operand ring) -- full-line writes instead of one 16 B
+  // segment per lane per store
+  int epi_tma;
 };
 
 }  // namespace dconv_sm100

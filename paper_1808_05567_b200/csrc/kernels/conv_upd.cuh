@@ -110,7 +110,8 @@ __device__ __forceinline__ void lsu_box(uint32_t dst0, const uint8_t* src_plane0
 template <int PA, int PB>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     conv_upd_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_do,
-                    const __grid_constant__ UpdParams p, int n_stages, int a_base, int accumulate) {
+                    const __grid_constant__ CUtensorMap map_part, const __grid_constant__ UpdParams p, int n_stages,
+                    int a_base, int accumulate) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
@@ -423,7 +424,61 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       __syncwarp();
     }
   }
-  if (warp >= 4) {
+  if (warp >= 4 && PA == 1 && PB == 1 && p.epi_tma && !accumulate) {
+    // ---------------------------------------------------------- epilogue, TMA stores (UpdParams::epi_tma)
+    // each warp stages 32 partial rows x 16 fp32 columns per store in two 2 KB slots
+    // carved from the operand ring, idle once acc_full completes (every stage consumed);
+    // SWIZZLE_64B: the row-per-lane float4 writes are bank-conflict free
+    const int qrow = (warp % 4) * 32;
+    if (iters > 0) {
+      mbar_wait(&acc_full[0], 0);
+      tc_fence_after();
+    }
+    uint8_t* stg0 = smem + (warp - 4) * 4096;
+    uint32_t n_st = 0;
+    const bool live = iters > 0;
+    const bool no_store = (kDevBuild ? p.dbg_mode : 0) & 2048;  // dev ablation
+    const int n_acc = ((kDevBuild ? p.dbg_mode : 0) & 4096) ? 0 : p.stack > 1 ? xsn : (mc > 1 ? mc : ntaps);
+    for (int t = 0; t < n_acc; ++t) {
+      // (host-checked: a warp's 32 TMEM rows are 32 consecutive partial rows of one tap)
+      const int rows_slot = 16 * p.cb_eff;
+      const int slot = p.stack > 1 ? qrow / rows_slot : 0;
+      if (p.stack > 1 && slot >= ntaps) continue;
+      const int sl = tap0 + slot;
+      if (p.xs > 1 && p.xs_slot_s[sl] + t >= p.xs_S) continue;
+      const int rs = p.xs > 1 ? p.xs_slot_r[sl] * p.xs_S + p.xs_slot_s[sl] + t
+                              : p.tap_src[tap0 + (p.stack > 1 ? slot : (mc > 1 ? 0 : t))];
+      const int c_row0 = p.stack > 1 ? qrow % rows_slot : (ctile * mc + (mc > 1 ? t : 0)) * 128 + qrow;
+      const int row0 = (split * p.n_taps + rs) * p.c_pad + c_row0;
+      for (int g = 0; g < p.nb; ++g) {
+        uint32_t r[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(qrow) << 16) + static_cast<uint32_t>(t * NT + g * 16), r);
+        tmem_ld_wait();
+        if (no_store) continue;
+        uint8_t* stg = stg0 + (n_st & 1u) * 2048u;
+        if (n_st >= 2) {  // this slot's previous store must have left shared memory
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = live ? make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                              __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_part, stg, ktile * NT + g * 16, row0);
+          bulk_commit_group();
+        }
+        ++n_st;
+      }
+    }
+    if (lane == 0) bulk_wait_group0();
+    __syncwarp();
+  } else if (warp >= 4) {
     // ---------------------------------------------------------- epilogue (lsu plans: after loading)
     // one pass per accumulation period: every period's buffer is added into the
     // partial slice (the first one overwrites it unless the launch accumulates)

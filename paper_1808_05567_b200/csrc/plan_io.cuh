@@ -31,7 +31,7 @@ namespace {
 #define DCONV_UPD_INT_FIELDS(X)                                                                                    \
   X(n_img) X(in_cb) X(do_cb) X(cb_in) X(kb_out) X(P) X(Q) X(wsub) X(linear) X(rows_ps) X(vs) X(a_px) X(in_rows)  \
   X(in_row0) X(in_col0) X(stride) X(stages_per_img) X(stages_total) X(splits) X(nb) X(tg) X(n_tgroups) X(stack)  \
-  X(cb_eff) X(half) X(sw32) X(mc) X(lsu) X(n_taps) X(c_pad) X(k_pad) X(drain) X(drain_bufs) X(xs) X(xs_S) X(pimg) X(img_pitch)
+  X(cb_eff) X(half) X(sw32) X(mc) X(lsu) X(n_taps) X(c_pad) X(k_pad) X(drain) X(drain_bufs) X(xs) X(xs_S) X(pimg) X(img_pitch) X(epi_tma)
 #define DCONV_UPD_ARRAYS(X)                                                                                     \
   X(tg_phase, kMaxTapGroups) X(tg_tap0, kMaxTapGroups) X(tg_ntaps, kMaxTapGroups) X(phase_row, kMaxPhases)      \
   X(phase_col, kMaxPhases) X(tap_shift, kMaxTaps) X(tap_src, kMaxTaps) X(tap_ph, kMaxTaps) X(tap_r2, kMaxTaps) \

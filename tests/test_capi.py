@@ -109,6 +109,19 @@ def test_status_strings_map_reference_exceptions(dconv):
     assert issubclass(dconv.PlanTensorMismatch, dconv.Error)
 
 
+def test_prep_batch_state_errors(dconv):
+    """dconv_prep_batch_begin / _end: one open batch per thread; _end without an
+    open batch is an error; an empty batch launches nothing (no GPU needed)."""
+    from paper_1808_05567_b200 import _lib
+
+    lib = _lib.lib()
+    assert lib.dconv_prep_batch_end(None) == 102
+    assert lib.dconv_prep_batch_begin() == 0
+    assert lib.dconv_prep_batch_begin() == 102
+    assert lib.dconv_prep_batch_end(None) == 0
+    assert lib.dconv_prep_batch_end(None) == 102
+
+
 def test_backward_route_selection(dconv):
     # propagation.cpp:35-40 and the Table I routes in SURVEY 8(a) a13
     d = dconv

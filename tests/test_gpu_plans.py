@@ -253,3 +253,61 @@ def test_cpp_shim_runs_both_engines(dconv):
     r = subprocess.run([binary], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0 and "SHIM CHECK OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("math", [0, 1])
+def test_batched_weight_prep_matches_inline_prep(dconv, orc, math):
+    """dconv_prep_batch_begin/end: three convs' forward and backward-data weight
+    preparations recorded (PREP_ONLY) and launched as ONE kernel; the WEIGHTS_READY
+    executes on those workspaces equal the inline-prep executes bitwise."""
+    from paper_1808_05567_b200._lib import EP_PREP_ONLY, EP_WEIGHTS_READY, Epilogue
+
+    M = dconv.Math(math)
+    dt = torch.float32 if M == dconv.Math.F32 else torch.bfloat16
+    lib = dconv._lib.lib()
+    B = dconv.BlockedActivation
+    layers = [(8, 64, 128, 28, 3), (8, 128, 256, 14, 1), (4, 48, 80, 9, 3)]  # (N, C, K, H, R); the last: ragged blocks
+    st = torch.cuda.current_stream().cuda_stream
+    cases = []
+    for i, (N, C_, K, H, R) in enumerate(layers):
+        pad = (R - 1) // 2
+        s = dconv.make_layer_spec(N, C_, K, H, H, R, R, 1, pad, pad, 16)
+        x = dconv.to_blocked_activation(dev(orc.uniform(40 + i, (N, C_, H, H))), 16, 0, 0, dtype=dt)
+        g = dconv.to_blocked_activation(dev(orc.uniform(50 + i, (N, K, H, H))), 16, 0, 0, dtype=dt)
+        w = dconv.to_blocked_weight(dev(orc.he_normal(60 + i, (K, C_, R, R), C_ * R * R)), s)
+        fp = dconv.ExecutionPlan(s, None, None, M, 0, 0)
+        bp = dconv.prepare_backward(s, w, 1, None, M)
+        wsf = torch.empty(lib.dconv_fwd_workspace_bytes(fp._h), dtype=torch.uint8, device="cuda")
+        wsb = torch.empty(lib.dconv_bwd_workspace_bytes(bp._h), dtype=torch.uint8, device="cuda")
+        cases.append((N, C_, K, H, x, g, w, fp, bp, wsf, wsb))
+
+    def run(batched):
+        outs = []
+        if batched:
+            assert lib.dconv_prep_batch_begin() == 0
+            for N, C_, K, H, x, g, w, fp, bp, wsf, wsb in cases:
+                y, dx = B(N, K, H, H, 16, 0, 0, dt), B(N, C_, H, H, 16, 0, 0, dt)
+                ep = Epilogue(None, None, 0, EP_PREP_ONLY)
+                assert lib.dconv_forward_ex(fp._h, C.byref(x.to_c()), C.byref(w.to_c()), C.byref(y.to_c()),
+                                            C.byref(ep), wsf.data_ptr(), st) == 0
+                assert lib.dconv_backward_data_ex(bp._h, C.byref(w.to_c()), C.byref(g.to_c()), C.byref(dx.to_c()),
+                                                  C.byref(ep), wsb.data_ptr(), st) == 0
+            assert lib.dconv_prep_batch_end(st) == 0
+        flag = EP_WEIGHTS_READY if batched else 0
+        for N, C_, K, H, x, g, w, fp, bp, wsf, wsb in cases:
+            y, dx = B(N, K, H, H, 16, 0, 0, dt), B(N, C_, H, H, 16, 0, 0, dt)
+            ep = Epilogue(None, None, 0, flag)
+            assert lib.dconv_forward_ex(fp._h, C.byref(x.to_c()), C.byref(w.to_c()), C.byref(y.to_c()), C.byref(ep),
+                                        wsf.data_ptr(), st) == 0
+            assert lib.dconv_backward_data_ex(bp._h, C.byref(w.to_c()), C.byref(g.to_c()), C.byref(dx.to_c()),
+                                              C.byref(ep), wsb.data_ptr(), st) == 0
+            outs += [y.data, dx.data]
+        torch.cuda.synchronize()
+        return [o.clone() for o in outs]
+
+    ref = run(False)
+    for wsf_b in [c[9] for c in cases] + [c[10] for c in cases]:
+        wsf_b.fill_(0xAB)  # the batch must rewrite every prepared byte the convs read
+    got = run(True)
+    for a, b in zip(got, ref):
+        assert torch.equal(a, b)
