@@ -646,6 +646,13 @@ void encode_fwd_act_map(FwdLaunch& L, const dconv_act_t& in) {
     const uint32_t box[4] = {16, static_cast<uint32_t>(hw), static_cast<uint32_t>(L.ts ? kc : 1),
                              static_cast<uint32_t>(p.mimg)};
     L.map_a = encode(!raw_f32, 4, in.data, dims, strides, box, nullptr, "activation multi-image", swz);
+  } else if (p.linear && p.a_sw128) {  // 128 B rows of four pixels, SWIZZLE_128B (read back through SW32 descriptors)
+    if (raw_f32 || (static_cast<uint64_t>(hp) * wp) % 4 != 0 || a_px % 32 != 0)
+      fail(DCONV_ERR_INVALID_DESCRIPTOR, "a_sw128 plan on a plane that is not a multiple of four pixels");
+    const uint64_t dims[3] = {64, static_cast<uint64_t>(hp) * wp / 4, planes};
+    const uint64_t strides[2] = {128, pix * hp * wp};
+    const uint32_t box[3] = {64, static_cast<uint32_t>((kc > 1 ? a_px : 128) / 4), static_cast<uint32_t>(kc)};
+    L.map_a = encode(1, 3, in.data, dims, strides, box, nullptr, "activation linear sw128", CU_TENSOR_MAP_SWIZZLE_128B);
   } else if (p.linear) {
     const uint64_t dims[3] = {16, static_cast<uint64_t>(hp) * wp, planes};
     const uint64_t strides[2] = {pix, pix * hp * wp};
@@ -698,6 +705,12 @@ void finalize_fwd(FwdLaunch& L) {
     p.tma_store = 1;
     L.smem_launch = L.smem + staging;
   }
+  // bf16 linear single-tap plans (1x1, stride 1, dense planes of 4k pixels): 128 B activation rows
+  p.a_sw128 = (p.tma_store && !L.raw_f32 && !L.ts && p.linear && p.mimg == 0 && p.img_pitch == 0 && p.n_taps == 1 &&
+               p.n_phases == 1 && p.tap_shift[0] == 0 && p.stride == 1 && p.in_row0 == 0 && p.in_col0 == 0 &&
+               (p.P * p.Q) % 4 == 0 && p.a_px % 32 == 0 && !DCONV_ENV("DCONV_NO_A_SW128"))
+                  ? 1
+                  : 0;
 }
 
 // output slab maps of a TMA-store launch (p.out set)
@@ -827,12 +840,12 @@ std::string json_tile(const FwdLaunch& L) {
                 "{\"mode\":\"%s\",\"wsub\":%d,\"mb\":%d,\"nb\":%d,\"pc_stages\":%d,\"raw_stages\":%d,\"w_stages\":%d,"
                 "\"smem\":%zu,\"ctas\":%u,\"tiles\":%d,\"pieces\":%d,\"raw_f32\":%d,\"phases\":%d,\"a_px\":%d,"
                 "\"mimg\":%d,\"a_in_tmem\":%d,\"kc\":%d,\"w_resident\":%d,\"tma_store\":%d,\"split_acc\":%d,"
-                "\"epi_groups\":%d}",
+                "\"epi_groups\":%d,\"a_sw128\":%d}",
                 L.p.linear ? "linear" : "rows", L.p.wsub, L.p.mb, L.p.nb, L.stages, L.raw_stages, L.w_stages, L.smem,
                 L.grid.x,
                 (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
                 L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store, L.p.split_acc,
-                (!L.raw_f32 && !L.ts && L.p.tma_store) ? 3 : (L.p.ts_epi2 && L.p.tma_store) ? 2 : 1);
+                (!L.raw_f32 && !L.ts && L.p.tma_store) ? 3 : (L.p.ts_epi2 && L.p.tma_store) ? 2 : 1, L.p.a_sw128);
   return buf;
 }
 

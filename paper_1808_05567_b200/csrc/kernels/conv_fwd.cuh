@@ -43,6 +43,7 @@ namespace dconv_sm100 {
 constexpr int kFwdThreads = 256;
 constexpr int kMaxStages = 8;
 constexpr int kFastTaps = 16;  // taps per weight stage issued by the unrolled MMA path
+constexpr int kWarp1Iters = 8;  // single-tap plans: stages per tile from which the whole MMA warp runs the issue loop
 constexpr int kConvWarp0 = 2;
 constexpr int kConvThreads = 192;  // warps 2..7
 
@@ -425,11 +426,12 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               for (int kk = 0; kk < p.kc; ++kk)  // box {16, hw, 1, mimg} per block: rows contiguous per block
                 tma_load_4d(dst + kk * p.a_px * 32, &map_a, &pc_full[s], 0, 0, cb * p.kc + kk, n);
             } else if (p.linear) {
+              const int rsh = p.a_sw128 ? 2 : 0;  // 128 B rows of four pixels
               if (p.kc > 1)  // one box {16, a_px, kc}
-                tma_load_3d(dst, &map_a, &pc_full[s], 0, a_px0, plane);
+                tma_load_3d(dst, &map_a, &pc_full[s], 0, a_px0 >> rsh, plane);
               else
                 for (int i = 0; i < p.lin_boxes; ++i)
-                  tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, a_px0 + i * 128, plane);
+                  tma_load_3d(dst + i * 128 * 32, &map_a, &pc_full[s], 0, (a_px0 + i * 128) >> rsh, plane);
             } else {
               tma_load_4d(dst, &map_a, &pc_full[s], 0, p.in_col0 + s_phase_col[ph],
                           p.in_row0 + p.stride * row0 + s_phase_row[ph], plane);
@@ -628,13 +630,24 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         // issues (warp-uniform descriptor arithmetic, measured 7-13 % on the 3x3 layers);
         // single-tap stages: lane 0 alone (the other lanes do not compete for issue slots with
         // the epilogue warps on this SM sub-partition, measured 5-10 % on fused epilogues)
-        constexpr bool kWarp = NTAPS > 1;
-        if (!kWarp) {
+        // Single-tap plans whose tiles are long reductions (>= kWarp1Iters full stages: the
+        // 14x14 / 7x7 1x1 layers, MMA-issue bound) also take the whole-warp loop: on the
+        // lane-0 path every MMA is a divergent-code waterfall (ELECT + 5 R2UR.BROADCAST per
+        // UTCHMMA, ~80 cycles) and the stage's commits / ring bookkeeping another ~400,
+        // which the 512-cycle stage of four 128x256x16 MMAs does not hide.
+        constexpr bool kMulti = NTAPS > 1;
+        bool warp_loop = kMulti;
+        if constexpr (!kMulti && KC > 0) {
+          warp_loop = p.n_phases == 1 && p.cb_in % p.kc == 0 && k_iters >= kWarp1Iters;
+          if (kDevBuild && (dbg_mode & 4096)) warp_loop = p.n_phases == 1 && p.cb_in % p.kc == 0;
+          if (kDevBuild && (dbg_mode & 8192)) warp_loop = false;
+        }
+        if (!warp_loop) {
           if (lane == 0) run1(mb_c, kc_c, nt_c);
           return;
         }
-        const unsigned wmask = kWarp ? 0xffffffffu : 1u;
-        auto issuer = [&]() { return kWarp ? elect_one() : true; };
+        constexpr unsigned wmask = 0xffffffffu;
+        auto issuer = [&]() { return elect_one(); };
         // full stages first (compile-time MMA sequence), then the partial one (runtime loop)
         const int k_full = (KC > 0 && p.n_phases == 1) ? p.cb_in / p.kc : 0;
         uint32_t tl = 0, g = 0;
@@ -680,21 +693,6 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
                     mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT),
                                 ak + 2u * static_cast<uint32_t>(p.tap_shift[tp]) + 256u * mb, a_hi,
                                 bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (kk == 0 && tp == 0) ? acc0 : 1u);
-              }
-            } else if constexpr (!kWarp) {  // (multi-tap plans carry whole stages: host-checked)
-              const int kc_eff = min(p.kc, p.cb_in - it * p.kc);
-              for (int kk = 0; kk < kc_eff; ++kk) {
-                const uint32_t ak = a_st + 2u * static_cast<uint32_t>(kk * p.a_px);
-                const uint32_t bk = b_st + ((static_cast<uint32_t>(kk * nt) * w_tap) >> 4);
-                const bool first_k = it == 0 && kk == 0;
-#pragma unroll
-                for (int tp = 0; tp < kFastTaps; ++tp) {
-                  if (tp >= nt) break;
-#pragma unroll
-                  for (int mb = 0; mb < MB; ++mb)
-                    mma_bf16_lo(d_base + static_cast<uint32_t>(mb * NT), ak + sh[tp] + 256u * mb, a_hi,
-                                bk + static_cast<uint32_t>(tp) * b_tap, b_hi, idesc, (first_k && tp == 0) ? 0u : 1u);
-                }
               }
             }
             if (trace) trace[3] = clock64() - t_start;
@@ -934,6 +932,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
     // two output blocks per step: one 32-column TMEM load per accumulator, one
     // proxy fence and one bulk store of a {16 lanes, 32 pixels, 2 blocks} box
     const int qrow = (warp % 4) * 32;
+    // pixel (within the warp's 32-row group) held by this lane's accumulator row: a_sw128
+    // stages permute the four pixels of each 128 B row (conv_params.h)
+    const int plane_px = p.a_sw128 ? (lane ^ ((lane >> 3) & 3)) : lane;
     const uint32_t esz = p.out_bf16 ? 2u : 4u;
     const uint32_t slot_bytes = 2u * 32u * 16u * esz;
     const int v_end = p.P * p.Q;  // dense output plane (wsub == Q)
@@ -981,7 +982,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               for (int e = 0; e < 16; ++e) vals[e] += p.bias[kb * 16 + e];
             }
             // dense output: pixel v of plane (n, kb) at ((n*out_cb + kb)*P*Q + v)*16 lanes
-            const int v = FUSED ? v0 + mb * 128 + qrow + lane : 0;
+            const int v = FUSED ? v0 + mb * 128 + qrow + plane_px : 0;
             const bool live = FUSED && v < v_end && kb < p.kb_out;
             const long long px_off = FUSED ? ((static_cast<long long>(n) * p.out_cb + kb) * v_end + v) * 16LL * esz : 0;
             if (FUSED && p.add != nullptr && live) {  // residual add / gradient sum
@@ -1000,7 +1001,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
-            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
+            const uint32_t row = static_cast<uint32_t>(j * 32 + plane_px);
             if (p.out_bf16) {
               const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
               const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
@@ -1048,7 +1049,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - (s / ng) * ng);
         const int kb0 = ntile * p.nb + g0;
         const bool pair = g0 + 1 < p.nb;
-        const int v = v0 + mb * 128 + qrow + lane;
+        const int v = v0 + mb * 128 + qrow + plane_px;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int kb = kb0 + j;
@@ -1130,7 +1131,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
 #pragma unroll
               for (int e = 0; e < 16; ++e) vals[e] = m[e] > 0.0f ? vals[e] : 0.0f;
             }
-            const uint32_t row = static_cast<uint32_t>(j * 32 + lane);
+            const uint32_t row = static_cast<uint32_t>(j * 32 + plane_px);
             const float a8[8] = {vals[0], vals[1], vals[2], vals[3], vals[4], vals[5], vals[6], vals[7]};
             const float b8[8] = {vals[8], vals[9], vals[10], vals[11], vals[12], vals[13], vals[14], vals[15]};
             *reinterpret_cast<uint4*>(stg + sw32(row, 0)) = cast8(a8);

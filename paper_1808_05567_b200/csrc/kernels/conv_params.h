@@ -43,6 +43,13 @@ struct FwdParams {
   // bottom padding the next one's top padding; one 5-D activation box of mimg + 1
   // images (images inside the channel-block planes) so the last image's is zero too
   int img_pitch;
+  // 1 (bf16 linear single-tap plans with the TMA-store epilogue, planes of 4k pixels): the
+  // activation stage is written as SWIZZLE_128B 128 B rows of four pixels and read through
+  // the unchanged K-major SW32 descriptors -- the TMA unit moves ~1 box row per clock whatever
+  // its width (27 B/clk/SM on 32 B rows, 68 on 128 B rows). MMA row q of each 32-row group
+  // then holds pixel q ^ ((q >> 3) & 3) (channel halves intact); the epilogue warps undo
+  // the permutation when they stage their 32-pixel slabs and fetch the fused operands.
+  int a_sw128;
   int a_px;            // pixels per chunk plane per stage
   int a_load_px;       // pixels the activation TMA writes per stage
   int lin_boxes;       // linear mode: 128-pixel boxes per chunk plane

@@ -24,7 +24,7 @@ namespace {
   X(mimg) X(a_px) X(a_load_px) X(lin_boxes) X(in_row0) X(in_col0) X(stride) X(n_phases) X(taps_box) X(w_taps)    \
   X(kc) X(w_resident) X(w_all) X(tma_store) X(out_fill) X(split_acc) X(ts_epi2) X(epi_groups) X(fill_h_end)       \
   X(fill_w_end) X(n_taps) X(n_ntiles) X(out_bf16) X(out_cb) X(out_hp) X(out_wp) X(out_y0) X(out_x0) X(out_scale)  \
-  X(out_halo_h) X(out_halo_w) X(img_pitch)
+  X(out_halo_h) X(out_halo_w) X(img_pitch) X(a_sw128)
 #define DCONV_FWD_ARRAYS(X) \
   X(phase_row, kMaxPhases) X(phase_col, kMaxPhases) X(phase_ntaps, kMaxPhases) X(phase_tap0, kMaxPhases) X(tap_shift, kMaxTaps)
 
