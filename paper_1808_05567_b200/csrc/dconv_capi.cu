@@ -845,7 +845,8 @@ std::string json_tile(const FwdLaunch& L) {
                 L.grid.x,
                 (L.p.mimg > 0 ? (L.p.n_img + L.p.mimg - 1) / L.p.mimg : L.p.n_img * L.p.tiles_per_img) * L.p.n_ntiles,
                 L.pieces, L.raw_f32 ? 1 : 0, L.p.n_phases, L.p.a_px, L.p.mimg, L.ts ? 1 : 0, L.p.kc, L.p.w_resident, L.p.tma_store, L.p.split_acc,
-                (!L.raw_f32 && !L.ts && L.p.tma_store) ? 3 : (L.p.ts_epi2 && L.p.tma_store) ? 2 : 1, L.p.a_sw128);
+                (!L.raw_f32 && !L.ts) ? std::max(1, std::min(3, L.p.epi_groups)) : (L.p.ts_epi2 && L.p.tma_store) ? 2 : 1,
+                L.p.a_sw128);
   return buf;
 }
 

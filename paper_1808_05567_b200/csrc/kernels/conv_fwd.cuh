@@ -306,6 +306,11 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
   // rows-mode layer) split each tile's (m-block, block pair) items over the same
   // groups: one warp per lane quarter is latency bound (dependent chains, no ILP)
   const bool epi_reg3 = !RAW_F32 && !TS && !p.tma_store;
+  // The groups' shares of a tile's items (block pairs) are uneven when the item count is not
+  // a multiple of the group count (8 pairs over 3 groups: 3, 3, 2; 4 items: 2, 1, 1), so the
+  // assignment rotates by the CTA's tile counter: over three tiles every group does the same
+  // work, and the double-buffered accumulators absorb the one-item skew (same values, same
+  // stores: only which warp moves them changes).
   const int n_epi_groups = (epi2 || epi_reg3) ? max(1, min(3, p.epi_groups)) : ts_epi2 ? 2 : 1;  // bf16: warps 4..7, 8..11, 12..15; ts_epi2: 4..7, 12..15
   // TS: A-piece ring in TMEM after the accumulators
   const uint32_t ring_col0 = static_cast<uint32_t>(p.acc_bufs) * acc_cols;
@@ -954,8 +959,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
+      const int egr = static_cast<int>((static_cast<uint32_t>(eg) + tl) % static_cast<uint32_t>(n_eg));  // rotated: see n_epi_groups
       for (int mb = 0; mb < p.mb; ++mb) {
-        for (int g0 = 2 * eg; g0 < p.nb; g0 += 2 * n_eg) {
+        for (int g0 = 2 * egr; g0 < p.nb; g0 += 2 * n_eg) {
           const int kb0 = ntile * p.nb + g0;
           if (kb0 >= p.kb_out) break;
           const bool pair = g0 + 1 < p.nb;
@@ -1045,8 +1051,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       const uint8_t* maskp = reinterpret_cast<const uint8_t*>(p.mask);
       // operand slots: [0, 4) the first operand (add if present, else mask), [4, 8) the mask when both
       const uint8_t* op0 = addp ? addp : maskp;
+      int egr = eg;  // this tile's rotated group index (see n_epi_groups)
       auto fetch = [&](int n, int v0, int ntile, int s, int ng, uint4 (&b)[NB]) {
-        const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - (s / ng) * ng);
+        const int mb = s / ng, g0 = 2 * egr + 2 * n_eg * (s - (s / ng) * ng);
         const int kb0 = ntile * p.nb + g0;
         const bool pair = g0 + 1 < p.nb;
         const int v = v0 + mb * 128 + qrow + plane_px;
@@ -1075,8 +1082,9 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
         int n, v0, ntile;
         tile_coords(t, n, v0, ntile);
+        egr = static_cast<int>((static_cast<uint32_t>(eg) + tl) % static_cast<uint32_t>(n_eg));
         int ng = 0;  // this group's block pairs in the tile
-        for (int g0 = 2 * eg; g0 < p.nb && ntile * p.nb + g0 < p.kb_out; g0 += 2 * n_eg) ++ng;
+        for (int g0 = 2 * egr; g0 < p.nb && ntile * p.nb + g0 < p.kb_out; g0 += 2 * n_eg) ++ng;
         const int total = p.mb * ng;
         uint4 buf[DEPTH + 1][NB];  // buf[0] = this step's operands, buf[d] = step + d's
 #pragma unroll
@@ -1089,7 +1097,7 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
         const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
         for (int s = 0; s < total; ++s) {
           if (s + DEPTH < total) fetch(n, v0, ntile, s + DEPTH, ng, buf[DEPTH]);
-          const int mb = s / ng, g0 = 2 * eg + 2 * n_eg * (s - mb * ng);
+          const int mb = s / ng, g0 = 2 * egr + 2 * n_eg * (s - mb * ng);
           const int kb0 = ntile * p.nb + g0;
           const bool pair = g0 + 1 < p.nb;
           uint32_t r[32], rl[32];
@@ -1332,7 +1340,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
       mbar_wait_t(&acc_full[acc], apar, dbg ? &c_a : nullptr);
       tc_fence_after();
       const uint32_t d_base = tmem_base + acc * acc_cols + (static_cast<uint32_t>(qrow) << 16);
-      for (int item = eg; item < p.mb * n_pairs; item += n_epi_groups) {
+      for (int item = static_cast<int>((static_cast<uint32_t>(eg) + tl) % static_cast<uint32_t>(n_epi_groups));
+           item < p.mb * n_pairs; item += n_epi_groups) {
         const int mb = item / n_pairs;
         int v = v0 + mb * 128 + qrow + lane;
         int nn = n;

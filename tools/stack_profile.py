@@ -11,6 +11,9 @@ import paper_1808_05567_b200 as d  # noqa: E402
 from paper_1808_05567_b200 import executor as ex  # noqa: E402
 
 N = int(os.environ.get("N", "256"))
+if os.environ.get("DBG"):  # dev lib: ablation / issue-loop bits (before any plan is built)
+    from paper_1808_05567_b200 import _lib
+    _lib.lib().dconv_debug_mode(int(os.environ["DBG"]))
 nodes = ex.resnet50_conv_stack()
 e = ex.ConvStackExecutor(nodes, N, 224, d.Math.BF16, "cuda", lr=0.0)
 c, h, w = e.shapes[nodes[-1].out]
