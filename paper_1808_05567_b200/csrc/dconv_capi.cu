@@ -325,6 +325,12 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
   // packed multi-tap tiles (FwdParams::img_pitch): small stride-1 same-padded images of a
   // bf16 rows plan, three 7x7 images per 256-row tile (57 % of the MMA rows real
   // pixels instead of 38 % for one image per 128-row tile)
+  // bf16 planes of <= 64 pixels (7x7, 8x8) also as 128-row tiles of two images x 256 output
+  // channels with double-buffered accumulators: the 256-row tile leaves TMEM room for only
+  // 128 channels per tile, whose N = 128 MMAs are issue bound (~107 cycles for a 64-cycle
+  // MMA) and whose activations are re-read by twice as many channel tiles; measured 13-25 %
+  // faster on the 7x7 / 8x8 1x1 layers although only 98 of 128 MMA rows are pixels at 7x7
+  const bool mimg_mb1 = !raw_f32 && hw <= 64 && !DCONV_ENV("DCONV_NO_MIMG_MB1");
   const int pk_pitch = (in.h + (-pb.row_off)) * (pb.Q + taps.s2max);
   const bool pk_ok = !raw_f32 && !linear && st == 1 && taps.n_phases == 1 && in.halo_h == 0 && in.halo_w == 0 &&
                      pb.P == in.h && pb.Q == in.w && pb.row_off <= 0 && pb.col_off <= 0 &&
@@ -450,7 +456,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
           apx = (pki + 1) * pk_pitch;
           if (apx < Lpx + maxshift) continue;  // the box must cover every row the MMA reads
         } else if (mimg_ok) {
-          if (mb != 2) continue;
+          if (mb != 2 && !(mb == 1 && mimg_mb1)) continue;
           apx = Lpx;
         } else if (linear) {
           lb = cdiv(Lpx + maxshift, 128);
@@ -598,7 +604,7 @@ FwdLaunch plan_fwd_launch(const ConvProblem& pb, const Taps& taps, const void* w
     p.mimg = (128 * tile.mb) / pk_pitch;
     p.img_pitch = pk_pitch;
     p.a_load_px = (p.mimg + 1) * pk_pitch;
-  } else if (mimg_ok && (tile.mb == 2 || L.ts)) {
+  } else if (mimg_ok && (tile.mb == 2 || L.ts || (tile.mb == 1 && mimg_mb1))) {
     p.mimg = (128 * tile.mb) / hw;
     p.a_load_px = p.mimg * hw;
   }
