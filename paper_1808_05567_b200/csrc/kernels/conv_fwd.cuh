@@ -1368,7 +1368,26 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
           // blocks is fetched before the TMEM loads: its HBM latency overlaps them
           const void* pre_src = (p.add != nullptr) != (p.mask != nullptr) ? (p.add ? p.add : p.mask) : nullptr;
           const bool pre_on = !RAW_F32 && p.out_bf16 && pre_src != nullptr;  // (bf16 kernels only: registers)
-          uint4 pre[2][2];
+          // both operands (backward-data of a block's first conv on multi-image / halo'd tiles:
+          // gradient sum + ReLU mask): the mask of both blocks goes through a second buffer
+          const bool pre_both = !RAW_F32 && p.out_bf16 && p.add != nullptr && p.mask != nullptr;
+          uint4 pre[2][2], prem[2][2];
+          if (pre_both) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int kb = ntile * p.nb + g0 + k;
+              const bool live = k < ng && valid && kb < p.kb_out;
+              const long long off =
+                  (((static_cast<long long>(nn) * p.out_cb + kb) * p.out_hp + y) * p.out_wp + x) * 32LL;
+              const uint4 z = make_uint4(0, 0, 0, 0);
+              const uint8_t* sa = reinterpret_cast<const uint8_t*>(p.add) + off;
+              const uint8_t* sm = reinterpret_cast<const uint8_t*>(p.mask) + off;
+              pre[k][0] = live ? *reinterpret_cast<const uint4*>(sa) : z;
+              pre[k][1] = live ? *reinterpret_cast<const uint4*>(sa + 16) : z;
+              prem[k][0] = live ? *reinterpret_cast<const uint4*>(sm) : z;
+              prem[k][1] = live ? *reinterpret_cast<const uint4*>(sm + 16) : z;
+            }
+          }
           if (pre_on) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -1408,6 +1427,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               float a[16];
               if (pre_on)
                 load16(&pre[k][0], 1, a);
+              else if (pre_both)
+                load16(&pre[k][0], 1, a);
               else
                 load16(reinterpret_cast<const uint8_t*>(p.add) + px_off, p.out_bf16, a);
 #pragma unroll
@@ -1421,6 +1442,8 @@ __global__ void __launch_bounds__((TS || !RAW_F32) ? kFwdThreadsTS : kFwdThreads
               float m[16];
               if (pre_on)
                 load16(&pre[k][0], 1, m);
+              else if (pre_both)
+                load16(&prem[k][0], 1, m);
               else
                 load16(reinterpret_cast<const uint8_t*>(p.mask) + px_off, p.out_bf16, m);
 #pragma unroll
