@@ -24,7 +24,7 @@ TRAFFIC = {"r02_ncu_l1_3x3_U": "r50_64_64_56_3x3s1_U", "r02_ncu_l1_3x3_F": "r50_
            "r02_ncu_l3_3x3_F": "r50_256_256_14_3x3s1_F", "r02_ncu_l3_1x1_F": "r50_1024_256_14_1x1s1_F",
            "r02_ncu_l3_1x1_U": "r50_256_1024_14_1x1s1_U", "r02_ncu_cfg2_U": "cfg2_U",
            "r02_ncu_l1_1x1_res_F": "r50_64_256_56_1x1s1_F", "r02_ncu_l4_3x3_U": "r50_512_512_7_3x3s1_U",
-           "r02_ncu_l4_3x3_F": "r50_512_512_7_3x3s1_F"}
+           "r02_ncu_l4_3x3_F": "r50_512_512_7_3x3s1_F", "r02_ncu_l4_1x1_F": "r50_2048_512_7_1x1s1_F"}
 
 
 def raw(rep):
