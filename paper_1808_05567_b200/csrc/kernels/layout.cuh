@@ -517,23 +517,31 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ in, T* __restrict__ out
     const int y = static_cast<int>(r % p);
     const long long plane = r / p;
     float best[16], v[16];
-    uint32_t bi[4] = {0, 0, 0, 0};  // 16 argmax bytes
+    uint32_t bc[16];  // argmax code per lane (two selects per lane and tap; packed to bytes once)
 #pragma unroll
-    for (int l = 0; l < 16; ++l) best[l] = -INFINITY;
+    for (int l = 0; l < 16; ++l) {
+      best[l] = -INFINITY;
+      bc[l] = 0;
+    }
+#pragma unroll
     for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
       for (int dx = 0; dx < 3; ++dx) {
         const int iy = 2 * y - 1 + dy, ix = 2 * x - 1 + dx;
         if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
         ld16f(in + ((plane * h + iy) * w + ix) * 16, v);
         const uint32_t code = static_cast<uint32_t>(dy * 3 + dx);
 #pragma unroll
-        for (int l = 0; l < 16; ++l)
-          if (v[l] > best[l]) {
-            best[l] = v[l];
-            bi[l / 4] = (bi[l / 4] & ~(0xFFu << (8 * (l % 4)))) | (code << (8 * (l % 4)));
-          }
+        for (int l = 0; l < 16; ++l) {
+          const bool gt = v[l] > best[l];
+          best[l] = gt ? v[l] : best[l];
+          bc[l] = gt ? code : bc[l];
+        }
       }
     st16f(out + e * 16, best);
+    uint32_t bi[4];  // 16 argmax bytes
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bi[k] = bc[4 * k] | (bc[4 * k + 1] << 8) | (bc[4 * k + 2] << 16) | (bc[4 * k + 3] << 24);
     reinterpret_cast<uint4*>(arg)[e] = make_uint4(bi[0], bi[1], bi[2], bi[3]);
   }
 }
