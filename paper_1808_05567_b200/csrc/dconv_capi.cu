@@ -2142,6 +2142,8 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
       for (int t0 = 0; t0 < static_cast<int>(taps.r.size()); t0 += p.stack)
         groups.push_back(std::min(p.stack, static_cast<int>(taps.r.size()) - t0));
     } else {
+      // (the model keeps the unbalanced 4 + 4 + 1 split it was calibrated with: fed the balanced
+      // groups the plan uses, it picked slower candidates for the 28x28 and 7x7 3x3 layers)
       for (int ph = 0; ph < taps.n_phases; ++ph)
         for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += tgv) groups.push_back(std::min(tgv, taps.phase_ntaps[ph] - t0));
     }
@@ -2301,14 +2303,22 @@ UpdLaunch plan_upd(const dconv_upd_plan& pl, const dconv_act_t& in, const dconv_
     // of a phase still fits and N = 3 NT is a legal MMA width.
     L.cat = L.raw && pieces == 3 && 3 * NT <= 256 && 3 * NT * taps.taps_box <= 512;
     p.tg = std::max(1, std::min(512 / (L.cat ? 3 * NT : NT), taps.taps_box));
-    for (int ph = 0; ph < taps.n_phases; ++ph)
-      for (int t0 = 0; t0 < taps.phase_ntaps[ph]; t0 += p.tg) {
+    // The launch is one wave of (tile, tap group, split) CTAs, so its time is the largest
+    // group's: a phase's taps are spread evenly over its groups (3x3 with four accumulators
+    // per CTA: 3 + 3 + 3 instead of 4 + 4 + 1, whose lone-tap CTAs staged the same operands
+    // for a quarter of the MMAs)
+    for (int ph = 0; ph < taps.n_phases; ++ph) {
+      const int nt_ph = taps.phase_ntaps[ph], ng = cdiv(nt_ph, p.tg);
+      for (int i = 0, t0 = 0; i < ng; ++i) {
         if (p.n_tgroups >= kMaxTapGroups) fail(DCONV_ERR_UNSUPPORTED, "too many tap groups");
+        const int cnt = nt_ph / ng + (i < nt_ph % ng ? 1 : 0);
         p.tg_phase[p.n_tgroups] = ph;
         p.tg_tap0[p.n_tgroups] = taps.phase_tap0[ph] + t0;
-        p.tg_ntaps[p.n_tgroups] = std::min(p.tg, taps.phase_ntaps[ph] - t0);
+        p.tg_ntaps[p.n_tgroups] = cnt;
+        t0 += cnt;
         ++p.n_tgroups;
       }
+    }
   }
   // split-K factor (choose_update_strategy analog, planner.cpp:54-143: the same
   // trade-off of partial-copy traffic against parallelism, for 148 SMs):
